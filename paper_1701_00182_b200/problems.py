@@ -1,0 +1,324 @@
+"""Seeded block-tridiagonal systems: the reference's generators and the
+BASELINE.json configurations C1-C5.
+
+Layout (shared by the product C-ABI ``include/acrgpu.h`` and the CPU oracle):
+a system of ``n`` planes of ``dim`` unknowns is stored as 3n-2 sparse plane
+blocks in COO form -- blocks ``0..n-1`` are D(j), ``n..2n-2`` are E(j) for
+j = 1..n-1 (E(j) couples plane j to plane j-1), ``2n-1..3n-3`` are F(j) for
+j = 0..n-2 (couples j to j+1); block b owns entries ``blk_off[b]:blk_off[b+1]``.
+This is ``BlockTridiagonalSystem`` (reference proj/core/include/acr/block.hpp:67-92)
+flattened.  Right-hand sides are ``rhs[r, j, i]`` (RHS r, plane j, point i).
+
+Generators:
+  poisson(n)            reference assemble_poisson   (proj/core/src/discretize.cpp:46-71)
+  poisson2d_block(n)    reference poisson2d_block    (discretize.cpp:227-242)
+  config_system(k)      BASELINE.json configs[k-1] with the builder decisions of
+                        SURVEY.md §8(d) (documented in DESIGN.md §2).
+The portable RNG is splitmix64 -> 53-bit doubles; Box-Muller for
+N(0,1).  It replaces the reference's implementation-defined std::uniform_real.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(seed: int, stream: int, count: int) -> np.ndarray:
+    """``count`` splitmix64 outputs of the counter sequence keyed by (seed, stream)."""
+    base = np.uint64((seed * 0x632BE59BD9B4E019 + stream * 0x9E3779B97F4A7C15 + 0x1234567) & 0xFFFFFFFFFFFFFFFF)
+    i = np.arange(1, count + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = base + i * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def uniform01(seed: int, stream: int, count: int) -> np.ndarray:
+    z = splitmix64(seed, stream, count)
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+def uniform_pm1(seed: int, stream: int, count: int) -> np.ndarray:
+    return 2.0 * uniform01(seed, stream, count) - 1.0
+
+
+def normal(seed: int, stream: int, count: int) -> np.ndarray:
+    m = (count + 1) // 2
+    u = uniform01(seed, stream, 2 * m)
+    u1 = np.maximum(u[:m], 1e-300)
+    u2 = u[m:]
+    r = np.sqrt(-2.0 * np.log(u1))
+    out = np.concatenate([r * np.cos(2 * math.pi * u2), r * np.sin(2 * math.pi * u2)])
+    return out[:count]
+
+
+@dataclasses.dataclass
+class System:
+    """A block-tridiagonal system in the shared COO layout (see module doc)."""
+
+    n: int
+    dim: int
+    coords: np.ndarray      # (dim, 2) float64, plane point coordinates
+    blk_off: np.ndarray     # (3n-1,) int64
+    rows: np.ndarray        # int32
+    cols: np.ndarray        # int32
+    vals: np.ndarray        # float64
+    rhs: np.ndarray         # (nrhs, n, dim) float64
+    name: str = ""
+
+    @property
+    def nblocks(self) -> int:
+        return 3 * self.n - 2
+
+    @property
+    def total_dim(self) -> int:
+        return self.n * self.dim
+
+    def block(self, b: int):
+        s, e = int(self.blk_off[b]), int(self.blk_off[b + 1])
+        return self.rows[s:e], self.cols[s:e], self.vals[s:e]
+
+    def D(self, j):
+        return self.block(j)
+
+    def E(self, j):  # couples j -> j-1, j in [1, n)
+        return self.block(self.n + j - 1)
+
+    def F(self, j):  # couples j -> j+1, j in [0, n-1)
+        return self.block(2 * self.n - 1 + j)
+
+    def apply(self, u: np.ndarray) -> np.ndarray:
+        """y_j = E_j u_{j-1} + D_j u_j + F_j u_{j+1} (reference block.cpp:89-107).
+        u: (nrhs, n, dim) or (n, dim)."""
+        squeeze = u.ndim == 2
+        if squeeze:
+            u = u[None]
+        y = np.zeros_like(u)
+        n = self.n
+        for j in range(n):
+            r, c, v = self.D(j)
+            np.add.at(y[:, j], (slice(None), r), (v[None, :] * u[:, j][:, c]))
+            if j > 0:
+                r, c, v = self.E(j)
+                np.add.at(y[:, j], (slice(None), r), (v[None, :] * u[:, j - 1][:, c]))
+            if j < n - 1:
+                r, c, v = self.F(j)
+                np.add.at(y[:, j], (slice(None), r), (v[None, :] * u[:, j + 1][:, c]))
+        return y[0] if squeeze else y
+
+    def relative_residual(self, u: np.ndarray, rhs: np.ndarray | None = None) -> float:
+        """||A u - f||_2 / ||f||_2 over all planes and RHS (reference block.cpp:109-123)."""
+        f = self.rhs if rhs is None else rhs
+        if u.ndim == 2:
+            u = u[None]
+        if f.ndim == 2:
+            f = f[None]
+        fn = float(np.sum(f * f))
+        if fn == 0.0:
+            raise ZeroDivisionError("relative residual undefined: right-hand side has zero norm")
+        r = self.apply(u) - f
+        return math.sqrt(float(np.sum(r * r)) / fn)
+
+    def to_dense(self) -> np.ndarray:
+        """Full operator (small n only; reference block.cpp:74-86)."""
+        N = self.total_dim
+        A = np.zeros((N, N))
+        d = self.dim
+        for j in range(self.n):
+            r, c, v = self.D(j)
+            np.add.at(A, (j * d + r, j * d + c), v)
+            if j > 0:
+                r, c, v = self.E(j)
+                np.add.at(A, (j * d + r, (j - 1) * d + c), v)
+            if j < self.n - 1:
+                r, c, v = self.F(j)
+                np.add.at(A, (j * d + r, (j + 1) * d + c), v)
+        return A
+
+
+def plane_coords(n: int) -> np.ndarray:
+    """Grid node coordinates ((i+1)h, (j+1)h), index j*n+i (discretize.cpp:12-19)."""
+    h = 1.0 / (n + 1)
+    j, i = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    return np.stack([(i.ravel() + 1) * h, (j.ravel() + 1) * h], axis=1).astype(np.float64)
+
+
+def _assemble(n, dim, coords, blocks, rhs, name=""):
+    """blocks: list of (rows, cols, vals) in block order D.., E(1..), F(..n-2)."""
+    counts = [len(b[0]) for b in blocks]
+    off = np.zeros(len(blocks) + 1, dtype=np.int64)
+    off[1:] = np.cumsum(counts)
+    rows = np.concatenate([np.asarray(b[0], np.int32) for b in blocks]) if blocks else np.zeros(0, np.int32)
+    cols = np.concatenate([np.asarray(b[1], np.int32) for b in blocks]) if blocks else np.zeros(0, np.int32)
+    vals = np.concatenate([np.asarray(b[2], np.float64) for b in blocks]) if blocks else np.zeros(0)
+    return System(n, dim, np.ascontiguousarray(coords, np.float64), off, rows, cols, vals,
+                  np.ascontiguousarray(rhs, np.float64), name)
+
+
+def _stencil_block(n, center, west, east, south, north):
+    j, i = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    i = i.ravel()
+    j = j.ravel()
+    r = j * n + i
+    m = n * n
+    rs, cs, vs = [r], [r], [np.broadcast_to(np.asarray(center, np.float64), (m,))]
+    for mask, off, coef in ((i > 0, -1, west), (i < n - 1, 1, east), (j > 0, -n, south), (j < n - 1, n, north)):
+        c = np.broadcast_to(np.asarray(coef, np.float64), (m,))
+        rs.append(r[mask])
+        cs.append(r[mask] + off)
+        vs.append(c[mask])
+    rows = np.concatenate(rs)
+    cols = np.concatenate(cs)
+    vals = np.concatenate(vs)
+    order = np.lexsort((cols, rows))
+    return rows[order].astype(np.int32), cols[order].astype(np.int32), vals[order].astype(np.float64)
+
+
+def _diag_block(m, diag):
+    r = np.arange(m, dtype=np.int32)
+    return r, r.copy(), np.broadcast_to(np.asarray(diag, np.float64), (m,)).copy()
+
+
+def _constant_coeff(n, center, west, east, south, north, elow, fhigh, rhs, name):
+    m = n * n
+    coords = plane_coords(n)
+    D = _stencil_block(n, center, west, east, south, north)
+    E = _diag_block(m, elow)
+    F = _diag_block(m, fhigh)
+    blocks = [D] * n + [E] * (n - 1) + [F] * (n - 1)
+    return _assemble(n, m, coords, blocks, rhs, name)
+
+
+def poisson(n: int, rhs: np.ndarray | None = None) -> System:
+    """Reference assemble_poisson: 7-point star, h^2-scaled, centre 6, E=F=-I,
+    f = h^2 (proj/core/src/discretize.cpp:46-71)."""
+    if n < 2:
+        raise ValueError("GridSpec: n must be >= 2")
+    h = 1.0 / (n + 1)
+    if rhs is None:
+        rhs = np.full((1, n, n * n), h * h)
+    return _constant_coeff(n, 6.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, rhs, f"poisson{n}")
+
+
+def poisson2d_block(n: int):
+    """Reference poisson2d_block: 5-point 2D Laplacian plane block (centre 4)
+    (discretize.cpp:227-242).  Returns (rows, cols, vals, coords)."""
+    r, c, v = _stencil_block(n, 4.0, -1.0, -1.0, -1.0, -1.0)
+    return r, c, v, plane_coords(n)
+
+
+def identity_system(n: int, dim: int, rhs: np.ndarray) -> System:
+    """n identity planes, no coupling (proj/tests/test_helpers.hpp:50-62)."""
+    side = int(round(math.sqrt(dim)))
+    coords = np.stack([np.arange(dim) % side, np.arange(dim) // side], axis=1).astype(np.float64)
+    I = _diag_block(dim, 1.0)
+    Z = (np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0))
+    blocks = [I] * n + [Z] * (2 * (n - 1))
+    return _assemble(n, dim, coords, blocks, rhs.reshape(1, n, dim), "identity")
+
+
+# ----------------------------------------------------------------------------
+# BASELINE.json configurations (SURVEY.md §8(d) builder decisions)
+# ----------------------------------------------------------------------------
+
+def seeded_rhs(seed: int, nrhs: int, n: int, dim: int) -> np.ndarray:
+    return uniform_pm1(seed, 1, nrhs * n * dim).reshape(nrhs, n, dim)
+
+
+def kappa_field(n: int, seed: int) -> np.ndarray:
+    """kappa = exp(g) on the (n+2)^3 node lattice (boundary nodes included):
+    g i.i.d. N(0,1), three 3x3x3 box-filter passes with clamp padding, then
+    standardised and scaled so max(g)-min(g) = ln(100) (contrast exactly 100)."""
+    g = normal(seed, 2, (n + 2) ** 3).reshape(n + 2, n + 2, n + 2)
+    for _ in range(3):
+        p = np.pad(g, 1, mode="edge")
+        acc = np.zeros_like(g)
+        for dz in range(3):
+            for dy in range(3):
+                for dx in range(3):
+                    acc += p[dz:dz + n + 2, dy:dy + n + 2, dx:dx + n + 2]
+        g = acc / 27.0
+    g = (g - g.mean()) / g.std()
+    g = g * (math.log(100.0) / (g.max() - g.min()))
+    return np.exp(g)  # indexed [z, y, x]
+
+
+def vardiff(n: int, seed: int, nrhs: int = 1, name: str = "") -> System:
+    """-div(kappa grad u) = f, 7-point FD, harmonic-mean face coefficients,
+    h^2-scaled, symmetric (BASELINE configs 2 and 5)."""
+    kap = kappa_field(n, seed)
+    m = n * n
+
+    def face(a, b):
+        return 2.0 * a * b / (a + b)
+
+    inner = kap[1:n + 1, 1:n + 1, 1:n + 1]  # [z, y, x] of the unknowns
+    kw = face(inner, kap[1:n + 1, 1:n + 1, 0:n])
+    ke = face(inner, kap[1:n + 1, 1:n + 1, 2:n + 2])
+    ks = face(inner, kap[1:n + 1, 0:n, 1:n + 1])
+    kn = face(inner, kap[1:n + 1, 2:n + 2, 1:n + 1])
+    kd = face(inner, kap[0:n, 1:n + 1, 1:n + 1])
+    ku = face(inner, kap[2:n + 2, 1:n + 1, 1:n + 1])
+    center = kw + ke + ks + kn + kd + ku
+    Ds, Es, Fs = [], [], []
+    for z in range(n):
+        Ds.append(_stencil_block(n, center[z].ravel(), -kw[z].ravel(), -ke[z].ravel(), -ks[z].ravel(), -kn[z].ravel()))
+    for z in range(1, n):
+        Es.append(_diag_block(m, -kd[z].ravel()))
+    for z in range(n - 1):
+        Fs.append(_diag_block(m, -ku[z].ravel()))
+    rhs = seeded_rhs(seed, nrhs, n, m)
+    return _assemble(n, m, plane_coords(n), Ds + Es + Fs, rhs, name or f"vardiff{n}")
+
+
+def convdiff_upwind(n: int, seed: int, beta: float = 50.0, nrhs: int = 1) -> System:
+    """-lap u + beta.grad u, beta = (b,b,b), first-order upwind (backward
+    differences for b > 0), h^2-scaled, nonsymmetric (BASELINE config 3)."""
+    h = 1.0 / (n + 1)
+    bh = beta * h
+    rhs = seeded_rhs(seed, nrhs, n, n * n)
+    return _constant_coeff(n, 6.0 + 3.0 * bh, -1.0 - bh, -1.0, -1.0 - bh, -1.0, -1.0 - bh, -1.0, rhs,
+                           f"convdiff{n}")
+
+
+def helmholtz7(n: int, seed: int, omega: float = 2 * math.pi * 6.4, nrhs: int = 1) -> System:
+    """-lap u - omega^2 u, 7-point FD, h^2-scaled; RHS = unit point source at
+    node (n/2, n/2, n/2) plus 1e-3 * U[-1,1] (BASELINE config 4)."""
+    h = 1.0 / (n + 1)
+    rhs = 1e-3 * seeded_rhs(seed, nrhs, n, n * n)
+    c = n // 2
+    rhs[:, c, c * n + c] += 1.0
+    return _constant_coeff(n, 6.0 - omega * omega * h * h, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, rhs,
+                           f"helmholtz{n}")
+
+
+#: BASELINE.json configs (1-based).  ``n`` may be overridden for parity-size runs.
+CONFIGS = {
+    1: dict(kind="poisson", n=32, leaf=32, eps=1e-6, nrhs=1),
+    2: dict(kind="vardiff", n=64, leaf=32, eps=1e-6, nrhs=1),
+    3: dict(kind="convdiff", n=64, leaf=32, eps=1e-6, nrhs=1),
+    4: dict(kind="helmholtz", n=64, leaf=32, eps=1e-4, nrhs=1),
+    5: dict(kind="vardiff", n=128, leaf=64, eps=1e-6, nrhs=16),
+}
+
+
+def config_system(k: int, n: int | None = None, seed: int = 2024, nrhs: int | None = None) -> System:
+    c = CONFIGS[k]
+    n = c["n"] if n is None else n
+    nrhs = c["nrhs"] if nrhs is None else nrhs
+    if c["kind"] == "poisson":
+        sysm = poisson(n, rhs=seeded_rhs(seed, nrhs, n, n * n))
+    elif c["kind"] == "vardiff":
+        sysm = vardiff(n, seed, nrhs)
+    elif c["kind"] == "convdiff":
+        sysm = convdiff_upwind(n, seed, nrhs=nrhs)
+    else:
+        sysm = helmholtz7(n, seed, nrhs=nrhs)
+    sysm.name = f"C{k}:{c['kind']}{n}"
+    return sysm
