@@ -1,0 +1,157 @@
+/*
+ * acrgpu.h — C-ABI of the B200-native ACR (Accelerated Cyclic Reduction)
+ * hierarchical-matrix factor/solve path.  libacrgpu.so (sm_100a) implements it.
+ *
+ * Drop-in boundary: these entry points replace the H-matrix-mode bodies of the
+ * reference's public API (all paths relative to /root/reference/proj):
+ *
+ *   acrgpu_factor        <- acr::acr_factor(const BlockTridiagonalSystem&, const AcrConfig&)
+ *                           core/include/acr/acr.hpp:222, core/src/acr.cpp:366-384
+ *                           (lift_hmatrix acr.cpp:316-333 + factor_impl acr.cpp:146-160)
+ *   acrgpu_solve         <- acr::AcrFactorization::solve(const std::vector<Eigen::VectorXd>&) const
+ *                           core/include/acr/acr.hpp:205, core/src/acr.cpp:350-352 (solve_impl 180-229);
+ *                           nrhs > 1 = one pass for r right-hand sides
+ *   acrgpu_stats         <- AcrFactorization::factor_bytes() / inverse_rank_stats()
+ *                           acr.hpp:207-209, acr.cpp:231-258
+ *   acrgpu_level_info    <- AcrFactorization::level_info()  acr.hpp:210, acr.cpp:260-300
+ *   acrgpu_dinv_ranks    <- (test surface) leaf ranks of one stored inverse, rank_stats walk
+ *                           core/src/hmatrix.cpp:538-554
+ *   acrgpu_structure     <- ClusterTree / BlockClusterTree (core/src/cluster.cpp:39-126):
+ *                           permutation + leaf table, for structure parity tests
+ *   acrgpu_ctx_* / acrgpu_factor_destroy  <- object lifetimes (value types in the reference)
+ *
+ * Errors map 1:1 onto the reference exception classes (core/include/acr/errors.hpp:10-60):
+ *   ACRGPU_E_DIMENSION  DimensionError(plane)        ACRGPU_E_SINGULAR  SingularBlockError(level, plane)
+ *   ACRGPU_E_LEAFMEM    LeafMemoryError               ACRGPU_E_USAGE     UsageError
+ *   ACRGPU_E_DEVICE     CUDA / device-memory failure (no reference equivalent)
+ *
+ * System layout: 3n-2 sparse plane blocks in COO form (plane-local indices):
+ *   block b in [0, n)        : D(b)
+ *   block b in [n, 2n-1)     : E(j), j = b-n+1   (couples plane j to plane j-1; block.hpp:79-80)
+ *   block b in [2n-1, 3n-2)  : F(j), j = b-2n+1  (couples plane j to plane j+1)
+ *   block b owns entries [blk_off[b], blk_off[b+1]) of rows/cols/vals; duplicates are summed
+ *   (PlaneBlock, core/src/block.cpp:7-29).  coords: 2*dim doubles (x0,y0,x1,y1,...) of the
+ *   plane points, used for geometric clustering (one cluster tree shared by all blocks).
+ * Vectors: f / u are [nrhs][n][dim] doubles, original (unpermuted) ordering.
+ *
+ * Ownership: caller owns every host buffer; the library owns device memory behind the
+ * opaque handles until *_destroy.  A factor handle is immutable after acrgpu_factor;
+ * solves on one handle are serialised on the context stream.  No callbacks.
+ */
+#ifndef ACRGPU_H
+#define ACRGPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    ACRGPU_OK = 0,
+    ACRGPU_E_DIMENSION = 1,
+    ACRGPU_E_SINGULAR = 2,
+    ACRGPU_E_LEAFMEM = 3,
+    ACRGPU_E_USAGE = 4,
+    ACRGPU_E_DEVICE = 5,
+    ACRGPU_E_INTERNAL = 9
+};
+
+/* AcrConfig (core/include/acr/acr.hpp:15-23), H-matrix mode. */
+typedef struct acrgpu_config {
+    double eps;             /* truncation tolerance (arithmetic runs at eps*0.5, acr.hpp:178-181) */
+    double eta;             /* admissibility parameter */
+    int leaf_size;          /* cluster-tree leaf size (<= 64 on the GPU path) */
+    int weak;               /* 0 = Admissibility::Standard, 1 = Admissibility::Weak */
+    int stop_planes;        /* remaining plane count at which reduction stops (>= 1) */
+    long leaf_memory_cap;   /* bytes per materialised leaf (hmatrix.hpp:60) */
+    int flags;              /* ACRGPU_F_* below */
+} acrgpu_config;
+
+/* Deliberate, documented deviation switch: dense*dense leaf products that land
+ * in dense target leaves are added exactly (GEMM) instead of SVD-truncated first
+ * (reference quirk, hmatrix.cpp:411-413).  Off by default (reference semantics). */
+#define ACRGPU_F_EXACT_DENSE_PRODUCTS 1
+
+typedef struct acrgpu_error {
+    int code;
+    int level;       /* SingularBlockError level (-1 if n/a) */
+    int plane;       /* SingularBlockError / DimensionError plane (-1 if n/a) */
+    int row_begin;   /* failing dense pivot rows (tree order), -1 if n/a */
+    int row_end;
+    char msg[256];
+} acrgpu_error;
+
+typedef struct acrgpu_system {
+    int n;                  /* plane count */
+    int dim;                /* unknowns per plane */
+    const double* coords;   /* 2*dim */
+    const long* blk_off;    /* 3n-1 */
+    const int* rows;
+    const int* cols;
+    const double* vals;
+} acrgpu_system;
+
+typedef struct acrgpu_rankstats {  /* RankStats (hmatrix.hpp:26-32) over stored inverses */
+    double average_rank;
+    int largest_rank;
+    int dense_leaf_count;
+    int lowrank_leaf_count;
+    long inverse_bytes;
+    long factor_bytes;             /* AcrFactorization::factor_bytes (acr.cpp:231-248) */
+} acrgpu_rankstats;
+
+typedef struct acrgpu_levelinfo {  /* LevelInfo (acr.hpp:185-192) */
+    int level;
+    int plane_count;
+    int eliminated;
+    long bytes;
+    int largest_rank;
+    double average_rank;
+} acrgpu_levelinfo;
+
+typedef struct acrgpu_timing {     /* device-event phase times of the last call (ms) */
+    double lift_ms;
+    double factor_ms;              /* includes lift */
+    double solve_ms;
+    double flops_nominal;          /* nominal FLOP count of the last factorization */
+    double flops_svd, flops_qr, flops_gemm, flops_lu;
+    long kernel_launches;          /* kernels launched by the last call */
+} acrgpu_timing;
+
+typedef struct acrgpu_ctx acrgpu_ctx;
+typedef struct acrgpu_fact acrgpu_fact;
+
+/* Context on one CUDA device (device < 0: current device). */
+int acrgpu_ctx_create(int device, acrgpu_ctx** out, acrgpu_error* err);
+void acrgpu_ctx_destroy(acrgpu_ctx* ctx);
+
+/* acr_factor in H-matrix mode.  System blocks are read from host memory. */
+int acrgpu_factor(acrgpu_ctx* ctx, const acrgpu_system* sys, const acrgpu_config* cfg,
+                  acrgpu_fact** out, acrgpu_error* err);
+void acrgpu_factor_destroy(acrgpu_fact* f);
+
+/* AcrFactorization::solve for nrhs right-hand sides; f, u host pointers ([nrhs][n][dim]). */
+int acrgpu_solve(acrgpu_fact* f, int nrhs, const double* f_host, double* u_host, acrgpu_error* err);
+/* Same, with f and u already resident in device memory (device pointers). */
+int acrgpu_solve_device(acrgpu_fact* f, int nrhs, const double* f_dev, double* u_dev, acrgpu_error* err);
+
+int acrgpu_stats(acrgpu_fact* f, acrgpu_rankstats* out);
+/* Fills up to cap entries (levels + apex); returns the count. */
+int acrgpu_level_info(acrgpu_fact* f, acrgpu_levelinfo* out, int cap);
+/* Leaf ranks (DFS order, -1 = dense leaf) of the stored inverse of plane j at level li
+ * (li == number of levels: apex).  Returns the leaf count, -1 if absent. */
+long acrgpu_dinv_ranks(acrgpu_fact* f, int li, int j, int* out, long cap);
+int acrgpu_timing_get(acrgpu_fact* f, acrgpu_timing* out);
+
+/* Structure only (no device work): permutation (tree pos -> original index, dim ints) and
+ * leaf table (DFS order; rb, re, cb, ce, kind with kind 0 = dense, 1 = low-rank).
+ * Returns the leaf count (leaves written up to cap), or -code on error. */
+long acrgpu_structure(int dim, const double* coords, int leaf_size, double eta, int weak,
+                      int* perm, int* leaves, long cap, acrgpu_error* err);
+
+/* Library build identification (sm arch, version). */
+const char* acrgpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACRGPU_H */

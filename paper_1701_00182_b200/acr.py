@@ -1,0 +1,348 @@
+"""Reference-facing API of the B200 ACR path (ctypes over libacrgpu.so).
+
+Mirrors the reference's public surface for the H-matrix hot path
+(/root/reference/proj/core/include/acr/acr.hpp:15-23,185-224 and errors.hpp:10-60):
+
+    AcrConfig                       acr.hpp:15-23
+    acr_factor(system, config)      acr.hpp:222      -> AcrFactorization
+    AcrFactorization.solve(f)       acr.hpp:205      (f: (n, dim) or (nrhs, n, dim))
+    .factor_bytes() / .inverse_rank_stats() / .level_info()   acr.hpp:207-210
+    acr_solve(fact, f)              acr.hpp:223
+    DimensionError / SingularBlockError / LeafMemoryError / UsageError   errors.hpp
+
+There is no CPU fallback: if libacrgpu.so is missing or no CUDA device is
+present, every call raises.  ``ArithmeticMode.Dense`` (the reference's exact
+DenseKernel oracle) is a CPU oracle mode and is rejected here (UsageError).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+import os
+
+import numpy as np
+
+from . import problems
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "libacrgpu.so")
+
+
+# ---------------------------------------------------------------- errors (errors.hpp)
+class Error(RuntimeError):
+    pass
+
+
+class DimensionError(Error):
+    def __init__(self, msg, plane=-1):
+        super().__init__(msg)
+        self.plane_index = plane
+
+
+class SingularBlockError(Error):
+    def __init__(self, msg, level=-1, plane=-1, rows=(-1, -1)):
+        super().__init__(msg)
+        self.level = level
+        self.plane = plane
+        self.rows = rows
+
+
+class LeafMemoryError(Error):
+    pass
+
+
+class UsageError(Error):
+    pass
+
+
+class DeviceError(Error):
+    pass
+
+
+class ArithmeticMode(enum.Enum):
+    Dense = 0
+    HMatrix = 1
+
+
+class Admissibility(enum.Enum):
+    Standard = 0
+    Weak = 1
+
+
+@dataclasses.dataclass
+class AcrConfig:
+    """AcrConfig (acr.hpp:15-23).  ``exact_dense_products`` is the documented
+    deviation switch, off by default."""
+
+    mode: ArithmeticMode = ArithmeticMode.HMatrix
+    eps: float = 1e-3
+    eta: float = 2.0
+    leaf_size: int = 32
+    admissibility: Admissibility = Admissibility.Standard
+    stop_planes: int = 1
+    leaf_memory_cap: int = 2 << 30
+    exact_dense_products: bool = False
+
+
+@dataclasses.dataclass
+class RankStats:
+    average_rank: float = 0.0
+    largest_rank: int = 0
+    dense_leaf_count: int = 0
+    lowrank_leaf_count: int = 0
+    bytes: int = 0
+
+
+@dataclasses.dataclass
+class LevelInfo:
+    level: int
+    plane_count: int
+    eliminated: int
+    bytes: int
+    largest_rank: int
+    average_rank: float
+
+
+# ---------------------------------------------------------------- ctypes layer
+class _Err(C.Structure):
+    _fields_ = [("code", C.c_int), ("level", C.c_int), ("plane", C.c_int), ("row_begin", C.c_int),
+                ("row_end", C.c_int), ("msg", C.c_char * 256)]
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("eps", C.c_double), ("eta", C.c_double), ("leaf_size", C.c_int), ("weak", C.c_int),
+                ("stop_planes", C.c_int), ("leaf_memory_cap", C.c_long), ("flags", C.c_int)]
+
+
+class _Sys(C.Structure):
+    _fields_ = [("n", C.c_int), ("dim", C.c_int), ("coords", C.POINTER(C.c_double)),
+                ("blk_off", C.POINTER(C.c_long)), ("rows", C.POINTER(C.c_int)), ("cols", C.POINTER(C.c_int)),
+                ("vals", C.POINTER(C.c_double))]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("average_rank", C.c_double), ("largest_rank", C.c_int), ("dense_leaf_count", C.c_int),
+                ("lowrank_leaf_count", C.c_int), ("inverse_bytes", C.c_long), ("factor_bytes", C.c_long)]
+
+
+class _Level(C.Structure):
+    _fields_ = [("level", C.c_int), ("plane_count", C.c_int), ("eliminated", C.c_int), ("bytes", C.c_long),
+                ("largest_rank", C.c_int), ("average_rank", C.c_double)]
+
+
+class _Timing(C.Structure):
+    _fields_ = [("lift_ms", C.c_double), ("factor_ms", C.c_double), ("solve_ms", C.c_double),
+                ("flops_nominal", C.c_double), ("flops_svd", C.c_double), ("flops_qr", C.c_double),
+                ("flops_gemm", C.c_double), ("flops_lu", C.c_double), ("kernel_launches", C.c_long)]
+
+
+SYMBOLS = {
+    "acrgpu_version": (C.c_char_p, []),
+    "acrgpu_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p), C.POINTER(_Err)]),
+    "acrgpu_ctx_destroy": (None, [C.c_void_p]),
+    "acrgpu_factor": (C.c_int, [C.c_void_p, C.POINTER(_Sys), C.POINTER(_Cfg), C.POINTER(C.c_void_p), C.POINTER(_Err)]),
+    "acrgpu_factor_destroy": (None, [C.c_void_p]),
+    "acrgpu_solve": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(_Err)]),
+    "acrgpu_solve_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(_Err)]),
+    "acrgpu_stats": (C.c_int, [C.c_void_p, C.POINTER(_Stats)]),
+    "acrgpu_level_info": (C.c_int, [C.c_void_p, C.POINTER(_Level), C.c_int]),
+    "acrgpu_dinv_ranks": (C.c_long, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_long]),
+    "acrgpu_timing_get": (C.c_int, [C.c_void_p, C.POINTER(_Timing)]),
+    "acrgpu_structure": (C.c_long, [C.c_int, C.POINTER(C.c_double), C.c_int, C.c_double, C.c_int,
+                                     C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_long, C.POINTER(_Err)]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libacrgpu.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise DeviceError(f"libacrgpu.so not built ({_LIB}); run paper_1701_00182_b200.build.build()")
+        L = C.CDLL(_LIB)
+        for name, (res, args) in SYMBOLS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _raise(err: _Err):
+    msg = err.msg.decode(errors="replace")
+    code = err.code
+    if code == 1:
+        raise DimensionError(msg, err.plane)
+    if code == 2:
+        raise SingularBlockError(msg, err.level, err.plane, (err.row_begin, err.row_end))
+    if code == 3:
+        raise LeafMemoryError(msg)
+    if code == 4:
+        raise UsageError(msg)
+    if code == 5:
+        raise DeviceError(msg)
+    raise Error(msg or f"acrgpu error {code}")
+
+
+def _p(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class Context:
+    """One CUDA device.  Reused across factorizations (device arenas are sized once)."""
+
+    def __init__(self, device: int = -1):
+        self.h = C.c_void_p()
+        err = _Err()
+        if lib().acrgpu_ctx_create(device, C.byref(self.h), C.byref(err)):
+            _raise(err)
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().acrgpu_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context()
+    return _default_ctx
+
+
+def _cfg(config: AcrConfig) -> _Cfg:
+    if config.mode != ArithmeticMode.HMatrix:
+        raise UsageError("the GPU path implements ArithmeticMode.HMatrix only (Dense mode is the CPU oracle)")
+    return _Cfg(config.eps, config.eta, config.leaf_size,
+                1 if config.admissibility == Admissibility.Weak else 0, config.stop_planes,
+                config.leaf_memory_cap, 1 if config.exact_dense_products else 0)
+
+
+class AcrFactorization:
+    """Reusable elimination record (acr.hpp:195-219); immutable after construction."""
+
+    def __init__(self, handle, system, config, ctx):
+        self.h = handle
+        self.config = config
+        self.n = system.n
+        self.dim = system.dim
+        self._ctx = ctx  # keep the context alive
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and self.h.value:
+                lib().acrgpu_factor_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def plane_count(self):
+        return self.n
+
+    def plane_dim(self):
+        return self.dim
+
+    def solve(self, f):
+        """f: (n, dim) -> (n, dim), or (nrhs, n, dim) -> (nrhs, n, dim) in one pass."""
+        f = np.asarray(f, dtype=np.float64)
+        squeeze = f.ndim == 2
+        f3 = f[None] if squeeze else f
+        if f3.ndim != 3 or f3.shape[1] != self.n:
+            raise DimensionError(f"solve: right-hand side has {f3.shape[1] if f3.ndim == 3 else '?'} planes, "
+                                 f"factorization has {self.n}")
+        if f3.shape[2] != self.dim:
+            raise DimensionError("solve: plane right-hand side dimension mismatch", 0)
+        f3 = np.ascontiguousarray(f3)
+        u = np.empty_like(f3)
+        err = _Err()
+        if lib().acrgpu_solve(self.h, f3.shape[0], f3.ctypes.data, u.ctypes.data, C.byref(err)):
+            _raise(err)
+        return u[0] if squeeze else u
+
+    def solve_device(self, f_ptr: int, u_ptr: int, nrhs: int):
+        """Device-resident solve (raw CUDA pointers, layout [nrhs][n][dim])."""
+        err = _Err()
+        if lib().acrgpu_solve_device(self.h, nrhs, C.c_void_p(f_ptr), C.c_void_p(u_ptr), C.byref(err)):
+            _raise(err)
+
+    def _stats(self):
+        s = _Stats()
+        lib().acrgpu_stats(self.h, C.byref(s))
+        return s
+
+    def factor_bytes(self) -> int:
+        return int(self._stats().factor_bytes)
+
+    def inverse_rank_stats(self) -> RankStats:
+        s = self._stats()
+        return RankStats(s.average_rank, s.largest_rank, s.dense_leaf_count, s.lowrank_leaf_count, s.inverse_bytes)
+
+    def level_info(self):
+        arr = (_Level * 64)()
+        k = lib().acrgpu_level_info(self.h, arr, 64)
+        return [LevelInfo(a.level, a.plane_count, a.eliminated, a.bytes, a.largest_rank, a.average_rank)
+                for a in arr[:k]]
+
+    def dinv_ranks(self, level: int, plane: int):
+        n = lib().acrgpu_dinv_ranks(self.h, level, plane, None, 0)
+        if n < 0:
+            return None
+        out = np.zeros(n, np.int32)
+        lib().acrgpu_dinv_ranks(self.h, level, plane, _p(out, C.c_int), n)
+        return out
+
+    def timing(self) -> dict:
+        t = _Timing()
+        lib().acrgpu_timing_get(self.h, C.byref(t))
+        return {k: getattr(t, k) for k, _ in _Timing._fields_}
+
+
+def acr_factor(system: problems.System, config: AcrConfig | None = None, ctx: Context | None = None):
+    """acr::acr_factor (acr.cpp:366-384) on the GPU."""
+    config = config or AcrConfig()
+    ctx = ctx or default_context()
+    cfg = _cfg(config)
+    coords = np.ascontiguousarray(system.coords, np.float64)
+    off = np.ascontiguousarray(system.blk_off, np.int64)
+    rows = np.ascontiguousarray(system.rows, np.int32)
+    cols = np.ascontiguousarray(system.cols, np.int32)
+    vals = np.ascontiguousarray(system.vals, np.float64)
+    s = _Sys(system.n, system.dim, _p(coords, C.c_double), _p(off, C.c_long), _p(rows, C.c_int), _p(cols, C.c_int),
+             _p(vals, C.c_double))
+    h = C.c_void_p()
+    err = _Err()
+    if lib().acrgpu_factor(ctx.h, C.byref(s), C.byref(cfg), C.byref(h), C.byref(err)):
+        _raise(err)
+    return AcrFactorization(h, system, config, ctx)
+
+
+def acr_solve(fact: AcrFactorization, f):
+    return fact.solve(f)
+
+
+def structure(coords, leaf_size=32, eta=2.0, weak=False):
+    """(perm, leaves) of the library's cluster / block cluster tree (no device needed)."""
+    coords = np.ascontiguousarray(coords, np.float64)
+    dim = coords.shape[0]
+    err = _Err()
+    n = lib().acrgpu_structure(dim, _p(coords, C.c_double), leaf_size, eta, 1 if weak else 0, None, None, 0,
+                               C.byref(err))
+    if n < 0:
+        _raise(err)
+    perm = np.zeros(dim, np.int32)
+    leaves = np.zeros((n, 5), np.int32)
+    lib().acrgpu_structure(dim, _p(coords, C.c_double), leaf_size, eta, 1 if weak else 0, _p(perm, C.c_int),
+                           _p(leaves, C.c_int), n, C.byref(err))
+    return perm, leaves

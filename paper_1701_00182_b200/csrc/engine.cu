@@ -1,0 +1,1600 @@
+// Host engine of libacrgpu.so: batched H-matrix arithmetic plans, the cyclic
+// reduction level driver, the solve, and the C-ABI (include/acrgpu.h).
+//
+// Reference path (relative to /root/reference/proj/core):
+//   acr_factor / lift_hmatrix / factor_impl   src/acr.cpp:146-160,316-384
+//   reduce_level                              src/acr.cpp:70-120
+//   eliminate_around / forward_rhs / back     include/acr/acr.hpp:78-132
+//   factor_apex / solve_apex / solve_impl     src/acr.cpp:123-144,162-229
+//   mult_add / mult_add_rec / deposit / flush src/hmatrix.cpp:352-479
+//   invert_node                               src/hmatrix.cpp:483-534
+//   recompress                                src/hmatrix.cpp:623-662
+//   stats                                     src/acr.cpp:231-300, src/hmatrix.cpp:538-554
+//
+// B200 design: every H-matrix of a factorization shares one structure, so the
+// mult_add / invert_node recursions depend only on leaf kinds and are compiled
+// once per structural triple into phase task lists ("plans").  All planes of a
+// cyclic-reduction level execute the same plan in one launch per phase
+// (grid.y = plane), ranks live in device memory, and data-dependent outputs are
+// carved from device bump arenas -- no host synchronisation inside a level.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/acrgpu.h"
+#include "kernels.hpp"
+#include "structure.hpp"
+
+namespace acrgpu {
+
+// ------------------------------------------------------------------ errors
+struct AcrError {
+    int code;
+    std::string msg;
+    int level = -1, plane = -1, rb = -1, re = -1;
+};
+
+#define CK(x)                                                                                     \
+    do {                                                                                          \
+        cudaError_t e_ = (x);                                                                     \
+        if (e_ != cudaSuccess)                                                                    \
+            throw AcrError{ACRGPU_E_DEVICE, std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x}; \
+    } while (0)
+
+template <class T>
+static T* dmalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    return (T*)p;
+}
+
+template <class T>
+static T* upload(const std::vector<T>& v, cudaStream_t st) {
+    T* p = dmalloc<T>(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return p;
+}
+
+// ------------------------------------------------------------------ context
+struct Ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    Arena persist{}, trans{};
+    double* persist_base = nullptr;
+    double* trans_base = nullptr;
+    unsigned long long* ctrs = nullptr;  // [0] persist, [1] trans
+    int* overflow = nullptr;             // [0] persist, [1] trans
+    DevError* err = nullptr;
+    FlopLedger* flops = nullptr;
+    Slot* slots = nullptr;
+    size_t slots_cap = 0;
+    double* scratch = nullptr;  // sigma / abs-cut scratch
+    size_t scratch_cap = 0;
+    unsigned long long call_id = 0;
+    std::vector<std::pair<int, std::vector<int>>> call_planes;  // call id -> (level, planes)
+
+    void init(int dev) {
+        if (dev >= 0) CK(cudaSetDevice(dev));
+        CK(cudaGetDevice(&device));
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        setup_kernels();
+        size_t freeb = 0, total = 0;
+        CK(cudaMemGetInfo(&freeb, &total));
+        const size_t pbytes = (size_t)(freeb * 0.42) & ~(size_t)4095;
+        const size_t tbytes = (size_t)(freeb * 0.14) & ~(size_t)4095;
+        persist_base = dmalloc<double>(pbytes / 8);
+        trans_base = dmalloc<double>(tbytes / 8);
+        ctrs = dmalloc<unsigned long long>(2);
+        overflow = dmalloc<int>(2);
+        err = dmalloc<DevError>(1);
+        flops = dmalloc<FlopLedger>(1);
+        persist = Arena{persist_base, pbytes / 8, ctrs, overflow};
+        trans = Arena{trans_base, tbytes / 8, ctrs + 1, overflow + 1};
+        reset_all();
+    }
+    void reset_all() {
+        CK(cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(overflow, 0, 2 * sizeof(int), st));
+        DevError e0;
+        std::memset(&e0, 0, sizeof(e0));
+        e0.key = ~0ull;
+        CK(cudaMemcpyAsync(err, &e0, sizeof(e0), cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(flops, 0, sizeof(FlopLedger), st));
+        CK(cudaStreamSynchronize(st));
+        call_id = 0;
+        call_planes.clear();
+    }
+    Slot* get_slots(size_t n) {
+        if (n > slots_cap) {
+            CK(cudaStreamSynchronize(st));
+            if (slots) cudaFree(slots);
+            slots_cap = std::max(n, slots_cap * 2);
+            slots = dmalloc<Slot>(slots_cap);
+        }
+        return slots;
+    }
+    double* get_scratch(size_t n) {
+        if (n > scratch_cap) {
+            CK(cudaStreamSynchronize(st));
+            if (scratch) cudaFree(scratch);
+            scratch_cap = std::max(n, scratch_cap * 2);
+            scratch = dmalloc<double>(scratch_cap);
+        }
+        return scratch;
+    }
+    void destroy() {
+        if (st) cudaStreamSynchronize(st);
+        for (void* p : std::initializer_list<void*>{persist_base, trans_base, ctrs, overflow, err, flops, slots, scratch})
+            if (p) cudaFree(p);
+        if (st) cudaStreamDestroy(st);
+        st = nullptr;
+    }
+};
+
+// ------------------------------------------------------------------ storage / views
+// One H-matrix instance over structure node `node`:
+// [dense pool slice | U ptrs | V ptrs | ranks] in one stream-ordered allocation.
+struct Store {
+    int node = 0;
+    void* block = nullptr;
+    double* dense = nullptr;
+    double** U = nullptr;
+    double** V = nullptr;
+    int* rank = nullptr;
+};
+using StoreP = std::shared_ptr<Store>;
+
+struct Engine;
+
+struct View {  // (store, sub-node)
+    StoreP s;
+    int node = 0;
+};
+
+// ------------------------------------------------------------------ compiled plans
+struct Plan {
+    int nprod = 0;
+    int nalloc = 0, napply = 0, ndd = 0, nflush = 0, ndep = 0;
+    AllocTask* allocs = nullptr;
+    ApplyTask* applies = nullptr;
+    ApplyLeaf* aleaves = nullptr;
+    int* x_ld = nullptr;
+    DDTask* dds = nullptr;
+    std::vector<std::pair<TruncTask*, int>> bb;  // phases
+    TruncTask* flush = nullptr;
+    DepTask* deps = nullptr;
+    Part* parts = nullptr;
+};
+
+struct Engine {
+    Ctx* ctx = nullptr;
+    Structure S;
+    acrgpu_config cfg{};
+    bool exact_dd = false;
+    std::map<std::tuple<int, int, int, int>, std::unique_ptr<Plan>> plans;
+    std::vector<void*> dev_allocs;  // plan arrays etc.
+
+    // structure-wide device tables
+    int* d_perm = nullptr;
+    int* d_iperm = nullptr;
+    long* d_doff = nullptr;
+    int* d_dm = nullptr;
+    int* d_dn = nullptr;
+    TruncTask* leaf_tasks = nullptr;  // one per Rk leaf (recompress)
+    Part* leaf_parts = nullptr;
+    SlabTask* slabs = nullptr;        // matvec slabs of the root
+    ApplyLeaf* slab_leaves = nullptr;
+    int nslabs = 0;
+
+    ~Engine() {
+        for (void* p : dev_allocs) cudaFree(p);
+    }
+    template <class T>
+    T* keep(T* p) {
+        dev_allocs.push_back((void*)p);
+        return p;
+    }
+    template <class T>
+    T* up(const std::vector<T>& v) {
+        return keep(upload(v, ctx->st));
+    }
+    cudaStream_t st() const { return ctx->st; }
+
+    // -------------------------------------------------------------- storage
+    StoreP new_store(int node) {
+        const SNode& n = S.node(node);
+        const size_t nk = n.k1 - n.k0;
+        const size_t bytes = n.dsize * 8 + nk * 16 + nk * 4 + 64;
+        auto s = std::make_shared<Store>();
+        s->node = node;
+        CK(cudaMallocAsync(&s->block, bytes, st()));
+        char* p = (char*)s->block;
+        s->dense = (double*)p;
+        s->U = (double**)(p + n.dsize * 8);
+        s->V = s->U + nk;
+        s->rank = (int*)(s->V + nk);
+        cudaStream_t stream = st();
+        return StoreP(s.get(), [s, stream](Store*) mutable {
+            if (s->block) cudaFreeAsync(s->block, stream);
+            s->block = nullptr;
+        });
+    }
+    HView hview(const View& v) const {
+        const SNode& root = S.node(v.s->node);
+        const SNode& n = S.node(v.node);
+        HView h;
+        h.dense = v.s->dense + (n.doff0 - root.doff0);
+        const int ko = n.k0 - root.k0;
+        h.rank = v.s->rank + ko;
+        h.U = v.s->U + ko;
+        h.V = v.s->V + ko;
+        return h;
+    }
+    static View child(const View& v, const Engine& e, int c) { return View{v.s, e.S.node(v.node).ch[c]}; }
+
+    void zero(const std::vector<View>& vs) {
+        for (size_t i0 = 0; i0 < vs.size(); i0 += MAXB) {
+            BatchViews bv{};
+            bv.count = (int)std::min<size_t>(MAXB, vs.size() - i0);
+            for (int b = 0; b < bv.count; ++b) bv.c[b] = hview(vs[i0 + b]);
+            const SNode& n = S.node(vs[i0].node);
+            launch_zero_views(st(), bv, n.dsize, n.k1 - n.k0);
+        }
+    }
+    void copy(const std::vector<View>& dst, const std::vector<View>& src) {
+        for (size_t i0 = 0; i0 < dst.size(); i0 += MAXB) {
+            BatchViews bv{};
+            bv.count = (int)std::min<size_t>(MAXB, dst.size() - i0);
+            for (int b = 0; b < bv.count; ++b) {
+                bv.c[b] = hview(dst[i0 + b]);
+                bv.a[b] = hview(src[i0 + b]);
+            }
+            const SNode& n = S.node(dst[i0].node);
+            launch_copy_views(st(), bv, n.dsize, n.k1 - n.k0);
+        }
+    }
+    std::vector<View> fresh(int node, size_t count) {
+        std::vector<View> v;
+        for (size_t i = 0; i < count; ++i) v.push_back(View{new_store(node), node});
+        return v;
+    }
+    std::vector<View> clone(const std::vector<View>& src) {
+        if (src.empty()) return {};
+        auto d = fresh(src[0].node, src.size());
+        copy(d, src);
+        return d;
+    }
+
+    // -------------------------------------------------------------- plan compiler
+    struct PlanBuild {
+        std::vector<AllocTask> allocs;
+        std::vector<ApplyTask> applies;
+        std::vector<ApplyLeaf> aleaves;
+        std::vector<int> x_ld;
+        std::vector<DDTask> dds;
+        std::vector<std::vector<TruncTask>> bb;
+        std::vector<TruncTask> flush;
+        std::vector<DepTask> deps;
+        std::vector<Part> parts;
+        std::vector<int> phase;  // per product
+        int nprod = 0;
+        // per target leaf deposit lists (ordered by first deposit)
+        std::vector<std::pair<int, std::vector<Part>>> dense_t, rk_t;
+        std::map<int, int> dense_idx, rk_idx;
+    };
+
+    void subtree_leaves(int node, std::vector<int>& out) const {
+        const SNode& n = S.node(node);
+        if (n.kind == K_BRANCH) {
+            for (int i = 0; i < 4; ++i) subtree_leaves(n.ch[i], out);
+        } else {
+            out.push_back(node);
+        }
+    }
+
+    // output slabs over [0, len) of the row (or column) range starting at tree position pos0
+    std::vector<std::pair<int, int>> slabs_of(int pos0, int len) const {
+        std::vector<std::pair<int, int>> sl;
+        int p = pos0;
+        const int end = pos0 + len;
+        while (p < end) {
+            int q = p;
+            // grow over whole leaf clusters while <= 64 rows
+            while (q < end) {
+                const int ci = S.cl_index[q];
+                const int ce = std::min(S.cl_end[ci], end);
+                if (ce - p > 64 && q > p) break;
+                q = ce;
+                if (q - p >= 64) break;
+            }
+            if (q - p > 64) q = p + 64;  // leaf clusters larger than 64 (unsupported leaf sizes)
+            sl.push_back({p - pos0, q - pos0});
+            p = q;
+        }
+        return sl;
+    }
+
+    // apply product: output over subtree `hnode` of operand with view root `hroot`
+    void emit_apply(PlanBuild& pb, int pid, int kind, int kx, int hnode, int hroot, int xld) {
+        const SNode& H = S.node(hnode);
+        const SNode& R = S.node(hroot);
+        const bool trans = kind == P_RK_LEFT;
+        std::vector<int> lv;
+        subtree_leaves(hnode, lv);
+        const int out_pos0 = trans ? H.cb : H.rb;
+        const int out_len = trans ? H.cols() : H.rows();
+        for (auto [r0, r1] : slabs_of(out_pos0, out_len)) {
+            ApplyTask t;
+            t.prod = pid;
+            t.kind = kind;
+            t.kx = kx;
+            t.r0 = r0;
+            t.r1 = r1;
+            t.lbeg = (int)pb.aleaves.size();
+            for (int li : lv) {
+                const SNode& L = S.node(li);
+                const int o0 = (trans ? L.cb - H.cb : L.rb - H.rb);
+                const int ol = trans ? L.cols() : L.rows();
+                if (o0 >= r1 || o0 + ol <= r0) continue;
+                ApplyLeaf a;
+                a.kind = L.kind;
+                a.id = L.kind == K_RK ? L.leaf - R.k0 : -1;
+                a.doff = L.kind == K_DENSE ? S.d_off[L.leaf] - R.doff0 : 0;
+                a.m = L.rows();
+                a.n = L.cols();
+                a.in_off = trans ? L.rb - H.rb : L.cb - H.cb;
+                a.out_off = o0;
+                pb.aleaves.push_back(a);
+            }
+            t.lend = (int)pb.aleaves.size();
+            pb.applies.push_back(t);
+            pb.x_ld.push_back(xld);
+        }
+    }
+
+    int emit_product(PlanBuild& pb, int a, int b, int aroot, int broot) {
+        const SNode& A = S.node(a);
+        const SNode& Bn = S.node(b);
+        const SNode& AR = S.node(aroot);
+        const SNode& BR = S.node(broot);
+        if (A.kind == K_RK) {
+            const int pid = pb.nprod++;
+            pb.phase.push_back(0);
+            AllocTask t{pid, P_RK_LEFT, A.leaf - AR.k0, Bn.cols(), A.rows()};
+            pb.allocs.push_back(t);
+            emit_apply(pb, pid, P_RK_LEFT, A.leaf - AR.k0, b, broot, A.cols());
+            return pid;
+        }
+        if (Bn.kind == K_RK) {
+            const int pid = pb.nprod++;
+            pb.phase.push_back(0);
+            AllocTask t{pid, P_RK_RIGHT, Bn.leaf - BR.k0, A.rows(), Bn.cols()};
+            pb.allocs.push_back(t);
+            emit_apply(pb, pid, P_RK_RIGHT, Bn.leaf - BR.k0, a, aroot, Bn.rows());
+            return pid;
+        }
+        if (A.kind == K_DENSE && Bn.kind == K_DENSE) {
+            const int pid = pb.nprod++;
+            pb.phase.push_back(0);
+            DDTask t;
+            t.prod = pid;
+            t.da = S.d_off[A.leaf] - AR.doff0;
+            t.db = S.d_off[Bn.leaf] - BR.doff0;
+            t.m = A.rows();
+            t.k = A.cols();
+            t.n = Bn.cols();
+            pb.dds.push_back(t);
+            return pid;
+        }
+        if (A.kind == K_BRANCH && Bn.kind == K_BRANCH) {
+            int kids[8], ar[8], bc[8], idx = 0, ph = 0;
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 2; ++j)
+                    for (int k = 0; k < 2; ++k) {
+                        ar[idx] = A.ch[i * 2 + k];
+                        bc[idx] = Bn.ch[k * 2 + j];
+                        kids[idx] = emit_product(pb, ar[idx], bc[idx], aroot, broot);
+                        ph = std::max(ph, pb.phase[kids[idx]]);
+                        ++idx;
+                    }
+            const int pid = pb.nprod++;
+            pb.phase.push_back(ph + 1);
+            TruncTask t;
+            t.out_kind = 0;
+            t.out_id = pid;
+            t.m = A.rows();
+            t.n = Bn.cols();
+            t.pbeg = (int)pb.parts.size();
+            for (int q = 0; q < 8; ++q) {
+                const SNode& ca = S.node(ar[q]);
+                const SNode& cb = S.node(bc[q]);
+                Part p{};
+                p.src = S_SLOT;
+                p.id = kids[q];
+                p.u_dst = ca.rb - A.rb;
+                p.v_dst = cb.cb - Bn.cb;
+                p.rows_u = ca.rows();
+                p.rows_v = cb.cols();
+                p.alpha = 1.0;
+                pb.parts.push_back(p);
+            }
+            t.pend = (int)pb.parts.size();
+            if ((int)pb.bb.size() < ph + 1) pb.bb.resize(ph + 1);
+            pb.bb[ph].push_back(t);
+            return pid;
+        }
+        throw AcrError{ACRGPU_E_USAGE,
+                       "GPU path: mixed dense/branch product (unbalanced cluster tree) is not supported"};
+    }
+
+    void deposit(PlanBuild& pb, int c, const Part& p0, int croot) {
+        const SNode& Cn = S.node(c);
+        if (Cn.kind == K_BRANCH) {
+            for (int i = 0; i < 4; ++i) {
+                const SNode& ch = S.node(Cn.ch[i]);
+                Part p = p0;
+                p.u_src += ch.rb - Cn.rb;
+                p.v_src += ch.cb - Cn.cb;
+                p.rows_u = ch.rows();
+                p.rows_v = ch.cols();
+                deposit(pb, Cn.ch[i], p, croot);
+            }
+            return;
+        }
+        Part p = p0;
+        p.rows_u = Cn.rows();
+        p.rows_v = Cn.cols();
+        p.u_dst = 0;
+        p.v_dst = 0;
+        if (Cn.kind == K_DENSE) {
+            auto it = pb.dense_idx.find(Cn.leaf);
+            if (it == pb.dense_idx.end()) {
+                pb.dense_idx[Cn.leaf] = (int)pb.dense_t.size();
+                pb.dense_t.push_back({Cn.leaf, {}});
+                it = pb.dense_idx.find(Cn.leaf);
+            }
+            pb.dense_t[it->second].second.push_back(p);
+        } else {
+            if (p.src == S_GEMM) throw AcrError{ACRGPU_E_INTERNAL, "exact product into a low-rank leaf"};
+            auto it = pb.rk_idx.find(Cn.leaf);
+            if (it == pb.rk_idx.end()) {
+                pb.rk_idx[Cn.leaf] = (int)pb.rk_t.size();
+                pb.rk_t.push_back({Cn.leaf, {}});
+                it = pb.rk_idx.find(Cn.leaf);
+            }
+            pb.rk_t[it->second].second.push_back(p);
+        }
+    }
+
+    void mult_rec(PlanBuild& pb, int c, int a, int b, double alpha, int croot, int aroot, int broot) {
+        const SNode& Cn = S.node(c);
+        const SNode& A = S.node(a);
+        const SNode& Bn = S.node(b);
+        if (A.kind == K_BRANCH && Bn.kind == K_BRANCH && Cn.kind == K_BRANCH) {
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 2; ++j)
+                    for (int k = 0; k < 2; ++k)
+                        mult_rec(pb, Cn.ch[i * 2 + j], A.ch[i * 2 + k], Bn.ch[k * 2 + j], alpha, croot, aroot, broot);
+            return;
+        }
+        Part p{};
+        p.alpha = alpha;
+        if (exact_dd && Cn.kind == K_DENSE && A.kind == K_DENSE && Bn.kind == K_DENSE) {
+            p.src = S_GEMM;
+            p.da = S.d_off[A.leaf] - S.node(aroot).doff0;
+            p.db = S.d_off[Bn.leaf] - S.node(broot).doff0;
+            p.gk = A.cols();
+            deposit(pb, c, p, croot);
+            return;
+        }
+        p.src = S_SLOT;
+        p.id = emit_product(pb, a, b, aroot, broot);
+        deposit(pb, c, p, croot);
+    }
+
+    Plan* plan(int c, int a, int b, double alpha) {
+        const auto key = std::make_tuple(c, a, b, alpha > 0 ? 1 : -1);
+        auto it = plans.find(key);
+        if (it != plans.end()) return it->second.get();
+        PlanBuild pb;
+        mult_rec(pb, c, a, b, alpha, c, a, b);
+        const SNode& CR = S.node(c);
+        for (auto& [leaf, list] : pb.rk_t) {
+            const SNode& L = S.node(S.k_node[leaf]);
+            TruncTask t;
+            t.out_kind = 1;
+            t.out_id = leaf - CR.k0;
+            t.m = L.rows();
+            t.n = L.cols();
+            t.pbeg = (int)pb.parts.size();
+            Part cur{};
+            cur.src = S_CLEAF;
+            cur.id = leaf - CR.k0;
+            cur.rows_u = L.rows();
+            cur.rows_v = L.cols();
+            cur.alpha = 1.0;
+            pb.parts.push_back(cur);
+            for (auto& p : list) pb.parts.push_back(p);
+            t.pend = (int)pb.parts.size();
+            pb.flush.push_back(t);
+        }
+        for (auto& [leaf, list] : pb.dense_t) {
+            const SNode& L = S.node(S.d_node[leaf]);
+            DepTask t;
+            t.doff = S.d_off[leaf] - CR.doff0;
+            t.m = L.rows();
+            t.n = L.cols();
+            t.pbeg = (int)pb.parts.size();
+            for (auto& p : list) pb.parts.push_back(p);
+            t.pend = (int)pb.parts.size();
+            pb.deps.push_back(t);
+        }
+        auto P = std::make_unique<Plan>();
+        P->nprod = pb.nprod;
+        P->nalloc = (int)pb.allocs.size();
+        P->napply = (int)pb.applies.size();
+        P->ndd = (int)pb.dds.size();
+        P->nflush = (int)pb.flush.size();
+        P->ndep = (int)pb.deps.size();
+        P->allocs = up(pb.allocs);
+        P->applies = up(pb.applies);
+        P->aleaves = up(pb.aleaves);
+        P->x_ld = up(pb.x_ld);
+        P->dds = up(pb.dds);
+        for (auto& ph : pb.bb) P->bb.push_back({up(ph), (int)ph.size()});
+        P->flush = up(pb.flush);
+        P->deps = up(pb.deps);
+        P->parts = up(pb.parts);
+        Plan* raw = P.get();
+        plans[key] = std::move(P);
+        return raw;
+    }
+
+    // -------------------------------------------------------------- batched operations
+    // C += alpha * A * B for every plane of the batch (reference mult_add, hmatrix.cpp:475-479).
+    void mult_add(const std::vector<View>& C, const std::vector<View>& A, const std::vector<View>& B, double alpha) {
+        if (C.empty()) return;
+        const double eps = cfg.eps * 0.5;  // arithmetic tolerance, acr.hpp:178-181
+        Plan* P = plan(C[0].node, A[0].node, B[0].node, alpha);
+        for (size_t i0 = 0; i0 < C.size(); i0 += MAXB) {
+            BatchViews bv{};
+            const int nb = (int)std::min<size_t>(MAXB, C.size() - i0);
+            bv.count = nb;
+            for (int b = 0; b < nb; ++b) {
+                bv.c[b] = hview(C[i0 + b]);
+                bv.a[b] = hview(A[i0 + b]);
+                bv.b[b] = hview(B[i0 + b]);
+            }
+            Slot* slots = ctx->get_slots((size_t)std::max(1, P->nprod) * nb);
+            launch_reset_counter(st(), ctx->trans.ctr);
+            launch_alloc_apply(st(), P->nalloc, P->allocs, slots, nb, ctx->trans, bv);
+            launch_apply(st(), P->napply, P->applies, P->aleaves, P->x_ld, slots, nb, ctx->flops, bv);
+            launch_dd(st(), P->ndd, P->dds, slots, nb, eps, ctx->trans, ctx->flops, bv);
+            for (auto& [tasks, n] : P->bb)
+                launch_truncate(st(), n, tasks, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->trans,
+                                ctx->trans, ctx->flops, bv);
+            launch_deposit(st(), P->ndep, P->deps, P->parts, slots, nb, ctx->flops, bv);
+            launch_truncate(st(), P->nflush, P->flush, P->parts, slots, nb, eps, nullptr, nullptr, false,
+                            ctx->persist, ctx->trans, ctx->flops, bv);
+        }
+    }
+
+    // out = inverse(in) (reference invert_node, hmatrix.cpp:483-534); out views pre-allocated
+    void invert(const std::vector<View>& out, const std::vector<View>& in, int level, const std::vector<int>& planes) {
+        const int node = in[0].node;
+        const SNode& n = S.node(node);
+        if (n.kind == K_DENSE) {
+            LuTask t;
+            t.doff = 0;
+            t.m = n.rows();
+            t.rb = n.rb;
+            t.re = n.re;
+            if (n.rows() != n.cols() || n.rows() > DENSE_MAX)
+                throw AcrError{ACRGPU_E_USAGE, "GPU path: dense diagonal leaf larger than 64"};
+            auto key = std::make_tuple(node, -1000, -1000, 0);
+            auto it = plans.find(key);
+            Plan* P;
+            if (it == plans.end()) {
+                auto np = std::make_unique<Plan>();
+                np->deps = (DepTask*)up(std::vector<LuTask>{t});
+                P = np.get();
+                plans[key] = std::move(np);
+            } else {
+                P = it->second.get();
+            }
+            for (size_t i0 = 0; i0 < out.size(); i0 += MAXB) {
+                BatchViews bv{};
+                bv.count = (int)std::min<size_t>(MAXB, out.size() - i0);
+                std::vector<int> pl;
+                for (int b = 0; b < bv.count; ++b) {
+                    bv.c[b] = hview(out[i0 + b]);
+                    bv.a[b] = hview(in[i0 + b]);
+                    pl.push_back(planes[i0 + b]);
+                }
+                const unsigned long long cid = ctx->call_id++;
+                ctx->call_planes.push_back({level, pl});
+                launch_lu(st(), 1, (const LuTask*)P->deps, ctx->err, cid, ctx->flops, bv, n.rows());
+            }
+            return;
+        }
+        if (n.kind != K_BRANCH) throw AcrError{ACRGPU_E_INTERNAL, "invert_node: admissible diagonal block"};
+        auto ch = [&](const std::vector<View>& v, int c) {
+            std::vector<View> r;
+            for (auto& x : v) r.push_back(child(x, *this, c));
+            return r;
+        };
+        auto A11 = ch(in, 0), A12 = ch(in, 1), A21 = ch(in, 2), A22 = ch(in, 3);
+        auto X11 = ch(out, 0), C12 = ch(out, 1), C21 = ch(out, 2), X22 = ch(out, 3);
+        invert(X11, A11, level, planes);
+        auto T12 = fresh(n.ch[1], in.size());
+        zero(T12);
+        mult_add(T12, X11, A12, 1.0);
+        auto T21 = fresh(n.ch[2], in.size());
+        zero(T21);
+        mult_add(T21, A21, X11, 1.0);
+        {
+            auto Sc = clone(A22);
+            mult_add(Sc, A21, T12, -1.0);
+            invert(X22, Sc, level, planes);
+        }
+        zero(C12);
+        mult_add(C12, T12, X22, -1.0);
+        zero(C21);
+        mult_add(C21, X22, T21, -1.0);
+        mult_add(X11, T12, C21, -1.0);
+    }
+
+    // stored-inverse recompression (reference recompress, hmatrix.cpp:655-662)
+    void recompress(const std::vector<View>& H) {
+        if (H.empty()) return;
+        const int nd = S.n_dense(), nk = S.n_rk();
+        for (size_t i0 = 0; i0 < H.size(); i0 += MAXB) {
+            const int nb = (int)std::min<size_t>(MAXB, H.size() - i0);
+            BatchViews bv{};
+            bv.count = nb;
+            for (int b = 0; b < nb; ++b) bv.c[b] = hview(H[i0 + b]);
+            double* sc = ctx->get_scratch((size_t)(nd + nk + 1) * nb + 64);
+            double* sig_d = sc;
+            double* sig_k = sc + (size_t)nd * nb;
+            double* cut = sig_k + (size_t)nk * nb;
+            launch_sigma1_dense(st(), nd, d_doff, d_dm, d_dn, nb, sig_d, ctx->flops, bv, S.max_dense_dim);
+            Slot* slots = ctx->get_slots(1);
+            launch_reset_counter(st(), ctx->trans.ctr);
+            launch_truncate(st(), nk, leaf_tasks, leaf_parts, slots, nb, 0.0, nullptr, sig_k, true, ctx->persist,
+                            ctx->trans, ctx->flops, bv);
+            launch_scale_reduce(st(), sig_d, nd, sig_k, nk, nb, cfg.eps, cut);
+            launch_reset_counter(st(), ctx->trans.ctr);
+            launch_truncate(st(), nk, leaf_tasks, leaf_parts, slots, nb, 0.0, cut, nullptr, false, ctx->persist,
+                            ctx->trans, ctx->flops, bv);
+        }
+    }
+
+    // -------------------------------------------------------------- structure tables
+    void prepare_structure() {
+        std::vector<long> doff(S.n_dense());
+        std::vector<int> dm(S.n_dense()), dn(S.n_dense());
+        for (int d = 0; d < S.n_dense(); ++d) {
+            const SNode& L = S.node(S.d_node[d]);
+            doff[d] = S.d_off[d];
+            dm[d] = L.rows();
+            dn[d] = L.cols();
+        }
+        d_doff = up(doff);
+        d_dm = up(dm);
+        d_dn = up(dn);
+        d_perm = up(S.perm);
+        d_iperm = up(S.iperm);
+        std::vector<TruncTask> lt;
+        std::vector<Part> lp;
+        for (int k = 0; k < S.n_rk(); ++k) {
+            const SNode& L = S.node(S.k_node[k]);
+            TruncTask t;
+            t.out_kind = 1;
+            t.out_id = k;
+            t.m = L.rows();
+            t.n = L.cols();
+            t.pbeg = (int)lp.size();
+            Part p{};
+            p.src = S_CLEAF;
+            p.id = k;
+            p.rows_u = L.rows();
+            p.rows_v = L.cols();
+            p.alpha = 1.0;
+            lp.push_back(p);
+            t.pend = (int)lp.size();
+            lt.push_back(t);
+        }
+        leaf_tasks = up(lt);
+        leaf_parts = up(lp);
+        // matvec slabs over leaf clusters (non-transposed apply of the root)
+        std::vector<int> lv;
+        subtree_leaves(0, lv);
+        std::vector<SlabTask> sl;
+        std::vector<ApplyLeaf> al;
+        for (auto [r0, r1] : slabs_of(0, S.dim)) {
+            SlabTask t;
+            t.r0 = r0;
+            t.r1 = r1;
+            t.lbeg = (int)al.size();
+            for (int li : lv) {
+                const SNode& L = S.node(li);
+                if (L.rb >= r1 || L.re <= r0) continue;
+                ApplyLeaf a;
+                a.kind = L.kind;
+                a.id = L.kind == K_RK ? L.leaf : -1;
+                a.doff = L.kind == K_DENSE ? S.d_off[L.leaf] : 0;
+                a.m = L.rows();
+                a.n = L.cols();
+                a.in_off = L.cb;
+                a.out_off = L.rb;
+                al.push_back(a);
+            }
+            t.lend = (int)al.size();
+            sl.push_back(t);
+        }
+        nslabs = (int)sl.size();
+        slabs = up(sl);
+        slab_leaves = up(al);
+    }
+};
+
+// ------------------------------------------------------------------ factorization object
+struct Level {
+    int plane_count = 0;
+    std::vector<int> elim, ret;
+    std::vector<StoreP> E, F, Dinv;  // indexed by plane position (null = absent)
+};
+
+static std::vector<int> eliminated_positions(int m) {
+    std::vector<int> v;
+    for (int j = 0; j < m; j += 2) v.push_back(j);
+    if (m % 2 == 1 && !v.empty()) v.pop_back();
+    return v;
+}
+static std::vector<int> retained_positions(int m) {
+    std::vector<int> v;
+    for (int j = 1; j < m; j += 2) v.push_back(j);
+    if (m % 2 == 1) v.push_back(m - 1);
+    return v;
+}
+
+}  // namespace acrgpu
+
+struct acrgpu_ctx {
+    acrgpu::Ctx c;
+};
+
+struct acrgpu_fact {
+    acrgpu_ctx* ctx = nullptr;
+    std::unique_ptr<acrgpu::Engine> eng;
+    int n = 0, dim = 0;
+    std::vector<acrgpu::Level> levels;
+    std::vector<acrgpu::StoreP> apexDinv, apexE, apexF;
+    acrgpu_timing timing{};
+    double* fbuf = nullptr;  // solve workspace
+    size_t fbuf_cap = 0;
+};
+
+namespace acrgpu {
+
+using SP = StoreP;
+
+static View root_view(const SP& s) { return View{s, 0}; }
+
+static std::vector<View> views(const std::vector<SP>& v) {
+    std::vector<View> r;
+    for (auto& s : v) r.push_back(root_view(s));
+    return r;
+}
+
+// ------------------------------------------------------------------ lifting
+static std::vector<SP> lift(Engine& E, const acrgpu_system* sys) {
+    const int n = sys->n, dim = sys->dim, nb = 3 * n - 2;
+    const Structure& S = E.S;
+    // validate + merge duplicates (PlaneBlock, block.cpp:7-29)
+    std::vector<int> rows, cols;
+    std::vector<double> vals;
+    std::vector<long> off(nb + 1, 0);
+    rows.reserve(sys->blk_off[nb]);
+    cols.reserve(sys->blk_off[nb]);
+    vals.reserve(sys->blk_off[nb]);
+    for (int b = 0; b < nb; ++b) {
+        const long s = sys->blk_off[b], e = sys->blk_off[b + 1];
+        if (e < s) throw AcrError{ACRGPU_E_DIMENSION, "block offsets must be nondecreasing"};
+        bool sorted = true;
+        for (long i = s; i < e; ++i) {
+            if (sys->rows[i] < 0 || sys->rows[i] >= dim || sys->cols[i] < 0 || sys->cols[i] >= dim)
+                throw AcrError{ACRGPU_E_DIMENSION, "PlaneBlock: entry index out of range"};
+            if (i > s) {
+                const long pr = sys->rows[i - 1], pc = sys->cols[i - 1];
+                if (!(pr < sys->rows[i] || (pr == sys->rows[i] && pc < sys->cols[i]))) sorted = false;
+            }
+        }
+        if (sorted) {
+            rows.insert(rows.end(), sys->rows + s, sys->rows + e);
+            cols.insert(cols.end(), sys->cols + s, sys->cols + e);
+            vals.insert(vals.end(), sys->vals + s, sys->vals + e);
+        } else {
+            std::vector<long> idx(e - s);
+            std::iota(idx.begin(), idx.end(), s);
+            std::stable_sort(idx.begin(), idx.end(), [&](long x, long y) {
+                return sys->rows[x] != sys->rows[y] ? sys->rows[x] < sys->rows[y] : sys->cols[x] < sys->cols[y];
+            });
+            for (long i : idx) {
+                if ((long)rows.size() > off[b] && rows.back() == sys->rows[i] && cols.back() == sys->cols[i])
+                    vals.back() += sys->vals[i];
+                else {
+                    rows.push_back(sys->rows[i]);
+                    cols.push_back(sys->cols[i]);
+                    vals.push_back(sys->vals[i]);
+                }
+            }
+        }
+        off[b + 1] = (long)rows.size();
+    }
+    cudaStream_t st = E.st();
+    int* d_rows = upload(rows, st);
+    int* d_cols = upload(cols, st);
+    double* d_vals = upload(vals, st);
+    long* d_off = upload(off, st);
+    // scatter tables
+    const int ncl = (int)S.cl_begin.size();
+    std::vector<int> leaf_of((size_t)ncl * ncl, -1);
+    for (int d = 0; d < S.n_dense(); ++d) {
+        const SNode& L = S.node(S.d_node[d]);
+        for (int ri = S.cl_index[L.rb]; ri < ncl && S.cl_begin[ri] < L.re; ++ri)
+            for (int ci = S.cl_index[L.cb]; ci < ncl && S.cl_begin[ci] < L.ce; ++ci) leaf_of[(size_t)ri * ncl + ci] = d;
+    }
+    std::vector<int> drb(S.n_dense()), dcb(S.n_dense()), drows(S.n_dense());
+    for (int d = 0; d < S.n_dense(); ++d) {
+        const SNode& L = S.node(S.d_node[d]);
+        drb[d] = L.rb;
+        dcb[d] = L.cb;
+        drows[d] = L.rows();
+    }
+    int* d_leaf_of = upload(leaf_of, st);
+    int* d_clidx = upload(S.cl_index, st);
+    int* d_clb = upload(S.cl_begin, st);
+    int* d_drb = upload(drb, st);
+    int* d_dcb = upload(dcb, st);
+    int* d_drows = upload(drows, st);
+    int* d_hits = dmalloc<int>(1);
+    CK(cudaMemsetAsync(d_hits, 0, sizeof(int), st));
+    std::vector<SP> blocks;
+    for (int b = 0; b < nb; ++b) blocks.push_back(E.new_store(0));
+    auto vs = views(blocks);
+    E.zero(vs);
+    ScatterLaunch sl{d_rows, d_cols, d_vals, nullptr, E.d_iperm, d_leaf_of, d_clidx, d_clb, ncl,
+                     E.d_doff, d_drows, d_drb, d_dcb, d_hits};
+    for (int i0 = 0; i0 < nb; i0 += MAXB) {
+        BatchViews bv{};
+        bv.count = std::min(MAXB, nb - i0);
+        for (int b = 0; b < bv.count; ++b) bv.c[b] = E.hview(vs[i0 + b]);
+        sl.off = d_off + i0;
+        launch_scatter(st, sl, bv);
+    }
+    int hits = 0;
+    CK(cudaMemcpyAsync(&hits, d_hits, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hits > 0) {
+        // entries inside admissible leaves: factor through the nonzero columns
+        // (build_from_sparse, hmatrix.cpp:127-147), then device truncation at eps
+        for (int b = 0; b < nb; ++b) {
+            std::map<int, std::vector<std::tuple<int, int, double>>> per_leaf;
+            for (long i = off[b]; i < off[b + 1]; ++i) {
+                const int r = S.iperm[rows[i]], c = S.iperm[cols[i]];
+                const int node = S.find_leaf(r, c);
+                if (S.node(node).kind == K_RK) per_leaf[S.node(node).leaf].push_back({r, c, vals[i]});
+            }
+            if (per_leaf.empty()) continue;
+            std::vector<int> ranks(S.n_rk(), 0);
+            std::vector<double*> Up(S.n_rk(), nullptr), Vp(S.n_rk(), nullptr);
+            std::vector<int> task_ids;
+            for (auto& [k, ent] : per_leaf) {
+                const SNode& L = S.node(S.k_node[k]);
+                std::vector<int> cl;
+                for (auto& e : ent) cl.push_back(std::get<1>(e));
+                std::sort(cl.begin(), cl.end());
+                cl.erase(std::unique(cl.begin(), cl.end()), cl.end());
+                const int c = (int)cl.size();
+                if (8L * (L.rows() + L.cols()) * c > E.cfg.leaf_memory_cap)
+                    throw AcrError{ACRGPU_E_LEAFMEM, "low-rank leaf factor of width " + std::to_string(c) +
+                                                         " exceeds memory cap"};
+                std::vector<double> U((size_t)L.rows() * c, 0.0), V((size_t)L.cols() * c, 0.0);
+                for (auto& [r, cc, v] : ent) {
+                    const int j = (int)(std::lower_bound(cl.begin(), cl.end(), cc) - cl.begin());
+                    U[(r - L.rb) + (size_t)j * L.rows()] += v;
+                }
+                for (int j = 0; j < c; ++j) V[(cl[j] - L.cb) + (size_t)j * L.cols()] = 1.0;
+                double* dU = E.keep(upload(U, st));
+                double* dV = E.keep(upload(V, st));
+                ranks[k] = c;
+                Up[k] = dU;
+                Vp[k] = dV;
+            }
+            CK(cudaMemcpyAsync(blocks[b]->rank, ranks.data(), ranks.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(blocks[b]->U, Up.data(), Up.size() * sizeof(double*), cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(blocks[b]->V, Vp.data(), Vp.size() * sizeof(double*), cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+            BatchViews bv{};
+            bv.count = 1;
+            bv.c[0] = E.hview(vs[b]);
+            Slot* slots = E.ctx->get_slots(1);
+            launch_reset_counter(st, E.ctx->trans.ctr);
+            launch_truncate(st, S.n_rk(), E.leaf_tasks, E.leaf_parts, slots, 1, E.cfg.eps, nullptr, nullptr, false,
+                            E.ctx->persist, E.ctx->trans, E.ctx->flops, bv);
+        }
+    }
+    // leaf memory cap for dense leaves (build_from_sparse, hmatrix.cpp:117-121)
+    for (int d = 0; d < S.n_dense(); ++d) {
+        const SNode& L = S.node(S.d_node[d]);
+        if (8L * L.rows() * L.cols() > E.cfg.leaf_memory_cap)
+            throw AcrError{ACRGPU_E_LEAFMEM, "dense leaf of " + std::to_string(L.rows()) + "x" +
+                                                 std::to_string(L.cols()) + " exceeds memory cap"};
+    }
+    CK(cudaStreamSynchronize(st));
+    for (void* p : std::initializer_list<void*>{d_rows, d_cols, d_vals, d_off, d_leaf_of, d_clidx, d_clb, d_drb, d_dcb,
+                                                d_drows, d_hits})
+        cudaFree(p);
+    return blocks;
+}
+
+}  // namespace acrgpu
+
+namespace acrgpu {
+
+// ------------------------------------------------------------------ factor driver
+static void check_device_errors(acrgpu_fact* F) {
+    Engine& E = *F->eng;
+    Ctx& C = *E.ctx;
+    CK(cudaStreamSynchronize(C.st));
+    CK(cudaGetLastError());
+    DevError de;
+    CK(cudaMemcpy(&de, C.err, sizeof(de), cudaMemcpyDeviceToHost));
+    int ovf[2];
+    CK(cudaMemcpy(ovf, C.overflow, sizeof(ovf), cudaMemcpyDeviceToHost));
+    if (de.key != ~0ull) {
+        const unsigned long long cid = de.key >> 16;
+        const int b = (int)(de.key & 0xffff);
+        AcrError e{ACRGPU_E_SINGULAR, ""};
+        if (cid < C.call_planes.size()) {
+            e.level = C.call_planes[cid].first;
+            const auto& pl = C.call_planes[cid].second;
+            e.plane = b < (int)pl.size() ? pl[b] : -1;
+        }
+        e.rb = de.rb;
+        e.re = de.re;
+        char buf[200];
+        std::snprintf(buf, sizeof(buf), "singular dense pivot on cluster rows [%d, %d), rcond=%g", de.rb, de.re,
+                      de.rcond);
+        e.msg = buf;
+        throw e;
+    }
+    if (ovf[0] || ovf[1])
+        throw AcrError{ACRGPU_E_DEVICE, std::string("device arena exhausted (") + (ovf[0] ? "persistent" : "transient") +
+                                            "); factorization too large for this GPU"};
+}
+
+static void do_factor(acrgpu_fact* F, const acrgpu_system* sys) {
+    Engine& E = *F->eng;
+    const int n = sys->n;
+    cudaEvent_t e0, e1, e2;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&e2));
+    CK(cudaEventRecord(e0, E.st()));
+    auto blocks = lift(E, sys);
+    CK(cudaEventRecord(e1, E.st()));
+    std::vector<SP> D(n), Ev(n), Fv(n);
+    for (int j = 0; j < n; ++j) D[j] = blocks[j];
+    for (int j = 1; j < n; ++j) Ev[j] = blocks[n + j - 1];
+    for (int j = 0; j + 1 < n; ++j) Fv[j] = blocks[2 * n - 1 + j];
+    blocks.clear();
+    const int stop = F->eng->cfg.stop_planes;
+    int lvl = 0;
+    while ((int)D.size() > stop) {
+        const int m = (int)D.size();
+        Level L;
+        L.plane_count = m;
+        L.elim = eliminated_positions(m);
+        L.ret = retained_positions(m);
+        L.E = Ev;
+        L.F = Fv;
+        L.Dinv.assign(m, nullptr);
+        std::vector<char> is_elim(m, 0);
+        for (int e : L.elim) is_elim[e] = 1;
+        // 1. invert the eliminated planes (batched over planes)
+        {
+            std::vector<SP> outs;
+            std::vector<View> ov, iv;
+            for (int e : L.elim) {
+                outs.push_back(E.new_store(0));
+                ov.push_back(root_view(outs.back()));
+                iv.push_back(root_view(D[e]));
+            }
+            if (!ov.empty()) E.invert(ov, iv, lvl, L.elim);
+            for (size_t t = 0; t < L.elim.size(); ++t) {
+                L.Dinv[L.elim[t]] = outs[t];
+                D[L.elim[t]].reset();
+            }
+        }
+        // 2. Schur updates of the retained planes (eliminate_around, acr.hpp:78-107)
+        const int mn = (int)L.ret.size();
+        std::vector<SP> Dn(mn), En(mn), Fn(mn);
+        for (int t = 0; t < mn; ++t) Dn[t] = D[L.ret[t]];
+        auto at = [&](const std::vector<SP>& v, int j) -> SP { return (j < 0 || j >= (int)v.size()) ? nullptr : v[j]; };
+        for (int side = 0; side < 2; ++side) {
+            std::vector<int> ts;
+            for (int t = 0; t < mn; ++t) {
+                const int j = L.ret[t];
+                const int nb = side == 0 ? j - 1 : j + 1;
+                if (nb >= 0 && nb < m && is_elim[nb]) ts.push_back(t);
+            }
+            if (ts.empty()) continue;
+            std::vector<View> Tv, Cpl, Dnb;
+            std::vector<SP> Ts;
+            for (int t : ts) {
+                const int j = L.ret[t];
+                const int nb = side == 0 ? j - 1 : j + 1;
+                Ts.push_back(E.new_store(0));
+                Tv.push_back(root_view(Ts.back()));
+                SP cpl = side == 0 ? at(L.E, j) : at(L.F, j);
+                if (!cpl) throw AcrError{ACRGPU_E_INTERNAL, "missing coupling block"};
+                Cpl.push_back(root_view(cpl));
+                Dnb.push_back(root_view(L.Dinv[nb]));
+            }
+            E.zero(Tv);
+            E.mult_add(Tv, Cpl, Dnb, 1.0);  // T = E_j Dinv_{j-1}  (or F_j Dinv_{j+1})
+            // D_j -= T * F_{j-1}   (or T * E_{j+1})
+            {
+                std::vector<View> c, a, b;
+                for (size_t q = 0; q < ts.size(); ++q) {
+                    const int j = L.ret[ts[q]];
+                    const int nb = side == 0 ? j - 1 : j + 1;
+                    SP x = side == 0 ? at(L.F, nb) : at(L.E, nb);
+                    if (!x) continue;
+                    c.push_back(root_view(Dn[ts[q]]));
+                    a.push_back(Tv[q]);
+                    b.push_back(root_view(x));
+                }
+                E.mult_add(c, a, b, -1.0);
+            }
+            // new coupling: E' = -T * E_{j-1}  (or F' = -T * F_{j+1})
+            {
+                std::vector<View> c, a, b;
+                std::vector<int> owners;
+                for (size_t q = 0; q < ts.size(); ++q) {
+                    const int j = L.ret[ts[q]];
+                    const int nb = side == 0 ? j - 1 : j + 1;
+                    SP x = side == 0 ? at(L.E, nb) : at(L.F, nb);
+                    if (!x) continue;
+                    SP nw = E.new_store(0);
+                    (side == 0 ? En : Fn)[ts[q]] = nw;
+                    c.push_back(root_view(nw));
+                    a.push_back(Tv[q]);
+                    b.push_back(root_view(x));
+                }
+                E.zero(c);
+                E.mult_add(c, a, b, -1.0);
+            }
+        }
+        // adjacent retained planes keep their coupling (acr.cpp:104-111)
+        for (int t = 0; t < mn; ++t) {
+            const int j = L.ret[t];
+            if (!En[t] && t > 0 && L.ret[t - 1] == j - 1 && at(L.E, j)) {
+                En[t] = E.new_store(0);
+                E.copy({root_view(En[t])}, {root_view(L.E[j])});
+            }
+            if (!Fn[t] && t + 1 < mn && L.ret[t + 1] == j + 1 && at(L.F, j)) {
+                Fn[t] = E.new_store(0);
+                E.copy({root_view(Fn[t])}, {root_view(L.F[j])});
+            }
+        }
+        D = std::move(Dn);
+        Ev = std::move(En);
+        Fv = std::move(Fn);
+        // 3. trim the stored inverses to full tolerance (acr.cpp:116-118)
+        {
+            std::vector<View> dv;
+            for (int e : L.elim) dv.push_back(root_view(L.Dinv[e]));
+            E.recompress(dv);
+        }
+        F->levels.push_back(std::move(L));
+        ++lvl;
+    }
+    // apex: block Thomas over the remaining planes (acr.cpp:123-144)
+    const int s = (int)D.size();
+    F->apexE = Ev;
+    F->apexF = Fv;
+    for (int i = 0; i < s; ++i) {
+        SP Di = D[i];
+        if (i > 0) {
+            SP T = E.new_store(0);
+            E.zero({root_view(T)});
+            E.mult_add({root_view(T)}, {root_view(F->apexE[i])}, {root_view(F->apexDinv[i - 1])}, 1.0);
+            E.mult_add({root_view(Di)}, {root_view(T)}, {root_view(F->apexF[i - 1])}, -1.0);
+        }
+        SP out = E.new_store(0);
+        E.invert({root_view(out)}, {root_view(Di)}, lvl, {i});
+        F->apexDinv.push_back(out);
+    }
+    E.recompress(views(F->apexDinv));
+    CK(cudaEventRecord(e2, E.st()));
+    check_device_errors(F);
+    float ms_lift = 0, ms_all = 0;
+    CK(cudaEventElapsedTime(&ms_lift, e0, e1));
+    CK(cudaEventElapsedTime(&ms_all, e0, e2));
+    F->timing.lift_ms = ms_lift;
+    F->timing.factor_ms = ms_all;
+    FlopLedger fl;
+    CK(cudaMemcpy(&fl, E.ctx->flops, sizeof(fl), cudaMemcpyDeviceToHost));
+    F->timing.flops_gemm = fl.f[F_GEMM];
+    F->timing.flops_qr = fl.f[F_GEQRF] + fl.f[F_ORGQR];
+    F->timing.flops_svd = fl.f[F_SVD];
+    F->timing.flops_lu = fl.f[F_LU];
+    F->timing.flops_nominal = fl.f[F_GEMM] + fl.f[F_GEQRF] + fl.f[F_ORGQR] + fl.f[F_SVD] + fl.f[F_LU];
+    F->timing.kernel_launches = launches_take();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+}
+
+// ------------------------------------------------------------------ solve
+struct MV {
+    SP H;
+    const double* x;
+    const double* base;
+    double* y;
+};
+
+static void matvec(Engine& E, const std::vector<MV>& items, int nrhs) {
+    for (size_t i0 = 0; i0 < items.size(); i0 += MAXB) {
+        MatvecBatch mb{};
+        mb.count = (int)std::min<size_t>(MAXB, items.size() - i0);
+        for (int b = 0; b < mb.count; ++b) {
+            const MV& it = items[i0 + b];
+            mb.h[b] = E.hview(root_view(it.H));
+            mb.x[b] = it.x;
+            mb.base[b] = it.base;
+            mb.y[b] = it.y;
+        }
+        launch_matvec(E.st(), E.nslabs, E.slabs, E.slab_leaves, nrhs, E.S.dim, E.ctx->flops, mb);
+    }
+}
+
+static void do_solve(acrgpu_fact* F, int nrhs, const double* f_dev, double* u_dev) {
+    Engine& E = *F->eng;
+    cudaStream_t st = E.st();
+    const int n = F->n, dim = F->dim;
+    const size_t pv = (size_t)dim * nrhs;  // one plane vector (tree order, column-major dim x nrhs)
+    // workspace: all level rhs + u + 2 temporaries per plane
+    size_t planes_total = 0;
+    std::vector<size_t> lvl_off;
+    int m = n;
+    for (auto& L : F->levels) {
+        lvl_off.push_back(planes_total);
+        planes_total += L.plane_count;
+        m = (int)L.ret.size();
+    }
+    lvl_off.push_back(planes_total);
+    planes_total += m;  // apex rhs
+    const size_t need = (planes_total + 3 * (size_t)n + 8) * pv;
+    if (need > F->fbuf_cap) {
+        if (F->fbuf) cudaFreeAsync(F->fbuf, st);
+        CK(cudaMallocAsync((void**)&F->fbuf, need * sizeof(double), st));
+        F->fbuf_cap = need;
+    }
+    double* fs = F->fbuf;
+    double* U0 = fs + planes_total * pv;  // n planes: solution (per current level)
+    double* T1 = U0 + (size_t)n * pv;
+    double* T2 = T1 + (size_t)n * pv;
+    auto P = [&](size_t li, int j) { return fs + (lvl_off[li] + j) * pv; };
+    launch_permute_in(st, f_dev, fs, E.d_perm, n, dim, nrhs);
+    // forward reduction (forward_rhs, acr.hpp:111-120)
+    for (size_t li = 0; li < F->levels.size(); ++li) {
+        const Level& L = F->levels[li];
+        const int mm = L.plane_count;
+        std::vector<MV> a, b, c, d;
+        for (size_t t = 0; t < L.ret.size(); ++t) {
+            const int j = L.ret[t];
+            const bool lo = j > 0 && L.Dinv[j - 1];
+            const bool hi = j + 1 < mm && L.Dinv[j + 1];
+            double* out = P(li + 1, (int)t);
+            if (lo) {
+                a.push_back({L.Dinv[j - 1], P(li, j - 1), nullptr, T1 + t * pv});
+                b.push_back({L.E[j], T1 + t * pv, P(li, j), out});
+            } else {
+                CK(cudaMemcpyAsync(out, P(li, j), pv * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            }
+            if (hi) {
+                c.push_back({L.Dinv[j + 1], P(li, j + 1), nullptr, T2 + t * pv});
+                d.push_back({L.F[j], T2 + t * pv, out, out});
+            }
+        }
+        matvec(E, a, nrhs);
+        matvec(E, b, nrhs);
+        matvec(E, c, nrhs);
+        matvec(E, d, nrhs);
+    }
+    // apex (solve_apex, acr.cpp:162-178)
+    const size_t la = F->levels.size();
+    const int s = (int)F->apexDinv.size();
+    for (int i = 1; i < s; ++i) {
+        matvec(E, {{F->apexDinv[i - 1], P(la, i - 1), nullptr, T1}}, nrhs);
+        matvec(E, {{F->apexE[i], T1, P(la, i), P(la, i)}}, nrhs);
+    }
+    // u for apex planes stored in U0[0..s)
+    for (int i = s - 1; i >= 0; --i) {
+        const double* r = P(la, i);
+        if (i + 1 < s) {
+            matvec(E, {{F->apexF[i], U0 + (size_t)(i + 1) * pv, P(la, i), T1}}, nrhs);
+            r = T1;
+        }
+        matvec(E, {{F->apexDinv[i], r, nullptr, U0 + (size_t)i * pv}}, nrhs);
+    }
+    // back substitution (back_substitute, acr.hpp:123-132), level by level
+    double* ucur = U0;
+    double* unext = T2;  // reuse as the next level's solution buffer (needs n planes)
+    std::vector<double> dummy;
+    double* ubuf = nullptr;
+    CK(cudaMallocAsync((void**)&ubuf, 2 * (size_t)n * pv * sizeof(double), st));
+    double* bufs[2] = {ubuf, ubuf + (size_t)n * pv};
+    CK(cudaMemcpyAsync(bufs[0], ucur, (size_t)s * pv * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    int cur = 0;
+    (void)unext;
+    for (int li = (int)F->levels.size() - 1; li >= 0; --li) {
+        const Level& L = F->levels[li];
+        const int mm = L.plane_count;
+        double* uin = bufs[cur];
+        double* uout = bufs[cur ^ 1];
+        for (size_t t = 0; t < L.ret.size(); ++t)
+            CK(cudaMemcpyAsync(uout + (size_t)L.ret[t] * pv, uin + t * pv, pv * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st));
+        std::vector<MV> a, b, c;
+        for (int e : L.elim) {
+            const double* r = P(li, e);
+            double* tmp = T1 + (size_t)e * pv;
+            const bool lo = e > 0 && L.E[e];
+            const bool hi = e + 1 < mm && L.F[e];
+            if (lo) {
+                a.push_back({L.E[e], uout + (size_t)(e - 1) * pv, r, tmp});
+                r = tmp;
+            }
+            if (hi) {
+                b.push_back({L.F[e], uout + (size_t)(e + 1) * pv, r, tmp});
+                r = tmp;
+            }
+            c.push_back({L.Dinv[e], r, nullptr, uout + (size_t)e * pv});
+        }
+        matvec(E, a, nrhs);
+        matvec(E, b, nrhs);
+        matvec(E, c, nrhs);
+        cur ^= 1;
+    }
+    launch_permute_out(st, bufs[cur], u_dev, E.d_perm, n, dim, nrhs);
+    CK(cudaFreeAsync(ubuf, st));
+}
+
+// ------------------------------------------------------------------ stats
+struct HostStats {
+    long rank_sum = 0;
+    int largest = 0, ndense = 0, nrk = 0;
+    long bytes = 0;
+};
+
+static HostStats store_stats(Engine& E, const SP& s) {
+    HostStats h;
+    if (!s) return h;
+    const int nk = E.S.n_rk();
+    std::vector<int> r(nk);
+    if (nk) CK(cudaMemcpy(r.data(), s->rank, nk * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int d = 0; d < E.S.n_dense(); ++d) {
+        const SNode& L = E.S.node(E.S.d_node[d]);
+        ++h.ndense;
+        h.bytes += 8L * L.rows() * L.cols();
+    }
+    for (int k = 0; k < nk; ++k) {
+        const SNode& L = E.S.node(E.S.k_node[k]);
+        ++h.nrk;
+        h.rank_sum += r[k];
+        h.largest = std::max(h.largest, r[k]);
+        h.bytes += 8L * (L.rows() + L.cols()) * r[k];
+    }
+    return h;
+}
+
+}  // namespace acrgpu
+
+// ================================================================== C-ABI
+using namespace acrgpu;
+
+static void fill_err(acrgpu_error* err, const AcrError& e) {
+    if (!err) return;
+    err->code = e.code;
+    err->level = e.level;
+    err->plane = e.plane;
+    err->row_begin = e.rb;
+    err->row_end = e.re;
+    std::snprintf(err->msg, sizeof(err->msg), "%s", e.msg.c_str());
+}
+
+static void clear_err(acrgpu_error* err) {
+    if (!err) return;
+    std::memset(err, 0, sizeof(*err));
+    err->level = err->plane = err->row_begin = err->row_end = -1;
+}
+
+#define ABI_TRY(...)                                                  \
+    clear_err(err);                                                    \
+    try {                                                              \
+        __VA_ARGS__                                                    \
+    } catch (const AcrError& e) {                                      \
+        fill_err(err, e);                                              \
+        return e.code;                                                 \
+    } catch (const StructureError& e) {                                \
+        fill_err(err, AcrError{e.code, e.msg});                        \
+        return e.code;                                                 \
+    } catch (const std::exception& e) {                                \
+        fill_err(err, AcrError{ACRGPU_E_INTERNAL, e.what()});          \
+        return ACRGPU_E_INTERNAL;                                      \
+    }
+
+extern "C" {
+
+const char* acrgpu_version(void) { return "acrgpu 0.1 sm_100a fp64"; }
+
+int acrgpu_ctx_create(int device, acrgpu_ctx** out, acrgpu_error* err) {
+    ABI_TRY({
+        auto* c = new acrgpu_ctx;
+        try {
+            c->c.init(device);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+        return 0;
+    })
+}
+
+void acrgpu_ctx_destroy(acrgpu_ctx* ctx) {
+    if (!ctx) return;
+    ctx->c.destroy();
+    delete ctx;
+}
+
+int acrgpu_factor(acrgpu_ctx* ctx, const acrgpu_system* sys, const acrgpu_config* cfg, acrgpu_fact** out,
+                  acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
+        if (!ctx || !sys || !cfg) throw AcrError{ACRGPU_E_USAGE, "null argument"};
+        if (sys->n < 1 || sys->dim < 1) throw AcrError{ACRGPU_E_DIMENSION, "acr_factor: empty system"};
+        if (cfg->stop_planes < 1) throw AcrError{ACRGPU_E_USAGE, "acr_factor: stop_planes must be >= 1"};
+        if (cfg->leaf_size > DENSE_MAX)
+            throw AcrError{ACRGPU_E_USAGE, "GPU path: leaf_size above 64 is not supported"};
+        ctx->c.reset_all();
+        launches_take();
+        auto F = std::make_unique<acrgpu_fact>();
+        F->ctx = ctx;
+        F->n = sys->n;
+        F->dim = sys->dim;
+        F->eng = std::make_unique<Engine>();
+        Engine& E = *F->eng;
+        E.ctx = &ctx->c;
+        E.cfg = *cfg;
+        E.exact_dd = (cfg->flags & ACRGPU_F_EXACT_DENSE_PRODUCTS) != 0;
+        E.S.build(sys->dim, sys->coords, cfg->leaf_size, cfg->eta, cfg->weak);
+        if (E.S.max_dense_dim > DENSE_MAX)
+            throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64 rows are not supported"};
+        if (!E.S.balanced)
+            throw AcrError{ACRGPU_E_USAGE, "GPU path: unbalanced cluster trees (mixed dense/branch products) are not supported"};
+        E.prepare_structure();
+        do_factor(F.get(), sys);
+        *out = F.release();
+        return 0;
+    })
+}
+
+void acrgpu_factor_destroy(acrgpu_fact* f) {
+    if (!f) return;
+    cudaStream_t st = f->eng->st();
+    cudaStreamSynchronize(st);
+    if (f->fbuf) cudaFreeAsync(f->fbuf, st);
+    f->levels.clear();
+    f->apexDinv.clear();
+    f->apexE.clear();
+    f->apexF.clear();
+    cudaStreamSynchronize(st);
+    delete f;
+}
+
+int acrgpu_solve_device(acrgpu_fact* f, int nrhs, const double* f_dev, double* u_dev, acrgpu_error* err) {
+    ABI_TRY({
+        if (nrhs < 1) throw AcrError{ACRGPU_E_DIMENSION, "solve: nrhs must be >= 1"};
+        Engine& E = *f->eng;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, E.st()));
+        do_solve(f, nrhs, f_dev, u_dev);
+        CK(cudaEventRecord(e1, E.st()));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaGetLastError());
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        f->timing.solve_ms = ms;
+        f->timing.kernel_launches = launches_take();
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return 0;
+    })
+}
+
+int acrgpu_solve(acrgpu_fact* f, int nrhs, const double* f_host, double* u_host, acrgpu_error* err) {
+    ABI_TRY({
+        if (nrhs < 1) throw AcrError{ACRGPU_E_DIMENSION, "solve: nrhs must be >= 1"};
+        Engine& E = *f->eng;
+        const size_t bytes = (size_t)nrhs * f->n * f->dim * sizeof(double);
+        double *df = nullptr, *du = nullptr;
+        CK(cudaMallocAsync((void**)&df, bytes, E.st()));
+        CK(cudaMallocAsync((void**)&du, bytes, E.st()));
+        CK(cudaMemcpyAsync(df, f_host, bytes, cudaMemcpyHostToDevice, E.st()));
+        const int rc = acrgpu_solve_device(f, nrhs, df, du, err);
+        if (rc == 0) CK(cudaMemcpyAsync(u_host, du, bytes, cudaMemcpyDeviceToHost, E.st()));
+        CK(cudaFreeAsync(df, E.st()));
+        CK(cudaFreeAsync(du, E.st()));
+        CK(cudaStreamSynchronize(E.st()));
+        return rc;
+    })
+}
+
+int acrgpu_stats(acrgpu_fact* f, acrgpu_rankstats* out) {
+    acrgpu_error e;
+    acrgpu_error* err = &e;
+    ABI_TRY({
+        Engine& E = *f->eng;
+        CK(cudaStreamSynchronize(E.st()));
+        HostStats inv;
+        long total = 0;
+        auto add = [&](const SP& s, bool is_inv) {
+            if (!s) return;
+            HostStats h = store_stats(E, s);
+            total += h.bytes;
+            if (is_inv) {
+                inv.rank_sum += h.rank_sum;
+                inv.largest = std::max(inv.largest, h.largest);
+                inv.ndense += h.ndense;
+                inv.nrk += h.nrk;
+                inv.bytes += h.bytes;
+            }
+        };
+        for (auto& L : f->levels) {
+            for (auto& s : L.E) add(s, false);
+            for (auto& s : L.F) add(s, false);
+            for (auto& s : L.Dinv) add(s, true);
+        }
+        for (auto& s : f->apexE) add(s, false);
+        for (auto& s : f->apexF) add(s, false);
+        for (auto& s : f->apexDinv) add(s, true);
+        out->average_rank = inv.nrk ? double(inv.rank_sum) / inv.nrk : 0.0;
+        out->largest_rank = inv.largest;
+        out->dense_leaf_count = inv.ndense;
+        out->lowrank_leaf_count = inv.nrk;
+        out->inverse_bytes = inv.bytes;
+        out->factor_bytes = total;
+        return 0;
+    })
+}
+
+int acrgpu_level_info(acrgpu_fact* f, acrgpu_levelinfo* out, int cap) {
+    acrgpu_error e;
+    acrgpu_error* err = &e;
+    ABI_TRY({
+        Engine& E = *f->eng;
+        int k = 0;
+        auto one = [&](int level, int pc, int elim, const std::vector<SP>& Dinv, const std::vector<SP>& Es,
+                       const std::vector<SP>& Fs) {
+            acrgpu_levelinfo li{};
+            li.level = level;
+            li.plane_count = pc;
+            li.eliminated = elim;
+            long rs = 0, nrk = 0;
+            for (auto& s : Dinv)
+                if (s) {
+                    HostStats h = store_stats(E, s);
+                    li.bytes += h.bytes;
+                    rs += h.rank_sum;
+                    nrk += h.nrk;
+                    li.largest_rank = std::max(li.largest_rank, h.largest);
+                }
+            for (auto& s : Es)
+                if (s) li.bytes += store_stats(E, s).bytes;
+            for (auto& s : Fs)
+                if (s) li.bytes += store_stats(E, s).bytes;
+            li.average_rank = nrk ? double(rs) / nrk : 0.0;
+            if (k < cap) out[k] = li;
+            ++k;
+        };
+        for (size_t i = 0; i < f->levels.size(); ++i) {
+            const Level& L = f->levels[i];
+            one((int)i, L.plane_count, (int)L.elim.size(), L.Dinv, L.E, L.F);
+        }
+        one((int)f->levels.size(), (int)f->apexDinv.size(), (int)f->apexDinv.size(), f->apexDinv, f->apexE, f->apexF);
+        return k;
+    })
+}
+
+long acrgpu_dinv_ranks(acrgpu_fact* f, int li, int j, int* out, long cap) {
+    Engine& E = *f->eng;
+    SP s;
+    if (li >= 0 && li < (int)f->levels.size()) {
+        const Level& L = f->levels[li];
+        if (j >= 0 && j < (int)L.Dinv.size()) s = L.Dinv[j];
+    } else if (li == (int)f->levels.size() && j >= 0 && j < (int)f->apexDinv.size()) {
+        s = f->apexDinv[j];
+    }
+    if (!s) return -1;
+    cudaStreamSynchronize(E.st());
+    std::vector<int> r(E.S.n_rk());
+    if (!r.empty()) cudaMemcpy(r.data(), s->rank, r.size() * sizeof(int), cudaMemcpyDeviceToHost);
+    // DFS order over all leaves, -1 for dense
+    long n = 0;
+    std::vector<int> lv;
+    E.subtree_leaves(0, lv);
+    for (int node : lv) {
+        const SNode& L = E.S.node(node);
+        if (out && n < cap) out[n] = L.kind == K_RK ? r[L.leaf] : -1;
+        ++n;
+    }
+    return n;
+}
+
+int acrgpu_timing_get(acrgpu_fact* f, acrgpu_timing* out) {
+    *out = f->timing;
+    return 0;
+}
+
+long acrgpu_structure(int dim, const double* coords, int leaf_size, double eta, int weak, int* perm, int* leaves,
+                      long cap, acrgpu_error* err) {
+    clear_err(err);
+    try {
+        Structure S;
+        S.build(dim, coords, leaf_size, eta, weak);
+        if (perm) std::copy(S.perm.begin(), S.perm.end(), perm);
+        long n = 0;
+        std::vector<int> st{0};
+        // DFS order
+        std::vector<int> order;
+        std::function<void(int)> walk = [&](int i) {
+            const SNode& nd = S.node(i);
+            if (nd.kind == K_BRANCH) {
+                for (int c = 0; c < 4; ++c) walk(nd.ch[c]);
+                return;
+            }
+            if (leaves && n < cap) {
+                int* o = leaves + 5 * n;
+                o[0] = nd.rb; o[1] = nd.re; o[2] = nd.cb; o[3] = nd.ce; o[4] = nd.kind;
+            }
+            ++n;
+        };
+        walk(0);
+        return n;
+    } catch (const StructureError& e) {
+        fill_err(err, AcrError{e.code, e.msg});
+        return -e.code;
+    }
+}
+
+}  // extern "C"

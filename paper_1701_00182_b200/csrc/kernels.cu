@@ -1,0 +1,1378 @@
+// sm_100a kernels of the batched H-matrix arithmetic (FP64).
+//
+// Every kernel is "task-parallel": blockIdx.x indexes a structural task of a
+// compiled plan, blockIdx.y the plane of the batch.  Sizes that depend on
+// ranks are read from device memory, outputs of data-dependent size are carved
+// from a device bump arena, so whole levels of the cyclic reduction are
+// enqueued without host synchronisation.
+//
+// Reference operations (file:line relative to /root/reference/proj/core/src):
+//   k_truncate      truncate_impl / flush / Branch*Branch agglomeration  hmatrix.cpp:56-84,373-392,415-440
+//   k_dd_product    Dense*Dense -> dense_to_lowrank                       hmatrix.cpp:87-99,411-413
+//   k_apply         node_apply / node_apply_trans (Rk*H, H*Rk products)   hmatrix.cpp:203-238,399-410
+//   k_deposit       deposit into dense targets                            hmatrix.cpp:354-371
+//   k_lu_inverse    PartialPivLU + rcond guard + inverse                  hmatrix.cpp:483-496
+//   k_sigma1_*      scale_walk (largest leaf spectral norm)               hmatrix.cpp:623-642
+//   k_matvec        happly / node_apply in the solve                      hmatrix.cpp:695-706
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "kernels.hpp"
+#include "structure.hpp"
+
+namespace acrgpu {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr double DEPS = 2.2204460492503131e-16;
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// block-wide sum (all threads get the result); red: >= NW doubles of smem
+__device__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = 0;
+    for (int i = 0; i < NW; ++i) s += red[i];
+    return s;
+}
+
+__device__ double* arena_alloc(const Arena& a, unsigned long long n) {
+    n = (n + 15ull) & ~15ull;  // 128-byte granules
+    const unsigned long long off = atomicAdd(a.ctr, n);
+    if (off + n > a.cap) {
+        atomicExch(a.overflow, 1);
+        return nullptr;
+    }
+    return a.base + off;
+}
+
+__device__ __forceinline__ void add_flops(FlopLedger* L, int cls, double f) {
+    if (L && f > 0) atomicAdd(&L->f[cls], f);
+}
+
+// nominal counts (identical formulas to oracle/acr_oracle.cpp)
+__device__ __forceinline__ double fl_gemm(double m, double n, double k) { return (m > 0 && n > 0 && k > 0) ? 2 * m * n * k : 0; }
+__device__ __forceinline__ double fl_geqrf(double m, double K) {
+    return m >= K ? 2 * m * K * K - 2.0 / 3.0 * K * K * K : 2 * K * m * m - 2.0 / 3.0 * m * m * m;
+}
+__device__ __forceinline__ double fl_orgqr(double m, double ku) { return 2 * m * ku * ku - 2.0 / 3.0 * ku * ku * ku; }
+// returns flops of the oracle's svd() of an r x c matrix, split into (svd, qr-ish, gemm)
+__device__ void fl_svd(double r, double c, double& fsvd, double& fqr, double& fgemm) {
+    if (r == c) { fsvd += 21 * r * r * r; return; }
+    const double p = r < c ? r : c, q = r < c ? c : r;
+    fqr += fl_geqrf(q, p) + fl_orgqr(q, p);
+    fsvd += 21 * p * p * p;
+    fgemm += fl_gemm(q, p, p);
+}
+
+// ------------------------------------------------------------------ one-sided Jacobi SVD
+// Columns of A (rows x cols, ld lda, rows >= cols) are orthogonalised by plane
+// rotations in round-robin (tournament) order; each pair is handled by one warp.
+// V (cols x cols, ld ldv) accumulates the right rotations when non-null.  On exit
+// column j of A = sigma_j u_j and sig[j] = ||a_j||.  Works on shared or global memory.
+// Equivalent algorithm class to the reference's JacobiSVD (hmatrix.cpp:67,89).
+__device__ void jacobi_svd(double* A, int lda, int rows, int cols, double* V, int ldv, double* sig) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (V)
+        for (int e = threadIdx.x; e < cols * cols; e += NT) {
+            const int i = e % cols, j = e / cols;
+            V[i + (size_t)j * ldv] = (i == j) ? 1.0 : 0.0;
+        }
+    __syncthreads();
+    if (cols > 1) {
+        const int P = cols + (cols & 1);
+        const int npairs = P / 2, rounds = P - 1;
+        const double tol = (double)(rows > 1 ? rows : 1) * DEPS;
+        for (int sweep = 0; sweep < 60; ++sweep) {
+            int rotated = 0;
+            for (int r = 0; r < rounds; ++r) {
+                for (int i = warp; i < npairs; i += NW) {
+                    int p, q;
+                    if (i == 0) {
+                        p = 0;
+                        q = 1 + r;
+                    } else {
+                        p = 1 + (r + i) % (P - 1);
+                        q = 1 + (r - i + P - 1) % (P - 1);
+                    }
+                    if (p > q) { const int t = p; p = q; q = t; }
+                    if (q >= cols) continue;
+                    double* ap = A + (size_t)p * lda;
+                    double* aq = A + (size_t)q * lda;
+                    double al = 0, be = 0, ga = 0;
+                    for (int e = lane; e < rows; e += 32) {
+                        const double x = ap[e], y = aq[e];
+                        al = fma(x, x, al);
+                        be = fma(y, y, be);
+                        ga = fma(x, y, ga);
+                    }
+                    al = warp_sum(al);
+                    be = warp_sum(be);
+                    ga = warp_sum(ga);
+                    if (!(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+                    const double zeta = (be - al) / (2.0 * ga);
+                    double t;
+                    if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+                    else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+                    for (int e = lane; e < rows; e += 32) {
+                        const double x = ap[e], y = aq[e];
+                        ap[e] = c * x - s * y;
+                        aq[e] = s * x + c * y;
+                    }
+                    if (V) {
+                        double* vp = V + (size_t)p * ldv;
+                        double* vq = V + (size_t)q * ldv;
+                        for (int e = lane; e < cols; e += 32) {
+                            const double x = vp[e], y = vq[e];
+                            vp[e] = c * x - s * y;
+                            vq[e] = s * x + c * y;
+                        }
+                    }
+                    rotated = 1;
+                }
+                __syncthreads();
+            }
+            if (!__syncthreads_or(rotated)) break;
+        }
+    }
+    for (int j = warp; j < cols; j += NW) {
+        const double* aj = A + (size_t)j * lda;
+        double s = 0;
+        for (int e = lane; e < rows; e += 32) s = fma(aj[e], aj[e], s);
+        s = warp_sum(s);
+        if (lane == 0) sig[j] = sqrt(s);
+    }
+    __syncthreads();
+}
+
+// order[t] = index of the t-th largest sig (ties by index); returns via smem.
+__device__ void sort_desc(const double* sig, int n, int* order) {
+    for (int j = threadIdx.x; j < n; j += NT) {
+        const double v = sig[j];
+        int pos = 0;
+        for (int i = 0; i < n; ++i) {
+            const double w = sig[i];
+            pos += (w > v) || (w == v && i < j);
+        }
+        order[pos] = j;
+    }
+    __syncthreads();
+}
+
+__device__ int rank_of(const double* sig, const int* order, int n, double eps, double abs_cut) {
+    if (n == 0) return 0;
+    const double s0 = sig[order[0]];
+    if (!(s0 > 0.0)) return 0;
+    const double cut = fmax(eps * s0, abs_cut);
+    int r = 0;
+    while (r < n && sig[order[r]] > cut) ++r;
+    return r;
+}
+
+// ------------------------------------------------------------------ Householder QR
+// In-place unpivoted Householder QR of W (rows x cols, ld): R in the upper
+// trapezoid, essential reflector parts below the diagonal, tau[j].  Eigen
+// HouseholderQR conventions (hmatrix.cpp:62-63): beta = -sign(c0)||x||, tau = 0
+// when the sub-diagonal tail is exactly zero.
+__device__ void householder_qr(double* W, int ld, int rows, int cols, double* tau, double* red) {
+    const int kmax = rows < cols ? rows : cols;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ double sh_beta, sh_tau, sh_inv;
+    for (int j = 0; j < kmax; ++j) {
+        double* wj = W + (size_t)j * ld;
+        double part = 0;
+        for (int i = j + 1 + threadIdx.x; i < rows; i += NT) part = fma(wj[i], wj[i], part);
+        const double tail = block_sum(part, red);
+        if (threadIdx.x == 0) {
+            const double c0 = wj[j];
+            if (tail <= DBL_MIN) {
+                sh_tau = 0.0;
+                sh_beta = c0;
+                sh_inv = 0.0;
+            } else {
+                double beta = sqrt(c0 * c0 + tail);
+                if (c0 >= 0) beta = -beta;
+                sh_inv = 1.0 / (c0 - beta);
+                sh_tau = (beta - c0) / beta;
+                sh_beta = beta;
+            }
+            tau[j] = sh_tau;
+        }
+        __syncthreads();
+        const double tj = sh_tau, inv = sh_inv;
+        if (tj == 0.0) {
+            for (int i = j + 1 + threadIdx.x; i < rows; i += NT) wj[i] = 0.0;
+        } else {
+            for (int i = j + 1 + threadIdx.x; i < rows; i += NT) wj[i] *= inv;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) wj[j] = sh_beta;
+        if (tj != 0.0) {
+            for (int c = j + 1 + warp; c < cols; c += NW) {
+                double* wc = W + (size_t)c * ld;
+                double s = 0;
+                for (int i = j + 1 + lane; i < rows; i += 32) s = fma(wj[i], wc[i], s);
+                s = warp_sum(s) + wc[j];
+                s *= tj;
+                if (lane == 0) wc[j] -= s;
+                for (int i = j + 1 + lane; i < rows; i += 32) wc[i] -= s * wj[i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Y (rows x ncol, ld) <- Q Y with Q = H_0 H_1 ... H_{k-1} from householder_qr(W).
+__device__ void apply_q(const double* W, int ldw, int rows, int k, const double* tau, double* Y, int ldy, int ncol) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = k - 1; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj != 0.0) {
+            const double* v = W + (size_t)j * ldw;
+            for (int c = warp; c < ncol; c += NW) {
+                double* y = Y + (size_t)c * ldy;
+                double s = 0;
+                for (int i = j + 1 + lane; i < rows; i += 32) s = fma(v[i], y[i], s);
+                s = (warp_sum(s) + y[j]) * tj;
+                if (lane == 0) y[j] -= s;
+                for (int i = j + 1 + lane; i < rows; i += 32) y[i] -= s * v[i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ part resolution
+struct PartRes {
+    const double* U;
+    const double* V;
+    int ldu, ldv, rank;
+};
+
+__device__ __forceinline__ PartRes resolve_part(const Part& p, const Slot* slots, int b, int B, const HView& C) {
+    PartRes r{nullptr, nullptr, 0, 0, 0};
+    if (p.src == S_SLOT) {
+        const Slot s = slots[(size_t)p.id * B + b];
+        r.rank = s.rank;
+        if (s.rank > 0) {
+            r.U = s.U + p.u_src;
+            r.V = s.V + p.v_src;
+            r.ldu = s.ldu;
+            r.ldv = s.ldv;
+        }
+    } else if (p.src == S_CLEAF) {
+        r.rank = C.rank[p.id];
+        if (r.rank > 0) {
+            r.U = C.U[p.id] + p.u_src;
+            r.V = C.V[p.id] + p.v_src;
+            r.ldu = p.rows_u;
+            r.ldv = p.rows_v;
+        }
+    }
+    return r;
+}
+
+// ------------------------------------------------------------------ dense-route SVD truncation
+// M (m x n, ld m) in smem.  Computes the truncated SVD and writes outputs
+// U' = U_r Sigma_r (m x r) and V' = V_r (n x r) into one arena allocation.
+// work: >= n*n + (m<n ? n*m + m*m - n*n : 0) doubles of smem; sig/order: >= max(m,n).
+// Returns r (block-uniform); *out_ptr receives the allocation (nullptr if r == 0).
+__device__ int svd_truncate_dense(double* M, int m, int n, double eps, double abs_cut, double* work, double* sig,
+                                  int* order, const Arena& arena, double** out_ptr, double* sig_max_out,
+                                  bool values_only) {
+    __shared__ double* sh_out;
+    __shared__ int sh_r;
+    const bool tall = m >= n;
+    double *A, *Vw;
+    int rows, cols;
+    if (tall) {
+        A = M;
+        rows = m;
+        cols = n;
+        Vw = values_only ? nullptr : work;
+    } else {  // work on M^T (n x m)
+        A = work;
+        rows = n;
+        cols = m;
+        for (int e = threadIdx.x; e < m * n; e += NT) {
+            const int i = e % m, j = e / m;
+            A[j + (size_t)i * n] = M[e];
+        }
+        Vw = values_only ? nullptr : work + (size_t)n * m;
+        __syncthreads();
+    }
+    jacobi_svd(A, rows, rows, cols, Vw, cols, sig);
+    sort_desc(sig, cols, order);
+    if (threadIdx.x == 0) {
+        sh_r = rank_of(sig, order, cols, eps, abs_cut);
+        if (sig_max_out) *sig_max_out = cols > 0 ? sig[order[0]] : 0.0;
+        sh_out = nullptr;
+        if (!values_only && sh_r > 0) sh_out = arena_alloc(arena, (unsigned long long)(m + n) * sh_r);
+    }
+    __syncthreads();
+    const int r = sh_r;
+    double* out = sh_out;
+    if (out_ptr) *out_ptr = out;
+    if (values_only || r == 0 || out == nullptr) return r;
+    double* Uo = out;
+    double* Vo = out + (size_t)m * r;
+    if (tall) {
+        for (int e = threadIdx.x; e < m * r; e += NT) {
+            const int i = e % m, t = e / m;
+            Uo[e] = A[i + (size_t)order[t] * rows];
+        }
+        for (int e = threadIdx.x; e < n * r; e += NT) {
+            const int i = e % n, t = e / n;
+            Vo[e] = Vw[i + (size_t)order[t] * cols];
+        }
+    } else {
+        // M^T J = W  =>  M = J W^T = (J Sigma)(W Sigma^{-1})^T
+        for (int e = threadIdx.x; e < m * r; e += NT) {
+            const int i = e % m, t = e / m;
+            const int j = order[t];
+            Uo[e] = Vw[i + (size_t)j * cols] * sig[j];
+        }
+        for (int e = threadIdx.x; e < n * r; e += NT) {
+            const int i = e % n, t = e / n;
+            const int j = order[t];
+            Vo[e] = A[i + (size_t)j * rows] / sig[j];
+        }
+    }
+    __syncthreads();
+    return r;
+}
+
+// ------------------------------------------------------------------ truncation kernel
+// One CTA per (task, plane).  Dense route (m, n <= DENSE_MAX): form the m x n
+// block M = sum alpha U V^T in shared memory and SVD it directly -- the same
+// singular triplets the reference obtains from QR(U), QR(V), SVD(Ru Rv^T),
+// without the two QRs.  QR route (larger blocks): concatenate into an arena
+// workspace, Householder QR both factors, SVD the ku x kv core, rebuild
+// U' = Qu Us Sigma, V' = Qv Vs by applying the reflectors.
+struct TruncArgs {
+    const TruncTask* tasks;
+    const Part* parts;
+    Slot* slots;
+    int B;
+    double eps;
+    const double* abs_cut;  // per plane (nullptr: 0)
+    double* sig_out;        // values-only mode: sigma_1 per (task, plane)
+    int values_only;
+    Arena out_arena;        // persistent (flush) or transient (products)
+    Arena work;             // transient workspace
+    FlopLedger* flops;
+};
+
+__global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) {
+    extern __shared__ double smem[];
+    __shared__ double red[NW];
+    __shared__ int sh_K;
+    __shared__ double* sh_ws;
+    const TruncTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    const int B = args.B;
+    const HView& C = bv.c[b];
+    const int m = task.m, n = task.n;
+    const double abs_cut = args.abs_cut ? args.abs_cut[b] : 0.0;
+
+    // total concatenated rank K
+    if (threadIdx.x == 0) {
+        int K = 0;
+        for (int pi = task.pbeg; pi < task.pend; ++pi) K += resolve_part(args.parts[pi], args.slots, b, B, C).rank;
+        sh_K = K;
+    }
+    __syncthreads();
+    const int K = sh_K;
+
+    auto write_out = [&](int r, double* U, double* V) {
+        if (threadIdx.x != 0 || args.values_only) return;
+        if (task.out_kind == 0) {
+            Slot& s = args.slots[(size_t)task.out_id * B + b];
+            s.rank = r;
+            s.U = U;
+            s.V = V;
+            s.ldu = m;
+            s.ldv = n;
+        } else {
+            C.rank[task.out_id] = r;
+            C.U[task.out_id] = U;
+            C.V[task.out_id] = V;
+        }
+    };
+
+    if (K == 0) {
+        write_out(0, nullptr, nullptr);
+        if (args.values_only && threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = 0.0;
+        return;
+    }
+
+    const int ku = m < K ? m : K, kv = n < K ? n : K;
+    double fsvd = 0, fqr = 0, fgemm = 0;
+
+    if (m <= DENSE_MAX && n <= DENSE_MAX) {
+        // ---------------- dense route
+        double* M = smem;                                   // m*n
+        double* work = M + (size_t)m * n;                   // up to 2*DENSE_MAX^2
+        double* sig = work + 2 * DENSE_MAX * DENSE_MAX;     // DENSE_MAX
+        int* order = (int*)(sig + DENSE_MAX);
+        for (int e = threadIdx.x; e < m * n; e += NT) M[e] = 0.0;
+        __syncthreads();
+        for (int pi = task.pbeg; pi < task.pend; ++pi) {
+            const Part p = args.parts[pi];
+            const PartRes pr = resolve_part(p, args.slots, b, B, C);
+            if (pr.rank == 0) continue;
+            const int ru = p.rows_u, rv = p.rows_v;
+            for (int e = threadIdx.x; e < ru * rv; e += NT) {
+                const int i = e % ru, j = e / ru;
+                double acc = 0;
+                for (int t = 0; t < pr.rank; ++t)
+                    acc = fma(pr.U[i + (size_t)t * pr.ldu], pr.V[j + (size_t)t * pr.ldv], acc);
+                M[(p.u_dst + i) + (size_t)(p.v_dst + j) * m] += p.alpha * acc;
+            }
+            __syncthreads();
+        }
+        double smax = 0;
+        double* out = nullptr;
+        const int r = svd_truncate_dense(M, m, n, args.eps, abs_cut, work, sig, order, args.out_arena, &out, &smax,
+                                         args.values_only != 0);
+        write_out(r, out, out ? out + (size_t)m * r : nullptr);
+        if (args.values_only && threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
+        // nominal (reference-algorithm) flops
+        if (threadIdx.x == 0) {
+            if (args.values_only) {
+                fqr += fl_geqrf(m, K) + fl_geqrf(n, K);
+                fgemm += fl_gemm(ku, kv, K);
+                fl_svd(ku, kv, fsvd, fqr, fgemm);
+            } else {
+                fqr += fl_geqrf(m, K) + fl_orgqr(m, ku) + fl_geqrf(n, K) + fl_orgqr(n, kv);
+                fgemm += fl_gemm(ku, kv, K) + fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
+                fl_svd(ku, kv, fsvd, fqr, fgemm);
+            }
+            add_flops(args.flops, F_SVD, fsvd);
+            add_flops(args.flops, F_GEQRF, fqr);
+            add_flops(args.flops, F_GEMM, fgemm);
+        }
+        return;
+    }
+
+    // ---------------- QR route
+    // workspace: Uc (m x K) | Vc (n x K) | tau_u (K) | tau_v (K) | [core + V if too big for smem]
+    const int pmax = ku > kv ? ku : kv, pmin = ku < kv ? ku : kv;
+    const bool core_in_smem = (size_t)pmax * pmin + (size_t)pmin * pmin + 2 * (size_t)pmax <= (size_t)SMEM_TRUNC / 8 - 64;
+    if (threadIdx.x == 0) {
+        unsigned long long need = (unsigned long long)(m + n) * K + 2ull * K + 32;
+        if (!core_in_smem) need += (unsigned long long)pmax * pmin + (unsigned long long)pmin * pmin + 2ull * pmax;
+        sh_ws = arena_alloc(args.work, need);
+    }
+    __syncthreads();
+    double* ws = sh_ws;
+    if (ws == nullptr) {  // arena exhausted: flag already raised; leave the target unchanged
+        return;
+    }
+    double* Uc = ws;
+    double* Vc = Uc + (size_t)m * K;
+    double* tau_u = Vc + (size_t)n * K;
+    double* tau_v = tau_u + K;
+    double* core;
+    if (core_in_smem) core = smem;
+    else core = tau_v + K + 32;
+    double* Vsv = core + (size_t)pmax * pmin;
+    double* sig = Vsv + (size_t)pmin * pmin;
+    int* order = (int*)(sig + pmax);
+
+    // concatenate (zero-fill, then place each part)
+    for (size_t e = threadIdx.x; e < (size_t)(m + n) * K; e += NT) ws[e] = 0.0;
+    __syncthreads();
+    {
+        int off = 0;
+        for (int pi = task.pbeg; pi < task.pend; ++pi) {
+            const Part p = args.parts[pi];
+            const PartRes pr = resolve_part(p, args.slots, b, B, C);
+            if (pr.rank == 0) continue;
+            for (int e = threadIdx.x; e < p.rows_u * pr.rank; e += NT) {
+                const int i = e % p.rows_u, t = e / p.rows_u;
+                Uc[(p.u_dst + i) + (size_t)(off + t) * m] = p.alpha * pr.U[i + (size_t)t * pr.ldu];
+            }
+            for (int e = threadIdx.x; e < p.rows_v * pr.rank; e += NT) {
+                const int i = e % p.rows_v, t = e / p.rows_v;
+                Vc[(p.v_dst + i) + (size_t)(off + t) * n] = pr.V[i + (size_t)t * pr.ldv];
+            }
+            off += pr.rank;
+        }
+    }
+    __syncthreads();
+    householder_qr(Uc, m, m, K, tau_u, red);
+    householder_qr(Vc, n, n, K, tau_v, red);
+    // core = Ru Rv^T (ku x kv); stored as A (rows >= cols) for the one-sided SVD
+    const bool tall = ku >= kv;
+    const int rows = tall ? ku : kv, cols = tall ? kv : ku;
+    for (int e = threadIdx.x; e < ku * kv; e += NT) {
+        const int i = e % ku, j = e / ku;
+        double acc = 0;
+        for (int t = (i > j ? i : j); t < K; ++t) acc = fma(Uc[i + (size_t)t * m], Vc[j + (size_t)t * n], acc);
+        if (tall) core[i + (size_t)j * rows] = acc;
+        else core[j + (size_t)i * rows] = acc;
+    }
+    __syncthreads();
+    jacobi_svd(core, rows, rows, cols, args.values_only ? nullptr : Vsv, cols, sig);
+    sort_desc(sig, cols, order);
+    __shared__ int sh_r;
+    __shared__ double* sh_out;
+    if (threadIdx.x == 0) {
+        sh_r = rank_of(sig, order, cols, args.eps, abs_cut);
+        sh_out = nullptr;
+        if (args.values_only) args.sig_out[(size_t)blockIdx.x * B + b] = sig[order[0]];
+        else if (sh_r > 0) sh_out = arena_alloc(args.out_arena, (unsigned long long)(m + n) * sh_r);
+    }
+    __syncthreads();
+    const int r = sh_r;
+    if (!args.values_only) {
+        double* out = sh_out;
+        if (r > 0 && out != nullptr) {
+            double* Uo = out;
+            double* Vo = out + (size_t)m * r;
+            // Us Sigma (ku x r) and Vs (kv x r) from the core SVD
+            for (int e = threadIdx.x; e < m * r; e += NT) Uo[e] = 0.0;
+            for (int e = threadIdx.x; e < n * r; e += NT) Vo[e] = 0.0;
+            __syncthreads();
+            for (int t = 0; t < r; ++t) {
+                const int j = order[t];
+                if (tall) {  // core = Ucore Sigma Vcore^T: A col j = sigma u_j, Vsv col j = v_j
+                    for (int i = threadIdx.x; i < ku; i += NT) Uo[i + (size_t)t * m] = core[i + (size_t)j * rows];
+                    for (int i = threadIdx.x; i < kv; i += NT) Vo[i + (size_t)t * n] = Vsv[i + (size_t)j * cols];
+                } else {  // core^T J = W: U = J Sigma, V = W Sigma^{-1}
+                    for (int i = threadIdx.x; i < ku; i += NT) Uo[i + (size_t)t * m] = Vsv[i + (size_t)j * cols] * sig[j];
+                    for (int i = threadIdx.x; i < kv; i += NT) Vo[i + (size_t)t * n] = core[i + (size_t)j * rows] / sig[j];
+                }
+            }
+            __syncthreads();
+            apply_q(Uc, m, m, ku, tau_u, Uo, m, r);
+            apply_q(Vc, n, n, kv, tau_v, Vo, n, r);
+        }
+        write_out(r, out, out ? out + (size_t)m * r : nullptr);
+    }
+    if (threadIdx.x == 0) {
+        fqr += fl_geqrf(m, K) + fl_geqrf(n, K);
+        if (!args.values_only) fqr += fl_orgqr(m, ku) + fl_orgqr(n, kv);
+        fgemm += fl_gemm(ku, kv, K);
+        if (!args.values_only) fgemm += fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
+        fl_svd(ku, kv, fsvd, fqr, fgemm);
+        add_flops(args.flops, F_SVD, fsvd);
+        add_flops(args.flops, F_GEQRF, fqr);
+        add_flops(args.flops, F_GEMM, fgemm);
+    }
+}
+
+// ------------------------------------------------------------------ dense * dense product
+struct DDArgs {
+    const DDTask* tasks;
+    Slot* slots;
+    int B;
+    double eps;
+    Arena out_arena;
+    FlopLedger* flops;
+};
+
+__global__ void __launch_bounds__(NT) k_dd_product(DDArgs args, BatchViews bv) {
+    extern __shared__ double smem[];
+    const DDTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    const int m = task.m, k = task.k, n = task.n;
+    const double* Ad = bv.a[b].dense + task.da;
+    const double* Bd = bv.b[b].dense + task.db;
+    double* M = smem;
+    double* As = M + (size_t)m * n;
+    double* Bs = As + (size_t)m * k;
+    for (int e = threadIdx.x; e < m * k; e += NT) As[e] = Ad[e];
+    for (int e = threadIdx.x; e < k * n; e += NT) Bs[e] = Bd[e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * n; e += NT) {
+        const int i = e % m, j = e / m;
+        double acc = 0;
+        for (int p = 0; p < k; ++p) acc = fma(As[i + (size_t)p * m], Bs[p + (size_t)j * k], acc);
+        M[e] = acc;
+    }
+    __syncthreads();
+    double* work = As;  // reuse operand space (>= 2*DENSE_MAX^2 reserved by the launcher)
+    double* sig = work + 2 * DENSE_MAX * DENSE_MAX;
+    int* order = (int*)(sig + DENSE_MAX);
+    double* out = nullptr;
+    const int r = svd_truncate_dense(M, m, n, args.eps, 0.0, work, sig, order, args.out_arena, &out, nullptr, false);
+    if (threadIdx.x == 0) {
+        Slot& s = args.slots[(size_t)task.prod * args.B + b];
+        s.rank = r;
+        s.U = out;
+        s.V = out ? out + (size_t)m * r : nullptr;
+        s.ldu = m;
+        s.ldv = n;
+        double fsvd = 0, fqr = 0, fgemm = fl_gemm(m, n, k);
+        fl_svd(m, n, fsvd, fqr, fgemm);
+        add_flops(args.flops, F_SVD, fsvd);
+        add_flops(args.flops, F_GEQRF, fqr);
+        add_flops(args.flops, F_GEMM, fgemm);
+    }
+}
+
+// ------------------------------------------------------------------ apply products
+struct AllocArgs {
+    const AllocTask* tasks;
+    int ntasks;
+    Slot* slots;
+    int B;
+    Arena arena;
+};
+
+__global__ void k_alloc_apply(AllocArgs args, BatchViews bv) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= args.ntasks * args.B) return;
+    const int ti = idx / args.B, b = idx % args.B;
+    const AllocTask t = args.tasks[ti];
+    Slot s;
+    s.pad = 0;
+    if (t.kind == P_RK_LEFT) {
+        const HView& A = bv.a[b];
+        s.rank = A.rank[t.kx];
+        s.U = s.rank ? A.U[t.kx] : nullptr;
+        s.ldu = t.rows_alias;
+        s.ldv = t.rows_out;
+        s.V = s.rank ? arena_alloc(args.arena, (unsigned long long)t.rows_out * s.rank) : nullptr;
+        if (s.rank && !s.V) s.rank = 0;
+    } else {
+        const HView& Bv = bv.b[b];
+        s.rank = Bv.rank[t.kx];
+        s.V = s.rank ? Bv.V[t.kx] : nullptr;
+        s.ldv = t.rows_alias;
+        s.ldu = t.rows_out;
+        s.U = s.rank ? arena_alloc(args.arena, (unsigned long long)t.rows_out * s.rank) : nullptr;
+        if (s.rank && !s.U) s.rank = 0;
+    }
+    args.slots[(size_t)t.prod * args.B + b] = s;
+}
+
+struct ApplyArgs {
+    const ApplyTask* tasks;
+    const ApplyLeaf* leaves;
+    Slot* slots;
+    int B;
+    int x_ld_mode;  // unused
+    const int* x_ld;  // per task: leading dimension of X
+    FlopLedger* flops;
+};
+
+constexpr int APPLY_ROWS = 64;  // max slab rows
+constexpr int APPLY_COLS = 32;  // rhs columns per pass
+constexpr int APPLY_TR = 64;    // Rk ranks per inner pass
+
+__global__ void __launch_bounds__(NT) k_apply(ApplyArgs args, BatchViews bv) {
+    __shared__ double T[APPLY_TR * APPLY_COLS];
+    const ApplyTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    const Slot s = args.slots[(size_t)task.prod * args.B + b];
+    const int k = s.rank;
+    if (k == 0) return;
+    const bool trans = task.kind == P_RK_LEFT;
+    const HView& H = trans ? bv.b[b] : bv.a[b];
+    const double* X = trans ? bv.a[b].V[task.kx] : bv.b[b].U[task.kx];
+    const int ldx = args.x_ld[blockIdx.x];
+    double* Y = trans ? s.V : s.U;
+    const int ldy = trans ? s.ldv : s.ldu;
+    const int r0 = task.r0, nr = task.r1 - task.r0;
+    double fl = 0;
+    for (int c0 = 0; c0 < k; c0 += APPLY_COLS) {
+        const int nc = min(APPLY_COLS, k - c0);
+        // each thread owns elements e = tid + t*NT of the nr x nc slab
+        double acc[(APPLY_ROWS * APPLY_COLS) / NT];
+#pragma unroll
+        for (int q = 0; q < (APPLY_ROWS * APPLY_COLS) / NT; ++q) acc[q] = 0.0;
+        for (int li = task.lbeg; li < task.lend; ++li) {
+            const ApplyLeaf L = args.leaves[li];
+            const int out_len = trans ? L.n : L.m;
+            const int in_len = trans ? L.m : L.n;
+            const int o0 = max(r0, L.out_off), o1 = min(task.r1, L.out_off + out_len);
+            if (o0 >= o1) continue;
+            if (L.kind == K_DENSE) {
+                const double* D = H.dense + L.doff;
+#pragma unroll
+                for (int q = 0; q < (APPLY_ROWS * APPLY_COLS) / NT; ++q) {
+                    const int e = threadIdx.x + q * NT;
+                    const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
+                    const int row = r0 + i;
+                    if (i >= nr || c >= nc || row < o0 || row >= o1) continue;
+                    const int lr = row - L.out_off;  // leaf output index
+                    const double* x = X + L.in_off + (size_t)(c0 + c) * ldx;
+                    double a = 0;
+                    if (!trans)
+                        for (int j = 0; j < in_len; ++j) a = fma(D[lr + (size_t)j * L.m], x[j], a);
+                    else
+                        for (int j = 0; j < in_len; ++j) a = fma(D[j + (size_t)lr * L.m], x[j], a);
+                    acc[q] += a;
+                }
+                if (threadIdx.x == 0) fl += 2.0 * (o1 - o0) * in_len * nc;
+            } else {
+                const int rr = H.rank[L.id];
+                if (rr == 0) continue;
+                const double* In = trans ? H.U[L.id] : H.V[L.id];   // contracted with X
+                const double* Out = trans ? H.V[L.id] : H.U[L.id];  // expands into Y
+                const int ld_in = in_len, ld_out = out_len;
+                for (int t0 = 0; t0 < rr; t0 += APPLY_TR) {
+                    const int nt = min(APPLY_TR, rr - t0);
+                    __syncthreads();
+                    for (int e = threadIdx.x; e < nt * nc; e += NT) {
+                        const int t = e % nt, c = e / nt;
+                        const double* in = In + (size_t)(t0 + t) * ld_in;
+                        const double* x = X + L.in_off + (size_t)(c0 + c) * ldx;
+                        double a = 0;
+                        for (int j = 0; j < in_len; ++j) a = fma(in[j], x[j], a);
+                        T[t + c * APPLY_TR] = a;
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int q = 0; q < (APPLY_ROWS * APPLY_COLS) / NT; ++q) {
+                        const int e = threadIdx.x + q * NT;
+                        const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
+                        const int row = r0 + i;
+                        if (i >= nr || c >= nc || row < o0 || row >= o1) continue;
+                        const int lr = row - L.out_off;
+                        double a = 0;
+                        for (int t = 0; t < nt; ++t) a = fma(Out[lr + (size_t)(t0 + t) * ld_out], T[t + c * APPLY_TR], a);
+                        acc[q] += a;
+                    }
+                }
+                if (threadIdx.x == 0) {
+                    fl += 2.0 * (o1 - o0) * rr * nc;
+                    if (L.out_off >= r0 && L.out_off < task.r1) fl += 2.0 * rr * in_len * nc;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < (APPLY_ROWS * APPLY_COLS) / NT; ++q) {
+            const int e = threadIdx.x + q * NT;
+            const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
+            if (i < nr && c < nc) Y[(r0 + i) + (size_t)(c0 + c) * ldy] = acc[q];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, fl);
+}
+
+// ------------------------------------------------------------------ dense-target deposits
+struct DepArgs {
+    const DepTask* tasks;
+    const Part* parts;
+    const Slot* slots;
+    int B;
+    FlopLedger* flops;
+};
+
+__global__ void __launch_bounds__(NT) k_deposit(DepArgs args, BatchViews bv) {
+    const DepTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    double* Cd = bv.c[b].dense + task.doff;
+    const int m = task.m, n = task.n;
+    double fl = 0;
+    for (int e = threadIdx.x; e < m * n; e += NT) {
+        const int i = e % m, j = e / m;
+        double c = Cd[e];
+        for (int pi = task.pbeg; pi < task.pend; ++pi) {
+            const Part p = args.parts[pi];
+            if (p.src == S_GEMM) {
+                const double* A = bv.a[b].dense + p.da;
+                const double* Bm = bv.b[b].dense + p.db;
+                double a = 0;
+                for (int t = 0; t < p.gk; ++t) a = fma(A[i + (size_t)t * m], Bm[t + (size_t)j * p.gk], a);
+                c += p.alpha * a;
+                if (e == 0) fl += 2.0 * m * n * p.gk;
+            } else {
+                const Slot s = args.slots[(size_t)p.id * args.B + b];
+                if (s.rank == 0) continue;
+                const double* U = s.U + p.u_src;
+                const double* V = s.V + p.v_src;
+                double a = 0;
+                for (int t = 0; t < s.rank; ++t) a = fma(p.alpha * U[i + (size_t)t * s.ldu], V[j + (size_t)t * s.ldv], a);
+                c += a;
+                if (e == 0) fl += 2.0 * m * n * s.rank;
+            }
+        }
+        Cd[e] = c;
+    }
+    if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, fl);
+}
+
+// ------------------------------------------------------------------ dense leaf inversion
+struct LuArgs {
+    const LuTask* tasks;
+    DevError* err;
+    unsigned long long call_id;
+    FlopLedger* flops;
+};
+
+__global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
+    extern __shared__ double smem[];
+    __shared__ int piv[DENSE_MAX];
+    __shared__ int sh_p;
+    __shared__ double sh_rcond;
+    const LuTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    const int n = task.m;
+    const double* A = bv.a[b].dense + task.doff;
+    double* Out = bv.c[b].dense + task.doff;
+    double* LU = smem;                 // n x n
+    double* Ao = LU + n * n;           // original (for the 1-norm)
+    double* vx = Ao + n * n;           // work vectors
+    double* vz = vx + n;
+    for (int e = threadIdx.x; e < n * n; e += NT) {
+        LU[e] = A[e];
+        Ao[e] = A[e];
+    }
+    __syncthreads();
+    bool zero_pivot = false;
+    for (int k = 0; k < n; ++k) {
+        if (threadIdx.x < 32) {
+            double best = -1;
+            int bi = k;
+            for (int i = k + threadIdx.x; i < n; i += 32) {
+                const double v = fabs(LU[i + k * n]);
+                if (v > best) { best = v; bi = i; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (threadIdx.x == 0) { sh_p = bi; piv[k] = bi; }
+        }
+        __syncthreads();
+        const int p = sh_p;
+        if (p != k)
+            for (int c = threadIdx.x; c < n; c += NT) {
+                const double t = LU[k + c * n];
+                LU[k + c * n] = LU[p + c * n];
+                LU[p + c * n] = t;
+            }
+        __syncthreads();
+        const double d = LU[k + k * n];
+        if (d == 0.0) zero_pivot = true;
+        if (d != 0.0) {
+            for (int i = k + 1 + threadIdx.x; i < n; i += NT) LU[i + k * n] /= d;
+            __syncthreads();
+            const int rem = n - k - 1;
+            for (int e = threadIdx.x; e < rem * rem; e += NT) {
+                const int i = k + 1 + e % rem, c = k + 1 + e / rem;
+                LU[i + c * n] -= LU[i + k * n] * LU[k + c * n];
+            }
+        }
+        __syncthreads();
+    }
+    // Hager / Higham 1-norm condition estimate (one warp, sequential solves)
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double anorm = 0;
+        for (int c = 0; c < n; ++c) {
+            double s = 0;
+            for (int i = lane; i < n; i += 32) s += fabs(Ao[i + c * n]);
+            s = warp_sum(s);
+            anorm = fmax(anorm, s);
+        }
+        auto solve = [&](double* x) {  // A x = b in place
+            __syncwarp();
+            if (lane == 0) {
+                for (int k = 0; k < n; ++k) { const double t = x[k]; x[k] = x[piv[k]]; x[piv[k]] = t; }
+                for (int k = 0; k < n; ++k)
+                    for (int i = k + 1; i < n; ++i) x[i] -= LU[i + k * n] * x[k];
+                for (int k = n - 1; k >= 0; --k) {
+                    x[k] /= LU[k + k * n];
+                    for (int i = 0; i < k; ++i) x[i] -= LU[i + k * n] * x[k];
+                }
+            }
+            __syncwarp();
+        };
+        auto solve_t = [&](double* x) {  // A^T x = b in place
+            __syncwarp();
+            if (lane == 0) {
+                for (int k = 0; k < n; ++k) {
+                    for (int i = 0; i < k; ++i) x[k] -= LU[i + k * n] * x[i];
+                    x[k] /= LU[k + k * n];
+                }
+                for (int k = n - 1; k >= 0; --k)
+                    for (int i = k + 1; i < n; ++i) x[k] -= LU[i + k * n] * x[i];
+                for (int k = n - 1; k >= 0; --k) { const double t = x[k]; x[k] = x[piv[k]]; x[piv[k]] = t; }
+            }
+            __syncwarp();
+        };
+        double rc = 0.0;
+        bool zp = false;
+        for (int k = 0; k < n; ++k) zp |= (LU[k + k * n] == 0.0);
+        if (anorm > 0 && !zp) {
+            double est = 0;
+            for (int i = lane; i < n; i += 32) vx[i] = 1.0 / n;
+            for (int it = 0; it < 5; ++it) {
+                __syncwarp();
+                for (int i = lane; i < n; i += 32) vz[i] = vx[i];
+                solve(vz);
+                double ny = 0;
+                for (int i = lane; i < n; i += 32) ny += fabs(vz[i]);
+                ny = warp_sum(ny);
+                if (it > 0 && ny <= est) break;
+                est = ny;
+                __syncwarp();
+                for (int i = lane; i < n; i += 32) vz[i] = vz[i] >= 0 ? 1.0 : -1.0;
+                solve_t(vz);
+                double zmax = -1;
+                int jmax = 0;
+                if (lane == 0)
+                    for (int i = 0; i < n; ++i)
+                        if (fabs(vz[i]) > zmax) { zmax = fabs(vz[i]); jmax = i; }
+                zmax = __shfl_sync(0xffffffffu, zmax, 0);
+                jmax = __shfl_sync(0xffffffffu, jmax, 0);
+                double ztx = 0;
+                for (int i = lane; i < n; i += 32) ztx += vz[i] * vx[i];
+                ztx = warp_sum(ztx);
+                if (it > 0 && zmax <= ztx) break;
+                __syncwarp();
+                for (int i = lane; i < n; i += 32) vx[i] = (i == jmax) ? 1.0 : 0.0;
+            }
+            __syncwarp();
+            for (int i = lane; i < n; i += 32) vz[i] = ((i % 2) ? -1.0 : 1.0) * (1.0 + double(i) / (n > 1 ? n - 1 : 1));
+            solve(vz);
+            double na = 0;
+            for (int i = lane; i < n; i += 32) na += fabs(vz[i]);
+            na = warp_sum(na);
+            est = fmax(est, 2.0 * na / (3.0 * n));
+            rc = (est > 0 && isfinite(est)) ? 1.0 / (anorm * est) : 0.0;
+        }
+        if (lane == 0) sh_rcond = rc;
+    }
+    __syncthreads();
+    const double rcond = sh_rcond;
+    zero_pivot = false;
+    for (int k = 0; k < n; ++k) zero_pivot |= (LU[k + k * n] == 0.0);
+    if (!(rcond > 1e-14)) {
+        if (threadIdx.x == 0) {
+            const unsigned long long key = (args.call_id << 16) | (unsigned long long)b;
+            const unsigned long long prev = atomicMin(&args.err->key, key);
+            if (key < prev) {
+                args.err->code = 2;
+                args.err->rb = task.rb;
+                args.err->re = task.re;
+                args.err->rcond = rcond;
+            }
+        }
+    }
+    // inverse: column c of A^{-1} solves A x = e_c (thread per column)
+    for (int c = threadIdx.x; c < n; c += NT) {
+        double* x = Out + (size_t)c * n;
+        if (zero_pivot) {
+            for (int i = 0; i < n; ++i) x[i] = 0.0;
+            continue;
+        }
+        double xr[DENSE_MAX];
+        for (int i = 0; i < n; ++i) xr[i] = (i == c) ? 1.0 : 0.0;
+        for (int k = 0; k < n; ++k) { const double t = xr[k]; xr[k] = xr[piv[k]]; xr[piv[k]] = t; }
+        for (int k = 0; k < n; ++k)
+            for (int i = k + 1; i < n; ++i) xr[i] -= LU[i + k * n] * xr[k];
+        for (int k = n - 1; k >= 0; --k) {
+            xr[k] /= LU[k + k * n];
+            for (int i = 0; i < k; ++i) xr[i] -= LU[i + k * n] * xr[k];
+        }
+        for (int i = 0; i < n; ++i) x[i] = xr[i];
+    }
+    if (threadIdx.x == 0) add_flops(args.flops, F_LU, 2.0 * n * n * n);
+}
+
+// ------------------------------------------------------------------ scale_walk for dense leaves
+struct Sig1Args {
+    const long* doff;
+    const int* dm;
+    const int* dn;
+    int nleaf;
+    int B;
+    double* sig_out;  // [leaf][b]
+    FlopLedger* flops;
+};
+
+__global__ void __launch_bounds__(NT) k_sigma1_dense(Sig1Args args, BatchViews bv) {
+    extern __shared__ double smem[];
+    const int leaf = blockIdx.x, b = blockIdx.y;
+    const int m = args.dm[leaf], n = args.dn[leaf];
+    const double* D = bv.c[b].dense + args.doff[leaf];
+    const bool tall = m >= n;
+    const int rows = tall ? m : n, cols = tall ? n : m;
+    double* A = smem;
+    double* sig = A + (size_t)rows * cols;
+    for (int e = threadIdx.x; e < m * n; e += NT) {
+        const int i = e % m, j = e / m;
+        if (tall) A[e] = D[e];
+        else A[j + (size_t)i * n] = D[e];
+    }
+    __syncthreads();
+    jacobi_svd(A, rows, rows, cols, nullptr, 0, sig);
+    if (threadIdx.x < 32) {
+        double s = 0;
+        for (int j = threadIdx.x; j < cols; j += 32) s = fmax(s, sig[j]);
+        s = warp_max(s);
+        if (threadIdx.x == 0) {
+            args.sig_out[(size_t)leaf * args.B + b] = s;
+            double fsvd = 0, fqr = 0, fgemm = 0;
+            fl_svd(m, n, fsvd, fqr, fgemm);
+            add_flops(args.flops, F_SVD, fsvd);
+            add_flops(args.flops, F_GEQRF, fqr);
+            add_flops(args.flops, F_GEMM, fgemm);
+        }
+    }
+}
+
+// abs_cut[b] = 0.05 * eps * max(sig[.][b])  (recompress, hmatrix.cpp:655-662)
+__global__ void k_scale_reduce(const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,
+                               double* abs_cut) {
+    const int b = blockIdx.x;
+    double s = 0;
+    for (int i = threadIdx.x; i < nd; i += blockDim.x) s = fmax(s, sig_d[(size_t)i * B + b]);
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) s = fmax(s, sig_k[(size_t)i * B + b]);
+    s = warp_max(s);
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fmax(m, red[i]);
+        abs_cut[b] = m > 0 ? 0.05 * eps * m : -1.0;  // -1: scale 0, leave leaves untouched
+    }
+}
+
+// ------------------------------------------------------------------ solve: batched H-matvec
+struct MatvecArgs {
+    const SlabTask* tasks;
+    const ApplyLeaf* leaves;
+    int nrhs;
+    int dim;
+    FlopLedger* flops;
+};
+
+// y[slab] = base[slab] - (H x)[slab]  (base null: y = H x).  Leaves in DFS order.
+__global__ void __launch_bounds__(NT) k_matvec(MatvecArgs args, MatvecBatch mb) {
+    __shared__ double T[APPLY_TR * 16];
+    const SlabTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    const HView& H = mb.h[b];
+    const double* X = mb.x[b];
+    const double* base = mb.base[b];
+    double* Y = mb.y[b];
+    const int ld = args.dim;
+    const int nr = task.r1 - task.r0;
+    double fl = 0;
+    for (int c0 = 0; c0 < args.nrhs; c0 += 16) {
+        const int nc = min(16, args.nrhs - c0);
+        constexpr int PER = (APPLY_ROWS * 16) / NT;  // 4
+        double acc[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) acc[q] = 0.0;
+        for (int li = task.lbeg; li < task.lend; ++li) {
+            const ApplyLeaf L = args.leaves[li];
+            const int o0 = max(task.r0, L.out_off), o1 = min(task.r1, L.out_off + L.m);
+            if (o0 >= o1) continue;
+            if (L.kind == K_DENSE) {
+                const double* D = H.dense + L.doff;
+#pragma unroll
+                for (int q = 0; q < PER; ++q) {
+                    const int e = threadIdx.x + q * NT;
+                    const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
+                    const int row = task.r0 + i;
+                    if (i >= nr || c >= nc || row < o0 || row >= o1) continue;
+                    const int lr = row - L.out_off;
+                    const double* x = X + L.in_off + (size_t)(c0 + c) * ld;
+                    double a = 0;
+                    for (int j = 0; j < L.n; ++j) a = fma(D[lr + (size_t)j * L.m], x[j], a);
+                    acc[q] += a;
+                }
+                if (threadIdx.x == 0) fl += 2.0 * (o1 - o0) * L.n * nc;
+            } else {
+                const int rr = H.rank[L.id];
+                if (rr == 0) continue;
+                const double* Vk = H.V[L.id];
+                const double* Uk = H.U[L.id];
+                for (int t0 = 0; t0 < rr; t0 += APPLY_TR) {
+                    const int nt = min(APPLY_TR, rr - t0);
+                    __syncthreads();
+                    for (int e = threadIdx.x; e < nt * nc; e += NT) {
+                        const int t = e % nt, c = e / nt;
+                        const double* v = Vk + (size_t)(t0 + t) * L.n;
+                        const double* x = X + L.in_off + (size_t)(c0 + c) * ld;
+                        double a = 0;
+                        for (int j = 0; j < L.n; ++j) a = fma(v[j], x[j], a);
+                        T[t + c * APPLY_TR] = a;
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int q = 0; q < PER; ++q) {
+                        const int e = threadIdx.x + q * NT;
+                        const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
+                        const int row = task.r0 + i;
+                        if (i >= nr || c >= nc || row < o0 || row >= o1) continue;
+                        const int lr = row - L.out_off;
+                        double a = 0;
+                        for (int t = 0; t < nt; ++t) a = fma(Uk[lr + (size_t)(t0 + t) * L.m], T[t + c * APPLY_TR], a);
+                        acc[q] += a;
+                    }
+                }
+                if (threadIdx.x == 0) {
+                    fl += 2.0 * (o1 - o0) * rr * nc;
+                    if (L.out_off >= task.r0 && L.out_off < task.r1) fl += 2.0 * rr * L.n * nc;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int e = threadIdx.x + q * NT;
+            const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
+            if (i < nr && c < nc) {
+                const size_t o = (task.r0 + i) + (size_t)(c0 + c) * ld;
+                Y[o] = base ? base[o] - acc[q] : acc[q];
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) add_flops(args.flops, F_APPLY, fl);
+}
+
+// ------------------------------------------------------------------ misc kernels
+// gather: out[j][r][i] = in[r][j][perm[i]] (to tree order);  scatter: inverse.
+__global__ void k_permute_in(const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
+    const size_t total = (size_t)n * dim * nrhs;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int i = e % dim;
+        const size_t rest = e / dim;
+        const int r = rest % nrhs;
+        const int j = rest / nrhs;
+        out[e] = in[((size_t)r * n + j) * dim + perm[i]];
+    }
+}
+
+__global__ void k_permute_out(const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
+    const size_t total = (size_t)n * dim * nrhs;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int i = e % dim;
+        const size_t rest = e / dim;
+        const int r = rest % nrhs;
+        const int j = rest / nrhs;
+        out[((size_t)r * n + j) * dim + perm[i]] = in[e];
+    }
+}
+
+// zero a batch of views: dense slice (dsize doubles) and nk Rk leaves
+__global__ void k_zero_views(BatchViews bv, long dsize, int nk) {
+    const int b = blockIdx.y;
+    const HView& v = bv.c[b];
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < dsize; e += (long)gridDim.x * blockDim.x)
+        v.dense[e] = 0.0;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < nk; e += (long)gridDim.x * blockDim.x) {
+        v.rank[e] = 0;
+        v.U[e] = nullptr;
+        v.V[e] = nullptr;
+    }
+}
+
+// copy a batch of views a -> c (dense data + rank/pointer tables; U/V buffers shared)
+__global__ void k_copy_views(BatchViews bv, long dsize, int nk) {
+    const int b = blockIdx.y;
+    const HView& s = bv.a[b];
+    const HView& d = bv.c[b];
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < dsize; e += (long)gridDim.x * blockDim.x)
+        d.dense[e] = s.dense[e];
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < nk; e += (long)gridDim.x * blockDim.x) {
+        d.rank[e] = s.rank[e];
+        d.U[e] = s.U[e];
+        d.V[e] = s.V[e];
+    }
+}
+
+// lift: scatter permuted COO entries into dense leaves (one block of entries per plane)
+struct ScatterArgs {
+    const int* rows;      // original indices
+    const int* cols;
+    const double* vals;
+    const long* off;      // per batch element: entry range
+    const int* iperm;
+    const int* leaf_of;   // [rowleaf * nleafclusters + colleaf] -> dense id or -1-rk
+    const int* cl_index;  // tree position -> leaf cluster index
+    const int* cl_begin;  // leaf cluster -> first tree position
+    int ncl;
+    const long* d_off;    // dense id -> pool offset
+    const int* d_rows;    // dense id -> rows
+    const int* d_rb;
+    const int* d_cb;
+    int* rk_hits;         // count of entries landing in Rk leaves
+};
+
+__global__ void k_scatter(ScatterArgs a, BatchViews bv) {
+    const int b = blockIdx.y;
+    const long s = a.off[b], e = a.off[b + 1];
+    double* dense = bv.c[b].dense;
+    for (long i = s + blockIdx.x * (long)blockDim.x + threadIdx.x; i < e; i += (long)gridDim.x * blockDim.x) {
+        const int r = a.iperm[a.rows[i]], c = a.iperm[a.cols[i]];
+        const int lr = a.cl_index[r], lc = a.cl_index[c];
+        const int leaf = a.leaf_of[(size_t)lr * a.ncl + lc];
+        if (leaf >= 0) {
+            const int m = a.d_rows[leaf];
+            dense[a.d_off[leaf] + (r - a.d_rb[leaf]) + (size_t)(c - a.d_cb[leaf]) * m] += a.vals[i];
+        } else {
+            atomicAdd(a.rk_hits, 1);
+        }
+    }
+}
+
+__global__ void k_reset_counter(unsigned long long* ctr) { *ctr = 0; }
+
+// ------------------------------------------------------------------ launchers
+static int g_launches = 0;
+long launches_take() {
+    const long v = g_launches;
+    g_launches = 0;
+    return v;
+}
+
+static size_t trunc_smem() { return SMEM_TRUNC; }
+
+void setup_kernels() {
+    cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
+    cudaFuncSetAttribute(k_dd_product, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
+    cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_sigma1_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+}
+
+void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots, int B,
+                     double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
+                     Arena work, FlopLedger* flops, const BatchViews& bv) {
+    if (ntasks == 0 || B == 0) return;
+    TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, work, flops};
+    k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+    ++g_launches;
+}
+
+void launch_dd(cudaStream_t st, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps, Arena out_arena,
+               FlopLedger* flops, const BatchViews& bv) {
+    if (ntasks == 0 || B == 0) return;
+    DDArgs a{tasks, slots, B, eps, out_arena, flops};
+    k_dd_product<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+    ++g_launches;
+}
+
+void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slot* slots, int B, Arena arena,
+                        const BatchViews& bv) {
+    if (ntasks == 0 || B == 0) return;
+    AllocArgs a{tasks, ntasks, slots, B, arena};
+    const int total = ntasks * B;
+    k_alloc_apply<<<(total + 127) / 128, 128, 0, st>>>(a, bv);
+    ++g_launches;
+}
+
+void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
+                  Slot* slots, int B, FlopLedger* flops, const BatchViews& bv) {
+    if (ntasks == 0 || B == 0) return;
+    ApplyArgs a{tasks, leaves, slots, B, 0, x_ld, flops};
+    k_apply<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
+    ++g_launches;
+}
+
+void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Part* parts, const Slot* slots, int B,
+                    FlopLedger* flops, const BatchViews& bv) {
+    if (ntasks == 0 || B == 0) return;
+    DepArgs a{tasks, parts, slots, B, flops};
+    k_deposit<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
+    ++g_launches;
+}
+
+void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, unsigned long long call_id,
+               FlopLedger* flops, const BatchViews& bv, int maxm) {
+    if (ntasks == 0 || bv.count == 0) return;
+    LuArgs a{tasks, err, call_id, flops};
+    const size_t sm = (2 * (size_t)maxm * maxm + 2 * maxm) * sizeof(double);
+    k_lu_inverse<<<dim3(ntasks, bv.count), NT, sm, st>>>(a, bv);
+    ++g_launches;
+}
+
+void launch_sigma1_dense(cudaStream_t st, int nleaf, const long* doff, const int* dm, const int* dn, int B,
+                         double* sig_out, FlopLedger* flops, const BatchViews& bv, int maxm) {
+    if (nleaf == 0 || B == 0) return;
+    Sig1Args a{doff, dm, dn, nleaf, B, sig_out, flops};
+    const size_t sm = ((size_t)maxm * maxm + maxm) * sizeof(double);
+    k_sigma1_dense<<<dim3(nleaf, B), NT, sm, st>>>(a, bv);
+    ++g_launches;
+}
+
+void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,
+                         double* abs_cut) {
+    if (B == 0) return;
+    k_scale_reduce<<<B, 256, 0, st>>>(sig_d, nd, sig_k, nk, B, eps, abs_cut);
+    ++g_launches;
+}
+
+void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, int nrhs, int dim,
+                   FlopLedger* flops, const MatvecBatch& mb) {
+    if (ntasks == 0 || mb.count == 0) return;
+    MatvecArgs a{tasks, leaves, nrhs, dim, flops};
+    k_matvec<<<dim3(ntasks, mb.count), NT, 0, st>>>(a, mb);
+    ++g_launches;
+}
+
+void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
+    k_permute_in<<<1184, 256, 0, st>>>(in, out, perm, n, dim, nrhs);
+    ++g_launches;
+}
+
+void launch_permute_out(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
+    k_permute_out<<<1184, 256, 0, st>>>(in, out, perm, n, dim, nrhs);
+    ++g_launches;
+}
+
+void launch_zero_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk) {
+    if (bv.count == 0) return;
+    const long work = dsize > nk ? dsize : nk;
+    int gx = (int)((work + 255) / 256);
+    if (gx > 64) gx = 64;
+    if (gx < 1) gx = 1;
+    k_zero_views<<<dim3(gx, bv.count), 256, 0, st>>>(bv, dsize, nk);
+    ++g_launches;
+}
+
+void launch_copy_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk) {
+    if (bv.count == 0) return;
+    const long work = dsize > nk ? dsize : nk;
+    int gx = (int)((work + 255) / 256);
+    if (gx > 64) gx = 64;
+    if (gx < 1) gx = 1;
+    k_copy_views<<<dim3(gx, bv.count), 256, 0, st>>>(bv, dsize, nk);
+    ++g_launches;
+}
+
+void launch_scatter(cudaStream_t st, const ScatterLaunch& s, const BatchViews& bv) {
+    if (bv.count == 0) return;
+    ScatterArgs a{s.rows, s.cols, s.vals, s.off, s.iperm, s.leaf_of, s.cl_index, s.cl_begin, s.ncl,
+                  s.d_off, s.d_rows, s.d_rb, s.d_cb, s.rk_hits};
+    k_scatter<<<dim3(16, bv.count), 256, 0, st>>>(a, bv);
+    ++g_launches;
+}
+
+void launch_reset_counter(cudaStream_t st, unsigned long long* ctr) {
+    k_reset_counter<<<1, 1, 0, st>>>(ctr);
+    ++g_launches;
+}
+
+}  // namespace acrgpu

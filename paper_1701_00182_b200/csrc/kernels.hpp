@@ -1,0 +1,59 @@
+// Launch wrappers of the sm_100a kernels (kernels.cu); used by engine.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "tasks.hpp"
+
+namespace acrgpu {
+
+constexpr int DENSE_MAX = 64;               // dense route / dense leaf limit
+constexpr size_t SMEM_TRUNC = 100 * 1024;   // dynamic smem of k_truncate / k_dd_product
+
+struct ScatterLaunch {
+    const int* rows;
+    const int* cols;
+    const double* vals;
+    const long* off;
+    const int* iperm;
+    const int* leaf_of;
+    const int* cl_index;
+    const int* cl_begin;
+    int ncl;
+    const long* d_off;
+    const int* d_rows;
+    const int* d_rb;
+    const int* d_cb;
+    int* rk_hits;
+};
+
+void setup_kernels();
+long launches_take();
+
+void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots, int B,
+                     double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
+                     Arena work, FlopLedger* flops, const BatchViews& bv);
+void launch_dd(cudaStream_t st, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps, Arena out_arena,
+               FlopLedger* flops, const BatchViews& bv);
+void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slot* slots, int B, Arena arena,
+                        const BatchViews& bv);
+void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
+                  Slot* slots, int B, FlopLedger* flops, const BatchViews& bv);
+void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Part* parts, const Slot* slots, int B,
+                    FlopLedger* flops, const BatchViews& bv);
+void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, unsigned long long call_id,
+               FlopLedger* flops, const BatchViews& bv, int maxm);
+void launch_sigma1_dense(cudaStream_t st, int nleaf, const long* doff, const int* dm, const int* dn, int B,
+                         double* sig_out, FlopLedger* flops, const BatchViews& bv, int maxm);
+void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,
+                         double* abs_cut);
+void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, int nrhs, int dim,
+                   FlopLedger* flops, const MatvecBatch& mb);
+void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs);
+void launch_permute_out(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs);
+void launch_zero_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk);
+void launch_copy_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk);
+void launch_scatter(cudaStream_t st, const ScatterLaunch& s, const BatchViews& bv);
+void launch_reset_counter(cudaStream_t st, unsigned long long* ctr);
+
+}  // namespace acrgpu
