@@ -114,7 +114,8 @@ typedef struct acrgpu_timing {     /* device-event phase times of the last call 
     double solve_ms;
     double flops_nominal;          /* nominal FLOP count of the last factorization */
     double flops_svd, flops_qr, flops_gemm, flops_lu;
-    long kernel_launches;          /* kernels launched by the last call */
+    long factor_launches;          /* kernels launched by the factorization */
+    long solve_launches;           /* kernels launched by the last solve */
 } acrgpu_timing;
 
 typedef struct acrgpu_ctx acrgpu_ctx;
@@ -147,6 +148,10 @@ int acrgpu_timing_get(acrgpu_fact* f, acrgpu_timing* out);
  * Returns the leaf count (leaves written up to cap), or -code on error. */
 long acrgpu_structure(int dim, const double* coords, int leaf_size, double eta, int weak,
                       int* perm, int* leaves, long cap, acrgpu_error* err);
+
+/* Per-kernel device time accumulated while ACRGPU_PROFILE=1 is set in the environment:
+ * lines "kernel total_ms launches ctas".  Returns the length written (NUL-terminated). */
+long acrgpu_profile_report(char* buf, long cap, int reset);
 
 /* Library build identification (sm arch, version). */
 const char* acrgpu_version(void);

@@ -134,7 +134,8 @@ class _Level(C.Structure):
 class _Timing(C.Structure):
     _fields_ = [("lift_ms", C.c_double), ("factor_ms", C.c_double), ("solve_ms", C.c_double),
                 ("flops_nominal", C.c_double), ("flops_svd", C.c_double), ("flops_qr", C.c_double),
-                ("flops_gemm", C.c_double), ("flops_lu", C.c_double), ("kernel_launches", C.c_long)]
+                ("flops_gemm", C.c_double), ("flops_lu", C.c_double), ("factor_launches", C.c_long),
+                ("solve_launches", C.c_long)]
 
 
 SYMBOLS = {
@@ -149,6 +150,7 @@ SYMBOLS = {
     "acrgpu_level_info": (C.c_int, [C.c_void_p, C.POINTER(_Level), C.c_int]),
     "acrgpu_dinv_ranks": (C.c_long, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_long]),
     "acrgpu_timing_get": (C.c_int, [C.c_void_p, C.POINTER(_Timing)]),
+    "acrgpu_profile_report": (C.c_long, [C.c_char_p, C.c_long, C.c_int]),
     "acrgpu_structure": (C.c_long, [C.c_int, C.POINTER(C.c_double), C.c_int, C.c_double, C.c_int,
                                      C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_long, C.POINTER(_Err)]),
 }
@@ -330,6 +332,14 @@ def acr_factor(system: problems.System, config: AcrConfig | None = None, ctx: Co
 
 def acr_solve(fact: AcrFactorization, f):
     return fact.solve(f)
+
+
+def profile_report(reset: bool = True) -> str:
+    """Per-kernel device totals collected when ACRGPU_PROFILE=1 (name -> ms, launches, CTAs)."""
+    n = lib().acrgpu_profile_report(None, 0, 0)
+    buf = C.create_string_buffer(n + 1)
+    lib().acrgpu_profile_report(buf, n + 1, 1 if reset else 0)
+    return buf.value.decode()
 
 
 def structure(coords, leaf_size=32, eta=2.0, weak=False):

@@ -164,16 +164,28 @@ struct View {  // (store, sub-node)
 };
 
 // ------------------------------------------------------------------ compiled plans
+// Task lists split by block size class: blocks <= 32 and <= 64 run the
+// register-resident Jacobi kernels (2*NC threads), larger ones the QR route.
+template <class T>
+struct Classed {
+    T* p[3] = {nullptr, nullptr, nullptr};
+    int n[3] = {0, 0, 0};
+};
+static int size_class(int m, int n) {
+    const int x = m > n ? m : n;
+    return x <= 32 ? 0 : (x <= 64 ? 1 : 2);
+}
+
 struct Plan {
     int nprod = 0;
-    int nalloc = 0, napply = 0, ndd = 0, nflush = 0, ndep = 0;
+    int nalloc = 0, napply = 0, ndep = 0;
     AllocTask* allocs = nullptr;
     ApplyTask* applies = nullptr;
     ApplyLeaf* aleaves = nullptr;
     int* x_ld = nullptr;
-    DDTask* dds = nullptr;
-    std::vector<std::pair<TruncTask*, int>> bb;  // phases
-    TruncTask* flush = nullptr;
+    Classed<DDTask> dds;
+    std::vector<Classed<TruncTask>> bb;  // phases
+    Classed<TruncTask> flush;
     DepTask* deps = nullptr;
     Part* parts = nullptr;
 };
@@ -194,6 +206,8 @@ struct Engine {
     int* d_dn = nullptr;
     TruncTask* leaf_tasks = nullptr;  // one per Rk leaf (recompress)
     Part* leaf_parts = nullptr;
+    Classed<TruncTask> leaf_cls;      // the same, split by size class
+    int leaf_cls_off[3] = {0, 0, 0};
     SlabTask* slabs = nullptr;        // matvec slabs of the root
     ApplyLeaf* slab_leaves = nullptr;
     int nslabs = 0;
@@ -211,6 +225,28 @@ struct Engine {
         return keep(upload(v, ctx->st));
     }
     cudaStream_t st() const { return ctx->st; }
+
+    template <class T>
+    Classed<T> up_classed(const std::vector<T>& v) {
+        Classed<T> c;
+        std::vector<T> parts[3];
+        for (const T& t : v) parts[size_class(t.m, t.n)].push_back(t);
+        for (int k = 0; k < 3; ++k) {
+            c.n[k] = (int)parts[k].size();
+            if (c.n[k]) c.p[k] = up(parts[k]);
+        }
+        return c;
+    }
+
+    void run_trunc(const Classed<TruncTask>& tl, const Part* parts, Slot* slots, int nb, double eps,
+                   const double* abs_cut, double* sig_out, bool values_only, Arena out, const BatchViews& bv) {
+        if (tl.n[0]) launch_trunc_small(st(), 32, tl.n[0], tl.p[0], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
+                                        ctx->flops, bv);
+        if (tl.n[1]) launch_trunc_small(st(), 64, tl.n[1], tl.p[1], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
+                                        ctx->flops, bv);
+        if (tl.n[2]) launch_truncate(st(), tl.n[2], tl.p[2], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
+                                     ctx->trans, ctx->flops, bv);
+    }
 
     // -------------------------------------------------------------- storage
     StoreP new_store(int node) {
@@ -545,16 +581,14 @@ struct Engine {
         P->nprod = pb.nprod;
         P->nalloc = (int)pb.allocs.size();
         P->napply = (int)pb.applies.size();
-        P->ndd = (int)pb.dds.size();
-        P->nflush = (int)pb.flush.size();
         P->ndep = (int)pb.deps.size();
         P->allocs = up(pb.allocs);
         P->applies = up(pb.applies);
         P->aleaves = up(pb.aleaves);
         P->x_ld = up(pb.x_ld);
-        P->dds = up(pb.dds);
-        for (auto& ph : pb.bb) P->bb.push_back({up(ph), (int)ph.size()});
-        P->flush = up(pb.flush);
+        P->dds = up_classed(pb.dds);
+        for (auto& ph : pb.bb) P->bb.push_back(up_classed(ph));
+        P->flush = up_classed(pb.flush);
         P->deps = up(pb.deps);
         P->parts = up(pb.parts);
         Plan* raw = P.get();
@@ -581,13 +615,12 @@ struct Engine {
             launch_reset_counter(st(), ctx->trans.ctr);
             launch_alloc_apply(st(), P->nalloc, P->allocs, slots, nb, ctx->trans, bv);
             launch_apply(st(), P->napply, P->applies, P->aleaves, P->x_ld, slots, nb, ctx->flops, bv);
-            launch_dd(st(), P->ndd, P->dds, slots, nb, eps, ctx->trans, ctx->flops, bv);
-            for (auto& [tasks, n] : P->bb)
-                launch_truncate(st(), n, tasks, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->trans,
-                                ctx->trans, ctx->flops, bv);
+            if (P->dds.n[0]) launch_dd_small(st(), 32, P->dds.n[0], P->dds.p[0], slots, nb, eps, ctx->trans, ctx->flops, bv);
+            if (P->dds.n[1]) launch_dd_small(st(), 64, P->dds.n[1], P->dds.p[1], slots, nb, eps, ctx->trans, ctx->flops, bv);
+            if (P->dds.n[2]) throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64"};
+            for (auto& ph : P->bb) run_trunc(ph, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->trans, bv);
             launch_deposit(st(), P->ndep, P->deps, P->parts, slots, nb, ctx->flops, bv);
-            launch_truncate(st(), P->nflush, P->flush, P->parts, slots, nb, eps, nullptr, nullptr, false,
-                            ctx->persist, ctx->trans, ctx->flops, bv);
+            run_trunc(P->flush, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->persist, bv);
         }
     }
 
@@ -669,15 +702,21 @@ struct Engine {
             double* sig_d = sc;
             double* sig_k = sc + (size_t)nd * nb;
             double* cut = sig_k + (size_t)nk * nb;
-            launch_sigma1_dense(st(), nd, d_doff, d_dm, d_dn, nb, sig_d, ctx->flops, bv, S.max_dense_dim);
+            launch_sigma1_small(st(), S.max_dense_dim <= 32 ? 32 : 64, nd, d_doff, d_dm, d_dn, nb, sig_d, ctx->flops, bv);
             Slot* slots = ctx->get_slots(1);
+            // sigma_1 per Rk leaf (values only); per-class task lists index sig_k by class offset
             launch_reset_counter(st(), ctx->trans.ctr);
-            launch_truncate(st(), nk, leaf_tasks, leaf_parts, slots, nb, 0.0, nullptr, sig_k, true, ctx->persist,
-                            ctx->trans, ctx->flops, bv);
+            for (int c = 0; c < 3; ++c)
+                if (leaf_cls.n[c]) {
+                    Classed<TruncTask> one;
+                    one.p[c] = leaf_cls.p[c];
+                    one.n[c] = leaf_cls.n[c];
+                    run_trunc(one, leaf_parts, slots, nb, 0.0, nullptr, sig_k + (size_t)leaf_cls_off[c] * nb, true,
+                              ctx->persist, bv);
+                }
             launch_scale_reduce(st(), sig_d, nd, sig_k, nk, nb, cfg.eps, cut);
             launch_reset_counter(st(), ctx->trans.ctr);
-            launch_truncate(st(), nk, leaf_tasks, leaf_parts, slots, nb, 0.0, cut, nullptr, false, ctx->persist,
-                            ctx->trans, ctx->flops, bv);
+            run_trunc(leaf_cls, leaf_parts, slots, nb, 0.0, cut, nullptr, false, ctx->persist, bv);
         }
     }
 
@@ -718,6 +757,10 @@ struct Engine {
         }
         leaf_tasks = up(lt);
         leaf_parts = up(lp);
+        leaf_cls = up_classed(lt);
+        leaf_cls_off[0] = 0;
+        leaf_cls_off[1] = leaf_cls.n[0];
+        leaf_cls_off[2] = leaf_cls.n[0] + leaf_cls.n[1];
         // matvec slabs over leaf clusters (non-transposed apply of the root)
         std::vector<int> lv;
         subtree_leaves(0, lv);
@@ -1145,7 +1188,7 @@ static void do_factor(acrgpu_fact* F, const acrgpu_system* sys) {
     F->timing.flops_svd = fl.f[F_SVD];
     F->timing.flops_lu = fl.f[F_LU];
     F->timing.flops_nominal = fl.f[F_GEMM] + fl.f[F_GEQRF] + fl.f[F_ORGQR] + fl.f[F_SVD] + fl.f[F_LU];
-    F->timing.kernel_launches = launches_take();
+    F->timing.factor_launches = launches_take();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
@@ -1355,6 +1398,17 @@ extern "C" {
 
 const char* acrgpu_version(void) { return "acrgpu 0.1 sm_100a fp64"; }
 
+long acrgpu_profile_report(char* buf, long cap, int reset) {
+    const std::string r = prof_report(reset != 0);
+    if (buf && cap > 0) {
+        const long n = std::min<long>(cap - 1, (long)r.size());
+        std::memcpy(buf, r.data(), n);
+        buf[n] = 0;
+        return n;
+    }
+    return (long)r.size();
+}
+
 int acrgpu_ctx_create(int device, acrgpu_ctx** out, acrgpu_error* err) {
     ABI_TRY({
         auto* c = new acrgpu_ctx;
@@ -1435,7 +1489,7 @@ int acrgpu_solve_device(acrgpu_fact* f, int nrhs, const double* f_dev, double* u
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, e0, e1));
         f->timing.solve_ms = ms;
-        f->timing.kernel_launches = launches_take();
+        f->timing.solve_launches = launches_take();
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         return 0;

@@ -18,9 +18,17 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
 
 #include "kernels.hpp"
 #include "structure.hpp"
+#include "svd_small.cuh"
+#include "svd_rrqr32.cuh"
+#include "svd_cta.cuh"
 
 namespace acrgpu {
 
@@ -29,17 +37,6 @@ constexpr int NW = NT / 32;
 constexpr double DEPS = 2.2204460492503131e-16;
 
 // ------------------------------------------------------------------ helpers
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
 
 // block-wide sum (all threads get the result); red: >= NW doubles of smem
 __device__ double block_sum(double v, double* red) {
@@ -96,6 +93,25 @@ __device__ void jacobi_svd(double* A, int lda, int rows, int cols, double* V, in
             V[i + (size_t)j * ldv] = (i == j) ? 1.0 : 0.0;
         }
     __syncthreads();
+    __shared__ double sh_fro;
+    {
+        double f = 0;
+        for (size_t e = threadIdx.x; e < (size_t)rows * cols; e += NT) {
+            const double x = A[(e % rows) + (e / rows) * (size_t)lda];
+            f = fma(x, x, f);
+        }
+        __shared__ double redf[NW];
+        f = warp_sum(f);
+        if (lane == 0) redf[warp] = f;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0;
+            for (int i = 0; i < NW; ++i) t += redf[i];
+            sh_fro = t;
+        }
+        __syncthreads();
+    }
+    const double zthr = sh_fro * (16.0 * DEPS * DEPS);
     if (cols > 1) {
         const int P = cols + (cols & 1);
         const int npairs = P / 2, rounds = P - 1;
@@ -126,7 +142,7 @@ __device__ void jacobi_svd(double* A, int lda, int rows, int cols, double* V, in
                     al = warp_sum(al);
                     be = warp_sum(be);
                     ga = warp_sum(ga);
-                    if (!(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+                    if (!(fabs(ga) > tol * sqrt(al) * sqrt(be)) || !(al > zthr) || !(be > zthr)) continue;
                     const double zeta = (be - al) / (2.0 * ga);
                     double t;
                     if (fabs(zeta) > 1e150) t = 0.5 / zeta;
@@ -367,6 +383,23 @@ __device__ int svd_truncate_dense(double* M, int m, int n, double eps, double ab
 // without the two QRs.  QR route (larger blocks): concatenate into an arena
 // workspace, Householder QR both factors, SVD the ku x kv core, rebuild
 // U' = Qu Us Sigma, V' = Qv Vs by applying the reflectors.
+// Carve an engine workspace for blocks up to p x p out of `base`.
+__device__ __forceinline__ CtaSvdWork cta_smem_work(double* base, int p) {
+    CtaSvdWork w;
+    w.A = base;
+    w.lda = p;
+    w.W = base + (size_t)p * p;
+    w.ldw = p;
+    w.J = w.W + (size_t)p * p;
+    w.ldj = p;
+    w.tau = w.J + (size_t)p * p;
+    w.nrm = w.tau + p;
+    w.sig = w.nrm + p;
+    w.perm = (int*)(w.sig + p);
+    w.order = w.perm + p;
+    return w;
+}
+
 struct TruncArgs {
     const TruncTask* tasks;
     const Part* parts;
@@ -392,6 +425,7 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
     const HView& C = bv.c[b];
     const int m = task.m, n = task.n;
     const double abs_cut = args.abs_cut ? args.abs_cut[b] : 0.0;
+    if (abs_cut < 0) return;  // recompress with zero matrix scale: leave untouched
 
     // total concatenated rank K
     if (threadIdx.x == 0) {
@@ -426,13 +460,15 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
 
     const int ku = m < K ? m : K, kv = n < K ? n : K;
     double fsvd = 0, fqr = 0, fgemm = 0;
+    __shared__ int sh_rp;
+    __shared__ double sh_smax;
+    __shared__ double* sh_out;
 
     if (m <= DENSE_MAX && n <= DENSE_MAX) {
-        // ---------------- dense route
-        double* M = smem;                                   // m*n
-        double* work = M + (size_t)m * n;                   // up to 2*DENSE_MAX^2
-        double* sig = work + 2 * DENSE_MAX * DENSE_MAX;     // DENSE_MAX
-        int* order = (int*)(sig + DENSE_MAX);
+        // ---------------- dense route: M = sum alpha U V^T in shared memory, rank-revealing SVD
+        CtaSvdWork w = cta_smem_work(smem, DENSE_MAX);
+        double* M = w.A;
+        w.lda = m;
         for (int e = threadIdx.x; e < m * n; e += NT) M[e] = 0.0;
         __syncthreads();
         for (int pi = task.pbeg; pi < task.pend; ++pi) {
@@ -449,23 +485,26 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
             }
             __syncthreads();
         }
-        double smax = 0;
-        double* out = nullptr;
-        const int r = svd_truncate_dense(M, m, n, args.eps, abs_cut, work, sig, order, args.out_arena, &out, &smax,
-                                         args.values_only != 0);
-        write_out(r, out, out ? out + (size_t)m * r : nullptr);
-        if (args.values_only && threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
-        // nominal (reference-algorithm) flops
+        int rp;
+        double smax;
+        const int r = cta_trunc_svd<NT>(w, m, n, args.eps, abs_cut, args.values_only != 0, &rp, &smax);
+        if (args.values_only) {
+            if (threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
+        } else {
+            if (threadIdx.x == 0) sh_out = r > 0 ? arena_alloc(args.out_arena, (unsigned long long)(m + n) * r) : nullptr;
+            __syncthreads();
+            double* out = sh_out;
+            if (out) cta_trunc_write<NT>(w, m, n, rp, r, out, m, out + (size_t)m * r, n);
+            write_out(out ? r : 0, out, out ? out + (size_t)m * r : nullptr);
+        }
         if (threadIdx.x == 0) {
-            if (args.values_only) {
-                fqr += fl_geqrf(m, K) + fl_geqrf(n, K);
-                fgemm += fl_gemm(ku, kv, K);
-                fl_svd(ku, kv, fsvd, fqr, fgemm);
-            } else {
-                fqr += fl_geqrf(m, K) + fl_orgqr(m, ku) + fl_geqrf(n, K) + fl_orgqr(n, kv);
-                fgemm += fl_gemm(ku, kv, K) + fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
-                fl_svd(ku, kv, fsvd, fqr, fgemm);
+            fqr += fl_geqrf(m, K) + fl_geqrf(n, K);
+            fgemm += fl_gemm(ku, kv, K);
+            if (!args.values_only) {
+                fqr += fl_orgqr(m, ku) + fl_orgqr(n, kv);
+                fgemm += fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
             }
+            fl_svd(ku, kv, fsvd, fqr, fgemm);
             add_flops(args.flops, F_SVD, fsvd);
             add_flops(args.flops, F_GEQRF, fqr);
             add_flops(args.flops, F_GEMM, fgemm);
@@ -474,31 +513,22 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
     }
 
     // ---------------- QR route
-    // workspace: Uc (m x K) | Vc (n x K) | tau_u (K) | tau_v (K) | [core + V if too big for smem]
-    const int pmax = ku > kv ? ku : kv, pmin = ku < kv ? ku : kv;
-    const bool core_in_smem = (size_t)pmax * pmin + (size_t)pmin * pmin + 2 * (size_t)pmax <= (size_t)SMEM_TRUNC / 8 - 64;
+    // workspace: Uc (m x K) | Vc (n x K) | tau_u (K) | tau_v (K) | [core engine work if too big for smem]
+    const int pmax = ku > kv ? ku : kv;
+    const bool core_in_smem = pmax <= DENSE_MAX;
     if (threadIdx.x == 0) {
         unsigned long long need = (unsigned long long)(m + n) * K + 2ull * K + 32;
-        if (!core_in_smem) need += (unsigned long long)pmax * pmin + (unsigned long long)pmin * pmin + 2ull * pmax;
+        if (!core_in_smem) need += 3ull * pmax * pmax + 6ull * pmax + 64;
         sh_ws = arena_alloc(args.work, need);
     }
     __syncthreads();
     double* ws = sh_ws;
-    if (ws == nullptr) {  // arena exhausted: flag already raised; leave the target unchanged
-        return;
-    }
+    if (ws == nullptr) return;  // arena exhausted: flag raised, target left unchanged
     double* Uc = ws;
     double* Vc = Uc + (size_t)m * K;
     double* tau_u = Vc + (size_t)n * K;
     double* tau_v = tau_u + K;
-    double* core;
-    if (core_in_smem) core = smem;
-    else core = tau_v + K + 32;
-    double* Vsv = core + (size_t)pmax * pmin;
-    double* sig = Vsv + (size_t)pmin * pmin;
-    int* order = (int*)(sig + pmax);
-
-    // concatenate (zero-fill, then place each part)
+    CtaSvdWork w = core_in_smem ? cta_smem_work(smem, DENSE_MAX) : cta_smem_work(tau_v + K + 32, pmax);
     for (size_t e = threadIdx.x; e < (size_t)(m + n) * K; e += NT) ws[e] = 0.0;
     __syncthreads();
     {
@@ -521,59 +551,44 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
     __syncthreads();
     householder_qr(Uc, m, m, K, tau_u, red);
     householder_qr(Vc, n, n, K, tau_v, red);
-    // core = Ru Rv^T (ku x kv); stored as A (rows >= cols) for the one-sided SVD
-    const bool tall = ku >= kv;
-    const int rows = tall ? ku : kv, cols = tall ? kv : ku;
+    // core = Ru Rv^T (ku x kv)
+    double* core = w.A;
+    w.lda = ku;
     for (int e = threadIdx.x; e < ku * kv; e += NT) {
         const int i = e % ku, j = e / ku;
         double acc = 0;
         for (int t = (i > j ? i : j); t < K; ++t) acc = fma(Uc[i + (size_t)t * m], Vc[j + (size_t)t * n], acc);
-        if (tall) core[i + (size_t)j * rows] = acc;
-        else core[j + (size_t)i * rows] = acc;
+        core[e] = acc;
     }
     __syncthreads();
-    jacobi_svd(core, rows, rows, cols, args.values_only ? nullptr : Vsv, cols, sig);
-    sort_desc(sig, cols, order);
-    __shared__ int sh_r;
-    __shared__ double* sh_out;
-    if (threadIdx.x == 0) {
-        sh_r = rank_of(sig, order, cols, args.eps, abs_cut);
-        sh_out = nullptr;
-        if (args.values_only) args.sig_out[(size_t)blockIdx.x * B + b] = sig[order[0]];
-        else if (sh_r > 0) sh_out = arena_alloc(args.out_arena, (unsigned long long)(m + n) * sh_r);
-    }
-    __syncthreads();
-    const int r = sh_r;
-    if (!args.values_only) {
+    int rp;
+    double smax;
+    const int r = cta_trunc_svd<NT>(w, ku, kv, args.eps, abs_cut, args.values_only != 0, &rp, &smax);
+    if (args.values_only) {
+        if (threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
+    } else {
+        if (threadIdx.x == 0) sh_out = r > 0 ? arena_alloc(args.out_arena, (unsigned long long)(m + n) * r) : nullptr;
+        __syncthreads();
         double* out = sh_out;
-        if (r > 0 && out != nullptr) {
+        if (out) {
             double* Uo = out;
             double* Vo = out + (size_t)m * r;
-            // Us Sigma (ku x r) and Vs (kv x r) from the core SVD
             for (int e = threadIdx.x; e < m * r; e += NT) Uo[e] = 0.0;
             for (int e = threadIdx.x; e < n * r; e += NT) Vo[e] = 0.0;
             __syncthreads();
-            for (int t = 0; t < r; ++t) {
-                const int j = order[t];
-                if (tall) {  // core = Ucore Sigma Vcore^T: A col j = sigma u_j, Vsv col j = v_j
-                    for (int i = threadIdx.x; i < ku; i += NT) Uo[i + (size_t)t * m] = core[i + (size_t)j * rows];
-                    for (int i = threadIdx.x; i < kv; i += NT) Vo[i + (size_t)t * n] = Vsv[i + (size_t)j * cols];
-                } else {  // core^T J = W: U = J Sigma, V = W Sigma^{-1}
-                    for (int i = threadIdx.x; i < ku; i += NT) Uo[i + (size_t)t * m] = Vsv[i + (size_t)j * cols] * sig[j];
-                    for (int i = threadIdx.x; i < kv; i += NT) Vo[i + (size_t)t * n] = core[i + (size_t)j * rows] / sig[j];
-                }
-            }
-            __syncthreads();
+            cta_trunc_write<NT>(w, ku, kv, rp, r, Uo, m, Vo, n);
             apply_q(Uc, m, m, ku, tau_u, Uo, m, r);
             apply_q(Vc, n, n, kv, tau_v, Vo, n, r);
         }
-        write_out(r, out, out ? out + (size_t)m * r : nullptr);
+        write_out(out ? r : 0, out, out ? out + (size_t)m * r : nullptr);
     }
     if (threadIdx.x == 0) {
         fqr += fl_geqrf(m, K) + fl_geqrf(n, K);
-        if (!args.values_only) fqr += fl_orgqr(m, ku) + fl_orgqr(n, kv);
         fgemm += fl_gemm(ku, kv, K);
-        if (!args.values_only) fgemm += fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
+        if (!args.values_only) {
+            fqr += fl_orgqr(m, ku) + fl_orgqr(n, kv);
+            fgemm += fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
+        }
         fl_svd(ku, kv, fsvd, fqr, fgemm);
         add_flops(args.flops, F_SVD, fsvd);
         add_flops(args.flops, F_GEQRF, fqr);
@@ -593,14 +608,18 @@ struct DDArgs {
 
 __global__ void __launch_bounds__(NT) k_dd_product(DDArgs args, BatchViews bv) {
     extern __shared__ double smem[];
+    __shared__ double* sh_out;
     const DDTask task = args.tasks[blockIdx.x];
     const int b = blockIdx.y;
     const int m = task.m, k = task.k, n = task.n;
     const double* Ad = bv.a[b].dense + task.da;
     const double* Bd = bv.b[b].dense + task.db;
-    double* M = smem;
-    double* As = M + (size_t)m * n;
-    double* Bs = As + (size_t)m * k;
+    CtaSvdWork w = cta_smem_work(smem, DENSE_MAX);
+    double* M = w.A;
+    w.lda = m;
+    // operands staged in the (not yet used) W / J areas
+    double* As = w.W;
+    double* Bs = w.J;
     for (int e = threadIdx.x; e < m * k; e += NT) As[e] = Ad[e];
     for (int e = threadIdx.x; e < k * n; e += NT) Bs[e] = Bd[e];
     __syncthreads();
@@ -611,14 +630,16 @@ __global__ void __launch_bounds__(NT) k_dd_product(DDArgs args, BatchViews bv) {
         M[e] = acc;
     }
     __syncthreads();
-    double* work = As;  // reuse operand space (>= 2*DENSE_MAX^2 reserved by the launcher)
-    double* sig = work + 2 * DENSE_MAX * DENSE_MAX;
-    int* order = (int*)(sig + DENSE_MAX);
-    double* out = nullptr;
-    const int r = svd_truncate_dense(M, m, n, args.eps, 0.0, work, sig, order, args.out_arena, &out, nullptr, false);
+    int rp;
+    double smax;
+    const int r = cta_trunc_svd<NT>(w, m, n, args.eps, 0.0, false, &rp, &smax);
+    if (threadIdx.x == 0) sh_out = r > 0 ? arena_alloc(args.out_arena, (unsigned long long)(m + n) * r) : nullptr;
+    __syncthreads();
+    double* out = sh_out;
+    if (out) cta_trunc_write<NT>(w, m, n, rp, r, out, m, out + (size_t)m * r, n);
     if (threadIdx.x == 0) {
         Slot& s = args.slots[(size_t)task.prod * args.B + b];
-        s.rank = r;
+        s.rank = out ? r : 0;
         s.U = out;
         s.V = out ? out + (size_t)m * r : nullptr;
         s.ldu = m;
@@ -1013,29 +1034,20 @@ __global__ void __launch_bounds__(NT) k_sigma1_dense(Sig1Args args, BatchViews b
     const int leaf = blockIdx.x, b = blockIdx.y;
     const int m = args.dm[leaf], n = args.dn[leaf];
     const double* D = bv.c[b].dense + args.doff[leaf];
-    const bool tall = m >= n;
-    const int rows = tall ? m : n, cols = tall ? n : m;
-    double* A = smem;
-    double* sig = A + (size_t)rows * cols;
-    for (int e = threadIdx.x; e < m * n; e += NT) {
-        const int i = e % m, j = e / m;
-        if (tall) A[e] = D[e];
-        else A[j + (size_t)i * n] = D[e];
-    }
+    CtaSvdWork w = cta_smem_work(smem, DENSE_MAX);
+    w.lda = m;
+    for (int e = threadIdx.x; e < m * n; e += NT) w.A[e] = D[e];
     __syncthreads();
-    jacobi_svd(A, rows, rows, cols, nullptr, 0, sig);
-    if (threadIdx.x < 32) {
-        double s = 0;
-        for (int j = threadIdx.x; j < cols; j += 32) s = fmax(s, sig[j]);
-        s = warp_max(s);
-        if (threadIdx.x == 0) {
-            args.sig_out[(size_t)leaf * args.B + b] = s;
-            double fsvd = 0, fqr = 0, fgemm = 0;
-            fl_svd(m, n, fsvd, fqr, fgemm);
-            add_flops(args.flops, F_SVD, fsvd);
-            add_flops(args.flops, F_GEQRF, fqr);
-            add_flops(args.flops, F_GEMM, fgemm);
-        }
+    int rp;
+    double smax;
+    cta_trunc_svd<NT>(w, m, n, 0.0, 0.0, true, &rp, &smax);
+    if (threadIdx.x == 0) {
+        args.sig_out[(size_t)leaf * args.B + b] = smax;
+        double fsvd = 0, fqr = 0, fgemm = 0;
+        fl_svd(m, n, fsvd, fqr, fgemm);
+        add_flops(args.flops, F_SVD, fsvd);
+        add_flops(args.flops, F_GEQRF, fqr);
+        add_flops(args.flops, F_GEMM, fgemm);
     }
 }
 
@@ -1240,12 +1252,269 @@ __global__ void k_scatter(ScatterArgs a, BatchViews bv) {
 
 __global__ void k_reset_counter(unsigned long long* ctr) { *ctr = 0; }
 
+// ------------------------------------------------------------------ register-resident small-block kernels
+// Shared task plumbing: part ranks, output slot writes, nominal flops.
+struct SmallTaskIO {
+    __device__ static int total_rank(const TruncArgs& args, const TruncTask& task, int b, const HView& C) {
+        int K = 0;
+        for (int pi = task.pbeg; pi < task.pend; ++pi) K += resolve_part(args.parts[pi], args.slots, b, args.B, C).rank;
+        return K;
+    }
+    __device__ static void write_out(const TruncArgs& args, const TruncTask& task, int b, const HView& C, int r,
+                                     double* U, double* V) {
+        if (args.values_only) return;
+        if (task.out_kind == 0) {
+            Slot& s = args.slots[(size_t)task.out_id * args.B + b];
+            s.rank = r;
+            s.U = U;
+            s.V = V;
+            s.ldu = task.m;
+            s.ldv = task.n;
+        } else {
+            C.rank[task.out_id] = r;
+            C.U[task.out_id] = U;
+            C.V[task.out_id] = V;
+        }
+    }
+    __device__ static void flops(const TruncArgs& args, int m, int n, int K, int r) {
+        const int ku = m < K ? m : K, kv = n < K ? n : K;
+        double fsvd = 0, fqr, fgemm;
+        if (args.values_only) {
+            fqr = fl_geqrf(m, K) + fl_geqrf(n, K);
+            fgemm = fl_gemm(ku, kv, K);
+        } else {
+            fqr = fl_geqrf(m, K) + fl_orgqr(m, ku) + fl_geqrf(n, K) + fl_orgqr(n, kv);
+            fgemm = fl_gemm(ku, kv, K) + fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
+        }
+        fl_svd(ku, kv, fsvd, fqr, fgemm);
+        add_flops(args.flops, F_SVD, fsvd);
+        add_flops(args.flops, F_GEQRF, fqr);
+        add_flops(args.flops, F_GEMM, fgemm);
+    }
+    __device__ static RowPart row_part(const Part& p, const PartRes& pr, bool tall) {
+        RowPart rp;
+        rp.k = pr.rank;
+        rp.upper = 0;
+        rp.alpha = p.alpha;
+        if (tall) {
+            rp.P = pr.U; rp.ps = 1; rp.pt = pr.ldu; rp.pd = p.u_dst; rp.pr = p.rows_u;
+            rp.Q = pr.V; rp.qs = 1; rp.qt = pr.ldv; rp.qd = p.v_dst; rp.qr = p.rows_v;
+        } else {
+            rp.P = pr.V; rp.ps = 1; rp.pt = pr.ldv; rp.pd = p.v_dst; rp.pr = p.rows_v;
+            rp.Q = pr.U; rp.qs = 1; rp.qt = pr.ldu; rp.qd = p.u_dst; rp.qr = p.rows_u;
+        }
+        return rp;
+    }
+    __device__ static RowPart dd_part(const double* Ad, const double* Bd, int m, int k, int n, bool tall) {
+        RowPart rp;
+        rp.k = k;
+        rp.upper = 0;
+        rp.alpha = 1.0;
+        if (tall) {  // A[i,j] = sum_t Ad(i,t) Bd(t,j)
+            rp.P = Ad; rp.ps = 1; rp.pt = m; rp.pd = 0; rp.pr = m;
+            rp.Q = Bd; rp.qs = k; rp.qt = 1; rp.qd = 0; rp.qr = n;
+        } else {     // A = M^T: A[i,j] = sum_t Bd(t,i) Ad(j,t)
+            rp.P = Bd; rp.ps = k; rp.pt = 1; rp.pd = 0; rp.pr = n;
+            rp.Q = Ad; rp.qs = 1; rp.qt = m; rp.qd = 0; rp.qr = m;
+        }
+        return rp;
+    }
+};
+
+// ---- blocks <= 32 x 32: one warp per task, four tasks per CTA
+constexpr int W32_TC = 16;
+
+// mode 0: truncation task list (TruncArgs); mode 1: dense*dense products (DDArgs).
+// Two warps per CTA, one task per warp (rank-revealing QR + Jacobi, svd_rrqr32.cuh).
+template <int MODE>
+__global__ void __launch_bounds__(64) k_small32(TruncArgs targs, DDArgs dargs, int ntasks, BatchViews bv) {
+    __shared__ Warp32Smem smem[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ti = blockIdx.x * 2 + warp;
+    if (ti >= ntasks) return;
+    Warp32Smem& sm = smem[warp];
+    const int b = blockIdx.y;
+    const HView& C = bv.c[b];
+    int m, n, K;
+    double eps, abs_cut = 0.0;
+    bool values_only = false;
+    TruncTask task{};
+    DDTask dt{};
+    if (MODE == 0) {
+        task = targs.tasks[ti];
+        m = task.m;
+        n = task.n;
+        eps = targs.eps;
+        values_only = targs.values_only != 0;
+        if (targs.abs_cut) {
+            abs_cut = targs.abs_cut[b];
+            if (abs_cut < 0) return;
+        }
+        K = 0;
+        if (lane == 0) K = SmallTaskIO::total_rank(targs, task, b, C);
+        K = __shfl_sync(0xffffffffu, K, 0);
+        if (K == 0) {
+            if (lane == 0) {
+                SmallTaskIO::write_out(targs, task, b, C, 0, nullptr, nullptr);
+                if (values_only) targs.sig_out[(size_t)ti * targs.B + b] = 0.0;
+            }
+            return;
+        }
+    } else {
+        dt = dargs.tasks[ti];
+        m = dt.m;
+        n = dt.n;
+        K = dt.k;
+        eps = dargs.eps;
+    }
+    double a[32], v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = 0.0;
+    if (MODE == 0) {
+        for (int pi = task.pbeg; pi < task.pend; ++pi) {
+            const Part p = targs.parts[pi];
+            const PartRes pr = resolve_part(p, targs.slots, b, targs.B, C);
+            if (pr.rank == 0) continue;
+            warp_accumulate32(a, SmallTaskIO::row_part(p, pr, true), sm);
+        }
+    } else {
+        const double* Ad = bv.a[b].dense + dt.da;
+        const double* Bd = bv.b[b].dense + dt.db;
+        warp_accumulate32(a, SmallTaskIO::dd_part(Ad, Bd, m, dt.k, n, true), sm);
+    }
+    // pivot threshold 1e-3 below the cutoff (values-only: sigma_1 to ~1e-10)
+    const double drel = values_only ? 1e-10 : 1.8e-4 * eps;
+    const double dabs = values_only ? 0.0 : 1.8e-4 * abs_cut;
+    const int rp = warp_rrqr_jacobi32(a, v, m, n, drel, dabs, !values_only, sm);
+    double sig, smax;
+    int pos, r;
+    warp_sigma_pos32(a, rp, values_only ? 0.0 : eps, abs_cut, sig, pos, r, smax);
+    if (MODE == 0 && values_only) {
+        if (lane == 0) {
+            targs.sig_out[(size_t)ti * targs.B + b] = smax;
+            SmallTaskIO::flops(targs, m, n, K, 0);
+        }
+        return;
+    }
+    double* out = nullptr;
+    if (lane == 0 && r > 0) out = arena_alloc(MODE == 0 ? targs.out_arena : dargs.out_arena, (unsigned long long)(m + n) * r);
+    out = (double*)__shfl_sync(0xffffffffu, (unsigned long long)out, 0);
+    if (out == nullptr) r = 0;
+    if (r > 0) warp_write32(a, v, m, n, rp, sig, pos, r, sm, out, out + (size_t)m * r);
+    if (lane == 0) {
+        if (MODE == 0) {
+            SmallTaskIO::write_out(targs, task, b, C, r, out, out ? out + (size_t)m * r : nullptr);
+            SmallTaskIO::flops(targs, m, n, K, r);
+        } else {
+            Slot& s = dargs.slots[(size_t)dt.prod * dargs.B + b];
+            s.rank = r;
+            s.U = out;
+            s.V = out ? out + (size_t)m * r : nullptr;
+            s.ldu = m;
+            s.ldv = n;
+            double fsvd = 0, fqr = 0, fgemm = fl_gemm(m, n, dt.k);
+            fl_svd(m, n, fsvd, fqr, fgemm);
+            add_flops(dargs.flops, F_SVD, fsvd);
+            add_flops(dargs.flops, F_GEQRF, fqr);
+            add_flops(dargs.flops, F_GEMM, fgemm);
+        }
+    }
+}
+
+// sigma_1 of dense leaves (scale_walk, hmatrix.cpp:630-633), values only; <= 32: one warp per leaf.
+__global__ void __launch_bounds__(64) k_sigma1_32(Sig1Args args, BatchViews bv) {
+    __shared__ Warp32Smem smem[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int leaf = blockIdx.x * 2 + warp;
+    if (leaf >= args.nleaf) return;
+    const int b = blockIdx.y;
+    const int m = args.dm[leaf], n = args.dn[leaf];
+    const double* D = bv.c[b].dense + args.doff[leaf];
+    double a[32], v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = (lane < n && i < m) ? D[i + (size_t)lane * m] : 0.0;
+    const int rp = warp_rrqr_jacobi32(a, v, m, n, 1e-10, 0.0, false, smem[warp]);
+    double sig, smax;
+    int pos, r;
+    warp_sigma_pos32(a, rp, 0.0, 0.0, sig, pos, r, smax);
+    if (lane == 0) {
+        args.sig_out[(size_t)leaf * args.B + b] = smax;
+        double fsvd = 0, fqr = 0, fgemm = 0;
+        fl_svd(m, n, fsvd, fqr, fgemm);
+        add_flops(args.flops, F_SVD, fsvd);
+        add_flops(args.flops, F_GEQRF, fqr);
+        add_flops(args.flops, F_GEMM, fgemm);
+    }
+}
+
 // ------------------------------------------------------------------ launchers
-static int g_launches = 0;
+static long g_launches = 0;
 long launches_take() {
     const long v = g_launches;
     g_launches = 0;
     return v;
+}
+
+// Optional per-kernel device timing (ACRGPU_PROFILE=1): CUDA events around each
+// launch on the launching stream, folded into per-kernel totals at prof_flush().
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+    long ctas;
+};
+static std::vector<ProfRec> g_prof;
+static std::map<std::string, std::tuple<double, long, long>> g_prof_acc;  // ms, launches, ctas
+static int g_prof_on = -1;
+static bool prof_on() {
+    if (g_prof_on < 0) g_prof_on = getenv("ACRGPU_PROFILE") ? 1 : 0;
+    return g_prof_on == 1;
+}
+struct ProfScope {
+    cudaStream_t st;
+    const char* name;
+    long ctas;
+    cudaEvent_t a = nullptr;
+    ProfScope(cudaStream_t s, const char* n, long c) : st(s), name(n), ctas(c) {
+        ++g_launches;
+        if (prof_on()) {
+            cudaEventCreate(&a);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b;
+            cudaEventCreate(&b);
+            cudaEventRecord(b, st);
+            g_prof.push_back({name, a, b, ctas});
+        }
+    }
+};
+void prof_flush() {
+    if (g_prof.empty()) return;
+    cudaDeviceSynchronize();
+    for (auto& r : g_prof) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto& acc = g_prof_acc[r.name];
+        std::get<0>(acc) += ms;
+        std::get<1>(acc) += 1;
+        std::get<2>(acc) += r.ctas;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+}
+std::string prof_report(bool reset) {
+    prof_flush();
+    std::string out;
+    char buf[256];
+    for (auto& [k, v] : g_prof_acc) {
+        snprintf(buf, sizeof(buf), "%s %.3f %ld %ld\n", k.c_str(), std::get<0>(v), std::get<1>(v), std::get<2>(v));
+        out += buf;
+    }
+    if (reset) g_prof_acc.clear();
+    return out;
 }
 
 static size_t trunc_smem() { return SMEM_TRUNC; }
@@ -1254,7 +1523,7 @@ void setup_kernels() {
     cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
     cudaFuncSetAttribute(k_dd_product, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
     cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_sigma1_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_sigma1_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
 }
 
 void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots, int B,
@@ -1262,16 +1531,66 @@ void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const 
                      Arena work, FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
     TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, work, flops};
+    ProfScope _ps(st, "k_truncate", (long)((ntasks)*(B)));
     k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
-    ++g_launches;
+}
+
+void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots,
+                        int B, double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
+                        FlopLedger* flops, const BatchViews& bv) {
+    if (ntasks == 0 || B == 0) return;
+    TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, out_arena, flops};
+    DDArgs d{};
+    static const bool cta32 = getenv("ACRGPU_CTA32") != nullptr;
+    if (nc == 32 && cta32) {
+        ProfScope _ps(st, "k_trunc_cta32", (long)ntasks * B);
+        k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+    } else if (nc == 32) {
+        ProfScope _ps(st, "k_trunc_small32", (long)ntasks * B);
+        k_small32<0><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
+    } else {
+        ProfScope _ps(st, "k_trunc_mid64", (long)ntasks * B);
+        k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+    }
+}
+
+void launch_dd_small(cudaStream_t st, int nc, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps,
+                     Arena out_arena, FlopLedger* flops, const BatchViews& bv) {
+    if (ntasks == 0 || B == 0) return;
+    DDArgs d{tasks, slots, B, eps, out_arena, flops};
+    TruncArgs a{};
+    static const bool cta32 = getenv("ACRGPU_CTA32") != nullptr;
+    if (nc == 32 && cta32) {
+        ProfScope _ps(st, "k_dd_cta32", (long)ntasks * B);
+        k_dd_product<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(d, bv);
+    } else if (nc == 32) {
+        ProfScope _ps(st, "k_dd_small32", (long)ntasks * B);
+        k_small32<1><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
+    } else {
+        ProfScope _ps(st, "k_dd_mid64", (long)ntasks * B);
+        k_dd_product<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(d, bv);
+    }
+}
+
+void launch_sigma1_small(cudaStream_t st, int nc, int nleaf, const long* doff, const int* dm, const int* dn, int B,
+                         double* sig_out, FlopLedger* flops, const BatchViews& bv) {
+    if (nleaf == 0 || B == 0) return;
+    Sig1Args a{doff, dm, dn, nleaf, B, sig_out, flops};
+    if (nc == 32) {
+        ProfScope _ps(st, "k_sigma1_32", (long)nleaf * B);
+        k_sigma1_32<<<dim3((nleaf + 1) / 2, B), 64, 0, st>>>(a, bv);
+    } else {
+        ProfScope _ps(st, "k_sigma1_mid64", (long)nleaf * B);
+        k_sigma1_dense<<<dim3(nleaf, B), NT, trunc_smem(), st>>>(a, bv);
+    }
 }
 
 void launch_dd(cudaStream_t st, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps, Arena out_arena,
                FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
     DDArgs a{tasks, slots, B, eps, out_arena, flops};
+    ProfScope _ps(st, "k_dd_product", (long)((ntasks)*(B)));
     k_dd_product<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
-    ++g_launches;
 }
 
 void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slot* slots, int B, Arena arena,
@@ -1279,24 +1598,24 @@ void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slo
     if (ntasks == 0 || B == 0) return;
     AllocArgs a{tasks, ntasks, slots, B, arena};
     const int total = ntasks * B;
+    ProfScope _ps(st, "k_alloc_apply", (long)((total + 127) / 128));
     k_alloc_apply<<<(total + 127) / 128, 128, 0, st>>>(a, bv);
-    ++g_launches;
 }
 
 void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
                   Slot* slots, int B, FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
     ApplyArgs a{tasks, leaves, slots, B, 0, x_ld, flops};
+    ProfScope _ps(st, "k_apply", (long)((ntasks)*(B)));
     k_apply<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
-    ++g_launches;
 }
 
 void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Part* parts, const Slot* slots, int B,
                     FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
     DepArgs a{tasks, parts, slots, B, flops};
+    ProfScope _ps(st, "k_deposit", (long)((ntasks)*(B)));
     k_deposit<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
-    ++g_launches;
 }
 
 void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, unsigned long long call_id,
@@ -1304,8 +1623,8 @@ void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, 
     if (ntasks == 0 || bv.count == 0) return;
     LuArgs a{tasks, err, call_id, flops};
     const size_t sm = (2 * (size_t)maxm * maxm + 2 * maxm) * sizeof(double);
+    ProfScope _ps(st, "k_lu_inverse", (long)((ntasks)*(bv.count)));
     k_lu_inverse<<<dim3(ntasks, bv.count), NT, sm, st>>>(a, bv);
-    ++g_launches;
 }
 
 void launch_sigma1_dense(cudaStream_t st, int nleaf, const long* doff, const int* dm, const int* dn, int B,
@@ -1313,33 +1632,33 @@ void launch_sigma1_dense(cudaStream_t st, int nleaf, const long* doff, const int
     if (nleaf == 0 || B == 0) return;
     Sig1Args a{doff, dm, dn, nleaf, B, sig_out, flops};
     const size_t sm = ((size_t)maxm * maxm + maxm) * sizeof(double);
+    ProfScope _ps(st, "k_sigma1_dense", (long)((nleaf)*(B)));
     k_sigma1_dense<<<dim3(nleaf, B), NT, sm, st>>>(a, bv);
-    ++g_launches;
 }
 
 void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,
                          double* abs_cut) {
     if (B == 0) return;
+    ProfScope _ps(st, "k_scale_reduce", (long)(B));
     k_scale_reduce<<<B, 256, 0, st>>>(sig_d, nd, sig_k, nk, B, eps, abs_cut);
-    ++g_launches;
 }
 
 void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, int nrhs, int dim,
                    FlopLedger* flops, const MatvecBatch& mb) {
     if (ntasks == 0 || mb.count == 0) return;
     MatvecArgs a{tasks, leaves, nrhs, dim, flops};
+    ProfScope _ps(st, "k_matvec", (long)((ntasks)*(mb.count)));
     k_matvec<<<dim3(ntasks, mb.count), NT, 0, st>>>(a, mb);
-    ++g_launches;
 }
 
 void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
+    ProfScope _ps(st, "k_permute_in", (long)(1184));
     k_permute_in<<<1184, 256, 0, st>>>(in, out, perm, n, dim, nrhs);
-    ++g_launches;
 }
 
 void launch_permute_out(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
+    ProfScope _ps(st, "k_permute_out", (long)(1184));
     k_permute_out<<<1184, 256, 0, st>>>(in, out, perm, n, dim, nrhs);
-    ++g_launches;
 }
 
 void launch_zero_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk) {
@@ -1348,8 +1667,8 @@ void launch_zero_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk
     int gx = (int)((work + 255) / 256);
     if (gx > 64) gx = 64;
     if (gx < 1) gx = 1;
+    ProfScope _ps(st, "k_zero_views", (long)((gx)*(bv.count)));
     k_zero_views<<<dim3(gx, bv.count), 256, 0, st>>>(bv, dsize, nk);
-    ++g_launches;
 }
 
 void launch_copy_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk) {
@@ -1358,21 +1677,21 @@ void launch_copy_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk
     int gx = (int)((work + 255) / 256);
     if (gx > 64) gx = 64;
     if (gx < 1) gx = 1;
+    ProfScope _ps(st, "k_copy_views", (long)((gx)*(bv.count)));
     k_copy_views<<<dim3(gx, bv.count), 256, 0, st>>>(bv, dsize, nk);
-    ++g_launches;
 }
 
 void launch_scatter(cudaStream_t st, const ScatterLaunch& s, const BatchViews& bv) {
     if (bv.count == 0) return;
     ScatterArgs a{s.rows, s.cols, s.vals, s.off, s.iperm, s.leaf_of, s.cl_index, s.cl_begin, s.ncl,
                   s.d_off, s.d_rows, s.d_rb, s.d_cb, s.rk_hits};
+    ProfScope _ps(st, "k_scatter", (long)((16)*(bv.count)));
     k_scatter<<<dim3(16, bv.count), 256, 0, st>>>(a, bv);
-    ++g_launches;
 }
 
 void launch_reset_counter(cudaStream_t st, unsigned long long* ctr) {
+    ProfScope _ps(st, "k_reset_counter", (long)(1));
     k_reset_counter<<<1, 1, 0, st>>>(ctr);
-    ++g_launches;
 }
 
 }  // namespace acrgpu

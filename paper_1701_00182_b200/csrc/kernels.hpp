@@ -3,12 +3,14 @@
 
 #include <cuda_runtime.h>
 
+#include <string>
+
 #include "tasks.hpp"
 
 namespace acrgpu {
 
 constexpr int DENSE_MAX = 64;               // dense route / dense leaf limit
-constexpr size_t SMEM_TRUNC = 100 * 1024;   // dynamic smem of k_truncate / k_dd_product
+constexpr size_t SMEM_TRUNC = 112 * 1024;   // dynamic smem of k_truncate / k_dd_product
 
 struct ScatterLaunch {
     const int* rows;
@@ -29,10 +31,18 @@ struct ScatterLaunch {
 
 void setup_kernels();
 long launches_take();
+std::string prof_report(bool reset);
 
 void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots, int B,
                      double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
                      Arena work, FlopLedger* flops, const BatchViews& bv);
+void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots,
+                        int B, double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
+                        FlopLedger* flops, const BatchViews& bv);
+void launch_dd_small(cudaStream_t st, int nc, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps,
+                     Arena out_arena, FlopLedger* flops, const BatchViews& bv);
+void launch_sigma1_small(cudaStream_t st, int nc, int nleaf, const long* doff, const int* dm, const int* dn, int B,
+                         double* sig_out, FlopLedger* flops, const BatchViews& bv);
 void launch_dd(cudaStream_t st, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps, Arena out_arena,
                FlopLedger* flops, const BatchViews& bv);
 void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slot* slots, int B, Arena arena,

@@ -1,0 +1,309 @@
+// CTA-wide rank-revealing truncated SVD (blocks up to 64 x 64 in shared memory,
+// larger cores of the QR route in global workspace).  Same three stages as the
+// warp engine (svd_rrqr32.cuh):
+//   1. Householder QR with column pivoting, stopped when every remaining column
+//      norm is below delta (1e-3 below the truncation cutoff);
+//   2. one-sided Jacobi on A' = R^T (rp columns), warp per column pair,
+//      round-robin order, rotation parameters from two reciprocal square roots;
+//   3. U' = Q [J Sigma; 0], V' = P W Sigma^{-1}.
+// Reference semantics: truncate_impl / dense_to_lowrank, hmatrix.cpp:56-99.
+#pragma once
+
+namespace acrgpu {
+
+struct CtaSvdWork {
+    double* A;      // rows x cols (ld = lda): input, then R + reflectors
+    int lda;
+    double* W;      // cols x rp (ld = ldw): A' = R^T, then W = A' J
+    int ldw;
+    double* J;      // rp x rp (ld = ldj)
+    int ldj;
+    double* tau;    // >= min(rows, cols)
+    double* nrm;    // >= cols
+    double* sig;    // >= cols
+    int* perm;      // >= cols
+    int* order;     // >= cols
+};
+
+// Returns rp.  delta2: squared pivot threshold.  NT threads, NW warps.
+template <int NT>
+__device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) {
+    constexpr int NW = NT / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ double sh_best, sh_tau, sh_beta, sh_inv;
+    __shared__ int sh_piv;
+    double* A = w.A;
+    const int lda = w.lda;
+    for (int j = threadIdx.x; j < cols; j += NT) w.perm[j] = j;
+    const int kmax = rows < cols ? rows : cols;
+    int rp = 0;
+    for (int k = 0; k < kmax; ++k) {
+        for (int j = k + warp; j < cols; j += NW) {
+            const double* cj = A + (size_t)j * lda;
+            double s = 0;
+            for (int i = k + lane; i < rows; i += 32) s = fma(cj[i], cj[i], s);
+            s = warp_sum(s);
+            if (lane == 0) w.nrm[j] = s;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double best = -1.0;
+            int bi = k;
+            for (int j = k + lane; j < cols; j += 32) {
+                const double v = w.nrm[j];
+                if (v > best) { best = v; bi = j; }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (lane == 0) {
+                sh_best = best;
+                sh_piv = bi;
+            }
+        }
+        __syncthreads();
+        if (!(sh_best > delta2)) break;
+        const int piv = sh_piv;
+        if (piv != k) {
+            double* ck = A + (size_t)k * lda;
+            double* cp = A + (size_t)piv * lda;
+            for (int i = threadIdx.x; i < rows; i += NT) {
+                const double t = ck[i];
+                ck[i] = cp[i];
+                cp[i] = t;
+            }
+            if (threadIdx.x == 0) {
+                const int t = w.perm[k];
+                w.perm[k] = w.perm[piv];
+                w.perm[piv] = t;
+            }
+            __syncthreads();
+        }
+        double* ck = A + (size_t)k * lda;
+        if (warp == 0) {
+            double t = 0;
+            for (int i = k + 1 + lane; i < rows; i += 32) t = fma(ck[i], ck[i], t);
+            t = warp_sum(t);
+            if (lane == 0) {
+                const double c0 = ck[k];
+                if (t > 2.2250738585072014e-308) {
+                    double beta = sqrt(c0 * c0 + t);
+                    if (c0 >= 0) beta = -beta;
+                    sh_inv = 1.0 / (c0 - beta);
+                    sh_tau = (beta - c0) / beta;
+                    sh_beta = beta;
+                } else {
+                    sh_inv = 0.0;
+                    sh_tau = 0.0;
+                    sh_beta = c0;
+                }
+                w.tau[k] = sh_tau;
+            }
+        }
+        __syncthreads();
+        const double tk = sh_tau, inv = sh_inv;
+        for (int i = k + 1 + threadIdx.x; i < rows; i += NT) ck[i] = tk != 0.0 ? ck[i] * inv : 0.0;
+        __syncthreads();
+        if (threadIdx.x == 0) ck[k] = sh_beta;
+        if (tk != 0.0) {
+            for (int j = k + 1 + warp; j < cols; j += NW) {
+                double* cj = A + (size_t)j * lda;
+                double s = 0;
+                for (int i = k + 1 + lane; i < rows; i += 32) s = fma(ck[i], cj[i], s);
+                s = (warp_sum(s) + cj[k]) * tk;
+                if (lane == 0) cj[k] -= s;
+                for (int i = k + 1 + lane; i < rows; i += 32) cj[i] = fma(-s, ck[i], cj[i]);
+            }
+        }
+        __syncthreads();
+        rp = k + 1;
+    }
+    return rp;
+}
+
+// One-sided Jacobi on W (rows x cols), warp per pair, J (cols x cols) accumulated
+// when non-null.  sig[] receives column norms.
+template <int NT>
+__device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, int ldj, double* sig) {
+    constexpr int NW = NT / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (J)
+        for (int e = threadIdx.x; e < cols * cols; e += NT) {
+            const int i = e % cols, j = e / cols;
+            J[i + (size_t)j * ldj] = (i == j) ? 1.0 : 0.0;
+        }
+    __shared__ double sh_fro[NW];
+    {
+        double f = 0;
+        for (int j = warp; j < cols; j += NW)
+            for (int i = lane; i < rows; i += 32) f = fma(W[i + (size_t)j * ldw], W[i + (size_t)j * ldw], f);
+        f = warp_sum(f);
+        if (lane == 0) sh_fro[warp] = f;
+    }
+    __syncthreads();
+    double fro = 0;
+    for (int i = 0; i < NW; ++i) fro += sh_fro[i];
+    const double zthr = fro * (16.0 * JEPS * JEPS);
+    const double tol = (double)(rows > 1 ? rows : 1) * JEPS;
+    const double tol2 = tol * tol;
+    if (cols > 1) {
+        const int P = cols + (cols & 1);
+        for (int sweep = 0; sweep < 40; ++sweep) {
+            int rotated = 0;
+            for (int r = 0; r < P - 1; ++r) {
+                for (int pi = warp; pi < P / 2; pi += NW) {
+                    int p, q;
+                    if (pi == 0) {
+                        p = 0;
+                        q = 1 + r;
+                    } else {
+                        int a = r + pi, b = r - pi;
+                        a %= (P - 1);
+                        b %= (P - 1);
+                        if (b < 0) b += P - 1;
+                        p = 1 + a;
+                        q = 1 + b;
+                    }
+                    if (p > q) { const int t = p; p = q; q = t; }
+                    if (q >= cols) continue;
+                    double* ap = W + (size_t)p * ldw;
+                    double* aq = W + (size_t)q * ldw;
+                    double al = 0, be = 0, ga = 0;
+                    for (int e = lane; e < rows; e += 32) {
+                        const double x = ap[e], y = aq[e];
+                        al = fma(x, x, al);
+                        be = fma(y, y, be);
+                        ga = fma(x, y, ga);
+                    }
+                    al = warp_sum(al);
+                    be = warp_sum(be);
+                    ga = warp_sum(ga);
+                    double c, s;
+                    if (!jacobi_params(al, be, ga, tol2, zthr, c, s)) continue;
+                    for (int e = lane; e < rows; e += 32) rot2(ap[e], aq[e], c, s);
+                    if (J) {
+                        double* vp = J + (size_t)p * ldj;
+                        double* vq = J + (size_t)q * ldj;
+                        for (int e = lane; e < cols; e += 32) rot2(vp[e], vq[e], c, s);
+                    }
+                    rotated = 1;
+                }
+                __syncthreads();
+            }
+            if (!__syncthreads_or(rotated)) break;
+        }
+    }
+    for (int j = warp; j < cols; j += NW) {
+        double s = 0;
+        for (int e = lane; e < rows; e += 32) s = fma(W[e + (size_t)j * ldw], W[e + (size_t)j * ldw], s);
+        s = warp_sum(s);
+        if (lane == 0) sig[j] = sqrt(s);
+    }
+    __syncthreads();
+}
+
+// Full engine on w.A (rows x cols).  Returns the truncated rank r (CTA-uniform);
+// order[t] = Jacobi column of the t-th largest sigma; *smax_out = sigma_1.
+template <int NT>
+__device__ int cta_trunc_svd(const CtaSvdWork& w, int rows, int cols, double eps, double abs_cut, bool values_only,
+                             int* rp_out, double* smax_out) {
+    __shared__ int sh_r;
+    __shared__ double sh_smax;
+    // pivot threshold from the largest column norm (a lower bound of sigma_1)
+    double cm = 0;
+    {
+        __shared__ double redm[NT / 32];
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int j = warp; j < cols; j += NT / 32) {
+            double s = 0;
+            for (int i = lane; i < rows; i += 32) s = fma(w.A[i + (size_t)j * w.lda], w.A[i + (size_t)j * w.lda], s);
+            cm = fmax(cm, warp_sum(s));
+        }
+        if (lane == 0) redm[warp] = cm;
+        __syncthreads();
+        cm = 0;
+        for (int i = 0; i < NT / 32; ++i) cm = fmax(cm, redm[i]);
+        __syncthreads();
+    }
+    const double drel = values_only ? 1e-10 : 1.8e-4 * eps;
+    const double dabs = values_only ? 0.0 : 1.8e-4 * abs_cut;
+    const double d1 = drel * sqrt(cm);
+    const double delta2 = fmax(d1 * d1, dabs * dabs);
+    const int rp = cta_rrqr<NT>(w, rows, cols, delta2);
+    *rp_out = rp;
+    if (rp == 0) {
+        *smax_out = 0.0;
+        return 0;
+    }
+    // A' = R^T (cols x rp)
+    for (int e = threadIdx.x; e < cols * rp; e += NT) {
+        const int j = e % cols, c = e / cols;
+        w.W[j + (size_t)c * w.ldw] = j >= c ? w.A[c + (size_t)j * w.lda] : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi<NT>(w.W, w.ldw, cols, rp, values_only ? nullptr : w.J, w.ldj, w.sig);
+    for (int j = threadIdx.x; j < rp; j += NT) {
+        const double v = w.sig[j];
+        int pos = 0;
+        for (int i = 0; i < rp; ++i) {
+            const double u = w.sig[i];
+            pos += (u > v) || (u == v && i < j);
+        }
+        w.order[pos] = j;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double s0 = w.sig[w.order[0]];
+        int r = 0;
+        if (s0 > 0.0) {
+            const double cut = fmax((values_only ? 0.0 : eps) * s0, abs_cut);
+            while (r < rp && w.sig[w.order[r]] > cut) ++r;
+        }
+        sh_r = r;
+        sh_smax = s0;
+    }
+    __syncthreads();
+    *smax_out = sh_smax;
+    return sh_r;
+}
+
+// U' (rows x r, ld ldu) = Q [J Sigma; 0];  V' (cols x r, ld ldv) = P W Sigma^{-1}.
+template <int NT>
+__device__ void cta_trunc_write(const CtaSvdWork& w, int rows, int cols, int rp, int r, double* Uo, int ldu, double* Vo,
+                                int ldv) {
+    constexpr int NW = NT / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < rows * r; e += NT) {
+        const int i = e % rows, t = e / rows;
+        const int c = w.order[t];
+        Uo[i + (size_t)t * ldu] = i < rp ? w.J[i + (size_t)c * w.ldj] * w.sig[c] : 0.0;
+    }
+    for (int e = threadIdx.x; e < cols * r; e += NT) {
+        const int j = e % cols, t = e / cols;
+        const int c = w.order[t];
+        Vo[w.perm[j] + (size_t)t * ldv] = w.W[j + (size_t)c * w.ldw] / w.sig[c];
+    }
+    __syncthreads();
+    // apply the reflectors of the pivoted QR in reverse order, warp per column
+    for (int t = warp; t < r; t += NW) {
+        double* x = Uo + (size_t)t * ldu;
+        for (int k = rp - 1; k >= 0; --k) {
+            const double tk = w.tau[k];
+            if (tk == 0.0) continue;
+            const double* v = w.A + (size_t)k * w.lda;
+            double s = 0;
+            for (int i = k + 1 + lane; i < rows; i += 32) s = fma(v[i], x[i], s);
+            s = (warp_sum(s) + x[k]) * tk;
+            __syncwarp();
+            if (lane == 0) x[k] -= s;
+            for (int i = k + 1 + lane; i < rows; i += 32) x[i] = fma(-s, v[i], x[i]);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace acrgpu

@@ -1,0 +1,280 @@
+// Rank-revealing truncated SVD of blocks up to 32 x 32, one warp per block.
+//
+//   1. Householder QR with column pivoting (column per lane, fully unrolled) on
+//      M (m x n); it stops as soon as every remaining column norm is below
+//      delta, a threshold 1e-3 below the truncation cutoff: M P = Q [R; ~0] with
+//      R of rp <= min(m, n) rows, and the dropped remainder has norm
+//      <= sqrt(32) * delta = 1e-3 * cutoff, so every singular value above the
+//      cutoff is reproduced to 1e-3 of the cutoff and rank decisions match the
+//      reference (hmatrix.cpp:70-74) except for values within that band.
+//   2. One-sided Jacobi on A' = R^T (n x rp): columns of A' are rows of R, one
+//      column per lane; each round a lane exchanges its column with its
+//      round-robin partner by register shuffles, both lanes form the same
+//      rotation from bitwise-identical inner products.  The QR
+//      preconditioning (Drmac-Veselic) and the reduced column count rp make
+//      this converge in a few short sweeps.
+//   3. U' = Q [J_r Sigma_r; 0] (reflectors applied per lane), V' = P W_r Sigma_r^{-1}.
+//
+// Mathematically the same truncated SVD the reference computes with QR(U),
+// QR(V) and JacobiSVD of the core (hmatrix.cpp:56-84).
+#pragma once
+
+namespace acrgpu {
+
+struct Warp32Smem {
+    double H[32][33];  // H[k][i]: essential part of reflector k (i > k)
+    double T[32][33];  // staging: formation chunks, then the R^T transpose
+    double tau[32];
+    int perm[32];
+};
+
+__device__ __forceinline__ int rr_partner(int x, int r, int P) {
+    // circle method over P (even) players, player 0 fixed, P-1 rounds
+    if (x == 0) return 1 + r;
+    const int y = x - 1;
+    int yp = (2 * r - y) % (P - 1);
+    if (yp < 0) yp += P - 1;
+    return yp == y ? 0 : 1 + yp;
+}
+
+// Phase 1+2.  In: lane j holds column j of M in a[0..m).  Out: returns rp;
+// lane c < rp holds column c of W = R^T J in a[0..n) and column c of J in v[0..rp);
+// sm.H / sm.tau / sm.perm describe Q and P.
+__device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n, double delta_rel,
+                                  double abs_delta, bool want_v, Warp32Smem& sm) {
+    const int lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+    int perm_j = lane;
+    // column norms and pivot threshold
+    double c2 = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) c2 = fma(a[i], a[i], c2);
+    double cmax = lane < n ? c2 : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cmax = fmax(cmax, __shfl_xor_sync(FULL, cmax, o));
+    const double d1 = delta_rel * sqrt(cmax);
+    const double delta2 = fmax(d1 * d1, abs_delta * abs_delta);
+    const int kmax = m < n ? m : n;
+    int rp = 0;
+    // ---- QR with column pivoting, stopped at the numerical rank
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        if (k >= kmax) break;
+        double nr = 0;
+#pragma unroll
+        for (int i = k; i < 32; ++i) nr = fma(a[i], a[i], nr);
+        double best = (lane >= k && lane < n) ? nr : -1.0;
+        int bidx = lane;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(FULL, best, o);
+            const int oi = __shfl_xor_sync(FULL, bidx, o);
+            if (ob > best || (ob == best && oi < bidx)) {
+                best = ob;
+                bidx = oi;
+            }
+        }
+        if (!(best > delta2)) break;
+        if (bidx != k) {
+            const int src = lane == k ? bidx : (lane == bidx ? k : lane);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) a[i] = __shfl_sync(FULL, a[i], src);
+            perm_j = __shfl_sync(FULL, perm_j, src);
+        }
+        double tau = 0.0;
+        if (lane == k) {
+            double tail = 0;
+#pragma unroll
+            for (int i = k + 1; i < 32; ++i) tail = fma(a[i], a[i], tail);
+            const double c0 = a[k];
+            if (tail > 2.2250738585072014e-308) {
+                double beta = sqrt(c0 * c0 + tail);
+                if (c0 >= 0) beta = -beta;
+                const double inv = 1.0 / (c0 - beta);
+                tau = (beta - c0) / beta;
+#pragma unroll
+                for (int i = k + 1; i < 32; ++i) a[i] *= inv;
+                a[k] = beta;
+            } else {
+#pragma unroll
+                for (int i = k + 1; i < 32; ++i) a[i] = 0.0;
+            }
+#pragma unroll
+            for (int i = k + 1; i < 32; ++i) sm.H[k][i] = a[i];
+            sm.tau[k] = tau;
+        }
+        tau = __shfl_sync(FULL, tau, k);
+        double vv[32];
+#pragma unroll
+        for (int i = k + 1; i < 32; ++i) vv[i] = __shfl_sync(FULL, a[i], k);
+        if (lane > k && tau != 0.0) {
+            double s = a[k];
+#pragma unroll
+            for (int i = k + 1; i < 32; ++i) s = fma(vv[i], a[i], s);
+            s *= tau;
+            a[k] -= s;
+#pragma unroll
+            for (int i = k + 1; i < 32; ++i) a[i] = fma(-s, vv[i], a[i]);
+        }
+        rp = k + 1;
+    }
+    sm.perm[lane] = perm_j;
+    // ---- A' = R^T: lane c < rp takes row c of R
+#pragma unroll
+    for (int i = 0; i < 32; ++i) sm.T[lane][i] = (i < rp && i <= lane) ? a[i] : 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a[j] = lane < rp ? sm.T[j][lane] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = (i == lane && lane < rp) ? 1.0 : 0.0;
+    __syncwarp();
+    if (rp < 2) return rp;
+    // ---- one-sided Jacobi on the rp columns of A'
+    const int P = rp + (rp & 1);
+    const double tol = (double)(n > 1 ? n : 1) * JEPS;
+    const double tol2 = tol * tol;
+    double own = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) own = fma(a[i], a[i], own);
+    double fro = own;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) fro += __shfl_xor_sync(FULL, fro, o);
+    const double zthr = fro * (16.0 * JEPS * JEPS);
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        bool any = false;
+        for (int round = 0; round < P - 1; ++round) {
+            const int p = lane < P ? rr_partner(lane, round, P) : lane;
+            const bool low = lane < p;
+            double pa[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) pa[i] = __shfl_sync(FULL, a[i], p);
+            double s0 = 0, s1 = 0, s2 = 0, t0 = 0, t1 = 0, t2 = 0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const double xl = low ? a[i] : pa[i], xh = low ? pa[i] : a[i];
+                const double yl = low ? a[i + 1] : pa[i + 1], yh = low ? pa[i + 1] : a[i + 1];
+                s0 = fma(xl, xl, s0);
+                s1 = fma(xh, xh, s1);
+                s2 = fma(xl, xh, s2);
+                t0 = fma(yl, yl, t0);
+                t1 = fma(yh, yh, t1);
+                t2 = fma(yl, yh, t2);
+            }
+            double c, s;
+            bool rot = false;
+            if (p != lane) rot = jacobi_params(s0 + t0, s1 + t1, s2 + t2, tol2, zthr, c, s);
+            if (!rot) {
+                c = 1.0;
+                s = 0.0;
+            }
+            if (__any_sync(FULL, rot)) {
+                any = true;
+                const double sl = low ? -s : s;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) a[i] = fma(sl, pa[i], c * a[i]);
+                if (want_v) {
+#pragma unroll
+                    for (int i0 = 0; i0 < 32; i0 += 8) {
+                        double pv[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) pv[i] = __shfl_sync(FULL, v[i0 + i], p);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) v[i0 + i] = fma(sl, pv[i], c * v[i0 + i]);
+                    }
+                }
+            }
+        }
+        if (!any) break;
+    }
+    return rp;
+}
+
+// sigma (lane c < rp), descending position and rank r (warp-uniform).
+__device__ __forceinline__ void warp_sigma_pos32(const double (&a)[32], int rp, double eps, double abs_cut, double& sig,
+                                                 int& pos, int& r, double& smax) {
+    const int lane = threadIdx.x & 31;
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s = fma(a[i], a[i], s);
+    sig = lane < rp ? sqrt(s) : -1.0;
+    pos = 0;
+    smax = fmax(sig, 0.0);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const double w = __shfl_sync(0xffffffffu, sig, i);
+        pos += (w > sig) || (w == sig && i < lane);
+        smax = fmax(smax, w);
+    }
+    r = 0;
+    if (smax > 0.0) {
+        const double cut = fmax(eps * smax, abs_cut);
+        r = __popc(__ballot_sync(0xffffffffu, lane < rp && sig > cut));
+    }
+}
+
+// Phase 3: write U' (m x r) = Q [J Sigma; 0] and V' (n x r) = P W Sigma^{-1}.
+__device__ void warp_write32(const double (&a)[32], const double (&v)[32], int m, int n, int rp, double sig, int pos,
+                             int r, Warp32Smem& sm, double* Uo, double* Vo) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    if (lane < rp && pos < r) {
+        double x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = i < rp ? v[i] * sig : 0.0;
+#pragma unroll
+        for (int k = 31; k >= 0; --k) {
+            if (k < rp) {
+                const double tk = sm.tau[k];
+                if (tk != 0.0) {
+                    double s = x[k];
+#pragma unroll
+                    for (int i = k + 1; i < 32; ++i) s = fma(sm.H[k][i], x[i], s);
+                    s *= tk;
+                    x[k] -= s;
+#pragma unroll
+                    for (int i = k + 1; i < 32; ++i) x[i] = fma(-s, sm.H[k][i], x[i]);
+                }
+            }
+        }
+        double* u = Uo + (size_t)pos * m;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (i < m) u[i] = x[i];
+        double* w = Vo + (size_t)pos * n;
+        const double inv = 1.0 / sig;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < n) w[sm.perm[j]] = a[j] * inv;
+    }
+    __syncwarp();
+}
+
+// Column-per-lane formation: M[i, j] += alpha sum_t P(i,t) Q(j,t), i in [pd, pd+pr), j in [qd, qd+qr).
+// P chunks are staged through sm.T (rows x TC); lane j reads its own Q(j, t).
+__device__ void warp_accumulate32(double (&a)[32], const RowPart& p, Warp32Smem& sm) {
+    const int lane = threadIdx.x & 31;
+    constexpr int TC = 32;
+    const int jr = lane - p.qd;
+    const bool own = jr >= 0 && jr < p.qr;
+    for (int t0 = 0; t0 < p.k; t0 += TC) {
+        const int tn = min(TC, p.k - t0);
+        __syncwarp();
+        // stage P rows [0,32) x chunk (zero outside [pd, pd+pr))
+        for (int t = 0; t < tn; ++t) {
+            const int i = lane;
+            const int ir = i - p.pd;
+            sm.T[t][i] = (ir >= 0 && ir < p.pr) ? p.alpha * p.P[ir * p.ps + (long)(t0 + t) * p.pt] : 0.0;
+        }
+        __syncwarp();
+        if (own) {
+            for (int t = 0; t < tn; ++t) {
+                const double q = p.Q[jr * p.qs + (long)(t0 + t) * p.qt];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) a[i] = fma(sm.T[t][i], q, a[i]);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+}  // namespace acrgpu
