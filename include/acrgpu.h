@@ -125,9 +125,16 @@ typedef struct acrgpu_fact acrgpu_fact;
 int acrgpu_ctx_create(int device, acrgpu_ctx** out, acrgpu_error* err);
 void acrgpu_ctx_destroy(acrgpu_ctx* ctx);
 
-/* acr_factor in H-matrix mode.  System blocks are read from host memory. */
+/* acr_factor in H-matrix mode.  System blocks are read from host memory (validated,
+ * duplicate-merged and uploaded inside the call). */
 int acrgpu_factor(acrgpu_ctx* ctx, const acrgpu_system* sys, const acrgpu_config* cfg,
                   acrgpu_fact** out, acrgpu_error* err);
+/* Device-resident input: validate + upload once, then factor from HBM (no host input traffic). */
+typedef struct acrgpu_dsystem acrgpu_dsystem;
+int acrgpu_system_upload(acrgpu_ctx* ctx, const acrgpu_system* sys, acrgpu_dsystem** out, acrgpu_error* err);
+void acrgpu_system_destroy(acrgpu_dsystem* sys);
+int acrgpu_factor_resident(acrgpu_ctx* ctx, const acrgpu_dsystem* sys, const acrgpu_config* cfg,
+                           acrgpu_fact** out, acrgpu_error* err);
 void acrgpu_factor_destroy(acrgpu_fact* f);
 
 /* AcrFactorization::solve for nrhs right-hand sides; f, u host pointers ([nrhs][n][dim]). */

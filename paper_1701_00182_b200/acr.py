@@ -144,6 +144,10 @@ SYMBOLS = {
     "acrgpu_ctx_destroy": (None, [C.c_void_p]),
     "acrgpu_factor": (C.c_int, [C.c_void_p, C.POINTER(_Sys), C.POINTER(_Cfg), C.POINTER(C.c_void_p), C.POINTER(_Err)]),
     "acrgpu_factor_destroy": (None, [C.c_void_p]),
+    "acrgpu_system_upload": (C.c_int, [C.c_void_p, C.POINTER(_Sys), C.POINTER(C.c_void_p), C.POINTER(_Err)]),
+    "acrgpu_system_destroy": (None, [C.c_void_p]),
+    "acrgpu_factor_resident": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Cfg), C.POINTER(C.c_void_p),
+                                         C.POINTER(_Err)]),
     "acrgpu_solve": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(_Err)]),
     "acrgpu_solve_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(_Err)]),
     "acrgpu_stats": (C.c_int, [C.c_void_p, C.POINTER(_Stats)]),
@@ -311,23 +315,56 @@ class AcrFactorization:
         return {k: getattr(t, k) for k, _ in _Timing._fields_}
 
 
-def acr_factor(system: problems.System, config: AcrConfig | None = None, ctx: Context | None = None):
-    """acr::acr_factor (acr.cpp:366-384) on the GPU."""
-    config = config or AcrConfig()
-    ctx = ctx or default_context()
-    cfg = _cfg(config)
-    coords = np.ascontiguousarray(system.coords, np.float64)
-    off = np.ascontiguousarray(system.blk_off, np.int64)
-    rows = np.ascontiguousarray(system.rows, np.int32)
-    cols = np.ascontiguousarray(system.cols, np.int32)
-    vals = np.ascontiguousarray(system.vals, np.float64)
+def _sys_struct(system):
+    keep = (np.ascontiguousarray(system.coords, np.float64), np.ascontiguousarray(system.blk_off, np.int64),
+            np.ascontiguousarray(system.rows, np.int32), np.ascontiguousarray(system.cols, np.int32),
+            np.ascontiguousarray(system.vals, np.float64))
+    coords, off, rows, cols, vals = keep
     s = _Sys(system.n, system.dim, _p(coords, C.c_double), _p(off, C.c_long), _p(rows, C.c_int), _p(cols, C.c_int),
              _p(vals, C.c_double))
+    return s, keep
+
+
+class DeviceSystem:
+    """A system validated and uploaded to HBM once (acrgpu_system_upload)."""
+
+    def __init__(self, system: problems.System, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.system = system
+        s, keep = _sys_struct(system)
+        self.h = C.c_void_p()
+        err = _Err()
+        if lib().acrgpu_system_upload(self.ctx.h, C.byref(s), C.byref(self.h), C.byref(err)):
+            _raise(err)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and self.h.value:
+                lib().acrgpu_system_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def acr_factor(system, config: AcrConfig | None = None, ctx: Context | None = None):
+    """acr::acr_factor (acr.cpp:366-384) on the GPU.  ``system`` is a problems.System
+    (host COO, uploaded inside the call) or a DeviceSystem (already resident in HBM)."""
+    config = config or AcrConfig()
+    cfg = _cfg(config)
     h = C.c_void_p()
     err = _Err()
-    if lib().acrgpu_factor(ctx.h, C.byref(s), C.byref(cfg), C.byref(h), C.byref(err)):
+    if isinstance(system, DeviceSystem):
+        ctx = system.ctx
+        rc = lib().acrgpu_factor_resident(ctx.h, system.h, C.byref(cfg), C.byref(h), C.byref(err))
+        host = system.system
+    else:
+        ctx = ctx or default_context()
+        s, keep = _sys_struct(system)
+        rc = lib().acrgpu_factor(ctx.h, C.byref(s), C.byref(cfg), C.byref(h), C.byref(err))
+        host = system
+    if rc:
         _raise(err)
-    return AcrFactorization(h, system, config, ctx)
+    return AcrFactorization(h, host, config, ctx)
 
 
 def acr_solve(fact: AcrFactorization, f):

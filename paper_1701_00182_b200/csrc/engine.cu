@@ -99,19 +99,22 @@ struct Ctx {
         ctrs = dmalloc<unsigned long long>(2);
         overflow = dmalloc<int>(2);
         err = dmalloc<DevError>(1);
-        flops = dmalloc<FlopLedger>(1);
+        flops = dmalloc<FlopLedger>(MAX_KERNELS);
+        set_report_ledger(flops);
         persist = Arena{persist_base, pbytes / 8, ctrs, overflow};
         trans = Arena{trans_base, tbytes / 8, ctrs + 1, overflow + 1};
         reset_all();
     }
     void reset_all() {
+        CK(cudaStreamSynchronize(st));
+        fold_ledger();
         CK(cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned long long), st));
         CK(cudaMemsetAsync(overflow, 0, 2 * sizeof(int), st));
         DevError e0;
         std::memset(&e0, 0, sizeof(e0));
         e0.key = ~0ull;
         CK(cudaMemcpyAsync(err, &e0, sizeof(e0), cudaMemcpyHostToDevice, st));
-        CK(cudaMemsetAsync(flops, 0, sizeof(FlopLedger), st));
+        CK(cudaMemsetAsync(flops, 0, MAX_KERNELS * sizeof(FlopLedger), st));
         CK(cudaStreamSynchronize(st));
         call_id = 0;
         call_planes.clear();
@@ -241,9 +244,9 @@ struct Engine {
     void run_trunc(const Classed<TruncTask>& tl, const Part* parts, Slot* slots, int nb, double eps,
                    const double* abs_cut, double* sig_out, bool values_only, Arena out, const BatchViews& bv) {
         if (tl.n[0]) launch_trunc_small(st(), 32, tl.n[0], tl.p[0], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
-                                        ctx->flops, bv);
+                                        ctx->trans, ctx->flops, bv);
         if (tl.n[1]) launch_trunc_small(st(), 64, tl.n[1], tl.p[1], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
-                                        ctx->flops, bv);
+                                        ctx->trans, ctx->flops, bv);
         if (tl.n[2]) launch_truncate(st(), tl.n[2], tl.p[2], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
                                      ctx->trans, ctx->flops, bv);
     }
@@ -828,6 +831,8 @@ struct acrgpu_fact {
     acrgpu_timing timing{};
     double* fbuf = nullptr;  // solve workspace
     size_t fbuf_cap = 0;
+    double* ubuf = nullptr;  // compacted low-rank factors of the stored blocks
+    long ubuf_doubles = 0;
 };
 
 namespace acrgpu {
@@ -843,13 +848,37 @@ static std::vector<View> views(const std::vector<SP>& v) {
 }
 
 // ------------------------------------------------------------------ lifting
-static std::vector<SP> lift(Engine& E, const acrgpu_system* sys) {
-    const int n = sys->n, dim = sys->dim, nb = 3 * n - 2;
-    const Structure& S = E.S;
-    // validate + merge duplicates (PlaneBlock, block.cpp:7-29)
+// Validated, duplicate-merged copy of a system (PlaneBlock, block.cpp:7-29):
+// host arrays plus their device-resident upload.
+struct DSys {
+    int n = 0, dim = 0;
+    std::vector<double> coords;
+    std::vector<long> off;
     std::vector<int> rows, cols;
     std::vector<double> vals;
-    std::vector<long> off(nb + 1, 0);
+    int* d_rows = nullptr;
+    int* d_cols = nullptr;
+    double* d_vals = nullptr;
+    long* d_off = nullptr;
+    int device = 0;
+    ~DSys() {
+        for (void* p : std::initializer_list<void*>{d_rows, d_cols, d_vals, d_off})
+            if (p) cudaFree(p);
+    }
+};
+
+static DSys* make_dsys(const acrgpu_system* sys, cudaStream_t st) {
+    if (sys->n < 1 || sys->dim < 1) throw AcrError{ACRGPU_E_DIMENSION, "acr_factor: empty system"};
+    auto ds = std::make_unique<DSys>();
+    const int n = sys->n, dim = sys->dim, nb = 3 * n - 2;
+    ds->n = n;
+    ds->dim = dim;
+    ds->coords.assign(sys->coords, sys->coords + 2L * dim);
+    std::vector<int>& rows = ds->rows;
+    std::vector<int>& cols = ds->cols;
+    std::vector<double>& vals = ds->vals;
+    std::vector<long>& off = ds->off;
+    off.assign(nb + 1, 0);
     rows.reserve(sys->blk_off[nb]);
     cols.reserve(sys->blk_off[nb]);
     vals.reserve(sys->blk_off[nb]);
@@ -859,7 +888,8 @@ static std::vector<SP> lift(Engine& E, const acrgpu_system* sys) {
         bool sorted = true;
         for (long i = s; i < e; ++i) {
             if (sys->rows[i] < 0 || sys->rows[i] >= dim || sys->cols[i] < 0 || sys->cols[i] >= dim)
-                throw AcrError{ACRGPU_E_DIMENSION, "PlaneBlock: entry index out of range"};
+                throw AcrError{ACRGPU_E_DIMENSION, "PlaneBlock: entry index out of range",
+                               -1, b < n ? b : (b < 2 * n - 1 ? b - n + 1 : b - 2 * n + 1)};
             if (i > s) {
                 const long pr = sys->rows[i - 1], pc = sys->cols[i - 1];
                 if (!(pr < sys->rows[i] || (pr == sys->rows[i] && pc < sys->cols[i]))) sorted = false;
@@ -887,11 +917,27 @@ static std::vector<SP> lift(Engine& E, const acrgpu_system* sys) {
         }
         off[b + 1] = (long)rows.size();
     }
+    ds->d_rows = upload(rows, st);
+    ds->d_cols = upload(cols, st);
+    ds->d_vals = upload(vals, st);
+    ds->d_off = upload(off, st);
+    CK(cudaGetDevice(&ds->device));
+    CK(cudaStreamSynchronize(st));
+    return ds.release();
+}
+
+static std::vector<SP> lift(Engine& E, const DSys& ds) {
+    const int n = ds.n, nb = 3 * n - 2;
+    const Structure& S = E.S;
+    const std::vector<int>& rows = ds.rows;
+    const std::vector<int>& cols = ds.cols;
+    const std::vector<double>& vals = ds.vals;
+    const std::vector<long>& off = ds.off;
     cudaStream_t st = E.st();
-    int* d_rows = upload(rows, st);
-    int* d_cols = upload(cols, st);
-    double* d_vals = upload(vals, st);
-    long* d_off = upload(off, st);
+    int* d_rows = ds.d_rows;
+    int* d_cols = ds.d_cols;
+    double* d_vals = ds.d_vals;
+    long* d_off = ds.d_off;
     // scatter tables
     const int ncl = (int)S.cl_begin.size();
     std::vector<int> leaf_of((size_t)ncl * ncl, -1);
@@ -988,9 +1034,7 @@ static std::vector<SP> lift(Engine& E, const acrgpu_system* sys) {
                                                  std::to_string(L.cols()) + " exceeds memory cap"};
     }
     CK(cudaStreamSynchronize(st));
-    for (void* p : std::initializer_list<void*>{d_rows, d_cols, d_vals, d_off, d_leaf_of, d_clidx, d_clb, d_drb, d_dcb,
-                                                d_drows, d_hits})
-        cudaFree(p);
+    for (void* p : std::initializer_list<void*>{d_leaf_of, d_clidx, d_clb, d_drb, d_dcb, d_drows, d_hits}) cudaFree(p);
     return blocks;
 }
 
@@ -1030,9 +1074,74 @@ static void check_device_errors(acrgpu_fact* F) {
                                             "); factorization too large for this GPU"};
 }
 
-static void do_factor(acrgpu_fact* F, const acrgpu_system* sys) {
+// Copy all stored low-rank factors into one exact-size allocation owned by the
+// factorization, so the shared device arenas can be reused by the next call.
+static void compact_factor(acrgpu_fact* F) {
     Engine& E = *F->eng;
-    const int n = sys->n;
+    cudaStream_t st = E.st();
+    std::vector<Store*> stores;
+    auto add = [&](const SP& s) {
+        if (s && std::find(stores.begin(), stores.end(), s.get()) == stores.end()) stores.push_back(s.get());
+    };
+    for (auto& L : F->levels) {
+        for (auto& s : L.E) add(s);
+        for (auto& s : L.F) add(s);
+        for (auto& s : L.Dinv) add(s);
+    }
+    for (auto& s : F->apexE) add(s);
+    for (auto& s : F->apexF) add(s);
+    for (auto& s : F->apexDinv) add(s);
+    const int nk = E.S.n_rk();
+    if (nk == 0 || stores.empty()) return;
+    CK(cudaStreamSynchronize(st));
+    std::vector<int> ranks((size_t)stores.size() * nk);
+    for (size_t i = 0; i < stores.size(); ++i)
+        CK(cudaMemcpyAsync(ranks.data() + i * nk, stores[i]->rank, nk * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<long> off(ranks.size(), -1);
+    std::vector<int> km(nk), kn(nk);
+    for (int k = 0; k < nk; ++k) {
+        const SNode& L = E.S.node(E.S.k_node[k]);
+        km[k] = L.rows();
+        kn[k] = L.cols();
+    }
+    long total = 0;
+    for (size_t i = 0; i < stores.size(); ++i)
+        for (int k = 0; k < nk; ++k) {
+            const int r = ranks[i * nk + k];
+            if (r > 0) {
+                off[i * nk + k] = total;
+                total += (long)(km[k] + kn[k]) * r;
+            }
+        }
+    if (F->ubuf) cudaFree(F->ubuf);
+    F->ubuf = dmalloc<double>(std::max<long>(total, 1));
+    F->ubuf_doubles = total;
+    long* d_off = upload(off, st);
+    int* d_km = upload(km, st);
+    int* d_kn = upload(kn, st);
+    std::vector<double**> Ut, Vt;
+    std::vector<int*> Rt;
+    for (Store* s : stores) {
+        Ut.push_back(s->U);
+        Vt.push_back(s->V);
+        Rt.push_back(s->rank);
+    }
+    double*** d_U = upload(Ut, st);
+    double*** d_V = upload(Vt, st);
+    int** d_R = upload(Rt, st);
+    for (size_t s0 = 0; s0 < stores.size(); s0 += 65535) {
+        const int cnt = (int)std::min<size_t>(65535, stores.size() - s0);
+        CompactArgs a{F->ubuf, d_off + s0 * nk, d_U + s0, d_V + s0, d_R + s0, d_km, d_kn, nk};
+        launch_compact(st, a, cnt);
+    }
+    CK(cudaStreamSynchronize(st));
+    for (void* p : std::initializer_list<void*>{d_off, d_km, d_kn, d_U, d_V, d_R}) cudaFree(p);
+}
+
+static void do_factor(acrgpu_fact* F, const DSys& sys) {
+    Engine& E = *F->eng;
+    const int n = sys.n;
     cudaEvent_t e0, e1, e2;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -1174,15 +1283,22 @@ static void do_factor(acrgpu_fact* F, const acrgpu_system* sys) {
         F->apexDinv.push_back(out);
     }
     E.recompress(views(F->apexDinv));
-    CK(cudaEventRecord(e2, E.st()));
     check_device_errors(F);
+    compact_factor(F);
+    CK(cudaEventRecord(e2, E.st()));
+    CK(cudaEventSynchronize(e2));
     float ms_lift = 0, ms_all = 0;
     CK(cudaEventElapsedTime(&ms_lift, e0, e1));
     CK(cudaEventElapsedTime(&ms_all, e0, e2));
     F->timing.lift_ms = ms_lift;
     F->timing.factor_ms = ms_all;
-    FlopLedger fl;
-    CK(cudaMemcpy(&fl, E.ctx->flops, sizeof(fl), cudaMemcpyDeviceToHost));
+    FlopLedger fl{};
+    {
+        std::vector<FlopLedger> led(MAX_KERNELS);
+        CK(cudaMemcpy(led.data(), E.ctx->flops, MAX_KERNELS * sizeof(FlopLedger), cudaMemcpyDeviceToHost));
+        for (auto& l : led)
+            for (int c = 0; c < F_NCLASS; ++c) fl.f[c] += l.f[c];
+    }
     F->timing.flops_gemm = fl.f[F_GEMM];
     F->timing.flops_qr = fl.f[F_GEQRF] + fl.f[F_ORGQR];
     F->timing.flops_svd = fl.f[F_SVD];
@@ -1429,12 +1545,54 @@ void acrgpu_ctx_destroy(acrgpu_ctx* ctx) {
     delete ctx;
 }
 
+struct acrgpu_dsystem {
+    std::unique_ptr<DSys> d;
+};
+
+int acrgpu_system_upload(acrgpu_ctx* ctx, const acrgpu_system* sys, acrgpu_dsystem** out, acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
+        if (!ctx || !sys) throw AcrError{ACRGPU_E_USAGE, "null argument"};
+        auto* h = new acrgpu_dsystem;
+        try {
+            h->d.reset(make_dsys(sys, ctx->c.st));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+        return 0;
+    })
+}
+
+void acrgpu_system_destroy(acrgpu_dsystem* s) { delete s; }
+
+static int factor_impl(acrgpu_ctx* ctx, const DSys& ds, const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err);
+
 int acrgpu_factor(acrgpu_ctx* ctx, const acrgpu_system* sys, const acrgpu_config* cfg, acrgpu_fact** out,
                   acrgpu_error* err) {
     ABI_TRY({
         *out = nullptr;
         if (!ctx || !sys || !cfg) throw AcrError{ACRGPU_E_USAGE, "null argument"};
-        if (sys->n < 1 || sys->dim < 1) throw AcrError{ACRGPU_E_DIMENSION, "acr_factor: empty system"};
+        if (cfg->stop_planes < 1) throw AcrError{ACRGPU_E_USAGE, "acr_factor: stop_planes must be >= 1"};
+        std::unique_ptr<DSys> ds(make_dsys(sys, ctx->c.st));
+        return factor_impl(ctx, *ds, cfg, out, err);
+    })
+}
+
+int acrgpu_factor_resident(acrgpu_ctx* ctx, const acrgpu_dsystem* sys, const acrgpu_config* cfg, acrgpu_fact** out,
+                           acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
+        if (!ctx || !sys || !cfg) throw AcrError{ACRGPU_E_USAGE, "null argument"};
+        return factor_impl(ctx, *sys->d, cfg, out, err);
+    })
+}
+
+static int factor_impl(acrgpu_ctx* ctx, const DSys& ds, const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err) {
+    const DSys* sys = &ds;
+    ABI_TRY({
+        *out = nullptr;
         if (cfg->stop_planes < 1) throw AcrError{ACRGPU_E_USAGE, "acr_factor: stop_planes must be >= 1"};
         if (cfg->leaf_size > DENSE_MAX)
             throw AcrError{ACRGPU_E_USAGE, "GPU path: leaf_size above 64 is not supported"};
@@ -1449,13 +1607,13 @@ int acrgpu_factor(acrgpu_ctx* ctx, const acrgpu_system* sys, const acrgpu_config
         E.ctx = &ctx->c;
         E.cfg = *cfg;
         E.exact_dd = (cfg->flags & ACRGPU_F_EXACT_DENSE_PRODUCTS) != 0;
-        E.S.build(sys->dim, sys->coords, cfg->leaf_size, cfg->eta, cfg->weak);
+        E.S.build(sys->dim, sys->coords.data(), cfg->leaf_size, cfg->eta, cfg->weak);
         if (E.S.max_dense_dim > DENSE_MAX)
             throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64 rows are not supported"};
         if (!E.S.balanced)
             throw AcrError{ACRGPU_E_USAGE, "GPU path: unbalanced cluster trees (mixed dense/branch products) are not supported"};
         E.prepare_structure();
-        do_factor(F.get(), sys);
+        do_factor(F.get(), *sys);
         *out = F.release();
         return 0;
     })
@@ -1471,6 +1629,7 @@ void acrgpu_factor_destroy(acrgpu_fact* f) {
     f->apexE.clear();
     f->apexF.clear();
     cudaStreamSynchronize(st);
+    if (f->ubuf) cudaFree(f->ubuf);
     delete f;
 }
 

@@ -1252,6 +1252,29 @@ __global__ void k_scatter(ScatterArgs a, BatchViews bv) {
 
 __global__ void k_reset_counter(unsigned long long* ctr) { *ctr = 0; }
 
+// Factor compaction: copy every low-rank leaf (U then V) of a batch of stores into
+// one exact-size buffer at host-computed offsets and repoint the leaf tables.
+__global__ void k_compact(CompactArgs a) {
+    const int leaf = blockIdx.x, s = blockIdx.y;
+    const long off = a.off[(size_t)s * a.nleaf + leaf];
+    if (off < 0) return;
+    double** U = a.U[s];
+    double** V = a.V[s];
+    const int r = a.rank[s][leaf];
+    const int m = a.km[leaf], n = a.kn[leaf];
+    double* dst = a.base + off;
+    const double* u = U[leaf];
+    const double* v = V[leaf];
+    for (long e = threadIdx.x; e < (long)m * r; e += blockDim.x) dst[e] = u[e];
+    for (long e = threadIdx.x; e < (long)n * r; e += blockDim.x) dst[(long)m * r + e] = v[e];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        U[leaf] = dst;
+        V[leaf] = dst + (long)m * r;
+    }
+}
+
+
 // ------------------------------------------------------------------ register-resident small-block kernels
 // Shared task plumbing: part ranks, output slot writes, nominal flops.
 struct SmallTaskIO {
@@ -1463,6 +1486,34 @@ struct ProfRec {
     long ctas;
 };
 static std::vector<ProfRec> g_prof;
+static std::vector<std::string> g_kernel_names;
+static FlopLedger* g_report_ledger = nullptr;  // device ledgers [MAX_KERNELS] of the active context
+int kernel_id(const char* name) {
+    for (size_t i = 0; i < g_kernel_names.size(); ++i)
+        if (g_kernel_names[i] == name) return (int)i;
+    g_kernel_names.push_back(name);
+    return (int)g_kernel_names.size() - 1;
+}
+static FlopLedger* ledger(FlopLedger* base, const char* name) {
+    if (!base) return nullptr;
+    const int id = kernel_id(name);
+    return id < MAX_KERNELS ? base + id : base;
+}
+void set_report_ledger(FlopLedger* l) { g_report_ledger = l; }
+static std::map<std::string, double> g_flop_acc;  // folded per-kernel nominal flops
+// Fold the device ledgers into the host accumulators (called before every ledger reset
+// and by prof_report), so totals survive across factorizations.
+void fold_ledger() {
+    if (!g_report_ledger) return;
+    std::vector<FlopLedger> led(MAX_KERNELS);
+    cudaMemcpy(led.data(), g_report_ledger, MAX_KERNELS * sizeof(FlopLedger), cudaMemcpyDeviceToHost);
+    for (size_t id = 0; id < g_kernel_names.size() && id < (size_t)MAX_KERNELS; ++id) {
+        double fl = 0;
+        for (int c = 0; c < F_NCLASS; ++c) fl += led[id].f[c];
+        g_flop_acc[g_kernel_names[id]] += fl;
+    }
+    cudaMemset(g_report_ledger, 0, MAX_KERNELS * sizeof(FlopLedger));
+}
 static std::map<std::string, std::tuple<double, long, long>> g_prof_acc;  // ms, launches, ctas
 static int g_prof_on = -1;
 static bool prof_on() {
@@ -1507,13 +1558,18 @@ void prof_flush() {
 }
 std::string prof_report(bool reset) {
     prof_flush();
+    fold_ledger();
     std::string out;
-    char buf[256];
+    char buf[320];
     for (auto& [k, v] : g_prof_acc) {
-        snprintf(buf, sizeof(buf), "%s %.3f %ld %ld\n", k.c_str(), std::get<0>(v), std::get<1>(v), std::get<2>(v));
+        const double fl = g_flop_acc.count(k) ? g_flop_acc[k] : 0.0;
+        snprintf(buf, sizeof(buf), "%s %.3f %ld %ld %.6e\n", k.c_str(), std::get<0>(v), std::get<1>(v), std::get<2>(v), fl);
         out += buf;
     }
-    if (reset) g_prof_acc.clear();
+    if (reset) {
+        g_prof_acc.clear();
+        g_flop_acc.clear();
+    }
     return out;
 }
 
@@ -1530,67 +1586,43 @@ void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const 
                      double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
                      Arena work, FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
-    TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, work, flops};
-    ProfScope _ps(st, "k_truncate", (long)((ntasks)*(B)));
+    TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, work,
+                ledger(flops, "k_truncate")};
+    ProfScope _ps(st, "k_truncate", (long)ntasks * B);
     k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
 }
 
 void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots,
                         int B, double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
-                        FlopLedger* flops, const BatchViews& bv) {
+                        Arena work, FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
-    TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, out_arena, flops};
+    const char* name = nc == 32 ? "k_trunc_small32" : "k_trunc_mid64";
+    TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, work, ledger(flops, name)};
     DDArgs d{};
-    static const bool cta32 = getenv("ACRGPU_CTA32") != nullptr;
-    if (nc == 32 && cta32) {
-        ProfScope _ps(st, "k_trunc_cta32", (long)ntasks * B);
-        k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
-    } else if (nc == 32) {
-        ProfScope _ps(st, "k_trunc_small32", (long)ntasks * B);
-        k_small32<0><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
-    } else {
-        ProfScope _ps(st, "k_trunc_mid64", (long)ntasks * B);
-        k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
-    }
+    ProfScope _ps(st, name, (long)ntasks * B);
+    if (nc == 32) k_small32<0><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
+    else k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
 }
 
 void launch_dd_small(cudaStream_t st, int nc, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps,
                      Arena out_arena, FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
-    DDArgs d{tasks, slots, B, eps, out_arena, flops};
+    const char* name = nc == 32 ? "k_dd_small32" : "k_dd_mid64";
+    DDArgs d{tasks, slots, B, eps, out_arena, ledger(flops, name)};
     TruncArgs a{};
-    static const bool cta32 = getenv("ACRGPU_CTA32") != nullptr;
-    if (nc == 32 && cta32) {
-        ProfScope _ps(st, "k_dd_cta32", (long)ntasks * B);
-        k_dd_product<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(d, bv);
-    } else if (nc == 32) {
-        ProfScope _ps(st, "k_dd_small32", (long)ntasks * B);
-        k_small32<1><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
-    } else {
-        ProfScope _ps(st, "k_dd_mid64", (long)ntasks * B);
-        k_dd_product<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(d, bv);
-    }
+    ProfScope _ps(st, name, (long)ntasks * B);
+    if (nc == 32) k_small32<1><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
+    else k_dd_product<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(d, bv);
 }
 
 void launch_sigma1_small(cudaStream_t st, int nc, int nleaf, const long* doff, const int* dm, const int* dn, int B,
                          double* sig_out, FlopLedger* flops, const BatchViews& bv) {
     if (nleaf == 0 || B == 0) return;
-    Sig1Args a{doff, dm, dn, nleaf, B, sig_out, flops};
-    if (nc == 32) {
-        ProfScope _ps(st, "k_sigma1_32", (long)nleaf * B);
-        k_sigma1_32<<<dim3((nleaf + 1) / 2, B), 64, 0, st>>>(a, bv);
-    } else {
-        ProfScope _ps(st, "k_sigma1_mid64", (long)nleaf * B);
-        k_sigma1_dense<<<dim3(nleaf, B), NT, trunc_smem(), st>>>(a, bv);
-    }
-}
-
-void launch_dd(cudaStream_t st, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps, Arena out_arena,
-               FlopLedger* flops, const BatchViews& bv) {
-    if (ntasks == 0 || B == 0) return;
-    DDArgs a{tasks, slots, B, eps, out_arena, flops};
-    ProfScope _ps(st, "k_dd_product", (long)((ntasks)*(B)));
-    k_dd_product<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+    const char* name = nc == 32 ? "k_sigma1_32" : "k_sigma1_mid64";
+    Sig1Args a{doff, dm, dn, nleaf, B, sig_out, ledger(flops, name)};
+    ProfScope _ps(st, name, (long)nleaf * B);
+    if (nc == 32) k_sigma1_32<<<dim3((nleaf + 1) / 2, B), 64, 0, st>>>(a, bv);
+    else k_sigma1_dense<<<dim3(nleaf, B), NT, trunc_smem(), st>>>(a, bv);
 }
 
 void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slot* slots, int B, Arena arena,
@@ -1605,7 +1637,7 @@ void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slo
 void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
                   Slot* slots, int B, FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
-    ApplyArgs a{tasks, leaves, slots, B, 0, x_ld, flops};
+    ApplyArgs a{tasks, leaves, slots, B, 0, x_ld, ledger(flops, "k_apply")};
     ProfScope _ps(st, "k_apply", (long)((ntasks)*(B)));
     k_apply<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
 }
@@ -1613,7 +1645,7 @@ void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const App
 void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Part* parts, const Slot* slots, int B,
                     FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
-    DepArgs a{tasks, parts, slots, B, flops};
+    DepArgs a{tasks, parts, slots, B, ledger(flops, "k_deposit")};
     ProfScope _ps(st, "k_deposit", (long)((ntasks)*(B)));
     k_deposit<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
 }
@@ -1621,19 +1653,10 @@ void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Par
 void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, unsigned long long call_id,
                FlopLedger* flops, const BatchViews& bv, int maxm) {
     if (ntasks == 0 || bv.count == 0) return;
-    LuArgs a{tasks, err, call_id, flops};
+    LuArgs a{tasks, err, call_id, ledger(flops, "k_lu_inverse")};
     const size_t sm = (2 * (size_t)maxm * maxm + 2 * maxm) * sizeof(double);
     ProfScope _ps(st, "k_lu_inverse", (long)((ntasks)*(bv.count)));
     k_lu_inverse<<<dim3(ntasks, bv.count), NT, sm, st>>>(a, bv);
-}
-
-void launch_sigma1_dense(cudaStream_t st, int nleaf, const long* doff, const int* dm, const int* dn, int B,
-                         double* sig_out, FlopLedger* flops, const BatchViews& bv, int maxm) {
-    if (nleaf == 0 || B == 0) return;
-    Sig1Args a{doff, dm, dn, nleaf, B, sig_out, flops};
-    const size_t sm = ((size_t)maxm * maxm + maxm) * sizeof(double);
-    ProfScope _ps(st, "k_sigma1_dense", (long)((nleaf)*(B)));
-    k_sigma1_dense<<<dim3(nleaf, B), NT, sm, st>>>(a, bv);
 }
 
 void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,
@@ -1646,7 +1669,7 @@ void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const dou
 void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, int nrhs, int dim,
                    FlopLedger* flops, const MatvecBatch& mb) {
     if (ntasks == 0 || mb.count == 0) return;
-    MatvecArgs a{tasks, leaves, nrhs, dim, flops};
+    MatvecArgs a{tasks, leaves, nrhs, dim, ledger(flops, "k_matvec")};
     ProfScope _ps(st, "k_matvec", (long)((ntasks)*(mb.count)));
     k_matvec<<<dim3(ntasks, mb.count), NT, 0, st>>>(a, mb);
 }
@@ -1692,6 +1715,12 @@ void launch_scatter(cudaStream_t st, const ScatterLaunch& s, const BatchViews& b
 void launch_reset_counter(cudaStream_t st, unsigned long long* ctr) {
     ProfScope _ps(st, "k_reset_counter", (long)(1));
     k_reset_counter<<<1, 1, 0, st>>>(ctr);
+}
+
+void launch_compact(cudaStream_t st, const CompactArgs& a, int nstores) {
+    if (nstores == 0 || a.nleaf == 0) return;
+    ProfScope _ps(st, "k_compact", (long)a.nleaf * nstores);
+    k_compact<<<dim3(a.nleaf, nstores), 128, 0, st>>>(a);
 }
 
 }  // namespace acrgpu

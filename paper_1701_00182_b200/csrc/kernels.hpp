@@ -9,7 +9,8 @@
 
 namespace acrgpu {
 
-constexpr int DENSE_MAX = 64;               // dense route / dense leaf limit
+constexpr int DENSE_MAX = 64;
+constexpr int MAX_KERNELS = 32;             // per-kernel flop ledgers               // dense route / dense leaf limit
 constexpr size_t SMEM_TRUNC = 112 * 1024;   // dynamic smem of k_truncate / k_dd_product
 
 struct ScatterLaunch {
@@ -29,16 +30,31 @@ struct ScatterLaunch {
     int* rk_hits;
 };
 
+struct CompactArgs {
+    double* base;
+    const long* off;      // [store][leaf] (-1: rank 0)
+    double** const* U;    // per store: U pointer table
+    double** const* V;
+    int* const* rank;     // per store: rank table
+    const int* km;
+    const int* kn;
+    int nleaf;
+};
+void launch_compact(cudaStream_t st, const CompactArgs& a, int nstores);
+
 void setup_kernels();
 long launches_take();
 std::string prof_report(bool reset);
+void set_report_ledger(FlopLedger* l);
+void fold_ledger();
+int kernel_id(const char* name);
 
 void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots, int B,
                      double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
                      Arena work, FlopLedger* flops, const BatchViews& bv);
 void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots,
                         int B, double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
-                        FlopLedger* flops, const BatchViews& bv);
+                        Arena work, FlopLedger* flops, const BatchViews& bv);
 void launch_dd_small(cudaStream_t st, int nc, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps,
                      Arena out_arena, FlopLedger* flops, const BatchViews& bv);
 void launch_sigma1_small(cudaStream_t st, int nc, int nleaf, const long* doff, const int* dm, const int* dn, int B,
@@ -53,8 +69,6 @@ void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Par
                     FlopLedger* flops, const BatchViews& bv);
 void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, unsigned long long call_id,
                FlopLedger* flops, const BatchViews& bv, int maxm);
-void launch_sigma1_dense(cudaStream_t st, int nleaf, const long* doff, const int* dm, const int* dn, int B,
-                         double* sig_out, FlopLedger* flops, const BatchViews& bv, int maxm);
 void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,
                          double* abs_cut);
 void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, int nrhs, int dim,
