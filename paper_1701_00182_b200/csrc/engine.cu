@@ -68,19 +68,31 @@ static T* upload(const std::vector<T>& v, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ context
-struct Ctx {
-    int device = 0;
+// Two execution lanes (stream + transient arena + product slots): independent
+// mult_adds of one recursion step (T12 || T21, C12 || C21 in invert_node; the
+// E'/F' couplings beside the D updates) run concurrently on the GPU.
+constexpr int NLANES = 2;
+struct Lane {
     cudaStream_t st = nullptr;
-    Arena persist{}, trans{};
-    double* persist_base = nullptr;
-    double* trans_base = nullptr;
-    unsigned long long* ctrs = nullptr;  // [0] persist, [1] trans
-    int* overflow = nullptr;             // [0] persist, [1] trans
-    DevError* err = nullptr;
-    FlopLedger* flops = nullptr;
+    Arena trans{};
     Slot* slots = nullptr;
     size_t slots_cap = 0;
-    double* scratch = nullptr;  // sigma / abs-cut scratch
+    cudaEvent_t ev = nullptr;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;  // == lanes[0].st (main stream)
+    Lane lanes[NLANES];
+    int cur = 0;                // active lane
+    Arena persist{};
+    double* persist_base = nullptr;
+    double* trans_base = nullptr;
+    unsigned long long* ctrs = nullptr;  // [0] persist, [1 + l] transient of lane l
+    int* overflow = nullptr;
+    DevError* err = nullptr;
+    FlopLedger* flops = nullptr;
+    double* scratch = nullptr;  // sigma / abs-cut scratch (main lane only)
     size_t scratch_cap = 0;
     unsigned long long call_id = 0;
     std::vector<std::pair<int, std::vector<int>>> call_planes;  // call id -> (level, planes)
@@ -88,28 +100,39 @@ struct Ctx {
     void init(int dev) {
         if (dev >= 0) CK(cudaSetDevice(dev));
         CK(cudaGetDevice(&device));
-        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (auto& l : lanes) {
+            CK(cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&l.ev, cudaEventDisableTiming));
+        }
+        st = lanes[0].st;
         setup_kernels();
         size_t freeb = 0, total = 0;
         CK(cudaMemGetInfo(&freeb, &total));
         const size_t pbytes = (size_t)(freeb * 0.42) & ~(size_t)4095;
-        const size_t tbytes = (size_t)(freeb * 0.14) & ~(size_t)4095;
+        const size_t tbytes = ((size_t)(freeb * 0.14) / NLANES) & ~(size_t)4095;
         persist_base = dmalloc<double>(pbytes / 8);
-        trans_base = dmalloc<double>(tbytes / 8);
-        ctrs = dmalloc<unsigned long long>(2);
-        overflow = dmalloc<int>(2);
+        trans_base = dmalloc<double>(NLANES * tbytes / 8);
+        ctrs = dmalloc<unsigned long long>(1 + NLANES);
+        overflow = dmalloc<int>(1 + NLANES);
         err = dmalloc<DevError>(1);
         flops = dmalloc<FlopLedger>(MAX_KERNELS);
         set_report_ledger(flops);
         persist = Arena{persist_base, pbytes / 8, ctrs, overflow};
-        trans = Arena{trans_base, tbytes / 8, ctrs + 1, overflow + 1};
+        for (int l = 0; l < NLANES; ++l)
+            lanes[l].trans = Arena{trans_base + (size_t)l * (tbytes / 8), tbytes / 8, ctrs + 1 + l, overflow + 1 + l};
         reset_all();
     }
+    Lane& lane() { return lanes[cur]; }
+    // lane `to` waits for the work issued so far on lane `from`
+    void depend(int to, int from) {
+        CK(cudaEventRecord(lanes[from].ev, lanes[from].st));
+        CK(cudaStreamWaitEvent(lanes[to].st, lanes[from].ev, 0));
+    }
     void reset_all() {
-        CK(cudaStreamSynchronize(st));
+        for (auto& l : lanes) CK(cudaStreamSynchronize(l.st));
         fold_ledger();
-        CK(cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned long long), st));
-        CK(cudaMemsetAsync(overflow, 0, 2 * sizeof(int), st));
+        CK(cudaMemsetAsync(ctrs, 0, (1 + NLANES) * sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(overflow, 0, (1 + NLANES) * sizeof(int), st));
         DevError e0;
         std::memset(&e0, 0, sizeof(e0));
         e0.key = ~0ull;
@@ -118,19 +141,21 @@ struct Ctx {
         CK(cudaStreamSynchronize(st));
         call_id = 0;
         call_planes.clear();
+        cur = 0;
     }
     Slot* get_slots(size_t n) {
-        if (n > slots_cap) {
-            CK(cudaStreamSynchronize(st));
-            if (slots) cudaFree(slots);
-            slots_cap = std::max(n, slots_cap * 2);
-            slots = dmalloc<Slot>(slots_cap);
+        Lane& l = lane();
+        if (n > l.slots_cap) {
+            for (auto& x : lanes) CK(cudaStreamSynchronize(x.st));
+            if (l.slots) cudaFree(l.slots);
+            l.slots_cap = std::max(n, l.slots_cap * 2);
+            l.slots = dmalloc<Slot>(l.slots_cap);
         }
-        return slots;
+        return l.slots;
     }
     double* get_scratch(size_t n) {
         if (n > scratch_cap) {
-            CK(cudaStreamSynchronize(st));
+            for (auto& x : lanes) CK(cudaStreamSynchronize(x.st));
             if (scratch) cudaFree(scratch);
             scratch_cap = std::max(n, scratch_cap * 2);
             scratch = dmalloc<double>(scratch_cap);
@@ -138,10 +163,16 @@ struct Ctx {
         return scratch;
     }
     void destroy() {
-        if (st) cudaStreamSynchronize(st);
-        for (void* p : std::initializer_list<void*>{persist_base, trans_base, ctrs, overflow, err, flops, slots, scratch})
+        for (auto& l : lanes)
+            if (l.st) cudaStreamSynchronize(l.st);
+        for (void* p : std::initializer_list<void*>{persist_base, trans_base, ctrs, overflow, err, flops, scratch})
             if (p) cudaFree(p);
-        if (st) cudaStreamDestroy(st);
+        for (auto& l : lanes) {
+            if (l.slots) cudaFree(l.slots);
+            if (l.ev) cudaEventDestroy(l.ev);
+            if (l.st) cudaStreamDestroy(l.st);
+            l = Lane{};
+        }
         st = nullptr;
     }
 };
@@ -169,14 +200,16 @@ struct View {  // (store, sub-node)
 // ------------------------------------------------------------------ compiled plans
 // Task lists split by block size class: blocks <= 32 and <= 64 run the
 // register-resident Jacobi kernels (2*NC threads), larger ones the QR route.
+constexpr int NCLASS = 4;
 template <class T>
 struct Classed {
-    T* p[3] = {nullptr, nullptr, nullptr};
-    int n[3] = {0, 0, 0};
+    T* p[NCLASS] = {nullptr, nullptr, nullptr, nullptr};
+    int n[NCLASS] = {0, 0, 0, 0};
 };
+// 0: <= 32 (warp engine), 1: <= 64, 2: <= 128 (CTA engine, dense route), 3: QR route
 static int size_class(int m, int n) {
     const int x = m > n ? m : n;
-    return x <= 32 ? 0 : (x <= 64 ? 1 : 2);
+    return x <= 32 ? 0 : (x <= 64 ? 1 : (x <= 128 ? 2 : 3));
 }
 
 struct Plan {
@@ -210,7 +243,7 @@ struct Engine {
     TruncTask* leaf_tasks = nullptr;  // one per Rk leaf (recompress)
     Part* leaf_parts = nullptr;
     Classed<TruncTask> leaf_cls;      // the same, split by size class
-    int leaf_cls_off[3] = {0, 0, 0};
+    int leaf_cls_off[NCLASS] = {0, 0, 0, 0};
     SlabTask* slabs = nullptr;        // matvec slabs of the root
     ApplyLeaf* slab_leaves = nullptr;
     int nslabs = 0;
@@ -223,18 +256,22 @@ struct Engine {
         dev_allocs.push_back((void*)p);
         return p;
     }
+    // Plan / structure tables: synchronous upload (compiled once; may be consumed by either lane).
     template <class T>
     T* up(const std::vector<T>& v) {
-        return keep(upload(v, ctx->st));
+        T* p = dmalloc<T>(v.size());
+        if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+        return keep(p);
     }
-    cudaStream_t st() const { return ctx->st; }
+    cudaStream_t st() const { return ctx->lanes[ctx->cur].st; }
+    cudaStream_t main_st() const { return ctx->st; }
 
     template <class T>
     Classed<T> up_classed(const std::vector<T>& v) {
         Classed<T> c;
-        std::vector<T> parts[3];
+        std::vector<T> parts[NCLASS];
         for (const T& t : v) parts[size_class(t.m, t.n)].push_back(t);
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < NCLASS; ++k) {
             c.n[k] = (int)parts[k].size();
             if (c.n[k]) c.p[k] = up(parts[k]);
         }
@@ -243,12 +280,15 @@ struct Engine {
 
     void run_trunc(const Classed<TruncTask>& tl, const Part* parts, Slot* slots, int nb, double eps,
                    const double* abs_cut, double* sig_out, bool values_only, Arena out, const BatchViews& bv) {
+        const Arena tr = ctx->lane().trans;
         if (tl.n[0]) launch_trunc_small(st(), 32, tl.n[0], tl.p[0], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
-                                        ctx->trans, ctx->flops, bv);
+                                        tr, ctx->flops, bv);
         if (tl.n[1]) launch_trunc_small(st(), 64, tl.n[1], tl.p[1], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
-                                        ctx->trans, ctx->flops, bv);
+                                        tr, ctx->flops, bv);
         if (tl.n[2]) launch_truncate(st(), tl.n[2], tl.p[2], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
-                                     ctx->trans, ctx->flops, bv);
+                                     tr, ctx->flops, bv, "k_trunc_d128");
+        if (tl.n[3]) launch_truncate(st(), tl.n[3], tl.p[3], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
+                                     tr, ctx->flops, bv, "k_trunc_qr");
     }
 
     // -------------------------------------------------------------- storage
@@ -258,13 +298,13 @@ struct Engine {
         const size_t bytes = n.dsize * 8 + nk * 16 + nk * 4 + 64;
         auto s = std::make_shared<Store>();
         s->node = node;
-        CK(cudaMallocAsync(&s->block, bytes, st()));
+        CK(cudaMallocAsync(&s->block, bytes, main_st()));
         char* p = (char*)s->block;
         s->dense = (double*)p;
         s->U = (double**)(p + n.dsize * 8);
         s->V = s->U + nk;
         s->rank = (int*)(s->V + nk);
-        cudaStream_t stream = st();
+        cudaStream_t stream = main_st();
         return StoreP(s.get(), [s, stream](Store*) mutable {
             if (s->block) cudaFreeAsync(s->block, stream);
             s->block = nullptr;
@@ -615,16 +655,34 @@ struct Engine {
                 bv.b[b] = hview(B[i0 + b]);
             }
             Slot* slots = ctx->get_slots((size_t)std::max(1, P->nprod) * nb);
-            launch_reset_counter(st(), ctx->trans.ctr);
-            launch_alloc_apply(st(), P->nalloc, P->allocs, slots, nb, ctx->trans, bv);
+            const Arena tr = ctx->lane().trans;
+            launch_reset_counter(st(), tr.ctr);
+            launch_alloc_apply(st(), P->nalloc, P->allocs, slots, nb, tr, bv);
             launch_apply(st(), P->napply, P->applies, P->aleaves, P->x_ld, slots, nb, ctx->flops, bv);
-            if (P->dds.n[0]) launch_dd_small(st(), 32, P->dds.n[0], P->dds.p[0], slots, nb, eps, ctx->trans, ctx->flops, bv);
-            if (P->dds.n[1]) launch_dd_small(st(), 64, P->dds.n[1], P->dds.p[1], slots, nb, eps, ctx->trans, ctx->flops, bv);
-            if (P->dds.n[2]) throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64"};
-            for (auto& ph : P->bb) run_trunc(ph, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->trans, bv);
+            if (P->dds.n[0]) launch_dd_small(st(), 32, P->dds.n[0], P->dds.p[0], slots, nb, eps, tr, ctx->flops, bv);
+            if (P->dds.n[1]) launch_dd_small(st(), 64, P->dds.n[1], P->dds.p[1], slots, nb, eps, tr, ctx->flops, bv);
+            if (P->dds.n[2] || P->dds.n[3]) throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64"};
+            for (auto& ph : P->bb) run_trunc(ph, P->parts, slots, nb, eps, nullptr, nullptr, false, tr, bv);
             launch_deposit(st(), P->ndep, P->deps, P->parts, slots, nb, ctx->flops, bv);
             run_trunc(P->flush, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->persist, bv);
         }
+    }
+
+    // Run two independent operations concurrently: f0 on lane 0, f1 on lane 1 (both issued
+    // after everything already queued on lane 0; lane 0 continues after both).
+    template <class F0, class F1>
+    void pair(F0&& f0, F1&& f1) {
+        if (NLANES < 2 || ctx->cur != 0) {
+            f0();
+            f1();
+            return;
+        }
+        ctx->depend(1, 0);
+        f0();
+        ctx->cur = 1;
+        f1();
+        ctx->cur = 0;
+        ctx->depend(0, 1);
     }
 
     // out = inverse(in) (reference invert_node, hmatrix.cpp:483-534); out views pre-allocated
@@ -675,20 +733,18 @@ struct Engine {
         auto X11 = ch(out, 0), C12 = ch(out, 1), C21 = ch(out, 2), X22 = ch(out, 3);
         invert(X11, A11, level, planes);
         auto T12 = fresh(n.ch[1], in.size());
-        zero(T12);
-        mult_add(T12, X11, A12, 1.0);
         auto T21 = fresh(n.ch[2], in.size());
+        zero(T12);
         zero(T21);
-        mult_add(T21, A21, X11, 1.0);
+        pair([&] { mult_add(T12, X11, A12, 1.0); }, [&] { mult_add(T21, A21, X11, 1.0); });
         {
             auto Sc = clone(A22);
             mult_add(Sc, A21, T12, -1.0);
             invert(X22, Sc, level, planes);
         }
         zero(C12);
-        mult_add(C12, T12, X22, -1.0);
         zero(C21);
-        mult_add(C21, X22, T21, -1.0);
+        pair([&] { mult_add(C12, T12, X22, -1.0); }, [&] { mult_add(C21, X22, T21, -1.0); });
         mult_add(X11, T12, C21, -1.0);
     }
 
@@ -708,8 +764,8 @@ struct Engine {
             launch_sigma1_small(st(), S.max_dense_dim <= 32 ? 32 : 64, nd, d_doff, d_dm, d_dn, nb, sig_d, ctx->flops, bv);
             Slot* slots = ctx->get_slots(1);
             // sigma_1 per Rk leaf (values only); per-class task lists index sig_k by class offset
-            launch_reset_counter(st(), ctx->trans.ctr);
-            for (int c = 0; c < 3; ++c)
+            launch_reset_counter(st(), ctx->lane().trans.ctr);
+            for (int c = 0; c < NCLASS; ++c)
                 if (leaf_cls.n[c]) {
                     Classed<TruncTask> one;
                     one.p[c] = leaf_cls.p[c];
@@ -718,7 +774,7 @@ struct Engine {
                               ctx->persist, bv);
                 }
             launch_scale_reduce(st(), sig_d, nd, sig_k, nk, nb, cfg.eps, cut);
-            launch_reset_counter(st(), ctx->trans.ctr);
+            launch_reset_counter(st(), ctx->lane().trans.ctr);
             run_trunc(leaf_cls, leaf_parts, slots, nb, 0.0, cut, nullptr, false, ctx->persist, bv);
         }
     }
@@ -764,6 +820,7 @@ struct Engine {
         leaf_cls_off[0] = 0;
         leaf_cls_off[1] = leaf_cls.n[0];
         leaf_cls_off[2] = leaf_cls.n[0] + leaf_cls.n[1];
+        leaf_cls_off[3] = leaf_cls_off[2] + leaf_cls.n[2];
         // matvec slabs over leaf clusters (non-transposed apply of the root)
         std::vector<int> lv;
         subtree_leaves(0, lv);
@@ -1021,9 +1078,9 @@ static std::vector<SP> lift(Engine& E, const DSys& ds) {
             bv.count = 1;
             bv.c[0] = E.hview(vs[b]);
             Slot* slots = E.ctx->get_slots(1);
-            launch_reset_counter(st, E.ctx->trans.ctr);
+            launch_reset_counter(st, E.ctx->lane().trans.ctr);
             launch_truncate(st, S.n_rk(), E.leaf_tasks, E.leaf_parts, slots, 1, E.cfg.eps, nullptr, nullptr, false,
-                            E.ctx->persist, E.ctx->trans, E.ctx->flops, bv);
+                            E.ctx->persist, E.ctx->lane().trans, E.ctx->flops, bv);
         }
     }
     // leaf memory cap for dense leaves (build_from_sparse, hmatrix.cpp:117-121)
@@ -1187,61 +1244,57 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
         std::vector<SP> Dn(mn), En(mn), Fn(mn);
         for (int t = 0; t < mn; ++t) Dn[t] = D[L.ret[t]];
         auto at = [&](const std::vector<SP>& v, int j) -> SP { return (j < 0 || j >= (int)v.size()) ? nullptr : v[j]; };
+        // Per side (lo: eliminated j-1, hi: eliminated j+1) three batched mult_adds:
+        //   T = E_j Dinv_{j-1};  D_j -= T F_{j-1};  E' = -T E_{j-1}      (mirrored for hi).
+        // Schedule over the two lanes: T_lo || T_hi, then {D_lo; D_hi} on lane 0 (same D_j,
+        // reference order lo then hi) || {E'; F'} on lane 1.
+        struct SideOps {
+            std::vector<SP> Ts;
+            std::vector<View> Tv, Cpl, Dnb;                 // T = Cpl * Dnb
+            std::vector<View> dc, da, db;                   // D -= T * x
+            std::vector<View> nc, na, nb;                   // new coupling = -T * y
+        } ops[2];
         for (int side = 0; side < 2; ++side) {
-            std::vector<int> ts;
+            SideOps& o = ops[side];
             for (int t = 0; t < mn; ++t) {
                 const int j = L.ret[t];
-                const int nb = side == 0 ? j - 1 : j + 1;
-                if (nb >= 0 && nb < m && is_elim[nb]) ts.push_back(t);
-            }
-            if (ts.empty()) continue;
-            std::vector<View> Tv, Cpl, Dnb;
-            std::vector<SP> Ts;
-            for (int t : ts) {
-                const int j = L.ret[t];
-                const int nb = side == 0 ? j - 1 : j + 1;
-                Ts.push_back(E.new_store(0));
-                Tv.push_back(root_view(Ts.back()));
+                const int nbp = side == 0 ? j - 1 : j + 1;
+                if (!(nbp >= 0 && nbp < m && is_elim[nbp])) continue;
+                o.Ts.push_back(E.new_store(0));
+                const View T = root_view(o.Ts.back());
+                o.Tv.push_back(T);
                 SP cpl = side == 0 ? at(L.E, j) : at(L.F, j);
                 if (!cpl) throw AcrError{ACRGPU_E_INTERNAL, "missing coupling block"};
-                Cpl.push_back(root_view(cpl));
-                Dnb.push_back(root_view(L.Dinv[nb]));
-            }
-            E.zero(Tv);
-            E.mult_add(Tv, Cpl, Dnb, 1.0);  // T = E_j Dinv_{j-1}  (or F_j Dinv_{j+1})
-            // D_j -= T * F_{j-1}   (or T * E_{j+1})
-            {
-                std::vector<View> c, a, b;
-                for (size_t q = 0; q < ts.size(); ++q) {
-                    const int j = L.ret[ts[q]];
-                    const int nb = side == 0 ? j - 1 : j + 1;
-                    SP x = side == 0 ? at(L.F, nb) : at(L.E, nb);
-                    if (!x) continue;
-                    c.push_back(root_view(Dn[ts[q]]));
-                    a.push_back(Tv[q]);
-                    b.push_back(root_view(x));
+                o.Cpl.push_back(root_view(cpl));
+                o.Dnb.push_back(root_view(L.Dinv[nbp]));
+                if (SP x = side == 0 ? at(L.F, nbp) : at(L.E, nbp)) {
+                    o.dc.push_back(root_view(Dn[t]));
+                    o.da.push_back(T);
+                    o.db.push_back(root_view(x));
                 }
-                E.mult_add(c, a, b, -1.0);
-            }
-            // new coupling: E' = -T * E_{j-1}  (or F' = -T * F_{j+1})
-            {
-                std::vector<View> c, a, b;
-                std::vector<int> owners;
-                for (size_t q = 0; q < ts.size(); ++q) {
-                    const int j = L.ret[ts[q]];
-                    const int nb = side == 0 ? j - 1 : j + 1;
-                    SP x = side == 0 ? at(L.E, nb) : at(L.F, nb);
-                    if (!x) continue;
+                if (SP y = side == 0 ? at(L.E, nbp) : at(L.F, nbp)) {
                     SP nw = E.new_store(0);
-                    (side == 0 ? En : Fn)[ts[q]] = nw;
-                    c.push_back(root_view(nw));
-                    a.push_back(Tv[q]);
-                    b.push_back(root_view(x));
+                    (side == 0 ? En : Fn)[t] = nw;
+                    o.nc.push_back(root_view(nw));
+                    o.na.push_back(T);
+                    o.nb.push_back(root_view(y));
                 }
-                E.zero(c);
-                E.mult_add(c, a, b, -1.0);
             }
+            E.zero(o.Tv);
+            E.zero(o.nc);
         }
+        E.pair([&] { E.mult_add(ops[0].Tv, ops[0].Cpl, ops[0].Dnb, 1.0); },
+               [&] { E.mult_add(ops[1].Tv, ops[1].Cpl, ops[1].Dnb, 1.0); });
+        E.ctx->depend(0, 1);  // both T batches visible to both lanes
+        E.pair(
+            [&] {
+                E.mult_add(ops[0].dc, ops[0].da, ops[0].db, -1.0);
+                E.mult_add(ops[1].dc, ops[1].da, ops[1].db, -1.0);
+            },
+            [&] {
+                E.mult_add(ops[0].nc, ops[0].na, ops[0].nb, -1.0);
+                E.mult_add(ops[1].nc, ops[1].na, ops[1].nb, -1.0);
+            });
         // adjacent retained planes keep their coupling (acr.cpp:104-111)
         for (int t = 0; t < mn; ++t) {
             const int j = L.ret[t];

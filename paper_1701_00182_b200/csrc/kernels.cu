@@ -28,7 +28,6 @@
 #include "structure.hpp"
 #include "svd_small.cuh"
 #include "svd_rrqr32.cuh"
-#include "svd_cta.cuh"
 
 namespace acrgpu {
 
@@ -59,6 +58,8 @@ __device__ double* arena_alloc(const Arena& a, unsigned long long n) {
     }
     return a.base + off;
 }
+
+#include "svd_cta.cuh"
 
 __device__ __forceinline__ void add_flops(FlopLedger* L, int cls, double f) {
     if (L && f > 0) atomicAdd(&L->f[cls], f);
@@ -133,6 +134,7 @@ __device__ void jacobi_svd(double* A, int lda, int rows, int cols, double* V, in
                     double* ap = A + (size_t)p * lda;
                     double* aq = A + (size_t)q * lda;
                     double al = 0, be = 0, ga = 0;
+                    #pragma unroll 4
                     for (int e = lane; e < rows; e += 32) {
                         const double x = ap[e], y = aq[e];
                         al = fma(x, x, al);
@@ -148,6 +150,7 @@ __device__ void jacobi_svd(double* A, int lda, int rows, int cols, double* V, in
                     if (fabs(zeta) > 1e150) t = 0.5 / zeta;
                     else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+                    #pragma unroll 4
                     for (int e = lane; e < rows; e += 32) {
                         const double x = ap[e], y = aq[e];
                         ap[e] = c * x - s * y;
@@ -172,6 +175,7 @@ __device__ void jacobi_svd(double* A, int lda, int rows, int cols, double* V, in
     for (int j = warp; j < cols; j += NW) {
         const double* aj = A + (size_t)j * lda;
         double s = 0;
+        #pragma unroll 4
         for (int e = lane; e < rows; e += 32) s = fma(aj[e], aj[e], s);
         s = warp_sum(s);
         if (lane == 0) sig[j] = sqrt(s);
@@ -245,10 +249,12 @@ __device__ void householder_qr(double* W, int ld, int rows, int cols, double* ta
             for (int c = j + 1 + warp; c < cols; c += NW) {
                 double* wc = W + (size_t)c * ld;
                 double s = 0;
+                #pragma unroll 4
                 for (int i = j + 1 + lane; i < rows; i += 32) s = fma(wj[i], wc[i], s);
                 s = warp_sum(s) + wc[j];
                 s *= tj;
                 if (lane == 0) wc[j] -= s;
+                #pragma unroll 4
                 for (int i = j + 1 + lane; i < rows; i += 32) wc[i] -= s * wj[i];
             }
         }
@@ -266,9 +272,11 @@ __device__ void apply_q(const double* W, int ldw, int rows, int k, const double*
             for (int c = warp; c < ncol; c += NW) {
                 double* y = Y + (size_t)c * ldy;
                 double s = 0;
+                #pragma unroll 4
                 for (int i = j + 1 + lane; i < rows; i += 32) s = fma(v[i], y[i], s);
                 s = (warp_sum(s) + y[j]) * tj;
                 if (lane == 0) y[j] -= s;
+                #pragma unroll 4
                 for (int i = j + 1 + lane; i < rows; i += 32) y[i] -= s * v[i];
             }
         }
@@ -384,15 +392,15 @@ __device__ int svd_truncate_dense(double* M, int m, int n, double eps, double ab
 // workspace, Householder QR both factors, SVD the ku x kv core, rebuild
 // U' = Qu Us Sigma, V' = Qv Vs by applying the reflectors.
 // Carve an engine workspace for blocks up to p x p out of `base`.
-__device__ __forceinline__ CtaSvdWork cta_smem_work(double* base, int p) {
+__device__ __forceinline__ CtaSvdWork cta_smem_work(double* base, int p, int rpcap) {
     CtaSvdWork w;
     w.A = base;
     w.lda = p;
     w.W = base + (size_t)p * p;
     w.ldw = p;
-    w.J = w.W + (size_t)p * p;
-    w.ldj = p;
-    w.tau = w.J + (size_t)p * p;
+    w.J = w.W + (size_t)p * rpcap;
+    w.ldj = rpcap;
+    w.tau = w.J + (size_t)rpcap * rpcap;
     w.nrm = w.tau + p;
     w.sig = w.nrm + p;
     w.perm = (int*)(w.sig + p);
@@ -414,7 +422,8 @@ struct TruncArgs {
     FlopLedger* flops;
 };
 
-__global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) {
+template <int DMAX, int RPCAP>
+__global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews bv) {
     extern __shared__ double smem[];
     __shared__ double red[NW];
     __shared__ int sh_K;
@@ -464,9 +473,9 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
     __shared__ double sh_smax;
     __shared__ double* sh_out;
 
-    if (m <= DENSE_MAX && n <= DENSE_MAX) {
+    if (m <= DMAX && n <= DMAX) {
         // ---------------- dense route: M = sum alpha U V^T in shared memory, rank-revealing SVD
-        CtaSvdWork w = cta_smem_work(smem, DENSE_MAX);
+        CtaSvdWork w = cta_smem_work(smem, DMAX, RPCAP);
         double* M = w.A;
         w.lda = m;
         for (int e = threadIdx.x; e < m * n; e += NT) M[e] = 0.0;
@@ -487,7 +496,7 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
         }
         int rp;
         double smax;
-        const int r = cta_trunc_svd<NT>(w, m, n, args.eps, abs_cut, args.values_only != 0, &rp, &smax);
+        const int r = cta_trunc_svd<NT>(w, m, n, args.eps, abs_cut, args.values_only != 0, &rp, &smax, RPCAP, &args.work);
         if (args.values_only) {
             if (threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
         } else {
@@ -515,7 +524,7 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
     // ---------------- QR route
     // workspace: Uc (m x K) | Vc (n x K) | tau_u (K) | tau_v (K) | [core engine work if too big for smem]
     const int pmax = ku > kv ? ku : kv;
-    const bool core_in_smem = pmax <= DENSE_MAX;
+    const bool core_in_smem = pmax <= DMAX;
     if (threadIdx.x == 0) {
         unsigned long long need = (unsigned long long)(m + n) * K + 2ull * K + 32;
         if (!core_in_smem) need += 3ull * pmax * pmax + 6ull * pmax + 64;
@@ -528,7 +537,7 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
     double* Vc = Uc + (size_t)m * K;
     double* tau_u = Vc + (size_t)n * K;
     double* tau_v = tau_u + K;
-    CtaSvdWork w = core_in_smem ? cta_smem_work(smem, DENSE_MAX) : cta_smem_work(tau_v + K + 32, pmax);
+    CtaSvdWork w = core_in_smem ? cta_smem_work(smem, DMAX, RPCAP) : cta_smem_work(tau_v + K + 32, pmax, pmax);
     for (size_t e = threadIdx.x; e < (size_t)(m + n) * K; e += NT) ws[e] = 0.0;
     __syncthreads();
     {
@@ -563,7 +572,8 @@ __global__ void __launch_bounds__(NT) k_truncate(TruncArgs args, BatchViews bv) 
     __syncthreads();
     int rp;
     double smax;
-    const int r = cta_trunc_svd<NT>(w, ku, kv, args.eps, abs_cut, args.values_only != 0, &rp, &smax);
+    const int r = cta_trunc_svd<NT>(w, ku, kv, args.eps, abs_cut, args.values_only != 0, &rp, &smax,
+                                    core_in_smem ? RPCAP : pmax, &args.work);
     if (args.values_only) {
         if (threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
     } else {
@@ -606,7 +616,7 @@ struct DDArgs {
     FlopLedger* flops;
 };
 
-__global__ void __launch_bounds__(NT) k_dd_product(DDArgs args, BatchViews bv) {
+__global__ void __launch_bounds__(NT, 1) k_dd_product(DDArgs args, BatchViews bv) {
     extern __shared__ double smem[];
     __shared__ double* sh_out;
     const DDTask task = args.tasks[blockIdx.x];
@@ -614,7 +624,7 @@ __global__ void __launch_bounds__(NT) k_dd_product(DDArgs args, BatchViews bv) {
     const int m = task.m, k = task.k, n = task.n;
     const double* Ad = bv.a[b].dense + task.da;
     const double* Bd = bv.b[b].dense + task.db;
-    CtaSvdWork w = cta_smem_work(smem, DENSE_MAX);
+    CtaSvdWork w = cta_smem_work(smem, DENSE_MAX, DENSE_MAX);
     double* M = w.A;
     w.lda = m;
     // operands staged in the (not yet used) W / J areas
@@ -632,7 +642,7 @@ __global__ void __launch_bounds__(NT) k_dd_product(DDArgs args, BatchViews bv) {
     __syncthreads();
     int rp;
     double smax;
-    const int r = cta_trunc_svd<NT>(w, m, n, args.eps, 0.0, false, &rp, &smax);
+    const int r = cta_trunc_svd<NT>(w, m, n, args.eps, 0.0, false, &rp, &smax, DENSE_MAX, nullptr);
     if (threadIdx.x == 0) sh_out = r > 0 ? arena_alloc(args.out_arena, (unsigned long long)(m + n) * r) : nullptr;
     __syncthreads();
     double* out = sh_out;
@@ -1034,13 +1044,13 @@ __global__ void __launch_bounds__(NT) k_sigma1_dense(Sig1Args args, BatchViews b
     const int leaf = blockIdx.x, b = blockIdx.y;
     const int m = args.dm[leaf], n = args.dn[leaf];
     const double* D = bv.c[b].dense + args.doff[leaf];
-    CtaSvdWork w = cta_smem_work(smem, DENSE_MAX);
+    CtaSvdWork w = cta_smem_work(smem, DENSE_MAX, DENSE_MAX);
     w.lda = m;
     for (int e = threadIdx.x; e < m * n; e += NT) w.A[e] = D[e];
     __syncthreads();
     int rp;
     double smax;
-    cta_trunc_svd<NT>(w, m, n, 0.0, 0.0, true, &rp, &smax);
+    cta_trunc_svd<NT>(w, m, n, 0.0, 0.0, true, &rp, &smax, DENSE_MAX, nullptr);
     if (threadIdx.x == 0) {
         args.sig_out[(size_t)leaf * args.B + b] = smax;
         double fsvd = 0, fqr = 0, fgemm = 0;
@@ -1574,9 +1584,15 @@ std::string prof_report(bool reset) {
 }
 
 static size_t trunc_smem() { return SMEM_TRUNC; }
+constexpr int BIG_DMAX = 128, BIG_RPCAP = 56;
+static size_t trunc_smem_big() {
+    return ((size_t)BIG_DMAX * BIG_DMAX + (size_t)BIG_DMAX * BIG_RPCAP + (size_t)BIG_RPCAP * BIG_RPCAP + 5 * BIG_DMAX + 64) *
+           sizeof(double);
+}
 
 void setup_kernels() {
-    cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
+    cudaFuncSetAttribute(k_truncate<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
+    cudaFuncSetAttribute(k_truncate<BIG_DMAX, BIG_RPCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_big());
     cudaFuncSetAttribute(k_dd_product, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
     cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaFuncSetAttribute(k_sigma1_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
@@ -1584,12 +1600,12 @@ void setup_kernels() {
 
 void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots, int B,
                      double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
-                     Arena work, FlopLedger* flops, const BatchViews& bv) {
+                     Arena work, FlopLedger* flops, const BatchViews& bv, const char* name) {
     if (ntasks == 0 || B == 0) return;
     TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, work,
-                ledger(flops, "k_truncate")};
-    ProfScope _ps(st, "k_truncate", (long)ntasks * B);
-    k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+                ledger(flops, name)};
+    ProfScope _ps(st, name, (long)ntasks * B);
+    k_truncate<BIG_DMAX, BIG_RPCAP><<<dim3(ntasks, B), NT, trunc_smem_big(), st>>>(a, bv);
 }
 
 void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots,
@@ -1601,7 +1617,7 @@ void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* ta
     DDArgs d{};
     ProfScope _ps(st, name, (long)ntasks * B);
     if (nc == 32) k_small32<0><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
-    else k_truncate<<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+    else k_truncate<64, 64><<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
 }
 
 void launch_dd_small(cudaStream_t st, int nc, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps,

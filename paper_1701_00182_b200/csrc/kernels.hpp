@@ -51,7 +51,7 @@ int kernel_id(const char* name);
 
 void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots, int B,
                      double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
-                     Arena work, FlopLedger* flops, const BatchViews& bv);
+                     Arena work, FlopLedger* flops, const BatchViews& bv, const char* name = "k_truncate");
 void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots,
                         int B, double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
                         Arena work, FlopLedger* flops, const BatchViews& bv);

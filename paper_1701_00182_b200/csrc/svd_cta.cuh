@@ -8,8 +8,7 @@
 //   3. U' = Q [J Sigma; 0], V' = P W Sigma^{-1}.
 // Reference semantics: truncate_impl / dense_to_lowrank, hmatrix.cpp:56-99.
 #pragma once
-
-namespace acrgpu {
+// (included inside namespace acrgpu by kernels.cu, after arena_alloc)
 
 struct CtaSvdWork {
     double* A;      // rows x cols (ld = lda): input, then R + reflectors
@@ -41,6 +40,7 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
         for (int j = k + warp; j < cols; j += NW) {
             const double* cj = A + (size_t)j * lda;
             double s = 0;
+            #pragma unroll 4
             for (int i = k + lane; i < rows; i += 32) s = fma(cj[i], cj[i], s);
             s = warp_sum(s);
             if (lane == 0) w.nrm[j] = s;
@@ -85,6 +85,7 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
         double* ck = A + (size_t)k * lda;
         if (warp == 0) {
             double t = 0;
+            #pragma unroll 4
             for (int i = k + 1 + lane; i < rows; i += 32) t = fma(ck[i], ck[i], t);
             t = warp_sum(t);
             if (lane == 0) {
@@ -112,9 +113,11 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
             for (int j = k + 1 + warp; j < cols; j += NW) {
                 double* cj = A + (size_t)j * lda;
                 double s = 0;
+                #pragma unroll 4
                 for (int i = k + 1 + lane; i < rows; i += 32) s = fma(ck[i], cj[i], s);
                 s = (warp_sum(s) + cj[k]) * tk;
                 if (lane == 0) cj[k] -= s;
+                #pragma unroll 4
                 for (int i = k + 1 + lane; i < rows; i += 32) cj[i] = fma(-s, ck[i], cj[i]);
             }
         }
@@ -139,6 +142,7 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
     {
         double f = 0;
         for (int j = warp; j < cols; j += NW)
+            #pragma unroll 4
             for (int i = lane; i < rows; i += 32) f = fma(W[i + (size_t)j * ldw], W[i + (size_t)j * ldw], f);
         f = warp_sum(f);
         if (lane == 0) sh_fro[warp] = f;
@@ -172,6 +176,7 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
                     double* ap = W + (size_t)p * ldw;
                     double* aq = W + (size_t)q * ldw;
                     double al = 0, be = 0, ga = 0;
+                    #pragma unroll 4
                     for (int e = lane; e < rows; e += 32) {
                         const double x = ap[e], y = aq[e];
                         al = fma(x, x, al);
@@ -183,6 +188,7 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
                     ga = warp_sum(ga);
                     double c, s;
                     if (!jacobi_params(al, be, ga, tol2, zthr, c, s)) continue;
+                    #pragma unroll 4
                     for (int e = lane; e < rows; e += 32) rot2(ap[e], aq[e], c, s);
                     if (J) {
                         double* vp = J + (size_t)p * ldj;
@@ -198,6 +204,7 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
     }
     for (int j = warp; j < cols; j += NW) {
         double s = 0;
+        #pragma unroll 4
         for (int e = lane; e < rows; e += 32) s = fma(W[e + (size_t)j * ldw], W[e + (size_t)j * ldw], s);
         s = warp_sum(s);
         if (lane == 0) sig[j] = sqrt(s);
@@ -207,11 +214,14 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
 
 // Full engine on w.A (rows x cols).  Returns the truncated rank r (CTA-uniform);
 // order[t] = Jacobi column of the t-th largest sigma; *smax_out = sigma_1.
+// rp_cap: columns the caller's W/J buffers can hold; a larger numerical rank moves
+// W and J to `spill` (device arena) -- CTA-uniform decision.
 template <int NT>
-__device__ int cta_trunc_svd(const CtaSvdWork& w, int rows, int cols, double eps, double abs_cut, bool values_only,
-                             int* rp_out, double* smax_out) {
+__device__ int cta_trunc_svd(CtaSvdWork& w, int rows, int cols, double eps, double abs_cut, bool values_only,
+                             int* rp_out, double* smax_out, int rp_cap, const Arena* spill) {
     __shared__ int sh_r;
     __shared__ double sh_smax;
+    __shared__ double* sh_spill;
     // pivot threshold from the largest column norm (a lower bound of sigma_1)
     double cm = 0;
     {
@@ -219,6 +229,7 @@ __device__ int cta_trunc_svd(const CtaSvdWork& w, int rows, int cols, double eps
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (int j = warp; j < cols; j += NT / 32) {
             double s = 0;
+            #pragma unroll 4
             for (int i = lane; i < rows; i += 32) s = fma(w.A[i + (size_t)j * w.lda], w.A[i + (size_t)j * w.lda], s);
             cm = fmax(cm, warp_sum(s));
         }
@@ -237,6 +248,19 @@ __device__ int cta_trunc_svd(const CtaSvdWork& w, int rows, int cols, double eps
     if (rp == 0) {
         *smax_out = 0.0;
         return 0;
+    }
+    if (rp > rp_cap) {
+        if (threadIdx.x == 0)
+            sh_spill = spill ? arena_alloc(*spill, (unsigned long long)cols * rp + (unsigned long long)rp * rp + 16) : nullptr;
+        __syncthreads();
+        if (sh_spill == nullptr) {  // no room: report rank 0 (arena overflow flag raised)
+            *smax_out = 0.0;
+            return 0;
+        }
+        w.W = sh_spill;
+        w.ldw = cols;
+        w.J = sh_spill + (size_t)cols * rp;
+        w.ldj = rp;
     }
     // A' = R^T (cols x rp)
     for (int e = threadIdx.x; e < cols * rp; e += NT) {
@@ -295,10 +319,12 @@ __device__ void cta_trunc_write(const CtaSvdWork& w, int rows, int cols, int rp,
             if (tk == 0.0) continue;
             const double* v = w.A + (size_t)k * w.lda;
             double s = 0;
+            #pragma unroll 4
             for (int i = k + 1 + lane; i < rows; i += 32) s = fma(v[i], x[i], s);
             s = (warp_sum(s) + x[k]) * tk;
             __syncwarp();
             if (lane == 0) x[k] -= s;
+            #pragma unroll 4
             for (int i = k + 1 + lane; i < rows; i += 32) x[i] = fma(-s, v[i], x[i]);
             __syncwarp();
         }
@@ -306,4 +332,4 @@ __device__ void cta_trunc_write(const CtaSvdWork& w, int rows, int cols, int rp,
     __syncthreads();
 }
 
-}  // namespace acrgpu
+
