@@ -286,6 +286,8 @@ def run_ours(args):
     # roofline of the dominant kernel (device time share)
     rows = []
     for line in prof.strip().splitlines():
+        if line.startswith("#"):
+            continue
         p = line.split()
         if len(p) >= 5:
             rows.append({"kernel": p[0], "ms": float(p[1]), "launches": int(p[2]), "ctas": int(p[3]), "flops": float(p[4])})

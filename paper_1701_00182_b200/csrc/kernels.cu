@@ -18,6 +18,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 #include <map>
 #include <string>
@@ -60,6 +61,19 @@ __device__ double* arena_alloc(const Arena& a, unsigned long long n) {
 }
 
 #include "svd_cta.cuh"
+#include "bqr.cuh"
+
+// QR-route phase timing (clock64 deltas of thread 0, summed over CTAs): diagnostics only
+__device__ unsigned long long g_phase_cyc[8];
+__device__ unsigned long long g_phase_cnt;
+#define PHASE_MARK(i)                                                          \
+    do {                                                                       \
+        if (threadIdx.x == 0) {                                                \
+            const unsigned long long t_ = clock64();                           \
+            atomicAdd(&g_phase_cyc[i], t_ - ph_t0);                            \
+            ph_t0 = t_;                                                        \
+        }                                                                      \
+    } while (0)
 
 __device__ __forceinline__ void add_flops(FlopLedger* L, int cls, double f) {
     if (L && f > 0) atomicAdd(&L->f[cls], f);
@@ -422,6 +436,56 @@ struct TruncArgs {
     FlopLedger* flops;
 };
 
+// C (ru x rv, ld ldc; shared memory) += alpha * A (ru x k) * B^T (rv x k), A/B column-major
+// in global memory.  256 threads as a 16 x 16 grid, each owning a TM x TM register tile
+// (rows ty + 16 i, columns tx + 16 j); k is staged through `stage` (>= 2*16*TM*KC doubles).
+template <int TM>
+__device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, const double* B, int ldb, int ru, int rv, int k,
+                              double alpha, double* stage, int stage_doubles) {
+    static_assert(NT == 256, "16 x 16 thread grid");
+    constexpr int R = 16 * TM;
+    int KC = stage_doubles / (2 * R);
+    if (KC > 32) KC = 32;
+    double* As = stage;           // R x KC
+    double* Bs = stage + R * KC;  // R x KC
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[TM][TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TM; ++j) acc[i][j] = 0.0;
+    for (int t0 = 0; t0 < k; t0 += KC) {
+        const int kc = min(KC, k - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < R * kc; e += NT) {
+            const int i = e % R, t = e / R;
+            As[i + t * R] = i < ru ? A[i + (size_t)(t0 + t) * lda] : 0.0;
+            Bs[i + t * R] = i < rv ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
+        }
+        __syncthreads();
+        for (int t = 0; t < kc; ++t) {
+            double a[TM], bb[TM];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) a[i] = As[ty + 16 * i + t * R];
+#pragma unroll
+            for (int j = 0; j < TM; ++j) bb[j] = Bs[tx + 16 * j + t * R];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TM; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TM; ++j) {
+            const int r = ty + 16 * i, c = tx + 16 * j;
+            if (r < ru && c < rv) C[r + (size_t)c * ldc] += alpha * acc[i][j];
+        }
+    __syncthreads();
+}
+
 template <int DMAX, int RPCAP>
 __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews bv) {
     extern __shared__ double smem[];
@@ -484,15 +548,8 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
             const Part p = args.parts[pi];
             const PartRes pr = resolve_part(p, args.slots, b, B, C);
             if (pr.rank == 0) continue;
-            const int ru = p.rows_u, rv = p.rows_v;
-            for (int e = threadIdx.x; e < ru * rv; e += NT) {
-                const int i = e % ru, j = e / ru;
-                double acc = 0;
-                for (int t = 0; t < pr.rank; ++t)
-                    acc = fma(pr.U[i + (size_t)t * pr.ldu], pr.V[j + (size_t)t * pr.ldv], acc);
-                M[(p.u_dst + i) + (size_t)(p.v_dst + j) * m] += p.alpha * acc;
-            }
-            __syncthreads();
+            gemm_nt_tiled<DMAX / 16>(M + p.u_dst + (size_t)p.v_dst * m, m, pr.U, pr.ldu, pr.V, pr.ldv, p.rows_u,
+                                     p.rows_v, pr.rank, p.alpha, w.W, DMAX * RPCAP + RPCAP * RPCAP);
         }
         int rp;
         double smax;
@@ -525,19 +582,27 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
     // workspace: Uc (m x K) | Vc (n x K) | tau_u (K) | tau_v (K) | [core engine work if too big for smem]
     const int pmax = ku > kv ? ku : kv;
     const bool core_in_smem = pmax <= DMAX;
+    const size_t smem_doubles = (size_t)DMAX * DMAX + (size_t)DMAX * RPCAP + (size_t)RPCAP * RPCAP + 5 * DMAX;
+    const bool blocked = (size_t)(m > n ? m : n) * BQR_NB + 2 * BQR_NB * BQR_NB <= smem_doubles;
+    const int npan = (K + BQR_NB - 1) / BQR_NB + 1;
     if (threadIdx.x == 0) {
-        unsigned long long need = (unsigned long long)(m + n) * K + 2ull * K + 32;
+        unsigned long long need = (unsigned long long)(m + n) * K + 2ull * K + 32 + 2ull * npan * BQR_NB * BQR_NB;
         if (!core_in_smem) need += 3ull * pmax * pmax + 6ull * pmax + 64;
         sh_ws = arena_alloc(args.work, need);
     }
     __syncthreads();
     double* ws = sh_ws;
     if (ws == nullptr) return;  // arena exhausted: flag raised, target left unchanged
+    unsigned long long ph_t0 = clock64();
+    if (threadIdx.x == 0) atomicAdd(&g_phase_cnt, 1ull);
     double* Uc = ws;
     double* Vc = Uc + (size_t)m * K;
     double* tau_u = Vc + (size_t)n * K;
     double* tau_v = tau_u + K;
-    CtaSvdWork w = core_in_smem ? cta_smem_work(smem, DMAX, RPCAP) : cta_smem_work(tau_v + K + 32, pmax, pmax);
+    double* Tu = tau_v + K + 32;
+    double* Tv = Tu + (size_t)npan * BQR_NB * BQR_NB;
+    CtaSvdWork w = core_in_smem ? cta_smem_work(smem, DMAX, RPCAP)
+                                : cta_smem_work(Tv + (size_t)npan * BQR_NB * BQR_NB, pmax, pmax);
     for (size_t e = threadIdx.x; e < (size_t)(m + n) * K; e += NT) ws[e] = 0.0;
     __syncthreads();
     {
@@ -558,8 +623,15 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
         }
     }
     __syncthreads();
-    householder_qr(Uc, m, m, K, tau_u, red);
-    householder_qr(Vc, n, n, K, tau_v, red);
+    PHASE_MARK(0);
+    if (blocked) {
+        bqr<NT>(Uc, m, m, K, tau_u, Tu, smem, smem_doubles, red);
+        bqr<NT>(Vc, n, n, K, tau_v, Tv, smem, smem_doubles, red);
+    } else {
+        householder_qr(Uc, m, m, K, tau_u, red);
+        householder_qr(Vc, n, n, K, tau_v, red);
+    }
+    PHASE_MARK(1);
     // core = Ru Rv^T (ku x kv)
     double* core = w.A;
     w.lda = ku;
@@ -570,10 +642,12 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
         core[e] = acc;
     }
     __syncthreads();
+    PHASE_MARK(2);
     int rp;
     double smax;
     const int r = cta_trunc_svd<NT>(w, ku, kv, args.eps, abs_cut, args.values_only != 0, &rp, &smax,
                                     core_in_smem ? RPCAP : pmax, &args.work);
+    PHASE_MARK(3);
     if (args.values_only) {
         if (threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
     } else {
@@ -587,8 +661,15 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
             for (int e = threadIdx.x; e < n * r; e += NT) Vo[e] = 0.0;
             __syncthreads();
             cta_trunc_write<NT>(w, ku, kv, rp, r, Uo, m, Vo, n);
-            apply_q(Uc, m, m, ku, tau_u, Uo, m, r);
-            apply_q(Vc, n, n, kv, tau_v, Vo, n, r);
+            PHASE_MARK(4);
+            if (blocked) {
+                bqr_apply<NT>(Uc, m, m, ku, Tu, Uo, m, r, smem);
+                bqr_apply<NT>(Vc, n, n, kv, Tv, Vo, n, r, smem);
+            } else {
+                apply_q(Uc, m, m, ku, tau_u, Uo, m, r);
+                apply_q(Vc, n, n, kv, tau_v, Vo, n, r);
+            }
+            PHASE_MARK(5);
         }
         write_out(out ? r : 0, out, out ? out + (size_t)m * r : nullptr);
     }
@@ -1551,12 +1632,14 @@ struct ProfScope {
         }
     }
 };
+static std::vector<std::tuple<float, std::string, long>> g_top;  // slowest launches
 void prof_flush() {
     if (g_prof.empty()) return;
     cudaDeviceSynchronize();
     for (auto& r : g_prof) {
         float ms = 0;
         cudaEventElapsedTime(&ms, r.a, r.b);
+        g_top.emplace_back(ms, r.name, r.ctas);
         auto& acc = g_prof_acc[r.name];
         std::get<0>(acc) += ms;
         std::get<1>(acc) += 1;
@@ -1565,6 +1648,8 @@ void prof_flush() {
         cudaEventDestroy(r.b);
     }
     g_prof.clear();
+    std::sort(g_top.begin(), g_top.end(), [](const auto& x, const auto& y) { return std::get<0>(x) > std::get<0>(y); });
+    if (g_top.size() > 40) g_top.resize(40);
 }
 std::string prof_report(bool reset) {
     prof_flush();
@@ -1576,9 +1661,28 @@ std::string prof_report(bool reset) {
         snprintf(buf, sizeof(buf), "%s %.3f %ld %ld %.6e\n", k.c_str(), std::get<0>(v), std::get<1>(v), std::get<2>(v), fl);
         out += buf;
     }
+    {
+        unsigned long long ph[8], cnt = 0;
+        cudaMemcpyFromSymbol(ph, g_phase_cyc, sizeof(ph));
+        cudaMemcpyFromSymbol(&cnt, g_phase_cnt, sizeof(cnt));
+        snprintf(buf, sizeof(buf), "#phase qr-route tasks %llu: concat %.3g qr %.3g core %.3g svd %.3g write %.3g applyq %.3g (Gcycles)\n",
+                 cnt, ph[0] / 1e9, ph[1] / 1e9, ph[2] / 1e9, ph[3] / 1e9, ph[4] / 1e9, ph[5] / 1e9);
+        out += buf;
+        if (reset) {
+            cudaMemset(ph, 0, 0);
+            const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            cudaMemcpyToSymbol(g_phase_cyc, z, sizeof(z));
+            cudaMemcpyToSymbol(g_phase_cnt, z, sizeof(unsigned long long));
+        }
+    }
+    for (auto& [ms, name, ctas] : g_top) {
+        snprintf(buf, sizeof(buf), "#top %s %.3f %ld\n", name.c_str(), ms, ctas);
+        out += buf;
+    }
     if (reset) {
         g_prof_acc.clear();
         g_flop_acc.clear();
+        g_top.clear();
     }
     return out;
 }

@@ -36,16 +36,17 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
     for (int j = threadIdx.x; j < cols; j += NT) w.perm[j] = j;
     const int kmax = rows < cols ? rows : cols;
     int rp = 0;
+    // remaining column norms (rows >= k); refreshed exactly inside the update pass below
+    for (int j = warp; j < cols; j += NW) {
+        const double* cj = A + (size_t)j * lda;
+        double s = 0;
+#pragma unroll 4
+        for (int i = lane; i < rows; i += 32) s = fma(cj[i], cj[i], s);
+        s = warp_sum(s);
+        if (lane == 0) w.nrm[j] = s;
+    }
+    __syncthreads();
     for (int k = 0; k < kmax; ++k) {
-        for (int j = k + warp; j < cols; j += NW) {
-            const double* cj = A + (size_t)j * lda;
-            double s = 0;
-            #pragma unroll 4
-            for (int i = k + lane; i < rows; i += 32) s = fma(cj[i], cj[i], s);
-            s = warp_sum(s);
-            if (lane == 0) w.nrm[j] = s;
-        }
-        __syncthreads();
         if (warp == 0) {
             double best = -1.0;
             int bi = k;
@@ -79,6 +80,9 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
                 const int t = w.perm[k];
                 w.perm[k] = w.perm[piv];
                 w.perm[piv] = t;
+                const double tn = w.nrm[k];
+                w.nrm[k] = w.nrm[piv];
+                w.nrm[piv] = tn;
             }
             __syncthreads();
         }
@@ -109,16 +113,26 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
         for (int i = k + 1 + threadIdx.x; i < rows; i += NT) ck[i] = tk != 0.0 ? ck[i] * inv : 0.0;
         __syncthreads();
         if (threadIdx.x == 0) ck[k] = sh_beta;
-        if (tk != 0.0) {
-            for (int j = k + 1 + warp; j < cols; j += NW) {
-                double* cj = A + (size_t)j * lda;
-                double s = 0;
-                #pragma unroll 4
+        // apply the reflector to the remaining columns and refresh their norms over rows > k
+        for (int j = k + 1 + warp; j < cols; j += NW) {
+            double* cj = A + (size_t)j * lda;
+            double s = 0;
+            if (tk != 0.0) {
+#pragma unroll 4
                 for (int i = k + 1 + lane; i < rows; i += 32) s = fma(ck[i], cj[i], s);
                 s = (warp_sum(s) + cj[k]) * tk;
-                if (lane == 0) cj[k] -= s;
-                #pragma unroll 4
-                for (int i = k + 1 + lane; i < rows; i += 32) cj[i] = fma(-s, ck[i], cj[i]);
+            }
+            double nn = 0;
+#pragma unroll 4
+            for (int i = k + 1 + lane; i < rows; i += 32) {
+                const double v = fma(-s, ck[i], cj[i]);
+                cj[i] = v;
+                nn = fma(v, v, nn);
+            }
+            nn = warp_sum(nn);
+            if (lane == 0) {
+                cj[k] -= s;
+                w.nrm[j] = nn;
             }
         }
         __syncthreads();

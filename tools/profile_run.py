@@ -15,8 +15,10 @@ st = f.inverse_rank_stats()
 print(json.dumps(dict(cfg=cfgk, n=sysm.n, exact=exact, res=sysm.relative_residual(u), tf=tf, ts=ts, largest=st.largest_rank,
                       avg=st.average_rank, fbytes=f.factor_bytes(), timing=f.timing())))
 rep = acr.profile_report()
-rows = [l.split() for l in rep.strip().splitlines()]
+rows = [l.split() for l in rep.strip().splitlines() if not l.startswith('#')]
+top = [l for l in rep.strip().splitlines() if l.startswith('#')]
 tot = sum(float(r[1]) for r in rows)
 for r in sorted(rows, key=lambda r: -float(r[1])):
     print("%-18s %10.2f ms %5.1f%%  launches %7s  ctas %10s" % (r[0], float(r[1]), 100 * float(r[1]) / tot, r[2], r[3]))
 print("total kernel ms", tot)
+print("\n".join(top[:25]))
