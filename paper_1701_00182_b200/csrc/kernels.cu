@@ -1514,7 +1514,7 @@ __global__ void __launch_bounds__(64) k_small32(TruncArgs targs, DDArgs dargs, i
     if (lane == 0 && r > 0) out = arena_alloc(MODE == 0 ? targs.out_arena : dargs.out_arena, (unsigned long long)(m + n) * r);
     out = (double*)__shfl_sync(0xffffffffu, (unsigned long long)out, 0);
     if (out == nullptr) r = 0;
-    if (r > 0) warp_write32(a, v, m, n, rp, sig, pos, r, sm, out, out + (size_t)m * r);
+    if (r > 0) warp_write32(a, m, n, rp, sig, pos, r, sm, out, out + (size_t)m * r);
     if (lane == 0) {
         if (MODE == 0) {
             SmallTaskIO::write_out(targs, task, b, C, r, out, out ? out + (size_t)m * r : nullptr);

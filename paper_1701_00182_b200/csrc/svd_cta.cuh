@@ -282,7 +282,7 @@ __device__ int cta_trunc_svd(CtaSvdWork& w, int rows, int cols, double eps, doub
         w.W[j + (size_t)c * w.ldw] = j >= c ? w.A[c + (size_t)j * w.lda] : 0.0;
     }
     __syncthreads();
-    cta_jacobi<NT>(w.W, w.ldw, cols, rp, values_only ? nullptr : w.J, w.ldj, w.sig);
+    cta_jacobi<NT>(w.W, w.ldw, cols, rp, nullptr, w.ldj, w.sig);  // J recovered as R W Sigma^{-2} at write time
     for (int j = threadIdx.x; j < rp; j += NT) {
         const double v = w.sig[j];
         int pos = 0;
@@ -314,10 +314,14 @@ __device__ void cta_trunc_write(const CtaSvdWork& w, int rows, int cols, int rp,
                                 int ldv) {
     constexpr int NW = NT / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // J_r Sigma_r = R W_r Sigma_r^{-1}  (R = J W^T: the rp x cols upper rows of the pivoted QR)
     for (int e = threadIdx.x; e < rows * r; e += NT) {
         const int i = e % rows, t = e / rows;
         const int c = w.order[t];
-        Uo[i + (size_t)t * ldu] = i < rp ? w.J[i + (size_t)c * w.ldj] * w.sig[c] : 0.0;
+        double acc = 0.0;
+        if (i < rp)
+            for (int j = i; j < cols; ++j) acc = fma(w.A[i + (size_t)j * w.lda], w.W[j + (size_t)c * w.ldw], acc);
+        Uo[i + (size_t)t * ldu] = acc / w.sig[c];
     }
     for (int e = threadIdx.x; e < cols * r; e += NT) {
         const int j = e % cols, t = e / cols;

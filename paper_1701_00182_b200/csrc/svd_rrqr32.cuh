@@ -13,7 +13,8 @@
 //      rotation from bitwise-identical inner products.  The QR
 //      preconditioning (Drmac-Veselic) and the reduced column count rp make
 //      this converge in a few short sweeps.
-//   3. U' = Q [J_r Sigma_r; 0] (reflectors applied per lane), V' = P W_r Sigma_r^{-1}.
+//   3. U' = Q [J_r Sigma_r; 0] (reflectors applied per lane), V' = P W_r Sigma_r^{-1},
+//      with J_r Sigma_r = R W_r Sigma_r^{-1} (R = J W^T), so J is never accumulated.
 //
 // Mathematically the same truncated SVD the reference computes with QR(U),
 // QR(V) and JacobiSVD of the core (hmatrix.cpp:56-84).
@@ -38,8 +39,8 @@ __device__ __forceinline__ int rr_partner(int x, int r, int P) {
 }
 
 // Phase 1+2.  In: lane j holds column j of M in a[0..m).  Out: returns rp;
-// lane c < rp holds column c of W = R^T J in a[0..n) and column c of J in v[0..rp);
-// sm.H / sm.tau / sm.perm describe Q and P.
+// lane c < rp holds column c of W = R^T J in a[0..n); sm.H / sm.tau / sm.perm describe
+// Q and P, sm.T holds R^T.  (v / want_v: unused, kept for call-site compatibility.)
 __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n, double delta_rel,
                                   double abs_delta, bool want_v, Warp32Smem& sm) {
     const int lane = threadIdx.x & 31;
@@ -125,8 +126,6 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 32; ++j) a[j] = lane < rp ? sm.T[j][lane] : 0.0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = (i == lane && lane < rp) ? 1.0 : 0.0;
     __syncwarp();
     if (rp < 2) return rp;
     // ---- one-sided Jacobi on the rp columns of A'
@@ -148,21 +147,22 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
             double pa[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) pa[i] = __shfl_sync(FULL, a[i], p);
-            double s0 = 0, s1 = 0, s2 = 0, t0 = 0, t1 = 0, t2 = 0;
+            // own / partner / cross inner products; both lanes of a pair run the same FMA
+            // sequence on the same values, so (alpha, beta, gamma) are bitwise identical
+            double so0 = 0, so1 = 0, sp0 = 0, sp1 = 0, sx0 = 0, sx1 = 0;
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
-                const double xl = low ? a[i] : pa[i], xh = low ? pa[i] : a[i];
-                const double yl = low ? a[i + 1] : pa[i + 1], yh = low ? pa[i + 1] : a[i + 1];
-                s0 = fma(xl, xl, s0);
-                s1 = fma(xh, xh, s1);
-                s2 = fma(xl, xh, s2);
-                t0 = fma(yl, yl, t0);
-                t1 = fma(yh, yh, t1);
-                t2 = fma(yl, yh, t2);
+                so0 = fma(a[i], a[i], so0);
+                so1 = fma(a[i + 1], a[i + 1], so1);
+                sp0 = fma(pa[i], pa[i], sp0);
+                sp1 = fma(pa[i + 1], pa[i + 1], sp1);
+                sx0 = fma(a[i], pa[i], sx0);
+                sx1 = fma(a[i + 1], pa[i + 1], sx1);
             }
+            const double so = so0 + so1, sp = sp0 + sp1, sx = sx0 + sx1;
             double c, s;
             bool rot = false;
-            if (p != lane) rot = jacobi_params(s0 + t0, s1 + t1, s2 + t2, tol2, zthr, c, s);
+            if (p != lane) rot = jacobi_params(low ? so : sp, low ? sp : so, sx, tol2, zthr, c, s);
             if (!rot) {
                 c = 1.0;
                 s = 0.0;
@@ -172,16 +172,6 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
                 const double sl = low ? -s : s;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) a[i] = fma(sl, pa[i], c * a[i]);
-                if (want_v) {
-#pragma unroll
-                    for (int i0 = 0; i0 < 32; i0 += 8) {
-                        double pv[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) pv[i] = __shfl_sync(FULL, v[i0 + i], p);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) v[i0 + i] = fma(sl, pv[i], c * v[i0 + i]);
-                    }
-                }
             }
         }
         if (!any) break;
@@ -213,14 +203,24 @@ __device__ __forceinline__ void warp_sigma_pos32(const double (&a)[32], int rp, 
 }
 
 // Phase 3: write U' (m x r) = Q [J Sigma; 0] and V' (n x r) = P W Sigma^{-1}.
-__device__ void warp_write32(const double (&a)[32], const double (&v)[32], int m, int n, int rp, double sig, int pos,
-                             int r, Warp32Smem& sm, double* Uo, double* Vo) {
+// J Sigma is recovered as R W Sigma^{-1} (R = J W^T), with R^T still staged in sm.T,
+// so the Jacobi sweeps never accumulate J.
+__device__ void warp_write32(const double (&a)[32], int m, int n, int rp, double sig, int pos, int r, Warp32Smem& sm,
+                             double* Uo, double* Vo) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
     if (lane < rp && pos < r) {
+        const double inv = 1.0 / sig;
         double x[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[i] = i < rp ? v[i] * sig : 0.0;
+        for (int i = 0; i < 32; ++i) {
+            double acc = 0.0;
+            if (i < rp) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc = fma(sm.T[j][i], a[j], acc);  // R[i][j] = T[j][i]
+            }
+            x[i] = acc * inv;
+        }
 #pragma unroll
         for (int k = 31; k >= 0; --k) {
             if (k < rp) {
@@ -241,7 +241,6 @@ __device__ void warp_write32(const double (&a)[32], const double (&v)[32], int m
         for (int i = 0; i < 32; ++i)
             if (i < m) u[i] = x[i];
         double* w = Vo + (size_t)pos * n;
-        const double inv = 1.0 / sig;
 #pragma unroll
         for (int j = 0; j < 32; ++j)
             if (j < n) w[sm.perm[j]] = a[j] * inv;
