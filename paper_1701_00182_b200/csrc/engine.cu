@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -1213,6 +1214,16 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
     blocks.clear();
     const int stop = F->eng->cfg.stop_planes;
     int lvl = 0;
+    static const bool verbose = getenv("ACRGPU_VERBOSE") != nullptr;
+    std::vector<cudaEvent_t> lev_ev;
+    auto mark = [&]() {
+        if (!verbose) return;
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, E.main_st()));
+        lev_ev.push_back(e);
+    };
+    mark();
     while ((int)D.size() > stop) {
         const int m = (int)D.size();
         Level L;
@@ -1317,6 +1328,7 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
             E.recompress(dv);
         }
         F->levels.push_back(std::move(L));
+        mark();
         ++lvl;
     }
     // apex: block Thomas over the remaining planes (acr.cpp:123-144)
@@ -1336,7 +1348,16 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
         F->apexDinv.push_back(out);
     }
     E.recompress(views(F->apexDinv));
+    mark();
     check_device_errors(F);
+    if (verbose) {
+        for (size_t i = 1; i < lev_ev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, lev_ev[i - 1], lev_ev[i]);
+            fprintf(stderr, "[acrgpu] level %zu: %.2f ms\n", i - 1, ms);
+        }
+        for (auto e : lev_ev) cudaEventDestroy(e);
+    }
     compact_factor(F);
     CK(cudaEventRecord(e2, E.st()));
     CK(cudaEventSynchronize(e2));

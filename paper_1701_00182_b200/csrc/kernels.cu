@@ -226,15 +226,22 @@ __device__ int rank_of(const double* sig, const int* order, int n, double eps, d
 // trapezoid, essential reflector parts below the diagonal, tau[j].  Eigen
 // HouseholderQR conventions (hmatrix.cpp:62-63): beta = -sign(c0)||x||, tau = 0
 // when the sub-diagonal tail is exactly zero.
+template <int NTH = NT>
 __device__ void householder_qr(double* W, int ld, int rows, int cols, double* tau, double* red) {
+    constexpr int NW = NTH / 32;
     const int kmax = rows < cols ? rows : cols;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ double sh_beta, sh_tau, sh_inv;
     for (int j = 0; j < kmax; ++j) {
         double* wj = W + (size_t)j * ld;
         double part = 0;
-        for (int i = j + 1 + threadIdx.x; i < rows; i += NT) part = fma(wj[i], wj[i], part);
-        const double tail = block_sum(part, red);
+        for (int i = j + 1 + threadIdx.x; i < rows; i += NTH) part = fma(wj[i], wj[i], part);
+        part = warp_sum(part);
+        __syncthreads();
+        if (lane == 0) red[warp] = part;
+        __syncthreads();
+        double tail = 0;
+        for (int q = 0; q < NW; ++q) tail += red[q];
         if (threadIdx.x == 0) {
             const double c0 = wj[j];
             if (tail <= DBL_MIN) {
@@ -253,9 +260,9 @@ __device__ void householder_qr(double* W, int ld, int rows, int cols, double* ta
         __syncthreads();
         const double tj = sh_tau, inv = sh_inv;
         if (tj == 0.0) {
-            for (int i = j + 1 + threadIdx.x; i < rows; i += NT) wj[i] = 0.0;
+            for (int i = j + 1 + threadIdx.x; i < rows; i += NTH) wj[i] = 0.0;
         } else {
-            for (int i = j + 1 + threadIdx.x; i < rows; i += NT) wj[i] *= inv;
+            for (int i = j + 1 + threadIdx.x; i < rows; i += NTH) wj[i] *= inv;
         }
         __syncthreads();
         if (threadIdx.x == 0) wj[j] = sh_beta;
@@ -277,7 +284,9 @@ __device__ void householder_qr(double* W, int ld, int rows, int cols, double* ta
 }
 
 // Y (rows x ncol, ld) <- Q Y with Q = H_0 H_1 ... H_{k-1} from householder_qr(W).
+template <int NTH = NT>
 __device__ void apply_q(const double* W, int ldw, int rows, int k, const double* tau, double* Y, int ldy, int ncol) {
+    constexpr int NW = NTH / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j = k - 1; j >= 0; --j) {
         const double tj = tau[j];
@@ -437,59 +446,63 @@ struct TruncArgs {
 };
 
 // C (ru x rv, ld ldc; shared memory) += alpha * A (ru x k) * B^T (rv x k), A/B column-major
-// in global memory.  256 threads as a 16 x 16 grid, each owning a TM x TM register tile
-// (rows ty + 16 i, columns tx + 16 j); k is staged through `stage` (>= 2*16*TM*KC doubles).
-template <int TM>
+// in global memory.  NTH threads as a GY x GX grid (GX = 16), each owning a TM x TN register
+// tile (rows ty + GY i, columns tx + 16 j); k is staged through `stage`.
+template <int NTH, int TM, int TN>
 __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, const double* B, int ldb, int ru, int rv, int k,
                               double alpha, double* stage, int stage_doubles) {
-    static_assert(NT == 256, "16 x 16 thread grid");
-    constexpr int R = 16 * TM;
-    int KC = stage_doubles / (2 * R);
+    constexpr int GX = 16, GY = NTH / GX;
+    constexpr int RA = GY * TM, RB = GX * TN;
+    int KC = stage_doubles / (RA + RB);
     if (KC > 32) KC = 32;
-    double* As = stage;           // R x KC
-    double* Bs = stage + R * KC;  // R x KC
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[TM][TM];
+    double* As = stage;            // RA x KC
+    double* Bs = stage + RA * KC;  // RB x KC
+    const int tx = threadIdx.x % GX, ty = threadIdx.x / GX;
+    double acc[TM][TN];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TM; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
     for (int t0 = 0; t0 < k; t0 += KC) {
         const int kc = min(KC, k - t0);
         __syncthreads();
-        for (int e = threadIdx.x; e < R * kc; e += NT) {
-            const int i = e % R, t = e / R;
-            As[i + t * R] = i < ru ? A[i + (size_t)(t0 + t) * lda] : 0.0;
-            Bs[i + t * R] = i < rv ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
+        for (int e = threadIdx.x; e < RA * kc; e += NTH) {
+            const int i = e % RA, t = e / RA;
+            As[i + t * RA] = i < ru ? A[i + (size_t)(t0 + t) * lda] : 0.0;
+        }
+        for (int e = threadIdx.x; e < RB * kc; e += NTH) {
+            const int i = e % RB, t = e / RB;
+            Bs[i + t * RB] = i < rv ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
         }
         __syncthreads();
         for (int t = 0; t < kc; ++t) {
-            double a[TM], bb[TM];
+            double a[TM], bb[TN];
 #pragma unroll
-            for (int i = 0; i < TM; ++i) a[i] = As[ty + 16 * i + t * R];
+            for (int i = 0; i < TM; ++i) a[i] = As[ty + GY * i + t * RA];
 #pragma unroll
-            for (int j = 0; j < TM; ++j) bb[j] = Bs[tx + 16 * j + t * R];
+            for (int j = 0; j < TN; ++j) bb[j] = Bs[tx + GX * j + t * RB];
 #pragma unroll
             for (int i = 0; i < TM; ++i)
 #pragma unroll
-                for (int j = 0; j < TM; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+                for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
         }
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TM; ++j) {
-            const int r = ty + 16 * i, c = tx + 16 * j;
+        for (int j = 0; j < TN; ++j) {
+            const int r = ty + GY * i, c = tx + GX * j;
             if (r < ru && c < rv) C[r + (size_t)c * ldc] += alpha * acc[i][j];
         }
     __syncthreads();
 }
 
-template <int DMAX, int RPCAP>
-__global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews bv) {
+template <int DMAX, int RPCAP, int NTH>
+__global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews bv) {
+    constexpr int NWH = NTH / 32;
     extern __shared__ double smem[];
-    __shared__ double red[NW];
+    __shared__ double red[NWH];
     __shared__ int sh_K;
     __shared__ double* sh_ws;
     const TruncTask task = args.tasks[blockIdx.x];
@@ -542,25 +555,25 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
         CtaSvdWork w = cta_smem_work(smem, DMAX, RPCAP);
         double* M = w.A;
         w.lda = m;
-        for (int e = threadIdx.x; e < m * n; e += NT) M[e] = 0.0;
+        for (int e = threadIdx.x; e < m * n; e += NTH) M[e] = 0.0;
         __syncthreads();
         for (int pi = task.pbeg; pi < task.pend; ++pi) {
             const Part p = args.parts[pi];
             const PartRes pr = resolve_part(p, args.slots, b, B, C);
             if (pr.rank == 0) continue;
-            gemm_nt_tiled<DMAX / 16>(M + p.u_dst + (size_t)p.v_dst * m, m, pr.U, pr.ldu, pr.V, pr.ldv, p.rows_u,
+            gemm_nt_tiled<NTH, DMAX * 16 / NTH, DMAX / 16>(M + p.u_dst + (size_t)p.v_dst * m, m, pr.U, pr.ldu, pr.V, pr.ldv, p.rows_u,
                                      p.rows_v, pr.rank, p.alpha, w.W, DMAX * RPCAP + RPCAP * RPCAP);
         }
         int rp;
         double smax;
-        const int r = cta_trunc_svd<NT>(w, m, n, args.eps, abs_cut, args.values_only != 0, &rp, &smax, RPCAP, &args.work);
+        const int r = cta_trunc_svd<NTH>(w, m, n, args.eps, abs_cut, args.values_only != 0, &rp, &smax, RPCAP, &args.work);
         if (args.values_only) {
             if (threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
         } else {
             if (threadIdx.x == 0) sh_out = r > 0 ? arena_alloc(args.out_arena, (unsigned long long)(m + n) * r) : nullptr;
             __syncthreads();
             double* out = sh_out;
-            if (out) cta_trunc_write<NT>(w, m, n, rp, r, out, m, out + (size_t)m * r, n);
+            if (out) cta_trunc_write<NTH>(w, m, n, rp, r, out, m, out + (size_t)m * r, n);
             write_out(out ? r : 0, out, out ? out + (size_t)m * r : nullptr);
         }
         if (threadIdx.x == 0) {
@@ -603,7 +616,7 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
     double* Tv = Tu + (size_t)npan * BQR_NB * BQR_NB;
     CtaSvdWork w = core_in_smem ? cta_smem_work(smem, DMAX, RPCAP)
                                 : cta_smem_work(Tv + (size_t)npan * BQR_NB * BQR_NB, pmax, pmax);
-    for (size_t e = threadIdx.x; e < (size_t)(m + n) * K; e += NT) ws[e] = 0.0;
+    for (size_t e = threadIdx.x; e < (size_t)(m + n) * K; e += NTH) ws[e] = 0.0;
     __syncthreads();
     {
         int off = 0;
@@ -611,11 +624,11 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
             const Part p = args.parts[pi];
             const PartRes pr = resolve_part(p, args.slots, b, B, C);
             if (pr.rank == 0) continue;
-            for (int e = threadIdx.x; e < p.rows_u * pr.rank; e += NT) {
+            for (int e = threadIdx.x; e < p.rows_u * pr.rank; e += NTH) {
                 const int i = e % p.rows_u, t = e / p.rows_u;
                 Uc[(p.u_dst + i) + (size_t)(off + t) * m] = p.alpha * pr.U[i + (size_t)t * pr.ldu];
             }
-            for (int e = threadIdx.x; e < p.rows_v * pr.rank; e += NT) {
+            for (int e = threadIdx.x; e < p.rows_v * pr.rank; e += NTH) {
                 const int i = e % p.rows_v, t = e / p.rows_v;
                 Vc[(p.v_dst + i) + (size_t)(off + t) * n] = pr.V[i + (size_t)t * pr.ldv];
             }
@@ -625,17 +638,17 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
     __syncthreads();
     PHASE_MARK(0);
     if (blocked) {
-        bqr<NT>(Uc, m, m, K, tau_u, Tu, smem, smem_doubles, red);
-        bqr<NT>(Vc, n, n, K, tau_v, Tv, smem, smem_doubles, red);
+        bqr<NTH>(Uc, m, m, K, tau_u, Tu, smem, smem_doubles, red);
+        bqr<NTH>(Vc, n, n, K, tau_v, Tv, smem, smem_doubles, red);
     } else {
-        householder_qr(Uc, m, m, K, tau_u, red);
-        householder_qr(Vc, n, n, K, tau_v, red);
+        householder_qr<NTH>(Uc, m, m, K, tau_u, red);
+        householder_qr<NTH>(Vc, n, n, K, tau_v, red);
     }
     PHASE_MARK(1);
     // core = Ru Rv^T (ku x kv)
     double* core = w.A;
     w.lda = ku;
-    for (int e = threadIdx.x; e < ku * kv; e += NT) {
+    for (int e = threadIdx.x; e < ku * kv; e += NTH) {
         const int i = e % ku, j = e / ku;
         double acc = 0;
         for (int t = (i > j ? i : j); t < K; ++t) acc = fma(Uc[i + (size_t)t * m], Vc[j + (size_t)t * n], acc);
@@ -645,7 +658,7 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
     PHASE_MARK(2);
     int rp;
     double smax;
-    const int r = cta_trunc_svd<NT>(w, ku, kv, args.eps, abs_cut, args.values_only != 0, &rp, &smax,
+    const int r = cta_trunc_svd<NTH>(w, ku, kv, args.eps, abs_cut, args.values_only != 0, &rp, &smax,
                                     core_in_smem ? RPCAP : pmax, &args.work);
     PHASE_MARK(3);
     if (args.values_only) {
@@ -657,17 +670,17 @@ __global__ void __launch_bounds__(NT, 1) k_truncate(TruncArgs args, BatchViews b
         if (out) {
             double* Uo = out;
             double* Vo = out + (size_t)m * r;
-            for (int e = threadIdx.x; e < m * r; e += NT) Uo[e] = 0.0;
-            for (int e = threadIdx.x; e < n * r; e += NT) Vo[e] = 0.0;
+            for (int e = threadIdx.x; e < m * r; e += NTH) Uo[e] = 0.0;
+            for (int e = threadIdx.x; e < n * r; e += NTH) Vo[e] = 0.0;
             __syncthreads();
-            cta_trunc_write<NT>(w, ku, kv, rp, r, Uo, m, Vo, n);
+            cta_trunc_write<NTH>(w, ku, kv, rp, r, Uo, m, Vo, n);
             PHASE_MARK(4);
             if (blocked) {
-                bqr_apply<NT>(Uc, m, m, ku, Tu, Uo, m, r, smem);
-                bqr_apply<NT>(Vc, n, n, kv, Tv, Vo, n, r, smem);
+                bqr_apply<NTH>(Uc, m, m, ku, Tu, Uo, m, r, smem);
+                bqr_apply<NTH>(Vc, n, n, kv, Tv, Vo, n, r, smem);
             } else {
-                apply_q(Uc, m, m, ku, tau_u, Uo, m, r);
-                apply_q(Vc, n, n, kv, tau_v, Vo, n, r);
+                apply_q<NTH>(Uc, m, m, ku, tau_u, Uo, m, r);
+                apply_q<NTH>(Vc, n, n, kv, tau_v, Vo, n, r);
             }
             PHASE_MARK(5);
         }
@@ -1688,15 +1701,15 @@ std::string prof_report(bool reset) {
 }
 
 static size_t trunc_smem() { return SMEM_TRUNC; }
-constexpr int BIG_DMAX = 128, BIG_RPCAP = 56;
+constexpr int BIG_DMAX = 128, BIG_RPCAP = 56, BIG_NT = 512;
 static size_t trunc_smem_big() {
     return ((size_t)BIG_DMAX * BIG_DMAX + (size_t)BIG_DMAX * BIG_RPCAP + (size_t)BIG_RPCAP * BIG_RPCAP + 5 * BIG_DMAX + 64) *
            sizeof(double);
 }
 
 void setup_kernels() {
-    cudaFuncSetAttribute(k_truncate<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
-    cudaFuncSetAttribute(k_truncate<BIG_DMAX, BIG_RPCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_big());
+    cudaFuncSetAttribute(k_truncate<64, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
+    cudaFuncSetAttribute(k_truncate<BIG_DMAX, BIG_RPCAP, BIG_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_big());
     cudaFuncSetAttribute(k_dd_product, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
     cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaFuncSetAttribute(k_sigma1_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
@@ -1709,7 +1722,7 @@ void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const 
     TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, work,
                 ledger(flops, name)};
     ProfScope _ps(st, name, (long)ntasks * B);
-    k_truncate<BIG_DMAX, BIG_RPCAP><<<dim3(ntasks, B), NT, trunc_smem_big(), st>>>(a, bv);
+    k_truncate<BIG_DMAX, BIG_RPCAP, BIG_NT><<<dim3(ntasks, B), BIG_NT, trunc_smem_big(), st>>>(a, bv);
 }
 
 void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots,
@@ -1721,7 +1734,7 @@ void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* ta
     DDArgs d{};
     ProfScope _ps(st, name, (long)ntasks * B);
     if (nc == 32) k_small32<0><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
-    else k_truncate<64, 64><<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+    else k_truncate<64, 64, 256><<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
 }
 
 void launch_dd_small(cudaStream_t st, int nc, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps,
