@@ -121,7 +121,9 @@ typedef struct acrgpu_timing {     /* device-event phase times of the last call 
 typedef struct acrgpu_ctx acrgpu_ctx;
 typedef struct acrgpu_fact acrgpu_fact;
 
-/* Context on one CUDA device (device < 0: current device). */
+/* Context on one CUDA device (device < 0: current device).  Destroying the
+   context handle while factorizations built on it are alive is allowed: its
+   device resources are released with the last of them. */
 int acrgpu_ctx_create(int device, acrgpu_ctx** out, acrgpu_error* err);
 void acrgpu_ctx_destroy(acrgpu_ctx* ctx);
 

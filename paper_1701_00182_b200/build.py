@@ -13,7 +13,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
 SOURCES = ["structure.cpp", "kernels.cu", "engine.cu"]
-HEADERS = ["structure.hpp", "kernels.hpp", "tasks.hpp", os.path.join("..", "..", "include", "acrgpu.h")]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh"))) + [os.path.join("..", "..", "include", "acrgpu.h")]
 
 
 def _stale(target, deps):

@@ -878,6 +878,7 @@ static std::vector<int> retained_positions(int m) {
 
 struct acrgpu_ctx {
     acrgpu::Ctx c;
+    int refs = 1;  // the caller's handle + one per live factorization
 };
 
 struct acrgpu_fact {
@@ -1613,10 +1614,18 @@ int acrgpu_ctx_create(int device, acrgpu_ctx** out, acrgpu_error* err) {
     })
 }
 
-void acrgpu_ctx_destroy(acrgpu_ctx* ctx) {
-    if (!ctx) return;
+// The context outlives its factorizations: destroying the handle first (as
+// garbage collectors may at interpreter exit) defers the release until the
+// last factorization built on it is destroyed.
+static void ctx_release(acrgpu_ctx* ctx) {
+    if (--ctx->refs > 0) return;
     ctx->c.destroy();
     delete ctx;
+}
+
+void acrgpu_ctx_destroy(acrgpu_ctx* ctx) {
+    if (!ctx) return;
+    ctx_release(ctx);
 }
 
 struct acrgpu_dsystem {
@@ -1687,7 +1696,14 @@ static int factor_impl(acrgpu_ctx* ctx, const DSys& ds, const acrgpu_config* cfg
         if (!E.S.balanced)
             throw AcrError{ACRGPU_E_USAGE, "GPU path: unbalanced cluster trees (mixed dense/branch products) are not supported"};
         E.prepare_structure();
-        do_factor(F.get(), *sys);
+        ++ctx->refs;
+        try {
+            do_factor(F.get(), *sys);
+        } catch (...) {
+            F.reset();
+            ctx_release(ctx);
+            throw;
+        }
         *out = F.release();
         return 0;
     })
@@ -1704,7 +1720,9 @@ void acrgpu_factor_destroy(acrgpu_fact* f) {
     f->apexF.clear();
     cudaStreamSynchronize(st);
     if (f->ubuf) cudaFree(f->ubuf);
+    acrgpu_ctx* ctx = f->ctx;
     delete f;
+    ctx_release(ctx);
 }
 
 int acrgpu_solve_device(acrgpu_fact* f, int nrhs, const double* f_dev, double* u_dev, acrgpu_error* err) {

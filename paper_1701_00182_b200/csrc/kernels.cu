@@ -60,11 +60,8 @@ __device__ double* arena_alloc(const Arena& a, unsigned long long n) {
     return a.base + off;
 }
 
-#include "svd_cta.cuh"
-#include "bqr.cuh"
-
 // QR-route phase timing (clock64 deltas of thread 0, summed over CTAs): diagnostics only
-__device__ unsigned long long g_phase_cyc[8];
+__device__ unsigned long long g_phase_cyc[16];
 __device__ unsigned long long g_phase_cnt;
 #define PHASE_MARK(i)                                                          \
     do {                                                                       \
@@ -74,6 +71,9 @@ __device__ unsigned long long g_phase_cnt;
             ph_t0 = t_;                                                        \
         }                                                                      \
     } while (0)
+
+#include "svd_cta.cuh"
+#include "bqr.cuh"
 
 __device__ __forceinline__ void add_flops(FlopLedger* L, int cls, double f) {
     if (L && f > 0) atomicAdd(&L->f[cls], f);
@@ -448,7 +448,7 @@ struct TruncArgs {
 // C (ru x rv, ld ldc; shared memory) += alpha * A (ru x k) * B^T (rv x k), A/B column-major
 // in global memory.  NTH threads as a GY x GX grid (GX = 16), each owning a TM x TN register
 // tile (rows ty + GY i, columns tx + 16 j); k is staged through `stage`.
-template <int NTH, int TM, int TN>
+template <int NTH, int TM, int TN, bool TRI = false>
 __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, const double* B, int ldb, int ru, int rv, int k,
                               double alpha, double* stage, int stage_doubles) {
     constexpr int GX = 16, GY = NTH / GX;
@@ -468,11 +468,11 @@ __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, cons
         __syncthreads();
         for (int e = threadIdx.x; e < RA * kc; e += NTH) {
             const int i = e % RA, t = e / RA;
-            As[i + t * RA] = i < ru ? A[i + (size_t)(t0 + t) * lda] : 0.0;
+            As[i + t * RA] = (i < ru && (!TRI || i <= t0 + t)) ? A[i + (size_t)(t0 + t) * lda] : 0.0;
         }
         for (int e = threadIdx.x; e < RB * kc; e += NTH) {
             const int i = e % RB, t = e / RB;
-            Bs[i + t * RB] = i < rv ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
+            Bs[i + t * RB] = (i < rv && (!TRI || i <= t0 + t)) ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
         }
         __syncthreads();
         for (int t = 0; t < kc; ++t) {
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
     const int pmax = ku > kv ? ku : kv;
     const bool core_in_smem = pmax <= DMAX;
     const size_t smem_doubles = (size_t)DMAX * DMAX + (size_t)DMAX * RPCAP + (size_t)RPCAP * RPCAP + 5 * DMAX;
-    const bool blocked = (size_t)(m > n ? m : n) * BQR_NB + 2 * BQR_NB * BQR_NB <= smem_doubles;
+    const bool blocked = bqr_smem_doubles(m > n ? m : n, K) <= smem_doubles;
     const int npan = (K + BQR_NB - 1) / BQR_NB + 1;
     if (threadIdx.x == 0) {
         unsigned long long need = (unsigned long long)(m + n) * K + 2ull * K + 32 + 2ull * npan * BQR_NB * BQR_NB;
@@ -607,7 +607,13 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
     double* ws = sh_ws;
     if (ws == nullptr) return;  // arena exhausted: flag raised, target left unchanged
     unsigned long long ph_t0 = clock64();
-    if (threadIdx.x == 0) atomicAdd(&g_phase_cnt, 1ull);
+    if (threadIdx.x == 0) {
+        atomicAdd(&g_phase_cnt, 1ull);
+        atomicAdd(&g_phase_cyc[6], (unsigned long long)K);
+        atomicAdd(&g_phase_cyc[7], (unsigned long long)(m > n ? m : n));
+        if (!core_in_smem) atomicAdd(&g_phase_cyc[8], 1ull);
+        if (!blocked) atomicAdd(&g_phase_cyc[9], 1ull);
+    }
     double* Uc = ws;
     double* Vc = Uc + (size_t)m * K;
     double* tau_u = Vc + (size_t)n * K;
@@ -638,8 +644,8 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
     __syncthreads();
     PHASE_MARK(0);
     if (blocked) {
-        bqr<NTH>(Uc, m, m, K, tau_u, Tu, smem, smem_doubles, red);
-        bqr<NTH>(Vc, n, n, K, tau_v, Tv, smem, smem_doubles, red);
+        bqr<NTH>(Uc, m, m, K, tau_u, Tu, smem, smem_doubles);
+        bqr<NTH>(Vc, n, n, K, tau_v, Tv, smem, smem_doubles);
     } else {
         householder_qr<NTH>(Uc, m, m, K, tau_u, red);
         householder_qr<NTH>(Vc, n, n, K, tau_v, red);
@@ -648,13 +654,19 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
     // core = Ru Rv^T (ku x kv)
     double* core = w.A;
     w.lda = ku;
-    for (int e = threadIdx.x; e < ku * kv; e += NTH) {
-        const int i = e % ku, j = e / ku;
-        double acc = 0;
-        for (int t = (i > j ? i : j); t < K; ++t) acc = fma(Uc[i + (size_t)t * m], Vc[j + (size_t)t * n], acc);
-        core[e] = acc;
+    if (core_in_smem) {
+        for (int e = threadIdx.x; e < ku * kv; e += NTH) core[e] = 0.0;
+        gemm_nt_tiled<NTH, DMAX * 16 / NTH, DMAX / 16, true>(core, ku, Uc, m, Vc, n, ku, kv, K, 1.0, w.W,
+                                                               DMAX * RPCAP + RPCAP * RPCAP);
+    } else {
+        for (int e = threadIdx.x; e < ku * kv; e += NTH) {
+            const int i = e % ku, j = e / ku;
+            double acc = 0;
+            for (int t = (i > j ? i : j); t < K; ++t) acc = fma(Uc[i + (size_t)t * m], Vc[j + (size_t)t * n], acc);
+            core[e] = acc;
+        }
+        __syncthreads();
     }
-    __syncthreads();
     PHASE_MARK(2);
     int rp;
     double smax;
@@ -676,8 +688,8 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
             cta_trunc_write<NTH>(w, ku, kv, rp, r, Uo, m, Vo, n);
             PHASE_MARK(4);
             if (blocked) {
-                bqr_apply<NTH>(Uc, m, m, ku, Tu, Uo, m, r, smem);
-                bqr_apply<NTH>(Vc, n, n, kv, Tv, Vo, n, r, smem);
+                bqr_apply<NTH>(Uc, m, m, ku, Tu, Uo, m, r, smem, smem_doubles);
+                bqr_apply<NTH>(Vc, n, n, kv, Tv, Vo, n, r, smem, smem_doubles);
             } else {
                 apply_q<NTH>(Uc, m, m, ku, tau_u, Uo, m, r);
                 apply_q<NTH>(Vc, n, n, kv, tau_v, Vo, n, r);
@@ -1675,15 +1687,17 @@ std::string prof_report(bool reset) {
         out += buf;
     }
     {
-        unsigned long long ph[8], cnt = 0;
+        unsigned long long ph[16], cnt = 0;
         cudaMemcpyFromSymbol(ph, g_phase_cyc, sizeof(ph));
         cudaMemcpyFromSymbol(&cnt, g_phase_cnt, sizeof(cnt));
-        snprintf(buf, sizeof(buf), "#phase qr-route tasks %llu: concat %.3g qr %.3g core %.3g svd %.3g write %.3g applyq %.3g (Gcycles)\n",
-                 cnt, ph[0] / 1e9, ph[1] / 1e9, ph[2] / 1e9, ph[3] / 1e9, ph[4] / 1e9, ph[5] / 1e9);
+        snprintf(buf, sizeof(buf), "#phase qr-route tasks %llu: concat %.3g qr %.3g core %.3g svd %.3g write %.3g applyq %.3g (Gcycles)"
+                 " avgK %.1f avg_maxdim %.1f core_spill %llu unblocked %llu | bqr: panel %.3g T %.3g update %.3g\n",
+                 cnt, ph[0] / 1e9, ph[1] / 1e9, ph[2] / 1e9, ph[3] / 1e9, ph[4] / 1e9, ph[5] / 1e9,
+                 cnt ? (double)ph[6] / cnt : 0.0, cnt ? (double)ph[7] / cnt : 0.0, ph[8], ph[9], ph[10] / 1e9,
+                 ph[11] / 1e9, ph[12] / 1e9);
         out += buf;
         if (reset) {
-            cudaMemset(ph, 0, 0);
-            const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const unsigned long long z[16] = {};
             cudaMemcpyToSymbol(g_phase_cyc, z, sizeof(z));
             cudaMemcpyToSymbol(g_phase_cnt, z, sizeof(unsigned long long));
         }

@@ -19,6 +19,8 @@ rows = [l.split() for l in rep.strip().splitlines() if not l.startswith('#')]
 top = [l for l in rep.strip().splitlines() if l.startswith('#')]
 tot = sum(float(r[1]) for r in rows)
 for r in sorted(rows, key=lambda r: -float(r[1])):
-    print("%-18s %10.2f ms %5.1f%%  launches %7s  ctas %10s" % (r[0], float(r[1]), 100 * float(r[1]) / tot, r[2], r[3]))
+    fl = float(r[4]) if len(r) > 4 else 0.0
+    print("%-18s %10.2f ms %5.1f%%  launches %7s  ctas %10s  %7.2f TF/s" % (r[0], float(r[1]), 100 * float(r[1]) / tot, r[2], r[3],
+                                                                      fl / float(r[1]) / 1e9 if float(r[1]) > 0 else 0))
 print("total kernel ms", tot)
 print("\n".join(top[:25]))
