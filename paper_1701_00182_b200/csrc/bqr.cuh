@@ -269,10 +269,11 @@ __device__ void panel_T(const double* V, int h, int ldp, int nb, const double* t
 
 // A (h x nc, global, ld lda) <- (I - V op(T) V^T) A with V (h x 16, smem, ld ldv, explicit,
 // zero columns past nb) and T (16 x 16, smem).  trans: op(T) = T^T (apply Q^T).
-// Ws: smem scratch of ws_cap >= BQR_LDW * ceil8(nc) doubles.  All NT threads participate.
+// Ws: smem scratch of ws_cap >= BQR_LDW * ceil8(nc) doubles; Tpad: 16 x 17 smem scratch.
+// All NT threads participate.
 template <int NT>
 __device__ void wy_update(double* A, int lda, int h, int nc, const double* V, int ldv, const double* T, bool trans,
-                          double* Ws, int ws_cap) {
+                          double* Ws, int ws_cap, double* Tpad) {
     constexpr int NW = NT / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
@@ -322,7 +323,9 @@ __device__ void wy_update(double* A, int lda, int h, int nc, const double* V, in
     }
     __syncthreads();
     // 2. W <- -op(T) (sum of slices): thread per (column, output row), in place by
-    // column-disjoint chunks
+    // column-disjoint chunks; T staged with ld 17 (conflict-free for both transposes)
+    for (int e = threadIdx.x; e < BQR_NB * BQR_NB; e += NT) Tpad[(e % BQR_NB) + (e / BQR_NB) * (BQR_NB + 1)] = T[e];
+    __syncthreads();
     {
         const int tot = nct * 8 * BQR_NB;
         for (int base = 0; base < tot; base += 4 * NT) {
@@ -334,10 +337,11 @@ __device__ void wy_update(double* A, int lda, int h, int nc, const double* V, in
                 if (e < tot) {
                     const int i = e % BQR_NB, c = e / BQR_NB;
                     double s = 0;
+#pragma unroll
                     for (int k = 0; k < BQR_NB; ++k) {
                         double wk = Ws[k + (size_t)c * BQR_LDW];
                         for (int sp = 1; sp < nsp; ++sp) wk += Ws[(size_t)sp * slice + k + (size_t)c * BQR_LDW];
-                        s = fma(trans ? T[k + i * BQR_NB] : T[i + k * BQR_NB], wk, s);
+                        s = fma(trans ? Tpad[k + i * (BQR_NB + 1)] : Tpad[i + k * (BQR_NB + 1)], wk, s);
                     }
                     y[q] = -s;
                 }
@@ -429,7 +433,7 @@ __device__ void bqr(double* W, int ld, int rows, int cols, double* tau, double* 
         double* Tp = Tall + (size_t)(j0 / BQR_NB) * BQR_NB * BQR_NB;
         for (int e = threadIdx.x; e < BQR_NB * BQR_NB; e += NT) Tp[e] = Ts[e];
         const int nc = cols - j0 - nb;
-        if (nc > 0) wy_update<NT>(W + j0 + (size_t)(j0 + nb) * ld, ld, h, nc, P, ldp, Ts, true, Ws, ws_cap);
+        if (nc > 0) wy_update<NT>(W + j0 + (size_t)(j0 + nb) * ld, ld, h, nc, P, ldp, Ts, true, Ws, ws_cap, scratch);
         __syncthreads();
         PHASE_MARK(12);
     }
@@ -442,7 +446,8 @@ __device__ void bqr_apply(const double* W, int ldw, int rows, int k, const doubl
                           double* smem, size_t smem_doubles) {
     const int np = (k + BQR_NB - 1) / BQR_NB;
     double* Ts = smem + BQR_NB * BQR_NB;
-    double* P = Ts + BQR_NB * BQR_NB + BQR_SCRATCH;
+    double* scratch = Ts + BQR_NB * BQR_NB;
+    double* P = scratch + BQR_SCRATCH;
     double* Ws = P + (size_t)bqr_ldp(rows) * BQR_NB;
     const int ws_cap = (int)(smem_doubles - (size_t)(Ws - smem));
     for (int p = np - 1; p >= 0; --p) {
@@ -458,7 +463,7 @@ __device__ void bqr_apply(const double* W, int ldw, int rows, int k, const doubl
             P[i + (size_t)c * ldp] = W[(j0 + i) + (size_t)(j0 + c) * ldw];
         }
         panel_explicit_v<NT>(P, h, ldp, nb);
-        wy_update<NT>(Y + j0, ldy, h, ncol, P, ldp, Ts, false, Ws, ws_cap);
+        wy_update<NT>(Y + j0, ldy, h, ncol, P, ldp, Ts, false, Ws, ws_cap, scratch);
     }
     __syncthreads();
 }

@@ -215,7 +215,8 @@ static int size_class(int m, int n) {
 
 struct Plan {
     int nprod = 0;
-    int nalloc = 0, napply = 0, ndep = 0;
+    int nalloc = 0, napply = 0, ndep = 0, ntt = 0;
+    ApplyTTask* tts = nullptr;
     AllocTask* allocs = nullptr;
     ApplyTask* applies = nullptr;
     ApplyLeaf* aleaves = nullptr;
@@ -362,6 +363,7 @@ struct Engine {
         std::vector<AllocTask> allocs;
         std::vector<ApplyTask> applies;
         std::vector<ApplyLeaf> aleaves;
+        std::vector<ApplyTTask> tts;
         std::vector<int> x_ld;
         std::vector<DDTask> dds;
         std::vector<std::vector<TruncTask>> bb;
@@ -415,6 +417,21 @@ struct Engine {
         subtree_leaves(hnode, lv);
         const int out_pos0 = trans ? H.cb : H.rb;
         const int out_len = trans ? H.cols() : H.rows();
+        std::map<int, int> tl_of;  // Rk leaf node -> T task
+        for (int li : lv) {
+            const SNode& L = S.node(li);
+            if (L.kind != K_RK) continue;
+            ApplyTTask tt;
+            tt.prod = pid;
+            tt.kind = kind;
+            tt.kx = kx;
+            tt.id = L.leaf - R.k0;
+            tt.in_off = trans ? L.rb - H.rb : L.cb - H.cb;
+            tt.in_len = trans ? L.rows() : L.cols();
+            tt.x_ld = xld;
+            tl_of[li] = (int)pb.tts.size();
+            pb.tts.push_back(tt);
+        }
         for (auto [r0, r1] : slabs_of(out_pos0, out_len)) {
             ApplyTask t;
             t.prod = pid;
@@ -436,6 +453,7 @@ struct Engine {
                 a.n = L.cols();
                 a.in_off = trans ? L.rb - H.rb : L.cb - H.cb;
                 a.out_off = o0;
+                a.tl = L.kind == K_RK ? tl_of[li] : -1;
                 pb.aleaves.push_back(a);
             }
             t.lend = (int)pb.aleaves.size();
@@ -625,6 +643,8 @@ struct Engine {
         P->nprod = pb.nprod;
         P->nalloc = (int)pb.allocs.size();
         P->napply = (int)pb.applies.size();
+        P->ntt = (int)pb.tts.size();
+        P->tts = up(pb.tts);
         P->ndep = (int)pb.deps.size();
         P->allocs = up(pb.allocs);
         P->applies = up(pb.applies);
@@ -655,11 +675,12 @@ struct Engine {
                 bv.a[b] = hview(A[i0 + b]);
                 bv.b[b] = hview(B[i0 + b]);
             }
-            Slot* slots = ctx->get_slots((size_t)std::max(1, P->nprod) * nb);
+            Slot* slots = ctx->get_slots((size_t)std::max(1, P->nprod + P->ntt) * nb);
             const Arena tr = ctx->lane().trans;
             launch_reset_counter(st(), tr.ctr);
             launch_alloc_apply(st(), P->nalloc, P->allocs, slots, nb, tr, bv);
-            launch_apply(st(), P->napply, P->applies, P->aleaves, P->x_ld, slots, nb, ctx->flops, bv);
+            launch_apply_t(st(), P->ntt, P->tts, slots, P->nprod, nb, tr, ctx->flops, bv);
+            launch_apply(st(), P->napply, P->applies, P->aleaves, P->x_ld, slots, P->nprod, nb, ctx->flops, bv);
             if (P->dds.n[0]) launch_dd_small(st(), 32, P->dds.n[0], P->dds.p[0], slots, nb, eps, tr, ctx->flops, bv);
             if (P->dds.n[1]) launch_dd_small(st(), 64, P->dds.n[1], P->dds.p[1], slots, nb, eps, tr, ctx->flops, bv);
             if (P->dds.n[2] || P->dds.n[3]) throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64"};
@@ -843,6 +864,7 @@ struct Engine {
                 a.n = L.cols();
                 a.in_off = L.cb;
                 a.out_off = L.rb;
+                a.tl = -1;
                 al.push_back(a);
             }
             t.lend = (int)al.size();

@@ -457,7 +457,7 @@ __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, cons
     if (KC > 32) KC = 32;
     double* As = stage;            // RA x KC
     double* Bs = stage + RA * KC;  // RB x KC
-    const int tx = threadIdx.x % GX, ty = threadIdx.x / GX;
+    const int ty = threadIdx.x % GY, tx = threadIdx.x / GY;  // consecutive lanes -> consecutive rows (no bank conflicts on C)
     double acc[TM][TN];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
@@ -809,17 +809,103 @@ struct ApplyArgs {
     const ApplyLeaf* leaves;
     Slot* slots;
     int B;
-    int x_ld_mode;  // unused
+    int nprod;        // T task t of the batch lives in slot (nprod + t)
     const int* x_ld;  // per task: leading dimension of X
     FlopLedger* flops;
 };
 
-constexpr int APPLY_ROWS = 64;  // max slab rows
-constexpr int APPLY_COLS = 32;  // rhs columns per pass
-constexpr int APPLY_TR = 64;    // Rk ranks per inner pass
+struct ApplyTArgs {
+    const ApplyTTask* tasks;
+    Slot* slots;
+    int B;
+    int nprod;
+    Arena arena;
+    FlopLedger* flops;
+};
 
+// Register tile of the apply kernels: a 64 x 32 output block, thread (tr, tc) owns rows
+// tr + 32 i (i < 2) and columns tc + 8 j (j < 4); the k-dimension is staged in shared
+// memory in chunks of 32 (A: 64 x 32, ld 65; B: 32 x 32, ld 33).
+constexpr int AP_LDA = 65, AP_LDB = 33;
+constexpr int APPLY_ROWS = 64;  // max slab rows (matvec)
+constexpr int APPLY_TR = 64;    // Rk ranks per inner pass (matvec)
+__device__ __forceinline__ void ap_accumulate(double (&acc)[2][4], const double* As, const double* Bs, int kc) {
+    const int tr = threadIdx.x & 31, tc = threadIdx.x >> 5;
+#pragma unroll 8
+    for (int t = 0; t < kc; ++t) {
+        const double a0 = As[tr + t * AP_LDA], a1 = As[tr + 32 + t * AP_LDA];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double bb = Bs[t + (tc + 8 * j) * AP_LDB];
+            acc[0][j] = fma(a0, bb, acc[0][j]);
+            acc[1][j] = fma(a1, bb, acc[1][j]);
+        }
+    }
+}
+
+// T = In^T X (rank x k) for one Rk leaf, once per (leaf, plane).
+__global__ void __launch_bounds__(NT) k_apply_t(ApplyTArgs args, BatchViews bv) {
+    __shared__ double As[64 * AP_LDA];  // In^T chunk: 64 ranks x 32 contracted
+    __shared__ double Bs[32 * AP_LDB];  // X chunk: 32 contracted x 32 columns
+    __shared__ double* sh_T;
+    const ApplyTTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    Slot& out = args.slots[(size_t)(args.nprod + blockIdx.x) * args.B + b];
+    const Slot s = args.slots[(size_t)task.prod * args.B + b];
+    const int k = s.rank;
+    const bool trans = task.kind == P_RK_LEFT;
+    const HView& H = trans ? bv.b[b] : bv.a[b];
+    const int rr = k ? H.rank[task.id] : 0;
+    if (rr == 0) {
+        if (threadIdx.x == 0) out.U = nullptr;
+        return;
+    }
+    if (threadIdx.x == 0) sh_T = arena_alloc(args.arena, (unsigned long long)rr * k);
+    __syncthreads();
+    double* T = sh_T;
+    if (threadIdx.x == 0) {
+        out.U = T;
+        out.rank = rr;
+    }
+    if (!T) return;  // arena exhausted: flagged; the slabs skip this leaf
+    const double* In = trans ? H.U[task.id] : H.V[task.id];
+    const double* X = (trans ? bv.a[b].V[task.kx] : bv.b[b].U[task.kx]) + task.in_off;
+    const int L = task.in_len, ldx = task.x_ld;
+    const int tr = threadIdx.x & 31, tc = threadIdx.x >> 5;
+    for (int t0 = 0; t0 < rr; t0 += 64)
+        for (int c0 = 0; c0 < k; c0 += 32) {
+            const int nt = min(64, rr - t0), nc = min(32, k - c0);
+            double acc[2][4] = {};
+            for (int j0 = 0; j0 < L; j0 += 32) {
+                const int jc = min(32, L - j0);
+                __syncthreads();
+                for (int e = threadIdx.x; e < 64 * 32; e += NT) {  // contracted index fastest: coalesced
+                    const int j = e & 31, t = e >> 5;
+                    As[t + j * AP_LDA] = (j < jc && t < nt) ? In[(j0 + j) + (size_t)(t0 + t) * L] : 0.0;
+                }
+                for (int e = threadIdx.x; e < 32 * 32; e += NT) {
+                    const int j = e & 31, c = e >> 5;
+                    Bs[j + c * AP_LDB] = (j < jc && c < nc) ? X[(j0 + j) + (size_t)(c0 + c) * ldx] : 0.0;
+                }
+                __syncthreads();
+                ap_accumulate(acc, As, Bs, jc);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int t = tr + 32 * i, c = tc + 8 * j;
+                    if (t < nt && c < nc) T[(t0 + t) + (size_t)(c0 + c) * rr] = acc[i][j];
+                }
+        }
+    if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, 2.0 * rr * L * k);
+}
+
+// One output slab (<= 64 rows, all k columns): Y = sum over dense leaves of D (or D^T) X
+// plus sum over Rk leaves of Out T, operands staged through shared memory.
 __global__ void __launch_bounds__(NT) k_apply(ApplyArgs args, BatchViews bv) {
-    __shared__ double T[APPLY_TR * APPLY_COLS];
+    __shared__ double As[64 * AP_LDA];
+    __shared__ double Bs[32 * AP_LDB];
     const ApplyTask task = args.tasks[blockIdx.x];
     const int b = blockIdx.y;
     const Slot s = args.slots[(size_t)task.prod * args.B + b];
@@ -832,13 +918,11 @@ __global__ void __launch_bounds__(NT) k_apply(ApplyArgs args, BatchViews bv) {
     double* Y = trans ? s.V : s.U;
     const int ldy = trans ? s.ldv : s.ldu;
     const int r0 = task.r0, nr = task.r1 - task.r0;
+    const int tr = threadIdx.x & 31, tc = threadIdx.x >> 5;
     double fl = 0;
-    for (int c0 = 0; c0 < k; c0 += APPLY_COLS) {
-        const int nc = min(APPLY_COLS, k - c0);
-        // each thread owns elements e = tid + t*NT of the nr x nc slab
-        double acc[(APPLY_ROWS * APPLY_COLS) / NT];
-#pragma unroll
-        for (int q = 0; q < (APPLY_ROWS * APPLY_COLS) / NT; ++q) acc[q] = 0.0;
+    for (int c0 = 0; c0 < k; c0 += 32) {
+        const int nc = min(32, k - c0);
+        double acc[2][4] = {};
         for (int li = task.lbeg; li < task.lend; ++li) {
             const ApplyLeaf L = args.leaves[li];
             const int out_len = trans ? L.n : L.m;
@@ -847,65 +931,64 @@ __global__ void __launch_bounds__(NT) k_apply(ApplyArgs args, BatchViews bv) {
             if (o0 >= o1) continue;
             if (L.kind == K_DENSE) {
                 const double* D = H.dense + L.doff;
-#pragma unroll
-                for (int q = 0; q < (APPLY_ROWS * APPLY_COLS) / NT; ++q) {
-                    const int e = threadIdx.x + q * NT;
-                    const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
-                    const int row = r0 + i;
-                    if (i >= nr || c >= nc || row < o0 || row >= o1) continue;
-                    const int lr = row - L.out_off;  // leaf output index
-                    const double* x = X + L.in_off + (size_t)(c0 + c) * ldx;
-                    double a = 0;
-                    if (!trans)
-                        for (int j = 0; j < in_len; ++j) a = fma(D[lr + (size_t)j * L.m], x[j], a);
-                    else
-                        for (int j = 0; j < in_len; ++j) a = fma(D[j + (size_t)lr * L.m], x[j], a);
-                    acc[q] += a;
+                for (int j0 = 0; j0 < in_len; j0 += 32) {
+                    const int jc = min(32, in_len - j0);
+                    __syncthreads();
+                    if (!trans) {
+                        for (int e = threadIdx.x; e < 64 * 32; e += NT) {  // output row fastest: coalesced
+                            const int i = e & 63, j = e >> 6;
+                            const int row = r0 + i;
+                            As[i + j * AP_LDA] = (row >= o0 && row < o1 && j < jc)
+                                                     ? D[(row - L.out_off) + (size_t)(j0 + j) * L.m] : 0.0;
+                        }
+                    } else {
+                        for (int e = threadIdx.x; e < 64 * 32; e += NT) {  // contracted index fastest
+                            const int j = e & 31, i = e >> 5;
+                            const int row = r0 + i;
+                            As[i + j * AP_LDA] = (row >= o0 && row < o1 && j < jc)
+                                                     ? D[(j0 + j) + (size_t)(row - L.out_off) * L.m] : 0.0;
+                        }
+                    }
+                    for (int e = threadIdx.x; e < 32 * 32; e += NT) {
+                        const int j = e & 31, c = e >> 5;
+                        Bs[j + c * AP_LDB] = (j < jc && c < nc) ? X[L.in_off + j0 + j + (size_t)(c0 + c) * ldx] : 0.0;
+                    }
+                    __syncthreads();
+                    ap_accumulate(acc, As, Bs, jc);
                 }
-                if (threadIdx.x == 0) fl += 2.0 * (o1 - o0) * in_len * nc;
+                fl += 2.0 * (o1 - o0) * in_len * nc;
             } else {
-                const int rr = H.rank[L.id];
-                if (rr == 0) continue;
-                const double* In = trans ? H.U[L.id] : H.V[L.id];   // contracted with X
-                const double* Out = trans ? H.V[L.id] : H.U[L.id];  // expands into Y
-                const int ld_in = in_len, ld_out = out_len;
-                for (int t0 = 0; t0 < rr; t0 += APPLY_TR) {
-                    const int nt = min(APPLY_TR, rr - t0);
+                const Slot ts = args.slots[(size_t)(args.nprod + L.tl) * args.B + b];
+                const double* T = ts.U;
+                if (!T) continue;
+                const int rr = ts.rank;
+                const double* Out = trans ? H.V[L.id] : H.U[L.id];
+                for (int t0 = 0; t0 < rr; t0 += 32) {
+                    const int tcn = min(32, rr - t0);
                     __syncthreads();
-                    for (int e = threadIdx.x; e < nt * nc; e += NT) {
-                        const int t = e % nt, c = e / nt;
-                        const double* in = In + (size_t)(t0 + t) * ld_in;
-                        const double* x = X + L.in_off + (size_t)(c0 + c) * ldx;
-                        double a = 0;
-                        for (int j = 0; j < in_len; ++j) a = fma(in[j], x[j], a);
-                        T[t + c * APPLY_TR] = a;
-                    }
-                    __syncthreads();
-#pragma unroll
-                    for (int q = 0; q < (APPLY_ROWS * APPLY_COLS) / NT; ++q) {
-                        const int e = threadIdx.x + q * NT;
-                        const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
+                    for (int e = threadIdx.x; e < 64 * 32; e += NT) {
+                        const int i = e & 63, t = e >> 6;
                         const int row = r0 + i;
-                        if (i >= nr || c >= nc || row < o0 || row >= o1) continue;
-                        const int lr = row - L.out_off;
-                        double a = 0;
-                        for (int t = 0; t < nt; ++t) a = fma(Out[lr + (size_t)(t0 + t) * ld_out], T[t + c * APPLY_TR], a);
-                        acc[q] += a;
+                        As[i + t * AP_LDA] = (row >= o0 && row < o1 && t < tcn)
+                                                 ? Out[(row - L.out_off) + (size_t)(t0 + t) * out_len] : 0.0;
                     }
+                    for (int e = threadIdx.x; e < 32 * 32; e += NT) {
+                        const int t = e & 31, c = e >> 5;
+                        Bs[t + c * AP_LDB] = (t < tcn && c < nc) ? T[(t0 + t) + (size_t)(c0 + c) * rr] : 0.0;
+                    }
+                    __syncthreads();
+                    ap_accumulate(acc, As, Bs, tcn);
                 }
-                if (threadIdx.x == 0) {
-                    fl += 2.0 * (o1 - o0) * rr * nc;
-                    if (L.out_off >= r0 && L.out_off < task.r1) fl += 2.0 * rr * in_len * nc;
-                }
+                fl += 2.0 * (o1 - o0) * rr * nc;
             }
         }
 #pragma unroll
-        for (int q = 0; q < (APPLY_ROWS * APPLY_COLS) / NT; ++q) {
-            const int e = threadIdx.x + q * NT;
-            const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
-            if (i < nr && c < nc) Y[(r0 + i) + (size_t)(c0 + c) * ldy] = acc[q];
-        }
-        __syncthreads();
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int r = tr + 32 * i, c = tc + 8 * j;
+                if (r < nr && c < nc) Y[(r0 + r) + (size_t)(c0 + c) * ldy] = acc[i][j];
+            }
     }
     if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, fl);
 }
@@ -1781,10 +1864,18 @@ void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slo
     k_alloc_apply<<<(total + 127) / 128, 128, 0, st>>>(a, bv);
 }
 
-void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
-                  Slot* slots, int B, FlopLedger* flops, const BatchViews& bv) {
+void launch_apply_t(cudaStream_t st, int ntasks, const ApplyTTask* tasks, Slot* slots, int nprod, int B, Arena arena,
+                    FlopLedger* flops, const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
-    ApplyArgs a{tasks, leaves, slots, B, 0, x_ld, ledger(flops, "k_apply")};
+    ApplyTArgs a{tasks, slots, B, nprod, arena, ledger(flops, "k_apply_t")};
+    ProfScope _ps(st, "k_apply_t", (long)ntasks * B);
+    k_apply_t<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
+}
+
+void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
+                  Slot* slots, int nprod, int B, FlopLedger* flops, const BatchViews& bv) {
+    if (ntasks == 0 || B == 0) return;
+    ApplyArgs a{tasks, leaves, slots, B, nprod, x_ld, ledger(flops, "k_apply")};
     ProfScope _ps(st, "k_apply", (long)((ntasks)*(B)));
     k_apply<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
 }

@@ -63,8 +63,10 @@ void launch_dd(cudaStream_t st, int ntasks, const DDTask* tasks, Slot* slots, in
                FlopLedger* flops, const BatchViews& bv);
 void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slot* slots, int B, Arena arena,
                         const BatchViews& bv);
+void launch_apply_t(cudaStream_t st, int ntasks, const ApplyTTask* tasks, Slot* slots, int nprod, int B, Arena arena,
+                    FlopLedger* flops, const BatchViews& bv);
 void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
-                  Slot* slots, int B, FlopLedger* flops, const BatchViews& bv);
+                  Slot* slots, int nprod, int B, FlopLedger* flops, const BatchViews& bv);
 void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Part* parts, const Slot* slots, int B,
                     FlopLedger* flops, const BatchViews& bv);
 void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, unsigned long long call_id,

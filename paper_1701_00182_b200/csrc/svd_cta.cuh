@@ -25,49 +25,65 @@ struct CtaSvdWork {
 };
 
 // Returns rp.  delta2: squared pivot threshold.  NT threads, NW warps.
+// One barrier per pivot step (two when the pivot moves): the update pass that
+// applies reflector k also leaves, per column, the norm over rows > k (pivot
+// choice) and over rows > k+1 (the next reflector's tail), and each warp's
+// best candidate; every thread then picks the pivot and derives the reflector
+// scalars itself.  Reflector k is applied unscaled (v = [1; x / (c0 - beta)])
+// and stored scaled one step later, when column k is no longer read.
 template <int NT>
 __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) {
     constexpr int NW = NT / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ double sh_best, sh_tau, sh_beta, sh_inv;
-    __shared__ int sh_piv;
+    __shared__ double sh_wbest[2][NW];  // per-warp pivot candidates, double-buffered by step parity
+    __shared__ int sh_wpiv[2][NW];
     double* A = w.A;
     const int lda = w.lda;
+    double* tail = w.sig;  // norm over rows > k of each remaining column
     for (int j = threadIdx.x; j < cols; j += NT) w.perm[j] = j;
     const int kmax = rows < cols ? rows : cols;
-    int rp = 0;
-    // remaining column norms (rows >= k); refreshed exactly inside the update pass below
-    for (int j = warp; j < cols; j += NW) {
-        const double* cj = A + (size_t)j * lda;
-        double s = 0;
+    {
+        double best = -1.0;
+        int bi = cols;
+        for (int j = warp; j < cols; j += NW) {
+            const double* cj = A + (size_t)j * lda;
+            double s = 0, tl = 0;
 #pragma unroll 4
-        for (int i = lane; i < rows; i += 32) s = fma(cj[i], cj[i], s);
-        s = warp_sum(s);
-        if (lane == 0) w.nrm[j] = s;
-    }
-    __syncthreads();
-    for (int k = 0; k < kmax; ++k) {
-        if (warp == 0) {
-            double best = -1.0;
-            int bi = k;
-            for (int j = k + lane; j < cols; j += 32) {
-                const double v = w.nrm[j];
-                if (v > best) { best = v; bi = j; }
+            for (int i = lane; i < rows; i += 32) {
+                s = fma(cj[i], cj[i], s);
+                if (i > 0) tl = fma(cj[i], cj[i], tl);
             }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-            }
+            s = warp_sum(s);
+            tl = warp_sum(tl);
             if (lane == 0) {
-                sh_best = best;
-                sh_piv = bi;
+                w.nrm[j] = s;
+                tail[j] = tl;
+            }
+            if (s > best) {
+                best = s;
+                bi = j;
             }
         }
-        __syncthreads();
-        if (!(sh_best > delta2)) break;
-        const int piv = sh_piv;
+        if (lane == 0) {
+            sh_wbest[0][warp] = best;
+            sh_wpiv[0][warp] = bi;
+        }
+    }
+    __syncthreads();
+    int rp = 0;
+    double p_inv = 0.0, p_beta = 0.0, p_tau = 0.0;
+    for (int k = 0; k < kmax; ++k) {
+        double best = -1.0;
+        int piv = cols;
+        for (int q = 0; q < NW; ++q) {
+            const double b = sh_wbest[k & 1][q];
+            const int i = sh_wpiv[k & 1][q];
+            if (b > best || (b == best && i < piv)) {
+                best = b;
+                piv = i;
+            }
+        }
+        if (!(best > delta2)) break;
         if (piv != k) {
             double* ck = A + (size_t)k * lda;
             double* cp = A + (size_t)piv * lda;
@@ -76,68 +92,87 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
                 ck[i] = cp[i];
                 cp[i] = t;
             }
+            __syncthreads();
             if (threadIdx.x == 0) {
                 const int t = w.perm[k];
                 w.perm[k] = w.perm[piv];
                 w.perm[piv] = t;
-                const double tn = w.nrm[k];
+                double tn = w.nrm[k];
                 w.nrm[k] = w.nrm[piv];
                 w.nrm[piv] = tn;
+                tn = tail[k];
+                tail[k] = tail[piv];
+                tail[piv] = tn;
             }
             __syncthreads();
         }
         double* ck = A + (size_t)k * lda;
-        if (warp == 0) {
-            double t = 0;
-            #pragma unroll 4
-            for (int i = k + 1 + lane; i < rows; i += 32) t = fma(ck[i], ck[i], t);
-            t = warp_sum(t);
-            if (lane == 0) {
-                const double c0 = ck[k];
-                if (t > 2.2250738585072014e-308) {
-                    double beta = sqrt(c0 * c0 + t);
-                    if (c0 >= 0) beta = -beta;
-                    sh_inv = 1.0 / (c0 - beta);
-                    sh_tau = (beta - c0) / beta;
-                    sh_beta = beta;
-                } else {
-                    sh_inv = 0.0;
-                    sh_tau = 0.0;
-                    sh_beta = c0;
-                }
-                w.tau[k] = sh_tau;
-            }
+        const double c0 = ck[k], t = tail[k];
+        double beta, tk, inv;
+        if (t > 2.2250738585072014e-308) {
+            beta = sqrt(c0 * c0 + t);
+            if (c0 >= 0) beta = -beta;
+            inv = 1.0 / (c0 - beta);
+            tk = (beta - c0) / beta;
+        } else {
+            inv = 0.0;
+            tk = 0.0;
+            beta = c0;
         }
-        __syncthreads();
-        const double tk = sh_tau, inv = sh_inv;
-        for (int i = k + 1 + threadIdx.x; i < rows; i += NT) ck[i] = tk != 0.0 ? ck[i] * inv : 0.0;
-        __syncthreads();
-        if (threadIdx.x == 0) ck[k] = sh_beta;
-        // apply the reflector to the remaining columns and refresh their norms over rows > k
+        if (threadIdx.x == 0) w.tau[k] = tk;
+        if (k > 0) {  // store reflector k-1 (column k-1 is not read in this step)
+            double* cq = A + (size_t)(k - 1) * lda;
+            for (int i = k + threadIdx.x; i < rows; i += NT) cq[i] = p_tau != 0.0 ? cq[i] * p_inv : 0.0;
+            if (threadIdx.x == 0) cq[k - 1] = p_beta;
+        }
+        // apply reflector k to the remaining columns; refresh norms; warp-local pivot candidates
+        double wb = -1.0;
+        int wi = cols;
         for (int j = k + 1 + warp; j < cols; j += NW) {
             double* cj = A + (size_t)j * lda;
             double s = 0;
             if (tk != 0.0) {
 #pragma unroll 4
                 for (int i = k + 1 + lane; i < rows; i += 32) s = fma(ck[i], cj[i], s);
-                s = (warp_sum(s) + cj[k]) * tk;
+                s = fma(warp_sum(s), inv, cj[k]) * tk;
             }
-            double nn = 0;
+            const double si = s * inv;
+            double nn = 0, tl = 0;
 #pragma unroll 4
             for (int i = k + 1 + lane; i < rows; i += 32) {
-                const double v = fma(-s, ck[i], cj[i]);
+                const double v = fma(-si, ck[i], cj[i]);
                 cj[i] = v;
                 nn = fma(v, v, nn);
+                if (i > k + 1) tl = fma(v, v, tl);
             }
             nn = warp_sum(nn);
+            tl = warp_sum(tl);
             if (lane == 0) {
                 cj[k] -= s;
                 w.nrm[j] = nn;
+                tail[j] = tl;
             }
+            if (nn > wb) {
+                wb = nn;
+                wi = j;
+            }
+        }
+        p_inv = inv;
+        p_beta = beta;
+        p_tau = tk;
+        if (lane == 0) {
+            sh_wbest[(k + 1) & 1][warp] = wb;
+            sh_wpiv[(k + 1) & 1][warp] = wi;
         }
         __syncthreads();
         rp = k + 1;
     }
+    if (rp > 0) {
+        double* cq = A + (size_t)(rp - 1) * lda;
+        for (int i = rp + threadIdx.x; i < rows; i += NT) cq[i] = p_tau != 0.0 ? cq[i] * p_inv : 0.0;
+        if (threadIdx.x == 0) cq[rp - 1] = p_beta;
+    }
+    __syncthreads();
     return rp;
 }
 

@@ -74,6 +74,21 @@ struct ApplyLeaf {
     int m, n;        // leaf rows / cols (untransposed)
     int in_off;      // X row of the leaf's first contracted index
     int out_off;     // Y row of the leaf's first output index (relative to slab output space)
+    int tl;          // K_RK: index of the leaf's T task (T = In^T X, shared by all its slabs)
+};
+
+// T = In^T X for one Rk leaf of an apply product (In = U for the transposed apply, V
+// otherwise), computed once and read by every output slab the leaf overlaps.  The
+// result (rank x k, ld rank) lives in the transient arena; its pointer goes to slot
+// (nprod + index) of the batch's slot table.
+struct ApplyTTask {
+    int prod;
+    int kind;
+    int kx;
+    int id;          // relative Rk id
+    int in_off;      // X row of the first contracted index
+    int in_len;
+    int x_ld;
 };
 
 struct DDTask {
