@@ -1007,7 +1007,9 @@ static DSys* make_dsys(const acrgpu_system* sys, cudaStream_t st) {
     return ds.release();
 }
 
-static std::vector<SP> lift(Engine& E, const DSys& ds) {
+// keep (optional, 3n-2 flags): lift only those blocks (the plane partition's own planes);
+// the others come back null.
+static std::vector<SP> lift(Engine& E, const DSys& ds, const std::vector<char>* keep = nullptr) {
     const int n = ds.n, nb = 3 * n - 2;
     const Structure& S = E.S;
     const std::vector<int>& rows = ds.rows;
@@ -1042,18 +1044,32 @@ static std::vector<SP> lift(Engine& E, const DSys& ds) {
     int* d_drows = upload(drows, st);
     int* d_hits = dmalloc<int>(1);
     CK(cudaMemsetAsync(d_hits, 0, sizeof(int), st));
-    std::vector<SP> blocks;
-    for (int b = 0; b < nb; ++b) blocks.push_back(E.new_store(0));
-    auto vs = views(blocks);
-    E.zero(vs);
+    auto kept = [&](int b) { return !keep || (*keep)[b]; };
+    std::vector<SP> blocks(nb);
+    std::vector<View> vs(nb);
+    std::vector<View> all;
+    for (int b = 0; b < nb; ++b)
+        if (kept(b)) {
+            blocks[b] = E.new_store(0);
+            vs[b] = root_view(blocks[b]);
+            all.push_back(vs[b]);
+        }
+    if (!all.empty()) E.zero(all);
     ScatterLaunch sl{d_rows, d_cols, d_vals, nullptr, E.d_iperm, d_leaf_of, d_clidx, d_clb, ncl,
                      E.d_doff, d_drows, d_drb, d_dcb, d_hits};
-    for (int i0 = 0; i0 < nb; i0 += MAXB) {
+    for (int b0 = 0; b0 < nb;) {  // runs of consecutive kept blocks share the offsets table
+        if (!kept(b0)) {
+            ++b0;
+            continue;
+        }
+        int b1 = b0;
+        while (b1 < nb && kept(b1) && b1 - b0 < MAXB) ++b1;
         BatchViews bv{};
-        bv.count = std::min(MAXB, nb - i0);
-        for (int b = 0; b < bv.count; ++b) bv.c[b] = E.hview(vs[i0 + b]);
-        sl.off = d_off + i0;
+        bv.count = b1 - b0;
+        for (int b = 0; b < bv.count; ++b) bv.c[b] = E.hview(vs[b0 + b]);
+        sl.off = d_off + b0;
         launch_scatter(st, sl, bv);
+        b0 = b1;
     }
     int hits = 0;
     CK(cudaMemcpyAsync(&hits, d_hits, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1062,6 +1078,7 @@ static std::vector<SP> lift(Engine& E, const DSys& ds) {
         // entries inside admissible leaves: factor through the nonzero columns
         // (build_from_sparse, hmatrix.cpp:127-147), then device truncation at eps
         for (int b = 0; b < nb; ++b) {
+            if (!kept(b)) continue;
             std::map<int, std::vector<std::tuple<int, int, double>>> per_leaf;
             for (long i = off[b]; i < off[b + 1]; ++i) {
                 const int r = S.iperm[rows[i]], c = S.iperm[cols[i]];
@@ -1220,146 +1237,210 @@ static void compact_factor(acrgpu_fact* F) {
     for (void* p : std::initializer_list<void*>{d_off, d_km, d_kn, d_U, d_V, d_R}) cudaFree(p);
 }
 
-static void do_factor(acrgpu_fact* F, const DSys& sys) {
-    Engine& E = *F->eng;
-    const int n = sys.n;
-    cudaEvent_t e0, e1, e2;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventCreate(&e2));
-    CK(cudaEventRecord(e0, E.st()));
-    auto blocks = lift(E, sys);
-    CK(cudaEventRecord(e1, E.st()));
-    std::vector<SP> D(n), Ev(n), Fv(n);
-    for (int j = 0; j < n; ++j) D[j] = blocks[j];
-    for (int j = 1; j < n; ++j) Ev[j] = blocks[n + j - 1];
-    for (int j = 0; j + 1 < n; ++j) Fv[j] = blocks[2 * n - 1 + j];
-    blocks.clear();
-    const int stop = F->eng->cfg.stop_planes;
-    int lvl = 0;
-    static const bool verbose = getenv("ACRGPU_VERBOSE") != nullptr;
+// Per-rank state of a factorization run: the planes this rank owns at the current
+// level (null elsewhere), indexed by position.  Single-GPU runs own every plane.
+struct PartRun {
+    acrgpu_fact* F = nullptr;
+    int rank = 0;
+    std::vector<SP> D, Ev, Fv;
     std::vector<cudaEvent_t> lev_ev;
-    auto mark = [&]() {
-        if (!verbose) return;
-        cudaEvent_t e;
-        CK(cudaEventCreate(&e));
-        CK(cudaEventRecord(e, E.main_st()));
-        lev_ev.push_back(e);
-    };
-    mark();
-    while ((int)D.size() > stop) {
-        const int m = (int)D.size();
-        Level L;
-        L.plane_count = m;
-        L.elim = eliminated_positions(m);
-        L.ret = retained_positions(m);
-        L.E = Ev;
-        L.F = Fv;
-        L.Dinv.assign(m, nullptr);
-        std::vector<char> is_elim(m, 0);
-        for (int e : L.elim) is_elim[e] = 1;
-        // 1. invert the eliminated planes (batched over planes)
-        {
-            std::vector<SP> outs;
-            std::vector<View> ov, iv;
-            for (int e : L.elim) {
-                outs.push_back(E.new_store(0));
-                ov.push_back(root_view(outs.back()));
-                iv.push_back(root_view(D[e]));
-            }
-            if (!ov.empty()) E.invert(ov, iv, lvl, L.elim);
-            for (size_t t = 0; t < L.elim.size(); ++t) {
-                L.Dinv[L.elim[t]] = outs[t];
-                D[L.elim[t]].reset();
-            }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+// plan_schedule (parallel.cpp:383-405): contiguous plane blocks at level 0; retained
+// planes keep their owner at every later level.  owners[l][j] = rank of plane j at level l.
+static std::vector<std::vector<int>> plan_owners(int n, int p) {
+    auto pow2 = [](int x) { return x > 0 && (x & (x - 1)) == 0; };
+    if (!pow2(n) || !pow2(p))
+        throw AcrError{ACRGPU_E_USAGE, "plan_schedule: plane and worker counts must be powers of two"};
+    if (p > n) throw AcrError{ACRGPU_E_USAGE, "plan_schedule: more workers than planes"};
+    std::vector<std::vector<int>> a;
+    std::vector<int> cur(n);
+    for (int j = 0; j < n; ++j) cur[j] = j / (n / p);
+    a.push_back(cur);
+    while (cur.size() > 1) {
+        std::vector<int> nx;
+        for (int t : retained_positions((int)cur.size())) nx.push_back(cur[t]);
+        cur = nx;
+        a.push_back(cur);
+    }
+    return a;
+}
+
+static void factor_begin(PartRun& R, const DSys& sys, const std::vector<std::vector<int>>* own) {
+    Engine& E = *R.F->eng;
+    const int n = sys.n;
+    CK(cudaEventCreate(&R.e0));
+    CK(cudaEventCreate(&R.e1));
+    CK(cudaEventRecord(R.e0, E.st()));
+    std::vector<char> keep(3 * n - 2, 1);
+    if (own) {
+        for (int j = 0; j < n; ++j) {
+            const char mine = (*own)[0][j] == R.rank;
+            keep[j] = mine;
+            if (j > 0) keep[n + j - 1] = mine;
+            if (j + 1 < n) keep[2 * n - 1 + j] = mine;
         }
-        // 2. Schur updates of the retained planes (eliminate_around, acr.hpp:78-107)
-        const int mn = (int)L.ret.size();
-        std::vector<SP> Dn(mn), En(mn), Fn(mn);
-        for (int t = 0; t < mn; ++t) Dn[t] = D[L.ret[t]];
-        auto at = [&](const std::vector<SP>& v, int j) -> SP { return (j < 0 || j >= (int)v.size()) ? nullptr : v[j]; };
-        // Per side (lo: eliminated j-1, hi: eliminated j+1) three batched mult_adds:
-        //   T = E_j Dinv_{j-1};  D_j -= T F_{j-1};  E' = -T E_{j-1}      (mirrored for hi).
-        // Schedule over the two lanes: T_lo || T_hi, then {D_lo; D_hi} on lane 0 (same D_j,
-        // reference order lo then hi) || {E'; F'} on lane 1.
-        struct SideOps {
-            std::vector<SP> Ts;
-            std::vector<View> Tv, Cpl, Dnb;                 // T = Cpl * Dnb
-            std::vector<View> dc, da, db;                   // D -= T * x
-            std::vector<View> nc, na, nb;                   // new coupling = -T * y
-        } ops[2];
-        for (int side = 0; side < 2; ++side) {
-            SideOps& o = ops[side];
-            for (int t = 0; t < mn; ++t) {
-                const int j = L.ret[t];
-                const int nbp = side == 0 ? j - 1 : j + 1;
-                if (!(nbp >= 0 && nbp < m && is_elim[nbp])) continue;
-                o.Ts.push_back(E.new_store(0));
-                const View T = root_view(o.Ts.back());
-                o.Tv.push_back(T);
-                SP cpl = side == 0 ? at(L.E, j) : at(L.F, j);
-                if (!cpl) throw AcrError{ACRGPU_E_INTERNAL, "missing coupling block"};
-                o.Cpl.push_back(root_view(cpl));
-                o.Dnb.push_back(root_view(L.Dinv[nbp]));
-                if (SP x = side == 0 ? at(L.F, nbp) : at(L.E, nbp)) {
-                    o.dc.push_back(root_view(Dn[t]));
-                    o.da.push_back(T);
-                    o.db.push_back(root_view(x));
-                }
-                if (SP y = side == 0 ? at(L.E, nbp) : at(L.F, nbp)) {
-                    SP nw = E.new_store(0);
-                    (side == 0 ? En : Fn)[t] = nw;
-                    o.nc.push_back(root_view(nw));
-                    o.na.push_back(T);
-                    o.nb.push_back(root_view(y));
-                }
-            }
-            E.zero(o.Tv);
-            E.zero(o.nc);
-        }
-        E.pair([&] { E.mult_add(ops[0].Tv, ops[0].Cpl, ops[0].Dnb, 1.0); },
-               [&] { E.mult_add(ops[1].Tv, ops[1].Cpl, ops[1].Dnb, 1.0); });
-        E.ctx->depend(0, 1);  // both T batches visible to both lanes
-        E.pair(
-            [&] {
-                E.mult_add(ops[0].dc, ops[0].da, ops[0].db, -1.0);
-                E.mult_add(ops[1].dc, ops[1].da, ops[1].db, -1.0);
-            },
-            [&] {
-                E.mult_add(ops[0].nc, ops[0].na, ops[0].nb, -1.0);
-                E.mult_add(ops[1].nc, ops[1].na, ops[1].nb, -1.0);
-            });
-        // adjacent retained planes keep their coupling (acr.cpp:104-111)
+    }
+    auto blocks = lift(E, sys, &keep);
+    CK(cudaEventRecord(R.e1, E.st()));
+    R.D.assign(n, nullptr);
+    R.Ev.assign(n, nullptr);
+    R.Fv.assign(n, nullptr);
+    for (int j = 0; j < n; ++j) R.D[j] = blocks[j];
+    for (int j = 1; j < n; ++j) R.Ev[j] = blocks[n + j - 1];
+    for (int j = 0; j + 1 < n; ++j) R.Fv[j] = blocks[2 * n - 1 + j];
+}
+
+static bool verbose_levels() {
+    static const bool v = getenv("ACRGPU_VERBOSE") != nullptr;
+    return v;
+}
+
+static void mark_level(PartRun& R) {
+    if (!verbose_levels()) return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, R.F->eng->main_st()));
+    R.lev_ev.push_back(e);
+}
+
+// Step 1 of reduce_level (acr.cpp:70-120): invert the owned eliminated planes (batched).
+static Level level_invert(PartRun& R, int lvl, const std::vector<char>& mine_pos) {
+    Engine& E = *R.F->eng;
+    const int m = (int)R.D.size();
+    Level L;
+    L.plane_count = m;
+    L.elim = eliminated_positions(m);
+    L.ret = retained_positions(m);
+    L.E = R.Ev;
+    L.F = R.Fv;
+    L.Dinv.assign(m, nullptr);
+    std::vector<SP> outs;
+    std::vector<View> ov, iv;
+    std::vector<int> planes;
+    for (int e : L.elim) {
+        if (!mine_pos[e]) continue;
+        outs.push_back(E.new_store(0));
+        ov.push_back(root_view(outs.back()));
+        iv.push_back(root_view(R.D[e]));
+        planes.push_back(e);
+    }
+    if (!ov.empty()) E.invert(ov, iv, lvl, planes);
+    for (size_t t = 0; t < planes.size(); ++t) {
+        L.Dinv[planes[t]] = outs[t];
+        R.D[planes[t]].reset();
+    }
+    return L;
+}
+
+// Steps 2-3 of reduce_level: Schur updates of the owned retained planes
+// (eliminate_around, acr.hpp:78-107), then the stored inverses trimmed to full
+// tolerance (acr.cpp:116-118).  Eliminated neighbours owned elsewhere must already
+// be present in L (received).
+static void level_update(PartRun& R, Level& L, const std::vector<char>& mine_pos) {
+    Engine& E = *R.F->eng;
+    const int m = L.plane_count;
+    std::vector<char> is_elim(m, 0);
+    for (int e : L.elim) is_elim[e] = 1;
+    const int mn = (int)L.ret.size();
+    std::vector<SP> Dn(mn), En(mn), Fn(mn);
+    for (int t = 0; t < mn; ++t)
+        if (mine_pos[L.ret[t]]) Dn[t] = R.D[L.ret[t]];
+    auto at = [&](const std::vector<SP>& v, int j) -> SP { return (j < 0 || j >= (int)v.size()) ? nullptr : v[j]; };
+    // Per side (lo: eliminated j-1, hi: eliminated j+1) three batched mult_adds:
+    //   T = E_j Dinv_{j-1};  D_j -= T F_{j-1};  E' = -T E_{j-1}      (mirrored for hi).
+    // Schedule over the two lanes: T_lo || T_hi, then {D_lo; D_hi} on lane 0 (same D_j,
+    // reference order lo then hi) || {E'; F'} on lane 1.
+    struct SideOps {
+        std::vector<SP> Ts;
+        std::vector<View> Tv, Cpl, Dnb;  // T = Cpl * Dnb
+        std::vector<View> dc, da, db;    // D -= T * x
+        std::vector<View> nc, na, nb;    // new coupling = -T * y
+    } ops[2];
+    for (int side = 0; side < 2; ++side) {
+        SideOps& o = ops[side];
         for (int t = 0; t < mn; ++t) {
             const int j = L.ret[t];
-            if (!En[t] && t > 0 && L.ret[t - 1] == j - 1 && at(L.E, j)) {
-                En[t] = E.new_store(0);
-                E.copy({root_view(En[t])}, {root_view(L.E[j])});
+            if (!mine_pos[j]) continue;
+            const int nbp = side == 0 ? j - 1 : j + 1;
+            if (!(nbp >= 0 && nbp < m && is_elim[nbp])) continue;
+            if (!L.Dinv[nbp]) throw AcrError{ACRGPU_E_INTERNAL, "missing eliminated neighbour"};
+            o.Ts.push_back(E.new_store(0));
+            const View T = root_view(o.Ts.back());
+            o.Tv.push_back(T);
+            SP cpl = side == 0 ? at(L.E, j) : at(L.F, j);
+            if (!cpl) throw AcrError{ACRGPU_E_INTERNAL, "missing coupling block"};
+            o.Cpl.push_back(root_view(cpl));
+            o.Dnb.push_back(root_view(L.Dinv[nbp]));
+            if (SP x = side == 0 ? at(L.F, nbp) : at(L.E, nbp)) {
+                o.dc.push_back(root_view(Dn[t]));
+                o.da.push_back(T);
+                o.db.push_back(root_view(x));
             }
-            if (!Fn[t] && t + 1 < mn && L.ret[t + 1] == j + 1 && at(L.F, j)) {
-                Fn[t] = E.new_store(0);
-                E.copy({root_view(Fn[t])}, {root_view(L.F[j])});
+            if (SP y = side == 0 ? at(L.E, nbp) : at(L.F, nbp)) {
+                SP nw = E.new_store(0);
+                (side == 0 ? En : Fn)[t] = nw;
+                o.nc.push_back(root_view(nw));
+                o.na.push_back(T);
+                o.nb.push_back(root_view(y));
             }
         }
-        D = std::move(Dn);
-        Ev = std::move(En);
-        Fv = std::move(Fn);
-        // 3. trim the stored inverses to full tolerance (acr.cpp:116-118)
-        {
-            std::vector<View> dv;
-            for (int e : L.elim) dv.push_back(root_view(L.Dinv[e]));
-            E.recompress(dv);
-        }
-        F->levels.push_back(std::move(L));
-        mark();
-        ++lvl;
+        E.zero(o.Tv);
+        E.zero(o.nc);
     }
-    // apex: block Thomas over the remaining planes (acr.cpp:123-144)
-    const int s = (int)D.size();
-    F->apexE = Ev;
-    F->apexF = Fv;
+    E.pair([&] { E.mult_add(ops[0].Tv, ops[0].Cpl, ops[0].Dnb, 1.0); },
+           [&] { E.mult_add(ops[1].Tv, ops[1].Cpl, ops[1].Dnb, 1.0); });
+    E.ctx->depend(0, 1);  // both T batches visible to both lanes
+    E.pair(
+        [&] {
+            E.mult_add(ops[0].dc, ops[0].da, ops[0].db, -1.0);
+            E.mult_add(ops[1].dc, ops[1].da, ops[1].db, -1.0);
+        },
+        [&] {
+            E.mult_add(ops[0].nc, ops[0].na, ops[0].nb, -1.0);
+            E.mult_add(ops[1].nc, ops[1].na, ops[1].nb, -1.0);
+        });
+    // adjacent retained planes keep their coupling (acr.cpp:104-111)
+    for (int t = 0; t < mn; ++t) {
+        const int j = L.ret[t];
+        if (!mine_pos[j]) continue;
+        if (!En[t] && t > 0 && L.ret[t - 1] == j - 1 && at(L.E, j)) {
+            En[t] = E.new_store(0);
+            E.copy({root_view(En[t])}, {root_view(L.E[j])});
+        }
+        if (!Fn[t] && t + 1 < mn && L.ret[t + 1] == j + 1 && at(L.F, j)) {
+            Fn[t] = E.new_store(0);
+            E.copy({root_view(Fn[t])}, {root_view(L.F[j])});
+        }
+    }
+    R.D = std::move(Dn);
+    R.Ev = std::move(En);
+    R.Fv = std::move(Fn);
+    {
+        std::vector<View> dv;
+        for (int e : L.elim)
+            if (mine_pos[e]) dv.push_back(root_view(L.Dinv[e]));
+        if (!dv.empty()) E.recompress(dv);
+    }
+    // received neighbours were level temporaries
+    for (int e : L.elim)
+        if (!mine_pos[e]) {
+            L.Dinv[e].reset();
+            L.E[e].reset();
+            L.F[e].reset();
+        }
+}
+
+// factor_apex (acr.cpp:123-144): block Thomas over the remaining planes.
+static void factor_apex(PartRun& R, int lvl) {
+    acrgpu_fact* F = R.F;
+    Engine& E = *F->eng;
+    const int s = (int)R.D.size();
+    F->apexE = R.Ev;
+    F->apexF = R.Fv;
     for (int i = 0; i < s; ++i) {
-        SP Di = D[i];
+        SP Di = R.D[i];
         if (i > 0) {
             SP T = E.new_store(0);
             E.zero({root_view(T)});
@@ -1371,22 +1452,30 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
         F->apexDinv.push_back(out);
     }
     E.recompress(views(F->apexDinv));
-    mark();
+}
+
+static void factor_finish(PartRun& R) {
+    acrgpu_fact* F = R.F;
+    Engine& E = *F->eng;
+    mark_level(R);
     check_device_errors(F);
-    if (verbose) {
-        for (size_t i = 1; i < lev_ev.size(); ++i) {
+    if (verbose_levels()) {
+        for (size_t i = 1; i < R.lev_ev.size(); ++i) {
             float ms = 0;
-            cudaEventElapsedTime(&ms, lev_ev[i - 1], lev_ev[i]);
-            fprintf(stderr, "[acrgpu] level %zu: %.2f ms\n", i - 1, ms);
+            cudaEventElapsedTime(&ms, R.lev_ev[i - 1], R.lev_ev[i]);
+            fprintf(stderr, "[acrgpu] rank %d level %zu: %.2f ms\n", R.rank, i - 1, ms);
         }
-        for (auto e : lev_ev) cudaEventDestroy(e);
+        for (auto e : R.lev_ev) cudaEventDestroy(e);
+        R.lev_ev.clear();
     }
     compact_factor(F);
+    cudaEvent_t e2;
+    CK(cudaEventCreate(&e2));
     CK(cudaEventRecord(e2, E.st()));
     CK(cudaEventSynchronize(e2));
     float ms_lift = 0, ms_all = 0;
-    CK(cudaEventElapsedTime(&ms_lift, e0, e1));
-    CK(cudaEventElapsedTime(&ms_all, e0, e2));
+    CK(cudaEventElapsedTime(&ms_lift, R.e0, R.e1));
+    CK(cudaEventElapsedTime(&ms_all, R.e0, e2));
     F->timing.lift_ms = ms_lift;
     F->timing.factor_ms = ms_all;
     FlopLedger fl{};
@@ -1402,9 +1491,28 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
     F->timing.flops_lu = fl.f[F_LU];
     F->timing.flops_nominal = fl.f[F_GEMM] + fl.f[F_GEQRF] + fl.f[F_ORGQR] + fl.f[F_SVD] + fl.f[F_LU];
     F->timing.factor_launches = launches_take();
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    cudaEventDestroy(R.e0);
+    cudaEventDestroy(R.e1);
     cudaEventDestroy(e2);
+}
+
+static void do_factor(acrgpu_fact* F, const DSys& sys) {
+    PartRun R;
+    R.F = F;
+    factor_begin(R, sys, nullptr);
+    const int stop = F->eng->cfg.stop_planes;
+    int lvl = 0;
+    mark_level(R);
+    while ((int)R.D.size() > stop) {
+        const std::vector<char> all(R.D.size(), 1);
+        Level L = level_invert(R, lvl, all);
+        level_update(R, L, all);
+        F->levels.push_back(std::move(L));
+        mark_level(R);
+        ++lvl;
+    }
+    factor_apex(R, lvl);
+    factor_finish(R);
 }
 
 // ------------------------------------------------------------------ solve
