@@ -19,6 +19,10 @@
  *   acrgpu_structure     <- ClusterTree / BlockClusterTree (core/src/cluster.cpp:39-126):
  *                           permutation + leaf table, for structure parity tests
  *   acrgpu_ctx_* / acrgpu_factor_destroy  <- object lifetimes (value types in the reference)
+ *   acrgpu_factor_partitioned / acrgpu_comm_*
+ *                        <- acr::execute_parallel_factor(system, plan, config)
+ *                           core/include/acr/parallel.hpp:60-61, core/src/parallel.cpp:96-297;
+ *                           plane ownership = plan_schedule(n, p) (parallel.cpp:383-405)
  *
  * Errors map 1:1 onto the reference exception classes (core/include/acr/errors.hpp:10-60):
  *   ACRGPU_E_DIMENSION  DimensionError(plane)        ACRGPU_E_SINGULAR  SingularBlockError(level, plane)
@@ -161,6 +165,29 @@ long acrgpu_structure(int dim, const double* coords, int leaf_size, double eta, 
 /* Per-kernel device time accumulated while ACRGPU_PROFILE=1 is set in the environment:
  * lines "kernel total_ms launches ctas".  Returns the length written (NUL-terminated). */
 long acrgpu_profile_report(char* buf, long cap, int reset);
+
+/* ---- Plane partition over several GPUs (execute_parallel_factor, parallel.cpp:96-297).
+ * Rank w owns the planes plan_schedule(n, p) assigns it (contiguous blocks at level 0;
+ * retained planes keep their owner).  Per level every rank inverts its eliminated planes
+ * and sends {Dinv_e, E_e, F_e} to the owner of each retained neighbour held by another
+ * rank; the solve exchanges plane vectors the same way.  n and p must be powers of two,
+ * stop_planes 1.  Results are bitwise identical for every p (test_parallel.cpp:75-89).
+ *
+ * Multi-process (one rank per GPU, NCCL point-to-point over NVLink): rank 0 calls
+ * acrgpu_comm_unique_id, the id is broadcast out of band (e.g. torch.distributed), and
+ * every rank calls acrgpu_comm_create on its device.  acrgpu_solve on such a handle fills
+ * the planes this rank owns (other planes of u are set to 0).
+ * In-process (acrgpu_comm_create_local): all p ranks run on the context's device in one
+ * call; the handle holds every rank and acrgpu_solve returns the full solution.  Used to
+ * check the partitioned data path on one GPU. */
+#define ACRGPU_COMM_ID_BYTES 128
+typedef struct acrgpu_comm acrgpu_comm;
+int acrgpu_comm_unique_id(unsigned char* id /* ACRGPU_COMM_ID_BYTES */, acrgpu_error* err);
+int acrgpu_comm_create(const unsigned char* id, int nranks, int rank, acrgpu_comm** out, acrgpu_error* err);
+int acrgpu_comm_create_local(int nranks, acrgpu_comm** out, acrgpu_error* err);
+void acrgpu_comm_destroy(acrgpu_comm* comm);
+int acrgpu_factor_partitioned(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_system* sys,
+                              const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err);
 
 /* Library build identification (sm arch, version). */
 const char* acrgpu_version(void);

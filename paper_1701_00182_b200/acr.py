@@ -157,7 +157,15 @@ SYMBOLS = {
     "acrgpu_profile_report": (C.c_long, [C.c_char_p, C.c_long, C.c_int]),
     "acrgpu_structure": (C.c_long, [C.c_int, C.POINTER(C.c_double), C.c_int, C.c_double, C.c_int,
                                      C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_long, C.POINTER(_Err)]),
+    "acrgpu_comm_unique_id": (C.c_int, [C.c_char_p, C.POINTER(_Err)]),
+    "acrgpu_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_Err)]),
+    "acrgpu_comm_create_local": (C.c_int, [C.c_int, C.POINTER(C.c_void_p), C.POINTER(_Err)]),
+    "acrgpu_comm_destroy": (None, [C.c_void_p]),
+    "acrgpu_factor_partitioned": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Sys), C.POINTER(_Cfg),
+                                            C.POINTER(C.c_void_p), C.POINTER(_Err)]),
 }
+
+COMM_ID_BYTES = 128
 
 _lib = None
 
@@ -365,6 +373,69 @@ def acr_factor(system, config: AcrConfig | None = None, ctx: Context | None = No
     if rc:
         _raise(err)
     return AcrFactorization(h, host, config, ctx)
+
+
+class Comm:
+    """Plane-partition communicator (execute_parallel_factor, parallel.hpp:60-61).
+
+    ``Comm.local(p)``: p ranks run in-process on one device (checks the partitioned
+    data path; the factorization handle holds every rank).  ``Comm.nccl(uid, p, rank)``:
+    one rank per process/GPU over NCCL point-to-point; ``uid`` from ``Comm.unique_id()``
+    on rank 0, shared out of band (e.g. ``torch.distributed.broadcast_object_list``)."""
+
+    def __init__(self, handle, nranks, rank, local):
+        self.h, self.nranks, self.rank, self.local = handle, nranks, rank, local
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(COMM_ID_BYTES)
+        err = _Err()
+        if lib().acrgpu_comm_unique_id(buf, C.byref(err)):
+            _raise(err)
+        return buf.raw
+
+    @classmethod
+    def local_ranks(cls, nranks: int) -> "Comm":
+        h = C.c_void_p()
+        err = _Err()
+        if lib().acrgpu_comm_create_local(nranks, C.byref(h), C.byref(err)):
+            _raise(err)
+        return cls(h, nranks, 0, True)
+
+    @classmethod
+    def nccl(cls, uid: bytes, nranks: int, rank: int) -> "Comm":
+        h = C.c_void_p()
+        err = _Err()
+        if lib().acrgpu_comm_create(uid, nranks, rank, C.byref(h), C.byref(err)):
+            _raise(err)
+        return cls(h, nranks, rank, False)
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().acrgpu_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def acr_factor_partitioned(system, comm: Comm, config: AcrConfig | None = None, ctx: Context | None = None):
+    """execute_parallel_factor (parallel.cpp:96-297) on GPUs: planes owned per
+    plan_schedule(n, comm.nranks); bitwise identical to acr_factor."""
+    config = config or AcrConfig()
+    cfg = _cfg(config)
+    ctx = ctx or default_context()
+    s, keep = _sys_struct(system)
+    h = C.c_void_p()
+    err = _Err()
+    if lib().acrgpu_factor_partitioned(ctx.h, comm.h, C.byref(s), C.byref(cfg), C.byref(h), C.byref(err)):
+        _raise(err)
+    f = AcrFactorization(h, system, config, ctx)
+    f._comm = comm  # keep the communicator alive
+    return f
 
 
 def acr_solve(fact: AcrFactorization, f):

@@ -246,6 +246,8 @@ struct Engine {
     Part* leaf_parts = nullptr;
     Classed<TruncTask> leaf_cls;      // the same, split by size class
     int leaf_cls_off[NCLASS] = {0, 0, 0, 0};
+    int* d_km = nullptr;              // Rk leaf rows / cols (wire images)
+    int* d_kn = nullptr;
     SlabTask* slabs = nullptr;        // matvec slabs of the root
     ApplyLeaf* slab_leaves = nullptr;
     int nslabs = 0;
@@ -914,6 +916,17 @@ struct acrgpu_fact {
     size_t fbuf_cap = 0;
     double* ubuf = nullptr;  // compacted low-rank factors of the stored blocks
     long ubuf_doubles = 0;
+    // plane partition (acrgpu_factor_partitioned)
+    acrgpu_comm* comm = nullptr;
+    int rank = 0;
+    std::vector<std::vector<int>> owners;  // per level: plane position -> rank
+    std::vector<acrgpu_fact*> vparts;      // in-process ranks of a local communicator (owned)
+};
+
+struct acrgpu_comm {
+    int nranks = 1, rank = 0;
+    bool local = true;
+    void* nccl = nullptr;  // ncclComm_t
 };
 
 namespace acrgpu {
@@ -1230,7 +1243,7 @@ static void compact_factor(acrgpu_fact* F) {
     int** d_R = upload(Rt, st);
     for (size_t s0 = 0; s0 < stores.size(); s0 += 65535) {
         const int cnt = (int)std::min<size_t>(65535, stores.size() - s0);
-        CompactArgs a{F->ubuf, d_off + s0 * nk, d_U + s0, d_V + s0, d_R + s0, d_km, d_kn, nk};
+        CompactArgs a{F->ubuf, d_off + s0 * nk, d_U + s0, d_V + s0, d_R + s0, d_km, d_kn, nk, 1};
         launch_compact(st, a, cnt);
     }
     CK(cudaStreamSynchronize(st));
@@ -1538,117 +1551,595 @@ static void matvec(Engine& E, const std::vector<MV>& items, int nrhs) {
     }
 }
 
-static void do_solve(acrgpu_fact* F, int nrhs, const double* f_dev, double* u_dev) {
-    Engine& E = *F->eng;
-    cudaStream_t st = E.st();
-    const int n = F->n, dim = F->dim;
+// ------------------------------------------------------------------ plane partition (multi-GPU)
+// execute_parallel_factor / the parallel solve (parallel.cpp:96-297): every rank
+// owns the planes plan_schedule gives it; per level it inverts its eliminated
+// planes, sends {Dinv_e, E_e, F_e} to the owner of each retained neighbour on
+// another rank (one message per distinct destination, parallel.cpp:142-161), and
+// updates its retained planes.  The solve exchanges plane vectors the same way
+// (parallel.cpp:252-292).  The arithmetic per plane is the single-GPU batch
+// arithmetic, so results are bitwise identical for every rank count
+// (test_parallel.cpp:75-89).
+//
+// Wire image of one H-matrix on the shared structure (doubles):
+//   [nk, dsize, lr, 0] [leaf offsets (nk, -1 = rank 0)] [ranks (nk)] [int ranks]
+//   [U/V pointer tables (2 nk, rebuilt by the receiver)] [dense pool] [U_k V_k ...]
+struct StoreImage {
+    double* buf = nullptr;
+    size_t n = 0;  // doubles; 0 = absent
+};
+struct ImageLayout {
+    size_t offs, ranks, irank, ptrs, dense, lr, total;
+};
+static ImageLayout image_layout(size_t nk, size_t dsize, size_t lr) {
+    ImageLayout L;
+    L.offs = 4;
+    L.ranks = L.offs + nk;
+    L.irank = L.ranks + nk;
+    L.ptrs = L.irank + (nk + 1) / 2;
+    L.dense = L.ptrs + 2 * nk;
+    L.lr = L.dense + dsize;
+    L.total = L.lr + lr;
+    return L;
+}
+
+static void ensure_kmn(Engine& E) {
+    if (E.d_km) return;
+    const int nk = E.S.n_rk();
+    std::vector<int> km(std::max(nk, 1)), kn(std::max(nk, 1));
+    for (int k = 0; k < nk; ++k) {
+        const SNode& L = E.S.node(E.S.k_node[k]);
+        km[k] = L.rows();
+        kn[k] = L.cols();
+    }
+    E.d_km = E.up(km);
+    E.d_kn = E.up(kn);
+}
+
+static StoreImage pack_store(Engine& E, const SP& s) {
+    cudaStream_t st = E.main_st();
+    ensure_kmn(E);
+    const int nk = E.S.n_rk();
+    const size_t dsize = E.S.node(0).dsize;
+    std::vector<int> r(nk);
+    if (nk) {
+        CK(cudaMemcpyAsync(r.data(), s->rank, nk * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    std::vector<long> off(std::max(nk, 1), -1);
+    long lr = 0;
+    for (int k = 0; k < nk; ++k)
+        if (r[k] > 0) {
+            const SNode& L = E.S.node(E.S.k_node[k]);
+            off[k] = lr;
+            lr += (long)(L.rows() + L.cols()) * r[k];
+        }
+    const ImageLayout L = image_layout(nk, dsize, lr);
+    StoreImage im;
+    im.n = L.total;
+    CK(cudaMallocAsync((void**)&im.buf, L.total * sizeof(double), st));
+    std::vector<double> head(L.ptrs, 0.0);
+    head[0] = nk;
+    head[1] = (double)dsize;
+    head[2] = (double)lr;
+    for (int k = 0; k < nk; ++k) {
+        head[L.offs + k] = (double)off[k];
+        head[L.ranks + k] = r[k];
+    }
+    CK(cudaMemcpyAsync(im.buf, head.data(), head.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(im.buf + L.dense, s->dense, dsize * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (lr > 0) {
+        long* d_off = upload(off, st);
+        std::vector<double**> Ut{s->U}, Vt{s->V};
+        std::vector<int*> Rt{s->rank};
+        double*** d_U = upload(Ut, st);
+        double*** d_V = upload(Vt, st);
+        int** d_R = upload(Rt, st);
+        CompactArgs a{im.buf + L.lr, d_off, d_U, d_V, d_R, E.d_km, E.d_kn, nk, 0};
+        launch_compact(st, a, 1);
+        CK(cudaStreamSynchronize(st));
+        for (void* p : std::initializer_list<void*>{d_off, d_U, d_V, d_R}) cudaFree(p);
+    }
+    CK(cudaStreamSynchronize(st));
+    return im;
+}
+
+// Take ownership of a received image and view it as a root store.
+static SP adopt_image(Engine& E, StoreImage im) {
+    cudaStream_t st = E.main_st();
+    ensure_kmn(E);
+    const int nk = E.S.n_rk();
+    const ImageLayout L = image_layout(nk, E.S.node(0).dsize, 0);
+    ImageFix fx{im.buf, nk, (long)L.offs, (long)L.ranks, (long)L.irank, (long)L.ptrs, (long)L.lr, E.d_km};
+    launch_image_fix(st, fx);
+    auto s = std::make_shared<Store>();
+    s->node = 0;
+    s->block = im.buf;
+    s->dense = im.buf + L.dense;
+    s->U = (double**)(im.buf + L.ptrs);
+    s->V = s->U + nk;
+    s->rank = (int*)(im.buf + L.irank);
+    return StoreP(s.get(), [s, st](Store*) mutable {
+        if (s->block) cudaFreeAsync(s->block, st);
+        s->block = nullptr;
+    });
+}
+
+// ------------------------------------------------------------------ transports
+struct Msg {
+    int src = 0, dst = 0;
+    long key = 0;
+    StoreImage im;
+};
+struct Expect {
+    int src = 0, dst = 0;
+    long key = 0;
+};
+static long msg_key(int kind, int lvl, int plane) { return ((long)kind << 40) | ((long)lvl << 24) | plane; }
+
+struct Transport {
+    virtual ~Transport() = default;
+    // out: images posted by local ranks (ownership passes to the transport); returns the
+    // images addressed to local ranks, one per entry of `expect`.
+    virtual std::vector<Msg> exchange(std::vector<Msg>& out, const std::vector<Expect>& expect) = 0;
+};
+
+// In-process virtual ranks on one device: delivery hands the sender's image over.
+struct LocalTransport : Transport {
+    std::vector<Msg> exchange(std::vector<Msg>& out, const std::vector<Expect>& expect) override {
+        std::vector<Msg> in;
+        std::vector<char> used(out.size(), 0);
+        for (const Expect& x : expect) {
+            size_t i = 0;
+            while (i < out.size() && (used[i] || out[i].src != x.src || out[i].dst != x.dst || out[i].key != x.key)) ++i;
+            if (i == out.size()) throw AcrError{ACRGPU_E_INTERNAL, "partition: expected message was not sent"};
+            used[i] = 1;
+            in.push_back(out[i]);
+        }
+        for (size_t i = 0; i < out.size(); ++i)
+            if (!used[i]) throw AcrError{ACRGPU_E_INTERNAL, "partition: message without a receiver"};
+        out.clear();
+        return in;
+    }
+};
+
+}  // namespace acrgpu
+
+// NCCL, resolved at run time (the process may already carry the copy torch loaded).
+#include <dlfcn.h>
+#include <nccl.h>
+namespace acrgpu {
+struct NcclApi {
+    void* h = nullptr;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+static NcclApi& nccl() {
+    static NcclApi api;
+    if (api.h) return api;
+    const char* env = getenv("ACRGPU_NCCL_LIB");
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h && env) h = dlopen(env, RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) throw AcrError{ACRGPU_E_DEVICE, "NCCL library (libnccl.so.2) not found"};
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+    api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+    api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.Send || !api.Recv || !api.GroupStart ||
+        !api.GroupEnd || !api.GetErrorString)
+        throw AcrError{ACRGPU_E_DEVICE, "NCCL library lacks point-to-point symbols"};
+    api.h = h;
+    return api;
+}
+#define NCK(x)                                                                                         \
+    do {                                                                                               \
+        ncclResult_t r_ = (x);                                                                         \
+        if (r_ != ncclSuccess)                                                                         \
+            throw AcrError{ACRGPU_E_DEVICE, std::string("NCCL: ") + nccl().GetErrorString(r_)};         \
+    } while (0)
+
+// One rank per process (GPU): sizes first, then the images, each phase one group.
+struct NcclTransport : Transport {
+    ncclComm_t comm = nullptr;
+    cudaStream_t st = nullptr;
+    std::vector<Msg> exchange(std::vector<Msg>& out, const std::vector<Expect>& expect) override {
+        NcclApi& N = nccl();
+        std::vector<size_t> oi(out.size()), ei(expect.size());
+        std::iota(oi.begin(), oi.end(), 0);
+        std::iota(ei.begin(), ei.end(), 0);
+        std::sort(oi.begin(), oi.end(), [&](size_t a, size_t b) {
+            return out[a].dst != out[b].dst ? out[a].dst < out[b].dst : out[a].key < out[b].key;
+        });
+        std::sort(ei.begin(), ei.end(), [&](size_t a, size_t b) {
+            return expect[a].src != expect[b].src ? expect[a].src < expect[b].src : expect[a].key < expect[b].key;
+        });
+        const size_t no = out.size(), ne = expect.size();
+        std::vector<long long> sz(no + ne, 0);
+        for (size_t i = 0; i < no; ++i) sz[i] = (long long)out[oi[i]].im.n;
+        long long* d_sz = nullptr;
+        CK(cudaMallocAsync((void**)&d_sz, std::max<size_t>(1, no + ne) * sizeof(long long), st));
+        CK(cudaMemcpyAsync(d_sz, sz.data(), sz.size() * sizeof(long long), cudaMemcpyHostToDevice, st));
+        NCK(N.GroupStart());
+        for (size_t i = 0; i < no; ++i) NCK(N.Send(d_sz + i, 1, ncclInt64, out[oi[i]].dst, comm, st));
+        for (size_t i = 0; i < ne; ++i) NCK(N.Recv(d_sz + no + i, 1, ncclInt64, expect[ei[i]].src, comm, st));
+        NCK(N.GroupEnd());
+        CK(cudaMemcpyAsync(sz.data(), d_sz, sz.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<Msg> in(ne);
+        for (size_t i = 0; i < ne; ++i) {
+            const Expect& x = expect[ei[i]];
+            Msg& m = in[ei[i]];
+            m.src = x.src;
+            m.dst = x.dst;
+            m.key = x.key;
+            m.im.n = (size_t)sz[no + i];
+            if (m.im.n) CK(cudaMallocAsync((void**)&m.im.buf, m.im.n * sizeof(double), st));
+        }
+        NCK(N.GroupStart());
+        for (size_t i = 0; i < no; ++i)
+            if (out[oi[i]].im.n) NCK(N.Send(out[oi[i]].im.buf, out[oi[i]].im.n, ncclFloat64, out[oi[i]].dst, comm, st));
+        for (size_t i = 0; i < ne; ++i) {
+            Msg& m = in[ei[i]];
+            if (m.im.n) NCK(N.Recv(m.im.buf, m.im.n, ncclFloat64, m.src, comm, st));
+        }
+        NCK(N.GroupEnd());
+        CK(cudaStreamSynchronize(st));
+        for (auto& m : out)
+            if (m.im.buf) CK(cudaFreeAsync(m.im.buf, st));
+        CK(cudaFreeAsync(d_sz, st));
+        out.clear();
+        return in;
+    }
+};
+
+// ------------------------------------------------------------------ partitioned factor
+static void factor_partitioned(std::vector<PartRun>& runs, const std::vector<std::vector<int>>& own, Transport& T,
+                               const DSys& sys) {
+    for (auto& R : runs) factor_begin(R, sys, &own);
+    const int stop = runs[0].F->eng->cfg.stop_planes;
+    if (stop != 1) throw AcrError{ACRGPU_E_USAGE, "partitioned factor: stop_planes must be 1"};
+    for (auto& R : runs) mark_level(R);
+    int lvl = 0, m = sys.n;
+    auto at = [](const std::vector<SP>& v, int j) -> SP { return (j < 0 || j >= (int)v.size()) ? nullptr : v[j]; };
+    while (m > stop) {
+        const std::vector<int>& ow = own[lvl];
+        const std::vector<int> elim = eliminated_positions(m), ret = retained_positions(m);
+        std::vector<char> is_elim(m, 0);
+        for (int e : elim) is_elim[e] = 1;
+        std::vector<Level> Ls(runs.size());
+        std::vector<std::vector<char>> mine(runs.size());
+        for (size_t r = 0; r < runs.size(); ++r) {
+            mine[r].assign(m, 0);
+            for (int j = 0; j < m; ++j) mine[r][j] = ow[j] == runs[r].rank;
+            Ls[r] = level_invert(runs[r], lvl, mine[r]);
+        }
+        std::vector<Msg> out;
+        std::vector<Expect> expect;
+        for (size_t r = 0; r < runs.size(); ++r) {
+            Engine& E = *runs[r].F->eng;
+            const int me = runs[r].rank;
+            for (int e : elim) {
+                if (ow[e] != me) continue;
+                std::vector<int> dests;
+                for (int nb : {e - 1, e + 1})
+                    if (nb >= 0 && nb < m && !is_elim[nb] && ow[nb] != me &&
+                        std::find(dests.begin(), dests.end(), ow[nb]) == dests.end())
+                        dests.push_back(ow[nb]);
+                for (int d : dests)
+                    for (int kind = 0; kind < 3; ++kind) {
+                        SP s = kind == 0 ? Ls[r].Dinv[e] : (kind == 1 ? at(Ls[r].E, e) : at(Ls[r].F, e));
+                        Msg msg;
+                        msg.src = me;
+                        msg.dst = d;
+                        msg.key = msg_key(kind, lvl, e);
+                        if (s) msg.im = pack_store(E, s);
+                        out.push_back(msg);
+                    }
+            }
+            std::vector<int> need;
+            for (int j : ret) {
+                if (ow[j] != me) continue;
+                for (int nb : {j - 1, j + 1})
+                    if (nb >= 0 && nb < m && is_elim[nb] && ow[nb] != me &&
+                        std::find(need.begin(), need.end(), nb) == need.end())
+                        need.push_back(nb);
+            }
+            for (int e : need)
+                for (int kind = 0; kind < 3; ++kind) expect.push_back(Expect{ow[e], me, msg_key(kind, lvl, e)});
+        }
+        std::vector<Msg> in = T.exchange(out, expect);
+        for (Msg& msg : in) {
+            size_t r = 0;
+            while (r < runs.size() && runs[r].rank != msg.dst) ++r;
+            const int kind = (int)(msg.key >> 40), e = (int)(msg.key & 0xffffff);
+            SP s = msg.im.n ? adopt_image(*runs[r].F->eng, msg.im) : nullptr;
+            Level& L = Ls[r];
+            (kind == 0 ? L.Dinv : (kind == 1 ? L.E : L.F))[e] = s;
+        }
+        for (size_t r = 0; r < runs.size(); ++r) {
+            level_update(runs[r], Ls[r], mine[r]);
+            runs[r].F->levels.push_back(std::move(Ls[r]));
+            mark_level(runs[r]);
+        }
+        m = (int)ret.size();
+        ++lvl;
+    }
+    for (auto& R : runs)
+        if (own[lvl][0] == R.rank) factor_apex(R, lvl);
+    for (auto& R : runs) factor_finish(R);
+}
+
+// ------------------------------------------------------------------ solve (single or partitioned)
+// solve_impl (acr.cpp:180-229): forward_rhs (acr.hpp:111-120) level by level, the apex
+// (solve_apex, acr.cpp:162-178), then back_substitute (acr.hpp:123-132) top-down.
+// g_e = Dinv_e f_e is formed once per eliminated plane by its owner and sent to the
+// owners of its retained neighbours; back substitution receives u of retained
+// neighbours owned elsewhere.  u_dev receives the planes owned by the local runs.
+struct SolveRun {
+    acrgpu_fact* F = nullptr;
+    int rank = 0;
+    double* ws = nullptr;
+    std::vector<size_t> lvl_off;
+    double *fs = nullptr, *G = nullptr, *T1 = nullptr, *ub[2] = {nullptr, nullptr}, *uperm = nullptr;
+};
+
+static StoreImage vec_image(cudaStream_t st, const double* src, size_t n) {
+    StoreImage im;
+    im.n = n;
+    CK(cudaMallocAsync((void**)&im.buf, n * sizeof(double), st));
+    CK(cudaMemcpyAsync(im.buf, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return im;
+}
+
+static void solve_runs(std::vector<SolveRun>& runs, const std::vector<std::vector<int>>* own, Transport* T, int nrhs,
+                       const double* f_dev, double* u_dev) {
+    acrgpu_fact* F0 = runs[0].F;
+    const int n = F0->n, dim = F0->dim;
     const size_t pv = (size_t)dim * nrhs;  // one plane vector (tree order, column-major dim x nrhs)
-    // workspace: all level rhs + u + 2 temporaries per plane
+    const int nlev = (int)F0->levels.size();
+    auto owner = [&](int li, int j) { return own ? (*own)[li][j] : runs[0].rank; };
     size_t planes_total = 0;
     std::vector<size_t> lvl_off;
-    int m = n;
-    for (auto& L : F->levels) {
+    {
+        int m = n;
+        for (int li = 0; li < nlev; ++li) {
+            lvl_off.push_back(planes_total);
+            planes_total += m;
+            m = (int)retained_positions(m).size();
+        }
         lvl_off.push_back(planes_total);
-        planes_total += L.plane_count;
-        m = (int)L.ret.size();
+        planes_total += m;  // apex rhs
     }
-    lvl_off.push_back(planes_total);
-    planes_total += m;  // apex rhs
-    const size_t need = (planes_total + 3 * (size_t)n + 8) * pv;
-    if (need > F->fbuf_cap) {
-        if (F->fbuf) cudaFreeAsync(F->fbuf, st);
-        CK(cudaMallocAsync((void**)&F->fbuf, need * sizeof(double), st));
-        F->fbuf_cap = need;
+    for (auto& R : runs) {
+        Engine& E = *R.F->eng;
+        cudaStream_t st = E.st();
+        const size_t need = (planes_total + 5 * (size_t)n) * pv;
+        if (need > R.F->fbuf_cap) {
+            if (R.F->fbuf) cudaFreeAsync(R.F->fbuf, st);
+            CK(cudaMallocAsync((void**)&R.F->fbuf, need * sizeof(double), st));
+            R.F->fbuf_cap = need;
+        }
+        R.fs = R.F->fbuf;
+        R.G = R.fs + planes_total * pv;
+        R.T1 = R.G + (size_t)n * pv;
+        R.ub[0] = R.T1 + (size_t)n * pv;
+        R.ub[1] = R.ub[0] + (size_t)n * pv;
+        R.uperm = R.ub[1] + (size_t)n * pv;
+        launch_permute_in(st, f_dev, R.fs, E.d_perm, n, dim, nrhs);
     }
-    double* fs = F->fbuf;
-    double* U0 = fs + planes_total * pv;  // n planes: solution (per current level)
-    double* T1 = U0 + (size_t)n * pv;
-    double* T2 = T1 + (size_t)n * pv;
-    auto P = [&](size_t li, int j) { return fs + (lvl_off[li] + j) * pv; };
-    launch_permute_in(st, f_dev, fs, E.d_perm, n, dim, nrhs);
-    // forward reduction (forward_rhs, acr.hpp:111-120)
-    for (size_t li = 0; li < F->levels.size(); ++li) {
-        const Level& L = F->levels[li];
-        const int mm = L.plane_count;
-        std::vector<MV> a, b, c, d;
-        for (size_t t = 0; t < L.ret.size(); ++t) {
-            const int j = L.ret[t];
-            const bool lo = j > 0 && L.Dinv[j - 1];
-            const bool hi = j + 1 < mm && L.Dinv[j + 1];
-            double* out = P(li + 1, (int)t);
-            if (lo) {
-                a.push_back({L.Dinv[j - 1], P(li, j - 1), nullptr, T1 + t * pv});
-                b.push_back({L.E[j], T1 + t * pv, P(li, j), out});
-            } else {
-                CK(cudaMemcpyAsync(out, P(li, j), pv * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    auto P = [&](SolveRun& R, size_t li, int j) { return R.fs + (lvl_off[li] + j) * pv; };
+    auto run_of = [&](int rank) -> SolveRun& {
+        for (auto& R : runs)
+            if (R.rank == rank) return R;
+        throw AcrError{ACRGPU_E_INTERNAL, "partition: no local run for rank"};
+    };
+    // forward reduction
+    for (int li = 0; li < nlev; ++li) {
+        const int m = F0->levels[li].plane_count;
+        const std::vector<int> elim = eliminated_positions(m), ret = retained_positions(m);
+        std::vector<char> is_elim(m, 0);
+        for (int e : elim) is_elim[e] = 1;
+        for (auto& R : runs) {
+            const Level& L = R.F->levels[li];
+            std::vector<MV> g;
+            for (int e : elim)
+                if (owner(li, e) == R.rank) g.push_back({L.Dinv[e], P(R, li, e), nullptr, R.G + (size_t)e * pv});
+            matvec(*R.F->eng, g, nrhs);
+        }
+        if (T) {
+            std::vector<Msg> out;
+            std::vector<Expect> expect;
+            for (auto& R : runs) {
+                cudaStream_t st = R.F->eng->st();
+                for (int e : elim) {
+                    if (owner(li, e) != R.rank) continue;
+                    std::vector<int> dests;
+                    for (int nb : {e - 1, e + 1})
+                        if (nb >= 0 && nb < m && !is_elim[nb] && owner(li, nb) != R.rank &&
+                            std::find(dests.begin(), dests.end(), owner(li, nb)) == dests.end())
+                            dests.push_back(owner(li, nb));
+                    for (int d : dests) {
+                        Msg msg;
+                        msg.src = R.rank;
+                        msg.dst = d;
+                        msg.key = msg_key(3, li, e);
+                        msg.im = vec_image(st, R.G + (size_t)e * pv, pv);
+                        out.push_back(msg);
+                    }
+                }
+                std::vector<int> need;
+                for (int j : ret) {
+                    if (owner(li, j) != R.rank) continue;
+                    for (int nb : {j - 1, j + 1})
+                        if (nb >= 0 && nb < m && is_elim[nb] && owner(li, nb) != R.rank &&
+                            std::find(need.begin(), need.end(), nb) == need.end())
+                            need.push_back(nb);
+                }
+                for (int e : need) expect.push_back(Expect{owner(li, e), R.rank, msg_key(3, li, e)});
             }
-            if (hi) {
-                c.push_back({L.Dinv[j + 1], P(li, j + 1), nullptr, T2 + t * pv});
-                d.push_back({L.F[j], T2 + t * pv, out, out});
+            for (auto& R : runs) CK(cudaStreamSynchronize(R.F->eng->st()));
+            for (Msg& msg : T->exchange(out, expect)) {
+                SolveRun& R = run_of(msg.dst);
+                cudaStream_t st = R.F->eng->st();
+                const int e = (int)(msg.key & 0xffffff);
+                CK(cudaMemcpyAsync(R.G + (size_t)e * pv, msg.im.buf, pv * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                CK(cudaFreeAsync(msg.im.buf, st));
             }
         }
-        matvec(E, a, nrhs);
-        matvec(E, b, nrhs);
-        matvec(E, c, nrhs);
-        matvec(E, d, nrhs);
-    }
-    // apex (solve_apex, acr.cpp:162-178)
-    const size_t la = F->levels.size();
-    const int s = (int)F->apexDinv.size();
-    for (int i = 1; i < s; ++i) {
-        matvec(E, {{F->apexDinv[i - 1], P(la, i - 1), nullptr, T1}}, nrhs);
-        matvec(E, {{F->apexE[i], T1, P(la, i), P(la, i)}}, nrhs);
-    }
-    // u for apex planes stored in U0[0..s)
-    for (int i = s - 1; i >= 0; --i) {
-        const double* r = P(la, i);
-        if (i + 1 < s) {
-            matvec(E, {{F->apexF[i], U0 + (size_t)(i + 1) * pv, P(la, i), T1}}, nrhs);
-            r = T1;
+        for (auto& R : runs) {
+            const Level& L = R.F->levels[li];
+            cudaStream_t st = R.F->eng->st();
+            std::vector<MV> b, d;
+            for (size_t t = 0; t < ret.size(); ++t) {
+                const int j = ret[t];
+                if (owner(li, j) != R.rank) continue;
+                const bool lo = j > 0 && is_elim[j - 1];
+                const bool hi = j + 1 < m && is_elim[j + 1];
+                double* outp = P(R, li + 1, (int)t);
+                if (lo)
+                    b.push_back({L.E[j], R.G + (size_t)(j - 1) * pv, P(R, li, j), outp});
+                else
+                    CK(cudaMemcpyAsync(outp, P(R, li, j), pv * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                if (hi) d.push_back({L.F[j], R.G + (size_t)(j + 1) * pv, outp, outp});
+            }
+            matvec(*R.F->eng, b, nrhs);
+            matvec(*R.F->eng, d, nrhs);
         }
-        matvec(E, {{F->apexDinv[i], r, nullptr, U0 + (size_t)i * pv}}, nrhs);
     }
-    // back substitution (back_substitute, acr.hpp:123-132), level by level
-    double* ucur = U0;
-    double* unext = T2;  // reuse as the next level's solution buffer (needs n planes)
-    std::vector<double> dummy;
-    double* ubuf = nullptr;
-    CK(cudaMallocAsync((void**)&ubuf, 2 * (size_t)n * pv * sizeof(double), st));
-    double* bufs[2] = {ubuf, ubuf + (size_t)n * pv};
-    CK(cudaMemcpyAsync(bufs[0], ucur, (size_t)s * pv * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    // apex (solve_apex, acr.cpp:162-178): on the owner of the remaining plane(s)
     int cur = 0;
-    (void)unext;
-    for (int li = (int)F->levels.size() - 1; li >= 0; --li) {
-        const Level& L = F->levels[li];
-        const int mm = L.plane_count;
-        double* uin = bufs[cur];
-        double* uout = bufs[cur ^ 1];
-        for (size_t t = 0; t < L.ret.size(); ++t)
-            CK(cudaMemcpyAsync(uout + (size_t)L.ret[t] * pv, uin + t * pv, pv * sizeof(double),
-                               cudaMemcpyDeviceToDevice, st));
-        std::vector<MV> a, b, c;
-        for (int e : L.elim) {
-            const double* r = P(li, e);
-            double* tmp = T1 + (size_t)e * pv;
-            const bool lo = e > 0 && L.E[e];
-            const bool hi = e + 1 < mm && L.F[e];
-            if (lo) {
-                a.push_back({L.E[e], uout + (size_t)(e - 1) * pv, r, tmp});
-                r = tmp;
-            }
-            if (hi) {
-                b.push_back({L.F[e], uout + (size_t)(e + 1) * pv, r, tmp});
-                r = tmp;
-            }
-            c.push_back({L.Dinv[e], r, nullptr, uout + (size_t)e * pv});
+    for (auto& R : runs) {
+        acrgpu_fact* F = R.F;
+        if (F->apexDinv.empty()) continue;
+        Engine& E = *F->eng;
+        const size_t la = nlev;
+        const int s = (int)F->apexDinv.size();
+        double* U0 = R.ub[0];
+        for (int i = 1; i < s; ++i) {
+            matvec(E, {{F->apexDinv[i - 1], P(R, la, i - 1), nullptr, R.T1}}, nrhs);
+            matvec(E, {{F->apexE[i], R.T1, P(R, la, i), P(R, la, i)}}, nrhs);
         }
-        matvec(E, a, nrhs);
-        matvec(E, b, nrhs);
-        matvec(E, c, nrhs);
+        for (int i = s - 1; i >= 0; --i) {
+            const double* r = P(R, la, i);
+            if (i + 1 < s) {
+                matvec(E, {{F->apexF[i], U0 + (size_t)(i + 1) * pv, P(R, la, i), R.T1}}, nrhs);
+                r = R.T1;
+            }
+            matvec(E, {{F->apexDinv[i], r, nullptr, U0 + (size_t)i * pv}}, nrhs);
+        }
+    }
+    // back substitution, level by level: ub[cur] holds u of level li+1 (positions t)
+    for (int li = nlev - 1; li >= 0; --li) {
+        const int m = F0->levels[li].plane_count;
+        const std::vector<int> elim = eliminated_positions(m), ret = retained_positions(m);
+        std::vector<char> is_elim(m, 0);
+        for (int e : elim) is_elim[e] = 1;
+        for (auto& R : runs) {
+            cudaStream_t st = R.F->eng->st();
+            for (size_t t = 0; t < ret.size(); ++t)
+                if (owner(li, ret[t]) == R.rank)
+                    CK(cudaMemcpyAsync(R.ub[cur ^ 1] + (size_t)ret[t] * pv, R.ub[cur] + t * pv, pv * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st));
+        }
+        if (T) {
+            std::vector<Msg> out;
+            std::vector<Expect> expect;
+            for (auto& R : runs) {
+                cudaStream_t st = R.F->eng->st();
+                for (int j : ret) {
+                    if (owner(li, j) != R.rank) continue;
+                    std::vector<int> dests;
+                    for (int nb : {j - 1, j + 1})
+                        if (nb >= 0 && nb < m && is_elim[nb] && owner(li, nb) != R.rank &&
+                            std::find(dests.begin(), dests.end(), owner(li, nb)) == dests.end())
+                            dests.push_back(owner(li, nb));
+                    for (int d : dests) {
+                        Msg msg;
+                        msg.src = R.rank;
+                        msg.dst = d;
+                        msg.key = msg_key(4, li, j);
+                        msg.im = vec_image(st, R.ub[cur ^ 1] + (size_t)j * pv, pv);
+                        out.push_back(msg);
+                    }
+                }
+                std::vector<int> need;
+                for (int e : elim) {
+                    if (owner(li, e) != R.rank) continue;
+                    for (int nb : {e - 1, e + 1})
+                        if (nb >= 0 && nb < m && !is_elim[nb] && owner(li, nb) != R.rank &&
+                            std::find(need.begin(), need.end(), nb) == need.end())
+                            need.push_back(nb);
+                }
+                for (int j : need) expect.push_back(Expect{owner(li, j), R.rank, msg_key(4, li, j)});
+            }
+            for (auto& R : runs) CK(cudaStreamSynchronize(R.F->eng->st()));
+            for (Msg& msg : T->exchange(out, expect)) {
+                SolveRun& R = run_of(msg.dst);
+                cudaStream_t st = R.F->eng->st();
+                const int j = (int)(msg.key & 0xffffff);
+                CK(cudaMemcpyAsync(R.ub[cur ^ 1] + (size_t)j * pv, msg.im.buf, pv * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+                CK(cudaFreeAsync(msg.im.buf, st));
+            }
+        }
+        for (auto& R : runs) {
+            const Level& L = R.F->levels[li];
+            double* uout = R.ub[cur ^ 1];
+            std::vector<MV> a, b, c;
+            for (int e : elim) {
+                if (owner(li, e) != R.rank) continue;
+                const double* r = P(R, li, e);
+                double* tmp = R.T1 + (size_t)e * pv;
+                const bool lo = e > 0 && L.E[e];
+                const bool hi = e + 1 < m && L.F[e];
+                if (lo) {
+                    a.push_back({L.E[e], uout + (size_t)(e - 1) * pv, r, tmp});
+                    r = tmp;
+                }
+                if (hi) {
+                    b.push_back({L.F[e], uout + (size_t)(e + 1) * pv, r, tmp});
+                    r = tmp;
+                }
+                c.push_back({L.Dinv[e], r, nullptr, uout + (size_t)e * pv});
+            }
+            matvec(*R.F->eng, a, nrhs);
+            matvec(*R.F->eng, b, nrhs);
+            matvec(*R.F->eng, c, nrhs);
+        }
         cur ^= 1;
     }
-    launch_permute_out(st, bufs[cur], u_dev, E.d_perm, n, dim, nrhs);
-    CK(cudaFreeAsync(ubuf, st));
+    // un-permute; with a partition each run contributes its own planes
+    for (auto& R : runs) {
+        Engine& E = *R.F->eng;
+        cudaStream_t st = E.st();
+        if (!own) {
+            launch_permute_out(st, R.ub[cur], u_dev, E.d_perm, n, dim, nrhs);
+            continue;
+        }
+        launch_permute_out(st, R.ub[cur], R.uperm, E.d_perm, n, dim, nrhs);
+        for (int j = 0; j < n; ++j)
+            if (owner(0, j) == R.rank)
+                CK(cudaMemcpy2DAsync(u_dev + (size_t)j * dim, (size_t)n * dim * sizeof(double),
+                                     R.uperm + (size_t)j * dim, (size_t)n * dim * sizeof(double), dim * sizeof(double),
+                                     nrhs, cudaMemcpyDeviceToDevice, st));
+    }
+}
+
+static void do_solve(acrgpu_fact* F, int nrhs, const double* f_dev, double* u_dev) {
+    std::vector<SolveRun> runs(1);
+    runs[0].F = F;
+    solve_runs(runs, nullptr, nullptr, nrhs, f_dev, u_dev);
 }
 
 // ------------------------------------------------------------------ stats
@@ -1802,33 +2293,37 @@ int acrgpu_factor_resident(acrgpu_ctx* ctx, const acrgpu_dsystem* sys, const acr
     })
 }
 
+// One factorization object (engine + structure) on ctx; holds a context reference.
+static std::unique_ptr<acrgpu_fact> make_part(acrgpu_ctx* ctx, const DSys& ds, const acrgpu_config* cfg) {
+    if (cfg->stop_planes < 1) throw AcrError{ACRGPU_E_USAGE, "acr_factor: stop_planes must be >= 1"};
+    if (cfg->leaf_size > DENSE_MAX) throw AcrError{ACRGPU_E_USAGE, "GPU path: leaf_size above 64 is not supported"};
+    auto F = std::make_unique<acrgpu_fact>();
+    F->ctx = ctx;
+    F->n = ds.n;
+    F->dim = ds.dim;
+    F->eng = std::make_unique<Engine>();
+    Engine& E = *F->eng;
+    E.ctx = &ctx->c;
+    E.cfg = *cfg;
+    E.exact_dd = (cfg->flags & ACRGPU_F_EXACT_DENSE_PRODUCTS) != 0;
+    E.S.build(ds.dim, ds.coords.data(), cfg->leaf_size, cfg->eta, cfg->weak);
+    if (E.S.max_dense_dim > DENSE_MAX)
+        throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64 rows are not supported"};
+    if (!E.S.balanced)
+        throw AcrError{ACRGPU_E_USAGE, "GPU path: unbalanced cluster trees (mixed dense/branch products) are not supported"};
+    E.prepare_structure();
+    ++ctx->refs;
+    return F;
+}
+
 static int factor_impl(acrgpu_ctx* ctx, const DSys& ds, const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err) {
-    const DSys* sys = &ds;
     ABI_TRY({
         *out = nullptr;
-        if (cfg->stop_planes < 1) throw AcrError{ACRGPU_E_USAGE, "acr_factor: stop_planes must be >= 1"};
-        if (cfg->leaf_size > DENSE_MAX)
-            throw AcrError{ACRGPU_E_USAGE, "GPU path: leaf_size above 64 is not supported"};
         ctx->c.reset_all();
         launches_take();
-        auto F = std::make_unique<acrgpu_fact>();
-        F->ctx = ctx;
-        F->n = sys->n;
-        F->dim = sys->dim;
-        F->eng = std::make_unique<Engine>();
-        Engine& E = *F->eng;
-        E.ctx = &ctx->c;
-        E.cfg = *cfg;
-        E.exact_dd = (cfg->flags & ACRGPU_F_EXACT_DENSE_PRODUCTS) != 0;
-        E.S.build(sys->dim, sys->coords.data(), cfg->leaf_size, cfg->eta, cfg->weak);
-        if (E.S.max_dense_dim > DENSE_MAX)
-            throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64 rows are not supported"};
-        if (!E.S.balanced)
-            throw AcrError{ACRGPU_E_USAGE, "GPU path: unbalanced cluster trees (mixed dense/branch products) are not supported"};
-        E.prepare_structure();
-        ++ctx->refs;
+        std::unique_ptr<acrgpu_fact> F = make_part(ctx, ds, cfg);
         try {
-            do_factor(F.get(), *sys);
+            do_factor(F.get(), ds);
         } catch (...) {
             F.reset();
             ctx_release(ctx);
@@ -1841,6 +2336,13 @@ static int factor_impl(acrgpu_ctx* ctx, const DSys& ds, const acrgpu_config* cfg
 
 void acrgpu_factor_destroy(acrgpu_fact* f) {
     if (!f) return;
+    if (!f->eng) {  // container of in-process ranks
+        for (acrgpu_fact* p : f->vparts) acrgpu_factor_destroy(p);
+        acrgpu_ctx* ctx = f->ctx;
+        delete f;
+        ctx_release(ctx);
+        return;
+    }
     cudaStream_t st = f->eng->st();
     cudaStreamSynchronize(st);
     if (f->fbuf) cudaFreeAsync(f->fbuf, st);
@@ -1855,16 +2357,38 @@ void acrgpu_factor_destroy(acrgpu_fact* f) {
     ctx_release(ctx);
 }
 
+static cudaStream_t fact_stream(acrgpu_fact* f) { return f->eng ? f->eng->st() : f->vparts[0]->eng->st(); }
+
 int acrgpu_solve_device(acrgpu_fact* f, int nrhs, const double* f_dev, double* u_dev, acrgpu_error* err) {
     ABI_TRY({
         if (nrhs < 1) throw AcrError{ACRGPU_E_DIMENSION, "solve: nrhs must be >= 1"};
-        Engine& E = *f->eng;
+        cudaStream_t st = fact_stream(f);
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
-        CK(cudaEventRecord(e0, E.st()));
-        do_solve(f, nrhs, f_dev, u_dev);
-        CK(cudaEventRecord(e1, E.st()));
+        CK(cudaEventRecord(e0, st));
+        if (!f->vparts.empty()) {  // in-process ranks
+            std::vector<SolveRun> runs;
+            for (acrgpu_fact* p : f->vparts) {
+                SolveRun R;
+                R.F = p;
+                R.rank = p->rank;
+                runs.push_back(R);
+            }
+            LocalTransport T;
+            solve_runs(runs, &f->owners, &T, nrhs, f_dev, u_dev);
+        } else if (f->comm) {  // one rank of a multi-process partition
+            std::vector<SolveRun> runs(1);
+            runs[0].F = f;
+            runs[0].rank = f->rank;
+            NcclTransport T;
+            T.comm = (ncclComm_t)f->comm->nccl;
+            T.st = st;
+            solve_runs(runs, &f->owners, &T, nrhs, f_dev, u_dev);
+        } else {
+            do_solve(f, nrhs, f_dev, u_dev);
+        }
+        CK(cudaEventRecord(e1, st));
         CK(cudaEventSynchronize(e1));
         CK(cudaGetLastError());
         float ms = 0;
@@ -1880,49 +2404,57 @@ int acrgpu_solve_device(acrgpu_fact* f, int nrhs, const double* f_dev, double* u
 int acrgpu_solve(acrgpu_fact* f, int nrhs, const double* f_host, double* u_host, acrgpu_error* err) {
     ABI_TRY({
         if (nrhs < 1) throw AcrError{ACRGPU_E_DIMENSION, "solve: nrhs must be >= 1"};
-        Engine& E = *f->eng;
+        cudaStream_t st = fact_stream(f);
         const size_t bytes = (size_t)nrhs * f->n * f->dim * sizeof(double);
         double *df = nullptr, *du = nullptr;
-        CK(cudaMallocAsync((void**)&df, bytes, E.st()));
-        CK(cudaMallocAsync((void**)&du, bytes, E.st()));
-        CK(cudaMemcpyAsync(df, f_host, bytes, cudaMemcpyHostToDevice, E.st()));
+        CK(cudaMallocAsync((void**)&df, bytes, st));
+        CK(cudaMallocAsync((void**)&du, bytes, st));
+        CK(cudaMemcpyAsync(df, f_host, bytes, cudaMemcpyHostToDevice, st));
+        if (f->comm && f->vparts.empty()) CK(cudaMemsetAsync(du, 0, bytes, st));  // planes owned elsewhere stay 0
         const int rc = acrgpu_solve_device(f, nrhs, df, du, err);
-        if (rc == 0) CK(cudaMemcpyAsync(u_host, du, bytes, cudaMemcpyDeviceToHost, E.st()));
-        CK(cudaFreeAsync(df, E.st()));
-        CK(cudaFreeAsync(du, E.st()));
-        CK(cudaStreamSynchronize(E.st()));
+        if (rc == 0) CK(cudaMemcpyAsync(u_host, du, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaFreeAsync(df, st));
+        CK(cudaFreeAsync(du, st));
+        CK(cudaStreamSynchronize(st));
         return rc;
     })
+}
+
+static std::vector<acrgpu_fact*> parts_of(acrgpu_fact* f) {
+    if (!f->vparts.empty()) return f->vparts;
+    return {f};
 }
 
 int acrgpu_stats(acrgpu_fact* f, acrgpu_rankstats* out) {
     acrgpu_error e;
     acrgpu_error* err = &e;
     ABI_TRY({
-        Engine& E = *f->eng;
-        CK(cudaStreamSynchronize(E.st()));
         HostStats inv;
         long total = 0;
-        auto add = [&](const SP& s, bool is_inv) {
-            if (!s) return;
-            HostStats h = store_stats(E, s);
-            total += h.bytes;
-            if (is_inv) {
-                inv.rank_sum += h.rank_sum;
-                inv.largest = std::max(inv.largest, h.largest);
-                inv.ndense += h.ndense;
-                inv.nrk += h.nrk;
-                inv.bytes += h.bytes;
+        for (acrgpu_fact* p : parts_of(f)) {
+            Engine& E = *p->eng;
+            CK(cudaStreamSynchronize(E.st()));
+            auto add = [&](const SP& s, bool is_inv) {
+                if (!s) return;
+                HostStats h = store_stats(E, s);
+                total += h.bytes;
+                if (is_inv) {
+                    inv.rank_sum += h.rank_sum;
+                    inv.largest = std::max(inv.largest, h.largest);
+                    inv.ndense += h.ndense;
+                    inv.nrk += h.nrk;
+                    inv.bytes += h.bytes;
+                }
+            };
+            for (auto& L : p->levels) {
+                for (auto& s : L.E) add(s, false);
+                for (auto& s : L.F) add(s, false);
+                for (auto& s : L.Dinv) add(s, true);
             }
-        };
-        for (auto& L : f->levels) {
-            for (auto& s : L.E) add(s, false);
-            for (auto& s : L.F) add(s, false);
-            for (auto& s : L.Dinv) add(s, true);
+            for (auto& s : p->apexE) add(s, false);
+            for (auto& s : p->apexF) add(s, false);
+            for (auto& s : p->apexDinv) add(s, true);
         }
-        for (auto& s : f->apexE) add(s, false);
-        for (auto& s : f->apexF) add(s, false);
-        for (auto& s : f->apexDinv) add(s, true);
         out->average_rank = inv.nrk ? double(inv.rank_sum) / inv.nrk : 0.0;
         out->largest_rank = inv.largest;
         out->dense_leaf_count = inv.ndense;
@@ -1937,68 +2469,204 @@ int acrgpu_level_info(acrgpu_fact* f, acrgpu_levelinfo* out, int cap) {
     acrgpu_error e;
     acrgpu_error* err = &e;
     ABI_TRY({
-        Engine& E = *f->eng;
-        int k = 0;
-        auto one = [&](int level, int pc, int elim, const std::vector<SP>& Dinv, const std::vector<SP>& Es,
-                       const std::vector<SP>& Fs) {
-            acrgpu_levelinfo li{};
-            li.level = level;
-            li.plane_count = pc;
-            li.eliminated = elim;
-            long rs = 0, nrk = 0;
-            for (auto& s : Dinv)
-                if (s) {
-                    HostStats h = store_stats(E, s);
-                    li.bytes += h.bytes;
-                    rs += h.rank_sum;
-                    nrk += h.nrk;
-                    li.largest_rank = std::max(li.largest_rank, h.largest);
-                }
-            for (auto& s : Es)
-                if (s) li.bytes += store_stats(E, s).bytes;
-            for (auto& s : Fs)
-                if (s) li.bytes += store_stats(E, s).bytes;
-            li.average_rank = nrk ? double(rs) / nrk : 0.0;
-            if (k < cap) out[k] = li;
-            ++k;
-        };
-        for (size_t i = 0; i < f->levels.size(); ++i) {
-            const Level& L = f->levels[i];
-            one((int)i, L.plane_count, (int)L.elim.size(), L.Dinv, L.E, L.F);
+        const std::vector<acrgpu_fact*> parts = parts_of(f);
+        const int nl = (int)parts[0]->levels.size();
+        std::vector<acrgpu_levelinfo> li(nl + 1);
+        std::vector<long> rs(nl + 1, 0), nrk(nl + 1, 0);
+        for (int i = 0; i <= nl; ++i) {
+            li[i].level = i;
+            if (i < nl) {
+                li[i].plane_count = parts[0]->levels[i].plane_count;
+                li[i].eliminated = (int)parts[0]->levels[i].elim.size();
+            }
         }
-        one((int)f->levels.size(), (int)f->apexDinv.size(), (int)f->apexDinv.size(), f->apexDinv, f->apexE, f->apexF);
-        return k;
+        for (acrgpu_fact* p : parts) {
+            Engine& E = *p->eng;
+            auto one = [&](int i, const std::vector<SP>& Dinv, const std::vector<SP>& Es, const std::vector<SP>& Fs) {
+                for (auto& s : Dinv)
+                    if (s) {
+                        HostStats h = store_stats(E, s);
+                        li[i].bytes += h.bytes;
+                        rs[i] += h.rank_sum;
+                        nrk[i] += h.nrk;
+                        li[i].largest_rank = std::max(li[i].largest_rank, h.largest);
+                    }
+                for (auto& s : Es)
+                    if (s) li[i].bytes += store_stats(E, s).bytes;
+                for (auto& s : Fs)
+                    if (s) li[i].bytes += store_stats(E, s).bytes;
+            };
+            for (int i = 0; i < nl; ++i) one(i, p->levels[i].Dinv, p->levels[i].E, p->levels[i].F);
+            one(nl, p->apexDinv, p->apexE, p->apexF);
+            if (!p->apexDinv.empty()) {
+                li[nl].plane_count = (int)p->apexDinv.size();
+                li[nl].eliminated = (int)p->apexDinv.size();
+            }
+        }
+        for (int i = 0; i <= nl; ++i) {
+            li[i].average_rank = nrk[i] ? double(rs[i]) / nrk[i] : 0.0;
+            if (i < cap) out[i] = li[i];
+        }
+        return nl + 1;
     })
 }
 
 long acrgpu_dinv_ranks(acrgpu_fact* f, int li, int j, int* out, long cap) {
-    Engine& E = *f->eng;
-    SP s;
-    if (li >= 0 && li < (int)f->levels.size()) {
-        const Level& L = f->levels[li];
-        if (j >= 0 && j < (int)L.Dinv.size()) s = L.Dinv[j];
-    } else if (li == (int)f->levels.size() && j >= 0 && j < (int)f->apexDinv.size()) {
-        s = f->apexDinv[j];
+    for (acrgpu_fact* p : parts_of(f)) {
+        Engine& E = *p->eng;
+        SP s;
+        if (li >= 0 && li < (int)p->levels.size()) {
+            const Level& L = p->levels[li];
+            if (j >= 0 && j < (int)L.Dinv.size()) s = L.Dinv[j];
+        } else if (li == (int)p->levels.size() && j >= 0 && j < (int)p->apexDinv.size()) {
+            s = p->apexDinv[j];
+        }
+        if (!s) continue;
+        cudaStreamSynchronize(E.st());
+        std::vector<int> r(E.S.n_rk());
+        if (!r.empty()) cudaMemcpy(r.data(), s->rank, r.size() * sizeof(int), cudaMemcpyDeviceToHost);
+        // DFS order over all leaves, -1 for dense
+        long n = 0;
+        std::vector<int> lv;
+        E.subtree_leaves(0, lv);
+        for (int node : lv) {
+            const SNode& L = E.S.node(node);
+            if (out && n < cap) out[n] = L.kind == K_RK ? r[L.leaf] : -1;
+            ++n;
+        }
+        return n;
     }
-    if (!s) return -1;
-    cudaStreamSynchronize(E.st());
-    std::vector<int> r(E.S.n_rk());
-    if (!r.empty()) cudaMemcpy(r.data(), s->rank, r.size() * sizeof(int), cudaMemcpyDeviceToHost);
-    // DFS order over all leaves, -1 for dense
-    long n = 0;
-    std::vector<int> lv;
-    E.subtree_leaves(0, lv);
-    for (int node : lv) {
-        const SNode& L = E.S.node(node);
-        if (out && n < cap) out[n] = L.kind == K_RK ? r[L.leaf] : -1;
-        ++n;
-    }
-    return n;
+    return -1;
 }
 
 int acrgpu_timing_get(acrgpu_fact* f, acrgpu_timing* out) {
-    *out = f->timing;
+    if (f->vparts.empty()) {
+        *out = f->timing;
+        return 0;
+    }
+    // in-process ranks run back to back on one device: factor time is the whole run's
+    *out = f->vparts[0]->timing;
+    out->flops_nominal = out->flops_gemm = out->flops_qr = out->flops_svd = out->flops_lu = 0;
+    for (acrgpu_fact* p : f->vparts) {
+        out->factor_ms = std::max(out->factor_ms, p->timing.factor_ms);
+        out->lift_ms = std::max(out->lift_ms, p->timing.lift_ms);
+    }
+    const acrgpu_timing& t = f->vparts.back()->timing;  // the ledger is shared by the ranks of one context
+    out->flops_nominal = t.flops_nominal;
+    out->flops_gemm = t.flops_gemm;
+    out->flops_qr = t.flops_qr;
+    out->flops_svd = t.flops_svd;
+    out->flops_lu = t.flops_lu;
+    out->solve_ms = f->timing.solve_ms;
+    out->solve_launches = f->timing.solve_launches;
     return 0;
+}
+
+// ------------------------------------------------------------------ plane partition C-ABI
+int acrgpu_comm_unique_id(unsigned char* id, acrgpu_error* err) {
+    ABI_TRY({
+        ncclUniqueId u;
+        NCK(nccl().GetUniqueId(&u));
+        static_assert(sizeof(u) == ACRGPU_COMM_ID_BYTES, "NCCL unique id size");
+        std::memcpy(id, &u, sizeof(u));
+        return 0;
+    })
+}
+
+int acrgpu_comm_create(const unsigned char* id, int nranks, int rank, acrgpu_comm** out, acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw AcrError{ACRGPU_E_USAGE, "comm: bad rank / size"};
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        ncclComm_t c = nullptr;
+        NCK(nccl().CommInitRank(&c, nranks, u, rank));
+        auto* cm = new acrgpu_comm;
+        cm->nranks = nranks;
+        cm->rank = rank;
+        cm->local = false;
+        cm->nccl = c;
+        *out = cm;
+        return 0;
+    })
+}
+
+int acrgpu_comm_create_local(int nranks, acrgpu_comm** out, acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
+        if (nranks < 1) throw AcrError{ACRGPU_E_USAGE, "comm: nranks must be >= 1"};
+        auto* cm = new acrgpu_comm;
+        cm->nranks = nranks;
+        cm->rank = 0;
+        cm->local = true;
+        *out = cm;
+        return 0;
+    })
+}
+
+void acrgpu_comm_destroy(acrgpu_comm* c) {
+    if (!c) return;
+    if (c->nccl) nccl().CommDestroy((ncclComm_t)c->nccl);
+    delete c;
+}
+
+int acrgpu_factor_partitioned(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_system* sys, const acrgpu_config* cfg,
+                              acrgpu_fact** out, acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
+        if (!ctx || !comm || !sys || !cfg) throw AcrError{ACRGPU_E_USAGE, "null argument"};
+        std::unique_ptr<DSys> ds(make_dsys(sys, ctx->c.st));
+        const std::vector<std::vector<int>> own = plan_owners(ds->n, comm->nranks);
+        ctx->c.reset_all();
+        launches_take();
+        const int nlocal = comm->local ? comm->nranks : 1;
+        std::vector<std::unique_ptr<acrgpu_fact>> parts;
+        std::vector<PartRun> runs;
+        try {
+            for (int i = 0; i < nlocal; ++i) {
+                parts.push_back(make_part(ctx, *ds, cfg));
+                parts.back()->rank = comm->local ? i : comm->rank;
+                parts.back()->owners = own;
+                parts.back()->comm = comm->local ? nullptr : comm;
+            }
+            for (auto& p : parts) {
+                PartRun R;
+                R.F = p.get();
+                R.rank = p->rank;
+                runs.push_back(R);
+            }
+            if (comm->local) {
+                LocalTransport T;
+                factor_partitioned(runs, own, T, *ds);
+            } else {
+                NcclTransport T;
+                T.comm = (ncclComm_t)comm->nccl;
+                T.st = ctx->c.st;
+                factor_partitioned(runs, own, T, *ds);
+            }
+        } catch (...) {
+            for (auto& p : parts) {
+                p.reset();
+                ctx_release(ctx);
+            }
+            throw;
+        }
+        if (!comm->local) {
+            *out = parts[0].release();
+            return 0;
+        }
+        auto* c = new acrgpu_fact;
+        c->ctx = ctx;
+        ++ctx->refs;
+        c->n = ds->n;
+        c->dim = ds->dim;
+        c->owners = own;
+        c->comm = comm;
+        for (auto& p : parts) c->vparts.push_back(p.release());
+        c->timing = c->vparts[0]->timing;
+        *out = c;
+        return 0;
+    })
 }
 
 long acrgpu_structure(int dim, const double* coords, int leaf_size, double eta, int weak, int* perm, int* leaves,

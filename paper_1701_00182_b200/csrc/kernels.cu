@@ -1467,11 +1467,24 @@ __global__ void k_compact(CompactArgs a) {
     for (long e = threadIdx.x; e < (long)m * r; e += blockDim.x) dst[e] = u[e];
     for (long e = threadIdx.x; e < (long)n * r; e += blockDim.x) dst[(long)m * r + e] = v[e];
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && a.repoint) {
         U[leaf] = dst;
         V[leaf] = dst + (long)m * r;
     }
 }
+
+__global__ void k_image_fix(ImageFix a) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.nk) return;
+    const long off = (long)a.buf[a.offs + k];
+    const int r = (int)a.buf[a.ranks + k];
+    ((int*)(a.buf + a.irank))[k] = r;
+    double** U = (double**)(a.buf + a.ptrs);
+    double** V = U + a.nk;
+    U[k] = off >= 0 ? a.buf + a.lr + off : nullptr;
+    V[k] = off >= 0 ? a.buf + a.lr + off + (long)a.km[k] * r : nullptr;
+}
+
 
 
 // ------------------------------------------------------------------ register-resident small-block kernels
@@ -1953,6 +1966,12 @@ void launch_scatter(cudaStream_t st, const ScatterLaunch& s, const BatchViews& b
 void launch_reset_counter(cudaStream_t st, unsigned long long* ctr) {
     ProfScope _ps(st, "k_reset_counter", (long)(1));
     k_reset_counter<<<1, 1, 0, st>>>(ctr);
+}
+
+void launch_image_fix(cudaStream_t st, const ImageFix& a) {
+    if (a.nk == 0) return;
+    ProfScope _ps(st, "k_image_fix", (long)((a.nk + 127) / 128));
+    k_image_fix<<<(a.nk + 127) / 128, 128, 0, st>>>(a);
 }
 
 void launch_compact(cudaStream_t st, const CompactArgs& a, int nstores) {

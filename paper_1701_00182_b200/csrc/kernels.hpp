@@ -39,8 +39,19 @@ struct CompactArgs {
     const int* km;
     const int* kn;
     int nleaf;
+    int repoint;          // 1: the stores' U/V tables are redirected to the copies
 };
 void launch_compact(cudaStream_t st, const CompactArgs& a, int nstores);
+
+// Wire image of one H-matrix (plane-partition exchange): after the bytes arrive,
+// rebuild the int rank table and the U/V pointer tables inside the image.
+struct ImageFix {
+    double* buf;
+    int nk;
+    long offs, ranks, irank, ptrs, lr;  // section offsets (doubles)
+    const int* km;
+};
+void launch_image_fix(cudaStream_t st, const ImageFix& a);
 
 void setup_kernels();
 long launches_take();
