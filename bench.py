@@ -19,8 +19,10 @@ roofline / cpu_baseline / clocks / gpu_launches: see DESIGN.md §6.
 itself cannot be built here -- no Eigen), all host threads, on a bounded sample of the
 same workload, extrapolated to the full configuration by its nominal FLOP count.
 
-Multi-GPU (--gpus N > 1 under torchrun): replicas -- every rank factors and solves its
-own seeded system (weak scaling; the plane-partitioned NCCL path is future work).
+Multi-GPU (--gpus N > 1 under torchrun): the plane partition of execute_parallel_factor
+(parallel.cpp:96-297) -- one system, rank w owns plan_schedule(n, N)'s planes, per-level
+NCCL point-to-point exchange inside libacrgpu (strong scaling: value = DOF / max-over-ranks
+step time).  --replicas instead runs N independent copies (weak scaling).
 """
 from __future__ import annotations
 
@@ -54,6 +56,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent copies instead of the partition")
     return ap.parse_args()
 
 
@@ -228,8 +231,19 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
+    comm = None
+    if ws > 1 and not args.replicas:
+        uid = [acr.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = acr.Comm.nccl(uid[0], ws, rank)
+    partitioned = comm is not None
+
     def step():
-        fact = acr.acr_factor(dsys, cfg)
+        if partitioned:
+            u_dev.zero_()  # planes owned by other ranks
+            fact = acr.acr_factor_partitioned(dsys, comm, cfg)
+        else:
+            fact = acr.acr_factor(dsys, cfg)
         fact.solve_device(f_dev.data_ptr(), u_dev.data_ptr(), nrhs)
         return fact
 
@@ -273,14 +287,26 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_mean = float(t.item())
     dof = sysm.total_dim * nrhs
-    value = ws * dof / (ms_mean / 1000.0)
-    # accuracy of the last factorization
+    value = (1 if partitioned else ws) * dof / (ms_mean / 1000.0)
+    # accuracy of the last factorization (a partition's ranks each hold their own planes)
+    if partitioned:
+        dist.all_reduce(u_dev, op=dist.ReduceOp.SUM)
     u = u_dev.cpu().numpy()
     res = sysm.relative_residual(u)
     st = fact.inverse_rank_stats()
     lv = fact.level_info()
     fb = fact.factor_bytes()
     tm = fact.timing()
+    avg_rank, largest = st.average_rank, st.largest_rank
+    if partitioned:
+        t = torch.tensor([st.average_rank * st.lowrank_leaf_count, st.lowrank_leaf_count, fb], device=f"cuda:{local}",
+                         dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        avg_rank = float(t[0] / t[1]) if float(t[1]) > 0 else 0.0
+        fb = int(t[2].item())
+        t = torch.tensor([st.largest_rank], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        largest = int(t.item())
     del fact
 
     # roofline of the dominant kernel (device time share)
@@ -326,7 +352,7 @@ def run_ours(args):
         for _ in range(max(1, min(args.steps, 2))):
             barrier()
             t0 = time.perf_counter()
-            fe = acr.acr_factor(hsys, cfg, ctx=ctx)
+            fe = acr.acr_factor_partitioned(hsys, comm, cfg, ctx=ctx) if partitioned else acr.acr_factor(hsys, cfg, ctx=ctx)
             ue = fe.solve(hsys.rhs)
             ts.append(time.perf_counter() - t0)
             del fe
@@ -335,7 +361,7 @@ def run_ours(args):
             t = torch.tensor([t_e2e], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_e2e = float(t.item())
-        e2e = {"value": ws * dof / t_e2e, "unit": "DOF/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": (1 if partitioned else ws) * dof / t_e2e, "unit": "DOF/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "seconds_per_step": t_e2e}
         acr.profile_report(reset=True)
 
@@ -355,12 +381,15 @@ def run_ours(args):
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_mean, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_mean, "higher_is_better": True,
+                "scaling": "strong" if partitioned else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload_name(args, sysm), "parallelism": "replicas" if ws > 1 else "single",
+                "config": {"workload": workload_name(args, sysm),
+                           "parallelism": f"plane-partition p{ws} (NCCL p2p)" if partitioned
+                           else ("replicas" if ws > 1 else "single"),
                            "l2": "working set (GB of H-matrix factors) far exceeds the 126 MB L2; no flush needed",
                            "exact_dense_products": bool(args.exact_dense_products)},
-                "relative_residual": res, "largest_rank": st.largest_rank, "average_rank": st.average_rank,
+                "relative_residual": res, "largest_rank": largest, "average_rank": avg_rank,
                 "factor_bytes": fb, "factor_ms": sum(t_fac) / len(t_fac), "solve_ms": sum(t_sol) / len(t_sol),
                 "ms_per_step_max": ms, "wall_s_per_step": max(wall),
                 "factor_dof_per_s": dof / nrhs / (sum(t_fac) / len(t_fac) / 1000.0),
@@ -372,6 +401,8 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
+        if comm is not None:
+            comm.close()
         dist.destroy_process_group()
     return 0
 

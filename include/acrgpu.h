@@ -188,6 +188,9 @@ int acrgpu_comm_create_local(int nranks, acrgpu_comm** out, acrgpu_error* err);
 void acrgpu_comm_destroy(acrgpu_comm* comm);
 int acrgpu_factor_partitioned(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_system* sys,
                               const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err);
+/* Same, on a system already uploaded with acrgpu_system_upload. */
+int acrgpu_factor_partitioned_resident(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_dsystem* sys,
+                                       const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err);
 
 /* Library build identification (sm arch, version). */
 const char* acrgpu_version(void);

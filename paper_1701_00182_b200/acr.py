@@ -163,6 +163,8 @@ SYMBOLS = {
     "acrgpu_comm_destroy": (None, [C.c_void_p]),
     "acrgpu_factor_partitioned": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Sys), C.POINTER(_Cfg),
                                             C.POINTER(C.c_void_p), C.POINTER(_Err)]),
+    "acrgpu_factor_partitioned_resident": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_Cfg),
+                                                     C.POINTER(C.c_void_p), C.POINTER(_Err)]),
 }
 
 COMM_ID_BYTES = 128
@@ -427,11 +429,17 @@ def acr_factor_partitioned(system, comm: Comm, config: AcrConfig | None = None, 
     plan_schedule(n, comm.nranks); bitwise identical to acr_factor."""
     config = config or AcrConfig()
     cfg = _cfg(config)
-    ctx = ctx or default_context()
-    s, keep = _sys_struct(system)
     h = C.c_void_p()
     err = _Err()
-    if lib().acrgpu_factor_partitioned(ctx.h, comm.h, C.byref(s), C.byref(cfg), C.byref(h), C.byref(err)):
+    if isinstance(system, DeviceSystem):
+        ctx = system.ctx
+        rc = lib().acrgpu_factor_partitioned_resident(ctx.h, comm.h, system.h, C.byref(cfg), C.byref(h), C.byref(err))
+        system = system.system
+    else:
+        ctx = ctx or default_context()
+        s, keep = _sys_struct(system)
+        rc = lib().acrgpu_factor_partitioned(ctx.h, comm.h, C.byref(s), C.byref(cfg), C.byref(h), C.byref(err))
+    if rc:
         _raise(err)
     f = AcrFactorization(h, system, config, ctx)
     f._comm = comm  # keep the communicator alive

@@ -2610,12 +2610,32 @@ void acrgpu_comm_destroy(acrgpu_comm* c) {
     delete c;
 }
 
+static int factor_partitioned_impl(acrgpu_ctx* ctx, acrgpu_comm* comm, const DSys* ds, const acrgpu_config* cfg,
+                                   acrgpu_fact** out, acrgpu_error* err);
+
 int acrgpu_factor_partitioned(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_system* sys, const acrgpu_config* cfg,
                               acrgpu_fact** out, acrgpu_error* err) {
     ABI_TRY({
         *out = nullptr;
         if (!ctx || !comm || !sys || !cfg) throw AcrError{ACRGPU_E_USAGE, "null argument"};
         std::unique_ptr<DSys> ds(make_dsys(sys, ctx->c.st));
+        return factor_partitioned_impl(ctx, comm, ds.get(), cfg, out, err);
+    })
+}
+
+int acrgpu_factor_partitioned_resident(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_dsystem* sys,
+                                       const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
+        if (!ctx || !comm || !sys || !cfg) throw AcrError{ACRGPU_E_USAGE, "null argument"};
+        return factor_partitioned_impl(ctx, comm, sys->d.get(), cfg, out, err);
+    })
+}
+
+static int factor_partitioned_impl(acrgpu_ctx* ctx, acrgpu_comm* comm, const DSys* ds, const acrgpu_config* cfg,
+                                   acrgpu_fact** out, acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
         const std::vector<std::vector<int>> own = plan_owners(ds->n, comm->nranks);
         ctx->c.reset_all();
         launches_take();

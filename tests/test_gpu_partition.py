@@ -81,3 +81,18 @@ def test_partitioned_singular_location(acr):                                    
     with pytest.raises(acr.SingularBlockError) as ei:
         acr.acr_factor_partitioned(sysm, acr.Comm.local_ranks(2), acr.AcrConfig(eps=1e-6, leaf_size=8))
     assert ei.value.level == 0 and ei.value.plane == 2
+
+
+def test_nccl_transport_single_rank(acr):
+    """NCCL communicator through the library (dlopen'ed libnccl): a one-rank partition runs
+    the same exchange code with empty message lists and matches the single-rank path."""
+    sysm = P.poisson(8)
+    cfg = acr.AcrConfig(eps=1e-3)
+    u1 = acr.acr_factor(sysm, cfg).solve(sysm.rhs)
+    uid = acr.Comm.unique_id()
+    assert len(uid) == acr.COMM_ID_BYTES
+    comm = acr.Comm.nccl(uid, 1, 0)
+    f = acr.acr_factor_partitioned(sysm, comm, cfg)
+    assert np.array_equal(f.solve(sysm.rhs), u1)
+    del f
+    comm.close()
