@@ -109,8 +109,11 @@ struct Ctx {
         setup_kernels();
         size_t freeb = 0, total = 0;
         CK(cudaMemGetInfo(&freeb, &total));
-        const size_t pbytes = (size_t)(freeb * 0.42) & ~(size_t)4095;
-        const size_t tbytes = ((size_t)(freeb * 0.14) / NLANES) & ~(size_t)4095;
+        // persistent arena (stored factors) 38%, one transient arena per lane 2 x 20%; the rest
+        // (cudaMallocAsync: dense pools of the stored blocks, solve workspace) stays free.
+        // C5-sized planes (16384 points) need ~13-15 GB of transient arena for one root product.
+        const size_t pbytes = (size_t)(freeb * 0.38) & ~(size_t)4095;
+        const size_t tbytes = ((size_t)(freeb * 0.40) / NLANES) & ~(size_t)4095;
         persist_base = dmalloc<double>(pbytes / 8);
         trans_base = dmalloc<double>(NLANES * tbytes / 8);
         ctrs = dmalloc<unsigned long long>(1 + NLANES);
@@ -226,6 +229,8 @@ struct Plan {
     Classed<TruncTask> flush;
     DepTask* deps = nullptr;
     Part* parts = nullptr;
+    double pp_gb = -1;   // measured transient arena use per plane (adaptive batching)
+    int pp_level = -1;
 };
 
 struct Engine {
@@ -233,6 +238,8 @@ struct Engine {
     Structure S;
     acrgpu_config cfg{};
     bool exact_dd = false;
+    double peak_transient_gb = 0, peak_transient_per_plane_gb = 0;  // ACRGPU_ARENA_STATS
+    int level_tag = 0;  // current cyclic-reduction level (adaptive batching)
     std::map<std::tuple<int, int, int, int>, std::unique_ptr<Plan>> plans;
     std::vector<void*> dev_allocs;  // plan arrays etc.
 
@@ -668,9 +675,24 @@ struct Engine {
         if (C.empty()) return;
         const double eps = cfg.eps * 0.5;  // arithmetic tolerance, acr.hpp:178-181
         Plan* P = plan(C[0].node, A[0].node, B[0].node, alpha);
-        for (size_t i0 = 0; i0 < C.size(); i0 += MAXB) {
+        // Planes per batch.  Up to C2-sized planes (dim <= 4096) the transient arena holds
+        // MAXB planes (8.9 GB peak measured at C2).  Larger planes (C5: 16384) size the batch
+        // from the plan's measured transient use per plane: the first batch of a plan at each
+        // level runs one plane and synchronises to read the arena counter.
+        const bool adaptive = S.dim > 4096;
+        for (size_t i0 = 0; i0 < C.size();) {
             BatchViews bv{};
-            const int nb = (int)std::min<size_t>(MAXB, C.size() - i0);
+            int chunk = MAXB;
+            bool measure = false;
+            if (adaptive) {
+                if (P->pp_gb < 0 || P->pp_level != level_tag) {
+                    measure = true;
+                    chunk = P->pp_gb < 0 ? 1 : batch_for(P->pp_gb);
+                } else {
+                    chunk = batch_for(P->pp_gb);
+                }
+            }
+            const int nb = (int)std::min<size_t>(chunk, C.size() - i0);
             bv.count = nb;
             for (int b = 0; b < nb; ++b) {
                 bv.c[b] = hview(C[i0 + b]);
@@ -689,7 +711,34 @@ struct Engine {
             for (auto& ph : P->bb) run_trunc(ph, P->parts, slots, nb, eps, nullptr, nullptr, false, tr, bv);
             launch_deposit(st(), P->ndep, P->deps, P->parts, slots, nb, ctx->flops, bv);
             run_trunc(P->flush, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->persist, bv);
+            if (measure) {
+                unsigned long long used = 0;
+                CK(cudaStreamSynchronize(st()));
+                CK(cudaMemcpy(&used, tr.ctr, sizeof(used), cudaMemcpyDeviceToHost));
+                P->pp_gb = std::max(P->pp_gb, used * 8.0 / 1e9 / nb);
+                P->pp_level = level_tag;
+                if (getenv("ACRGPU_VERBOSE"))
+                    fprintf(stderr, "[acrgpu] plan nodes (%d,%d,%d) level %d: %.3f GB transient per plane -> batch %d\n",
+                            C[0].node, A[0].node, B[0].node, level_tag, P->pp_gb, batch_for(P->pp_gb));
+            }
+            static const bool arena_stats = getenv("ACRGPU_ARENA_STATS") != nullptr;
+            if (arena_stats) {  // debugging aid: peak transient use per batch (synchronises)
+                unsigned long long used = 0;
+                CK(cudaStreamSynchronize(st()));
+                CK(cudaMemcpy(&used, tr.ctr, sizeof(used), cudaMemcpyDeviceToHost));
+                const double gb = used * 8.0 / 1e9;
+                if (gb > peak_transient_gb) peak_transient_gb = gb;
+                peak_transient_per_plane_gb = std::max(peak_transient_per_plane_gb, gb / nb);
+            }
+            i0 += nb;
         }
+    }
+    // planes per batch for a plan using pp_gb of transient arena per plane (half the lane's
+    // arena: ranks grow with the level after the measurement)
+    int batch_for(double pp_gb) const {
+        const double cap_gb = ctx->lanes[0].trans.cap * 8.0 / 1e9;
+        const double b = 0.5 * cap_gb / std::max(pp_gb, 1e-6);
+        return (int)std::max(1.0, std::min((double)MAXB, std::floor(b)));
     }
 
     // Run two independent operations concurrently: f0 on lane 0, f1 on lane 1 (both issued
@@ -1321,6 +1370,7 @@ static void mark_level(PartRun& R) {
 // Step 1 of reduce_level (acr.cpp:70-120): invert the owned eliminated planes (batched).
 static Level level_invert(PartRun& R, int lvl, const std::vector<char>& mine_pos) {
     Engine& E = *R.F->eng;
+    E.level_tag = lvl;
     const int m = (int)R.D.size();
     Level L;
     L.plane_count = m;
@@ -1449,6 +1499,7 @@ static void level_update(PartRun& R, Level& L, const std::vector<char>& mine_pos
 static void factor_apex(PartRun& R, int lvl) {
     acrgpu_fact* F = R.F;
     Engine& E = *F->eng;
+    E.level_tag = lvl;
     const int s = (int)R.D.size();
     F->apexE = R.Ev;
     F->apexF = R.Fv;
@@ -1471,6 +1522,13 @@ static void factor_finish(PartRun& R) {
     acrgpu_fact* F = R.F;
     Engine& E = *F->eng;
     mark_level(R);
+    if (getenv("ACRGPU_ARENA_STATS")) {
+        unsigned long long used = 0;
+        CK(cudaMemcpy(&used, E.ctx->persist.ctr, sizeof(used), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[acrgpu] rank %d arena peak transient %.3f GB (%.4f GB / plane), persistent %.3f GB of %.3f\n",
+                R.rank, E.peak_transient_gb, E.peak_transient_per_plane_gb, used * 8.0 / 1e9,
+                E.ctx->persist.cap * 8.0 / 1e9);
+    }
     check_device_errors(F);
     if (verbose_levels()) {
         for (size_t i = 1; i < R.lev_ev.size(); ++i) {

@@ -221,92 +221,6 @@ __device__ int rank_of(const double* sig, const int* order, int n, double eps, d
     return r;
 }
 
-// ------------------------------------------------------------------ Householder QR
-// In-place unpivoted Householder QR of W (rows x cols, ld): R in the upper
-// trapezoid, essential reflector parts below the diagonal, tau[j].  Eigen
-// HouseholderQR conventions (hmatrix.cpp:62-63): beta = -sign(c0)||x||, tau = 0
-// when the sub-diagonal tail is exactly zero.
-template <int NTH = NT>
-__device__ void householder_qr(double* W, int ld, int rows, int cols, double* tau, double* red) {
-    constexpr int NW = NTH / 32;
-    const int kmax = rows < cols ? rows : cols;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ double sh_beta, sh_tau, sh_inv;
-    for (int j = 0; j < kmax; ++j) {
-        double* wj = W + (size_t)j * ld;
-        double part = 0;
-        for (int i = j + 1 + threadIdx.x; i < rows; i += NTH) part = fma(wj[i], wj[i], part);
-        part = warp_sum(part);
-        __syncthreads();
-        if (lane == 0) red[warp] = part;
-        __syncthreads();
-        double tail = 0;
-        for (int q = 0; q < NW; ++q) tail += red[q];
-        if (threadIdx.x == 0) {
-            const double c0 = wj[j];
-            if (tail <= DBL_MIN) {
-                sh_tau = 0.0;
-                sh_beta = c0;
-                sh_inv = 0.0;
-            } else {
-                double beta = sqrt(c0 * c0 + tail);
-                if (c0 >= 0) beta = -beta;
-                sh_inv = 1.0 / (c0 - beta);
-                sh_tau = (beta - c0) / beta;
-                sh_beta = beta;
-            }
-            tau[j] = sh_tau;
-        }
-        __syncthreads();
-        const double tj = sh_tau, inv = sh_inv;
-        if (tj == 0.0) {
-            for (int i = j + 1 + threadIdx.x; i < rows; i += NTH) wj[i] = 0.0;
-        } else {
-            for (int i = j + 1 + threadIdx.x; i < rows; i += NTH) wj[i] *= inv;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) wj[j] = sh_beta;
-        if (tj != 0.0) {
-            for (int c = j + 1 + warp; c < cols; c += NW) {
-                double* wc = W + (size_t)c * ld;
-                double s = 0;
-                #pragma unroll 4
-                for (int i = j + 1 + lane; i < rows; i += 32) s = fma(wj[i], wc[i], s);
-                s = warp_sum(s) + wc[j];
-                s *= tj;
-                if (lane == 0) wc[j] -= s;
-                #pragma unroll 4
-                for (int i = j + 1 + lane; i < rows; i += 32) wc[i] -= s * wj[i];
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// Y (rows x ncol, ld) <- Q Y with Q = H_0 H_1 ... H_{k-1} from householder_qr(W).
-template <int NTH = NT>
-__device__ void apply_q(const double* W, int ldw, int rows, int k, const double* tau, double* Y, int ldy, int ncol) {
-    constexpr int NW = NTH / 32;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = k - 1; j >= 0; --j) {
-        const double tj = tau[j];
-        if (tj != 0.0) {
-            const double* v = W + (size_t)j * ldw;
-            for (int c = warp; c < ncol; c += NW) {
-                double* y = Y + (size_t)c * ldy;
-                double s = 0;
-                #pragma unroll 4
-                for (int i = j + 1 + lane; i < rows; i += 32) s = fma(v[i], y[i], s);
-                s = (warp_sum(s) + y[j]) * tj;
-                if (lane == 0) y[j] -= s;
-                #pragma unroll 4
-                for (int i = j + 1 + lane; i < rows; i += 32) y[i] -= s * v[i];
-            }
-        }
-        __syncthreads();
-    }
-}
-
 // ------------------------------------------------------------------ part resolution
 struct PartRes {
     const double* U;
@@ -450,7 +364,7 @@ struct TruncArgs {
 // tile (rows ty + GY i, columns tx + 16 j); k is staged through `stage`.
 template <int NTH, int TM, int TN, bool TRI = false>
 __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, const double* B, int ldb, int ru, int rv, int k,
-                              double alpha, double* stage, int stage_doubles) {
+                              double alpha, double* stage, int stage_doubles, int ra0 = 0, int rb0 = 0) {
     constexpr int GX = 16, GY = NTH / GX;
     constexpr int RA = GY * TM, RB = GX * TN;
     int KC = stage_doubles / (RA + RB);
@@ -468,11 +382,11 @@ __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, cons
         __syncthreads();
         for (int e = threadIdx.x; e < RA * kc; e += NTH) {
             const int i = e % RA, t = e / RA;
-            As[i + t * RA] = (i < ru && (!TRI || i <= t0 + t)) ? A[i + (size_t)(t0 + t) * lda] : 0.0;
+            As[i + t * RA] = (i < ru && (!TRI || ra0 + i <= t0 + t)) ? A[i + (size_t)(t0 + t) * lda] : 0.0;
         }
         for (int e = threadIdx.x; e < RB * kc; e += NTH) {
             const int i = e % RB, t = e / RB;
-            Bs[i + t * RB] = (i < rv && (!TRI || i <= t0 + t)) ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
+            Bs[i + t * RB] = (i < rv && (!TRI || rb0 + i <= t0 + t)) ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
         }
         __syncthreads();
         for (int t = 0; t < kc; ++t) {
@@ -596,13 +510,15 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
     const int pmax = ku > kv ? ku : kv;
     const bool core_in_smem = pmax <= DMAX;
     const size_t smem_doubles = (size_t)DMAX * DMAX + (size_t)DMAX * RPCAP + (size_t)RPCAP * RPCAP + 5 * DMAX;
-    const bool blocked = bqr_smem_doubles(m > n ? m : n, K) <= smem_doubles;
+    // blocked QR staging (panel, W, T) in shared memory, or in global workspace for panels too
+    // tall for it (C5's 2048-row leaves)
+    const size_t bneed = bqr_smem_doubles(m > n ? m : n, K);
+    const bool blocked = bneed <= smem_doubles;
     const int npan = (K + BQR_NB - 1) / BQR_NB + 1;
-    if (threadIdx.x == 0) {
-        unsigned long long need = (unsigned long long)(m + n) * K + 2ull * K + 32 + 2ull * npan * BQR_NB * BQR_NB;
-        if (!core_in_smem) need += 3ull * pmax * pmax + 6ull * pmax + 64;
-        sh_ws = arena_alloc(args.work, need);
-    }
+    const unsigned long long base_need =
+        (unsigned long long)(m + n) * K + 2ull * K + 32 + 2ull * npan * BQR_NB * BQR_NB;
+    const unsigned long long core_need = core_in_smem ? 0ull : 3ull * pmax * pmax + 6ull * pmax + 64;
+    if (threadIdx.x == 0) sh_ws = arena_alloc(args.work, base_need + core_need + (blocked ? 0ull : bneed));
     __syncthreads();
     double* ws = sh_ws;
     if (ws == nullptr) return;  // arena exhausted: flag raised, target left unchanged
@@ -643,13 +559,10 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
     }
     __syncthreads();
     PHASE_MARK(0);
-    if (blocked) {
-        bqr<NTH>(Uc, m, m, K, tau_u, Tu, smem, smem_doubles);
-        bqr<NTH>(Vc, n, n, K, tau_v, Tv, smem, smem_doubles);
-    } else {
-        householder_qr<NTH>(Uc, m, m, K, tau_u, red);
-        householder_qr<NTH>(Vc, n, n, K, tau_v, red);
-    }
+    double* qs = blocked ? smem : ws + base_need + core_need;
+    const size_t qs_doubles = blocked ? smem_doubles : bneed;
+    bqr<NTH>(Uc, m, m, K, tau_u, Tu, qs, qs_doubles);
+    bqr<NTH>(Vc, n, n, K, tau_v, Tv, qs, qs_doubles);
     PHASE_MARK(1);
     // core = Ru Rv^T (ku x kv)
     double* core = w.A;
@@ -658,14 +571,15 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
         for (int e = threadIdx.x; e < ku * kv; e += NTH) core[e] = 0.0;
         gemm_nt_tiled<NTH, DMAX * 16 / NTH, DMAX / 16, true>(core, ku, Uc, m, Vc, n, ku, kv, K, 1.0, w.W,
                                                                DMAX * RPCAP + RPCAP * RPCAP);
-    } else {
-        for (int e = threadIdx.x; e < ku * kv; e += NTH) {
-            const int i = e % ku, j = e / ku;
-            double acc = 0;
-            for (int t = (i > j ? i : j); t < K; ++t) acc = fma(Uc[i + (size_t)t * m], Vc[j + (size_t)t * n], acc);
-            core[e] = acc;
-        }
+    } else {  // core in global workspace: 128 x 128 output tiles
+        for (size_t e = threadIdx.x; e < (size_t)ku * kv; e += NTH) core[e] = 0.0;
         __syncthreads();
+        for (int r0 = 0; r0 < ku; r0 += DMAX)
+            for (int c0 = 0; c0 < kv; c0 += DMAX)
+                gemm_nt_tiled<NTH, DMAX * 16 / NTH, DMAX / 16, true>(core + r0 + (size_t)c0 * ku, ku, Uc + r0, m,
+                                                                       Vc + c0, n, min(DMAX, ku - r0),
+                                                                       min(DMAX, kv - c0), K, 1.0, smem,
+                                                                       DMAX * RPCAP + RPCAP * RPCAP, r0, c0);
     }
     PHASE_MARK(2);
     int rp;
@@ -687,13 +601,8 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
             __syncthreads();
             cta_trunc_write<NTH>(w, ku, kv, rp, r, Uo, m, Vo, n);
             PHASE_MARK(4);
-            if (blocked) {
-                bqr_apply<NTH>(Uc, m, m, ku, Tu, Uo, m, r, smem, smem_doubles);
-                bqr_apply<NTH>(Vc, n, n, kv, Tv, Vo, n, r, smem, smem_doubles);
-            } else {
-                apply_q<NTH>(Uc, m, m, ku, tau_u, Uo, m, r);
-                apply_q<NTH>(Vc, n, n, kv, tau_v, Vo, n, r);
-            }
+            bqr_apply<NTH>(Uc, m, m, ku, Tu, Uo, m, r, qs, qs_doubles);
+            bqr_apply<NTH>(Vc, n, n, kv, Tv, Vo, n, r, qs, qs_doubles);
             PHASE_MARK(5);
         }
         write_out(out ? r : 0, out, out ? out + (size_t)m * r : nullptr);
@@ -1745,6 +1654,15 @@ struct ProfScope {
         }
     }
     ~ProfScope() {
+        static const bool dbg = getenv("ACRGPU_DEBUG_SYNC") != nullptr;
+        if (dbg) {  // debugging aid: attribute launch / execution errors to the kernel
+            cudaError_t e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) {
+                fprintf(stderr, "[acrgpu] %s (%ld CTAs): %s\n", name, ctas, cudaGetErrorString(e));
+                abort();
+            }
+        }
         if (a) {
             cudaEvent_t b;
             cudaEventCreate(&b);
@@ -1821,7 +1739,8 @@ void setup_kernels() {
     cudaFuncSetAttribute(k_truncate<64, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
     cudaFuncSetAttribute(k_truncate<BIG_DMAX, BIG_RPCAP, BIG_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_big());
     cudaFuncSetAttribute(k_dd_product, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
-    cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((2 * DENSE_MAX * DENSE_MAX + 2 * DENSE_MAX) * sizeof(double)));
     cudaFuncSetAttribute(k_sigma1_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
 }
 

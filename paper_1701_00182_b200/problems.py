@@ -298,6 +298,19 @@ def helmholtz7(n: int, seed: int, omega: float = 2 * math.pi * 6.4, nrhs: int = 
                            f"helmholtz{n}")
 
 
+def first_planes(sysm: System, k: int) -> System:
+    """The first k planes of a system (its leading k x k block sub-system: D_0..D_{k-1},
+    E_1..E_{k-1}, F_0..F_{k-2}, rhs planes 0..k-1).  Used to exercise a configuration's
+    full plane size (e.g. C5's 16384-point planes, leaf 64) with fewer planes."""
+    if not 1 <= k <= sysm.n:
+        raise ValueError("first_planes: need 1 <= k <= n")
+    n = sysm.n
+    blocks = [sysm.block(j) for j in range(k)]
+    blocks += [sysm.block(n + j - 1) for j in range(1, k)]
+    blocks += [sysm.block(2 * n - 1 + j) for j in range(k - 1)]
+    return _assemble(k, sysm.dim, sysm.coords, blocks, sysm.rhs[:, :k], f"{sysm.name}[:{k}]")
+
+
 #: BASELINE.json configs (1-based).  ``n`` may be overridden for parity-size runs.
 CONFIGS = {
     1: dict(kind="poisson", n=32, leaf=32, eps=1e-6, nrhs=1),

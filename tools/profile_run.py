@@ -5,7 +5,10 @@ from paper_1701_00182_b200 import acr, problems as P
 cfgk = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 n = int(sys.argv[2]) if len(sys.argv) > 2 else None
 exact = len(sys.argv) > 3 and sys.argv[3] == "exact"
+planes = int(os.environ.get("PLANES", "0"))
 sysm = P.config_system(cfgk, n=n)
+if planes:
+    sysm = P.first_planes(sysm, planes)
 c = P.CONFIGS[cfgk]
 cfg = acr.AcrConfig(eps=c["eps"], leaf_size=c["leaf"], exact_dense_products=exact)
 acr.default_context()
