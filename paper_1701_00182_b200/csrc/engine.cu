@@ -112,8 +112,13 @@ struct Ctx {
         // persistent arena (stored factors) 38%, one transient arena per lane 2 x 20%; the rest
         // (cudaMallocAsync: dense pools of the stored blocks, solve workspace) stays free.
         // C5-sized planes (16384 points) need ~13-15 GB of transient arena for one root product.
-        const size_t pbytes = (size_t)(freeb * 0.38) & ~(size_t)4095;
-        const size_t tbytes = ((size_t)(freeb * 0.40) / NLANES) & ~(size_t)4095;
+        auto frac = [](const char* name, double dflt) {
+            const char* v = getenv(name);
+            const double f = v ? atof(v) : dflt;
+            return (f > 0.0 && f < 0.9) ? f : dflt;
+        };
+        const size_t pbytes = (size_t)(freeb * frac("ACRGPU_PERSIST_FRAC", 0.38)) & ~(size_t)4095;
+        const size_t tbytes = ((size_t)(freeb * frac("ACRGPU_TRANS_FRAC", 0.40)) / NLANES) & ~(size_t)4095;
         persist_base = dmalloc<double>(pbytes / 8);
         trans_base = dmalloc<double>(NLANES * tbytes / 8);
         ctrs = dmalloc<unsigned long long>(1 + NLANES);
@@ -1360,6 +1365,17 @@ static bool verbose_levels() {
 }
 
 static void mark_level(PartRun& R) {
+    static const bool arena_stats = getenv("ACRGPU_ARENA_STATS") != nullptr;
+    if (arena_stats) {  // debugging aid (synchronises): arena and free-memory use per level
+        Engine& E = *R.F->eng;
+        unsigned long long used = 0;
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(&used, E.ctx->persist.ctr, sizeof(used), cudaMemcpyDeviceToHost));
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        fprintf(stderr, "[acrgpu] rank %d mark %zu: persistent %.2f / %.2f GB, peak transient %.2f GB, device free %.2f GB\n",
+                R.rank, R.lev_ev.size(), used * 8.0 / 1e9, E.ctx->persist.cap * 8.0 / 1e9, E.peak_transient_gb, fr / 1e9);
+    }
     if (!verbose_levels()) return;
     cudaEvent_t e;
     CK(cudaEventCreate(&e));

@@ -1607,6 +1607,26 @@ struct ProfRec {
     long ctas;
 };
 static std::vector<ProfRec> g_prof;
+// recycled timing events (no create/destroy per launch), per device
+static std::map<int, std::vector<cudaEvent_t>> g_ev_pool;
+static cudaEvent_t ev_get() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto& pool = g_ev_pool[dev];
+    cudaEvent_t e;
+    if (!pool.empty()) {
+        e = pool.back();
+        pool.pop_back();
+    } else {
+        cudaEventCreate(&e);
+    }
+    return e;
+}
+static void ev_put(cudaEvent_t e) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    g_ev_pool[dev].push_back(e);
+}
 static std::vector<std::string> g_kernel_names;
 static FlopLedger* g_report_ledger = nullptr;  // device ledgers [MAX_KERNELS] of the active context
 int kernel_id(const char* name) {
@@ -1649,7 +1669,7 @@ struct ProfScope {
     ProfScope(cudaStream_t s, const char* n, long c) : st(s), name(n), ctas(c) {
         ++g_launches;
         if (prof_on()) {
-            cudaEventCreate(&a);
+            a = ev_get();
             cudaEventRecord(a, st);
         }
     }
@@ -1664,8 +1684,7 @@ struct ProfScope {
             }
         }
         if (a) {
-            cudaEvent_t b;
-            cudaEventCreate(&b);
+            cudaEvent_t b = ev_get();
             cudaEventRecord(b, st);
             g_prof.push_back({name, a, b, ctas});
         }
@@ -1683,8 +1702,8 @@ void prof_flush() {
         std::get<0>(acc) += ms;
         std::get<1>(acc) += 1;
         std::get<2>(acc) += r.ctas;
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
+        ev_put(r.a);
+        ev_put(r.b);
     }
     g_prof.clear();
     std::sort(g_top.begin(), g_top.end(), [](const auto& x, const auto& y) { return std::get<0>(x) > std::get<0>(y); });
