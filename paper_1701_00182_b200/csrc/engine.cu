@@ -31,6 +31,7 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/acrgpu.h"
@@ -87,7 +88,10 @@ struct Ctx {
     Lane lanes[NLANES];
     int cur = 0;                // active lane
     Arena persist{};
-    double* persist_base = nullptr;
+    double* persist_base = nullptr;     // two semi-spaces of persist_half doubles each
+    size_t persist_half = 0;
+    int space = 0;                      // semi-space the persistent arena allocates from
+    int factoring = 0;                  // factorizations in progress on this context
     double* trans_base = nullptr;
     unsigned long long* ctrs = nullptr;  // [0] persist, [1 + l] transient of lane l
     int* overflow = nullptr;
@@ -109,24 +113,28 @@ struct Ctx {
         setup_kernels();
         size_t freeb = 0, total = 0;
         CK(cudaMemGetInfo(&freeb, &total));
-        // persistent arena (stored factors) 38%, one transient arena per lane 2 x 20%; the rest
-        // (cudaMallocAsync: dense pools of the stored blocks, solve workspace) stays free.
-        // C5-sized planes (16384 points) need ~13-15 GB of transient arena for one root product.
+        // persistent arena (flush outputs) 50% as two semi-spaces, one transient arena per lane
+        // 2 x 11%; the rest (cudaMallocAsync: dense pools of the stored blocks, solve workspace)
+        // stays free.  Small systems use one semi-space; C5-sized planes (16384 points)
+        // compact their live low-rank data into the other when one fills (Engine::gc).
+        // One C5 root product needs ~7 GB of transient arena per plane.
         auto frac = [](const char* name, double dflt) {
             const char* v = getenv(name);
             const double f = v ? atof(v) : dflt;
             return (f > 0.0 && f < 0.9) ? f : dflt;
         };
-        const size_t pbytes = (size_t)(freeb * frac("ACRGPU_PERSIST_FRAC", 0.38)) & ~(size_t)4095;
-        const size_t tbytes = ((size_t)(freeb * frac("ACRGPU_TRANS_FRAC", 0.40)) / NLANES) & ~(size_t)4095;
-        persist_base = dmalloc<double>(pbytes / 8);
+        const size_t pbytes = ((size_t)(freeb * frac("ACRGPU_PERSIST_FRAC", 0.50)) / 2) & ~(size_t)4095;
+        const size_t tbytes = ((size_t)(freeb * frac("ACRGPU_TRANS_FRAC", 0.22)) / NLANES) & ~(size_t)4095;
+        persist_half = pbytes / 8;
+        persist_base = dmalloc<double>(2 * persist_half);
         trans_base = dmalloc<double>(NLANES * tbytes / 8);
         ctrs = dmalloc<unsigned long long>(1 + NLANES);
         overflow = dmalloc<int>(1 + NLANES);
         err = dmalloc<DevError>(1);
         flops = dmalloc<FlopLedger>(MAX_KERNELS);
         set_report_ledger(flops);
-        persist = Arena{persist_base, pbytes / 8, ctrs, overflow};
+        space = 0;
+        persist = Arena{persist_base, persist_half, ctrs, overflow};
         for (int l = 0; l < NLANES; ++l)
             lanes[l].trans = Arena{trans_base + (size_t)l * (tbytes / 8), tbytes / 8, ctrs + 1 + l, overflow + 1 + l};
         reset_all();
@@ -151,6 +159,11 @@ struct Ctx {
         call_id = 0;
         call_planes.clear();
         cur = 0;
+    }
+    double* other_space() const { return persist_base + (size_t)(1 - space) * persist_half; }
+    void swap_space() {
+        space = 1 - space;
+        persist.base = persist_base + (size_t)space * persist_half;
     }
     Slot* get_slots(size_t n) {
         Lane& l = lane();
@@ -246,6 +259,11 @@ struct Engine {
     double peak_transient_gb = 0, peak_transient_per_plane_gb = 0;  // ACRGPU_ARENA_STATS
     int level_tag = 0;  // current cyclic-reduction level (adaptive batching)
     std::map<std::tuple<int, int, int, int>, std::unique_ptr<Plan>> plans;
+    // every live Store of this engine (compaction of the persistent arena, gc())
+    std::shared_ptr<std::unordered_set<Store*>> live = std::make_shared<std::unordered_set<Store*>>();
+    bool in_pair = false;
+    double gc_next = 0.6;  // compaction threshold (fraction of a semi-space)
+    int gc_count = 0;
     std::vector<void*> dev_allocs;  // plan arrays etc.
 
     // structure-wide device tables
@@ -321,7 +339,9 @@ struct Engine {
         s->V = s->U + nk;
         s->rank = (int*)(s->V + nk);
         cudaStream_t stream = main_st();
-        return StoreP(s.get(), [s, stream](Store*) mutable {
+        live->insert(s.get());
+        return StoreP(s.get(), [s, stream, reg = live](Store*) mutable {
+            reg->erase(s.get());
             if (s->block) cudaFreeAsync(s->block, stream);
             s->block = nullptr;
         });
@@ -679,6 +699,7 @@ struct Engine {
     void mult_add(const std::vector<View>& C, const std::vector<View>& A, const std::vector<View>& B, double alpha) {
         if (C.empty()) return;
         const double eps = cfg.eps * 0.5;  // arithmetic tolerance, acr.hpp:178-181
+        gc_check();
         Plan* P = plan(C[0].node, A[0].node, B[0].node, alpha);
         // Planes per batch.  Up to C2-sized planes (dim <= 4096) the transient arena holds
         // MAXB planes (8.9 GB peak measured at C2).  Larger planes (C5: 16384) size the batch
@@ -692,7 +713,8 @@ struct Engine {
             if (adaptive) {
                 if (P->pp_gb < 0 || P->pp_level != level_tag) {
                     measure = true;
-                    chunk = P->pp_gb < 0 ? 1 : batch_for(P->pp_gb);
+                    // new plan, or a new level (ranks grew): measure on a conservative batch
+                    chunk = P->pp_gb < 0 ? 1 : batch_for(3.0 * P->pp_gb);
                 } else {
                     chunk = batch_for(P->pp_gb);
                 }
@@ -738,6 +760,113 @@ struct Engine {
             i0 += nb;
         }
     }
+    // -------------------------------------------------------------- persistent-arena compaction
+    // Flush outputs are bump-allocated and never freed inside a factorization; at C5 that is
+    // ~100 GB, ~4x the live low-rank data (temporaries of invert_node, superseded leaf
+    // factors).  For C5-sized planes, when the current semi-space passes gc_next, every live
+    // store's U/V is copied into the other semi-space (k_compact, repointing the store's
+    // tables) and allocation continues there.  Safe point: entry of a mult_add outside
+    // pair() with both lanes drained -- no product slot or in-flight kernel holds an arena
+    // pointer.  Results are unchanged (copies are bitwise).  Only one factorization may be in
+    // progress on the context (in-process ranks share it, so they never compact).
+    // ACRGPU_GC_FORCE=<fraction>: compact at any size once the semi-space is that full
+    // (tests: 0 compacts at every safe point); ACRGPU_NO_GC disables compaction.
+    bool gc_enabled() const {
+        if (ctx->factoring != 1 || getenv("ACRGPU_NO_GC")) return false;
+        return S.dim > 4096 || getenv("ACRGPU_GC_FORCE");
+    }
+    void gc_check() {
+        if (in_pair || ctx->cur != 0 || !gc_enabled()) return;
+        for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.st));
+        unsigned long long used = 0;
+        CK(cudaMemcpy(&used, ctx->persist.ctr, sizeof(used), cudaMemcpyDeviceToHost));
+        const char* force = getenv("ACRGPU_GC_FORCE");
+        const double at = force ? atof(force) : gc_next;
+        if (used == 0 || (double)used < at * (double)ctx->persist.cap) return;
+        gc();
+    }
+    void gc() {
+        cudaStream_t s0 = main_st();
+        ensure_kmn_tables();
+        std::map<int, std::vector<Store*>> by_node;
+        for (Store* st : *live)
+            if (st->block) by_node[st->node].push_back(st);
+        struct Group {
+            int node, nk;
+            std::vector<Store*> ss;
+            std::vector<int> ranks;
+        };
+        std::vector<Group> groups;
+        for (auto& [node, ss] : by_node) {
+            const SNode& N = S.node(node);
+            Group g{node, N.k1 - N.k0, ss, {}};
+            if (g.nk == 0) continue;
+            g.ranks.resize((size_t)ss.size() * g.nk);
+            for (size_t i = 0; i < ss.size(); ++i)
+                CK(cudaMemcpyAsync(g.ranks.data() + i * g.nk, ss[i]->rank, g.nk * sizeof(int), cudaMemcpyDeviceToHost, s0));
+            groups.push_back(std::move(g));
+        }
+        CK(cudaStreamSynchronize(s0));
+        double* base = ctx->other_space();
+        unsigned long long total = 0;
+        std::vector<void*> tmp;
+        for (auto& g : groups) {
+            const SNode& N = S.node(g.node);
+            std::vector<long> off(g.ranks.size(), -1);
+            for (size_t i = 0; i < g.ss.size(); ++i)
+                for (int k = 0; k < g.nk; ++k) {
+                    const int r = g.ranks[i * g.nk + k];
+                    if (r <= 0) continue;
+                    const SNode& L = S.node(S.k_node[N.k0 + k]);
+                    off[i * g.nk + k] = (long)total;
+                    total += (unsigned long long)(L.rows() + L.cols()) * r;
+                    total = (total + 15) & ~15ull;  // 128-byte granules, as arena_alloc
+                }
+            if (total > ctx->persist_half)
+                throw AcrError{ACRGPU_E_DEVICE, "device arena exhausted (persistent, live data after compaction); "
+                                                "factorization too large for this GPU"};
+            std::vector<double**> Ut, Vt;
+            std::vector<int*> Rt;
+            for (Store* st : g.ss) {
+                Ut.push_back(st->U);
+                Vt.push_back(st->V);
+                Rt.push_back(st->rank);
+            }
+            long* d_off = upload(off, s0);
+            double*** d_U = upload(Ut, s0);
+            double*** d_V = upload(Vt, s0);
+            int** d_R = upload(Rt, s0);
+            tmp.insert(tmp.end(), {(void*)d_off, (void*)d_U, (void*)d_V, (void*)d_R});
+            for (size_t s_0 = 0; s_0 < g.ss.size(); s_0 += 65535) {
+                const int cnt = (int)std::min<size_t>(65535, g.ss.size() - s_0);
+                CompactArgs a{base, d_off + s_0 * g.nk, d_U + s_0, d_V + s_0, d_R + s_0, d_km + N.k0, d_kn + N.k0, g.nk, 1};
+                launch_compact(s0, a, cnt);
+            }
+        }
+        CK(cudaMemcpyAsync(ctx->persist.ctr, &total, sizeof(total), cudaMemcpyHostToDevice, s0));
+        CK(cudaStreamSynchronize(s0));
+        for (void* p : tmp) cudaFree(p);
+        ctx->swap_space();
+        ++gc_count;
+        const double live_frac = (double)total / (double)ctx->persist.cap;
+        gc_next = std::min(0.9, std::max(0.6, live_frac + 0.3));
+        if (getenv("ACRGPU_VERBOSE"))
+            fprintf(stderr, "[acrgpu] compaction %d (level %d): %zu stores, live %.2f GB of %.2f GB semi-space\n", gc_count,
+                    level_tag, live->size(), total * 8.0 / 1e9, ctx->persist.cap * 8.0 / 1e9);
+    }
+    void ensure_kmn_tables() {
+        if (d_km) return;
+        const int nk = S.n_rk();
+        std::vector<int> km(std::max(nk, 1)), kn(std::max(nk, 1));
+        for (int k = 0; k < nk; ++k) {
+            const SNode& L = S.node(S.k_node[k]);
+            km[k] = L.rows();
+            kn[k] = L.cols();
+        }
+        d_km = up(km);
+        d_kn = up(kn);
+    }
+
     // planes per batch for a plan using pp_gb of transient arena per plane (half the lane's
     // arena: ranks grow with the level after the measurement)
     int batch_for(double pp_gb) const {
@@ -755,11 +884,14 @@ struct Engine {
             f1();
             return;
         }
+        gc_check();  // safe point before both lanes start
         ctx->depend(1, 0);
+        in_pair = true;
         f0();
         ctx->cur = 1;
         f1();
         ctx->cur = 0;
+        in_pair = false;
         ctx->depend(0, 1);
     }
 
@@ -1545,8 +1677,8 @@ static void factor_finish(PartRun& R) {
                 R.rank, E.peak_transient_gb, E.peak_transient_per_plane_gb, used * 8.0 / 1e9,
                 E.ctx->persist.cap * 8.0 / 1e9);
     }
-    check_device_errors(F);
     if (verbose_levels()) {
+        CK(cudaDeviceSynchronize());
         for (size_t i = 1; i < R.lev_ev.size(); ++i) {
             float ms = 0;
             cudaEventElapsedTime(&ms, R.lev_ev[i - 1], R.lev_ev[i]);
@@ -1555,6 +1687,7 @@ static void factor_finish(PartRun& R) {
         for (auto e : R.lev_ev) cudaEventDestroy(e);
         R.lev_ev.clear();
     }
+    check_device_errors(F);
     compact_factor(F);
     cudaEvent_t e2;
     CK(cudaEventCreate(&e2));
@@ -1583,7 +1716,16 @@ static void factor_finish(PartRun& R) {
     cudaEventDestroy(e2);
 }
 
+// ctx->factoring while a factorization runs (the persistent arena may only be compacted
+// when a single one is in progress)
+struct FactoringScope {
+    Ctx* c;
+    explicit FactoringScope(Ctx* x) : c(x) { ++c->factoring; }
+    ~FactoringScope() { --c->factoring; }
+};
+
 static void do_factor(acrgpu_fact* F, const DSys& sys) {
+    FactoringScope fs(F->eng->ctx);
     PartRun R;
     R.F = F;
     factor_begin(R, sys, nullptr);
@@ -1657,18 +1799,7 @@ static ImageLayout image_layout(size_t nk, size_t dsize, size_t lr) {
     return L;
 }
 
-static void ensure_kmn(Engine& E) {
-    if (E.d_km) return;
-    const int nk = E.S.n_rk();
-    std::vector<int> km(std::max(nk, 1)), kn(std::max(nk, 1));
-    for (int k = 0; k < nk; ++k) {
-        const SNode& L = E.S.node(E.S.k_node[k]);
-        km[k] = L.rows();
-        kn[k] = L.cols();
-    }
-    E.d_km = E.up(km);
-    E.d_kn = E.up(kn);
-}
+static void ensure_kmn(Engine& E) { E.ensure_kmn_tables(); }
 
 static StoreImage pack_store(Engine& E, const SP& s) {
     cudaStream_t st = E.main_st();
@@ -1733,7 +1864,9 @@ static SP adopt_image(Engine& E, StoreImage im) {
     s->U = (double**)(im.buf + L.ptrs);
     s->V = s->U + nk;
     s->rank = (int*)(im.buf + L.irank);
-    return StoreP(s.get(), [s, st](Store*) mutable {
+    E.live->insert(s.get());
+    return StoreP(s.get(), [s, st, reg = E.live](Store*) mutable {
+        reg->erase(s.get());
         if (s->block) cudaFreeAsync(s->block, st);
         s->block = nullptr;
     });
@@ -1880,6 +2013,8 @@ struct NcclTransport : Transport {
 // ------------------------------------------------------------------ partitioned factor
 static void factor_partitioned(std::vector<PartRun>& runs, const std::vector<std::vector<int>>& own, Transport& T,
                                const DSys& sys) {
+    std::vector<std::unique_ptr<FactoringScope>> fscopes;
+    for (auto& R : runs) fscopes.push_back(std::make_unique<FactoringScope>(R.F->eng->ctx));
     for (auto& R : runs) factor_begin(R, sys, &own);
     const int stop = runs[0].F->eng->cfg.stop_planes;
     if (stop != 1) throw AcrError{ACRGPU_E_USAGE, "partitioned factor: stop_planes must be 1"};

@@ -139,6 +139,24 @@ def test_factorization_deterministic(acr):
     assert np.array_equal(u1, u2)
 
 
+@pytest.mark.parametrize("at", ["0", "0.000001"])
+def test_persistent_arena_compaction_is_bitwise_neutral(acr, monkeypatch, at):
+    # Engine::gc (C5-sized planes compact live low-rank data into the other semi-space of the
+    # persistent arena) forced at small size: every safe point ("0") or once past a tiny fill.
+    sysm = P.config_system(2, n=12)
+    cfg = acr.AcrConfig(eps=1e-6)
+    f1 = acr.acr_factor(sysm, cfg)
+    u1 = f1.solve(sysm.rhs)
+    monkeypatch.setenv("ACRGPU_GC_FORCE", at)
+    f2 = acr.acr_factor(sysm, cfg)
+    u2 = f2.solve(sysm.rhs)
+    monkeypatch.delenv("ACRGPU_GC_FORCE")
+    assert np.array_equal(u1, u2)
+    s1, s2 = f1.inverse_rank_stats(), f2.inverse_rank_stats()
+    assert (s1.largest_rank, s1.average_rank) == (s2.largest_rank, s2.average_rank)
+    assert f1.factor_bytes() == f2.factor_bytes()
+
+
 def test_resident_system_matches_host_path(acr):
     sysm = P.config_system(4, n=16)
     cfg = acr.AcrConfig(eps=1e-4)
