@@ -26,7 +26,7 @@ import numpy as np
 from . import problems
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(_HERE, "libacrgpu.so")
+_LIB = os.environ.get("ACRGPU_LIB") or os.path.join(_HERE, "libacrgpu.so")  # override: A/B of kernel variants
 
 
 # ---------------------------------------------------------------- errors (errors.hpp)

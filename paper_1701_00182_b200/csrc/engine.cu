@@ -88,7 +88,7 @@ struct Ctx {
     Lane lanes[NLANES];
     int cur = 0;                // active lane
     Arena persist{};
-    double* persist_base = nullptr;     // two semi-spaces of persist_half doubles each
+    double* persist_sp[2] = {nullptr, nullptr};  // two semi-spaces of persist_half doubles each
     size_t persist_half = 0;
     int space = 0;                      // semi-space the persistent arena allocates from
     int factoring = 0;                  // factorizations in progress on this context
@@ -126,7 +126,8 @@ struct Ctx {
         const size_t pbytes = ((size_t)(freeb * frac("ACRGPU_PERSIST_FRAC", 0.50)) / 2) & ~(size_t)4095;
         const size_t tbytes = ((size_t)(freeb * frac("ACRGPU_TRANS_FRAC", 0.22)) / NLANES) & ~(size_t)4095;
         persist_half = pbytes / 8;
-        persist_base = dmalloc<double>(2 * persist_half);
+        persist_sp[0] = dmalloc<double>(persist_half);
+        persist_sp[1] = dmalloc<double>(persist_half);
         trans_base = dmalloc<double>(NLANES * tbytes / 8);
         ctrs = dmalloc<unsigned long long>(1 + NLANES);
         overflow = dmalloc<int>(1 + NLANES);
@@ -134,7 +135,7 @@ struct Ctx {
         flops = dmalloc<FlopLedger>(MAX_KERNELS);
         set_report_ledger(flops);
         space = 0;
-        persist = Arena{persist_base, persist_half, ctrs, overflow};
+        persist = Arena{persist_sp[0], persist_half, ctrs, overflow};
         for (int l = 0; l < NLANES; ++l)
             lanes[l].trans = Arena{trans_base + (size_t)l * (tbytes / 8), tbytes / 8, ctrs + 1 + l, overflow + 1 + l};
         reset_all();
@@ -147,6 +148,7 @@ struct Ctx {
     }
     void reset_all() {
         for (auto& l : lanes) CK(cudaStreamSynchronize(l.st));
+        persist.base = space_ptr(space);
         fold_ledger();
         CK(cudaMemsetAsync(ctrs, 0, (1 + NLANES) * sizeof(unsigned long long), st));
         CK(cudaMemsetAsync(overflow, 0, (1 + NLANES) * sizeof(int), st));
@@ -160,10 +162,21 @@ struct Ctx {
         call_planes.clear();
         cur = 0;
     }
-    double* other_space() const { return persist_base + (size_t)(1 - space) * persist_half; }
+    // semi-space `i`, allocated again if a factorization took it over (take_space)
+    double* space_ptr(int i) {
+        if (!persist_sp[i]) persist_sp[i] = dmalloc<double>(persist_half);
+        return persist_sp[i];
+    }
+    double* other_space() { return space_ptr(1 - space); }
     void swap_space() {
         space = 1 - space;
-        persist.base = persist_base + (size_t)space * persist_half;
+        persist.base = space_ptr(space);
+    }
+    // hand the current semi-space (and the low-rank data in it) to a factorization
+    double* take_space() {
+        double* p = persist_sp[space];
+        persist_sp[space] = nullptr;
+        return p;
     }
     Slot* get_slots(size_t n) {
         Lane& l = lane();
@@ -187,7 +200,7 @@ struct Ctx {
     void destroy() {
         for (auto& l : lanes)
             if (l.st) cudaStreamSynchronize(l.st);
-        for (void* p : std::initializer_list<void*>{persist_base, trans_base, ctrs, overflow, err, flops, scratch})
+        for (void* p : std::initializer_list<void*>{persist_sp[0], persist_sp[1], trans_base, ctrs, overflow, err, flops, scratch})
             if (p) cudaFree(p);
         for (auto& l : lanes) {
             if (l.slots) cudaFree(l.slots);
@@ -261,7 +274,6 @@ struct Engine {
     std::map<std::tuple<int, int, int, int>, std::unique_ptr<Plan>> plans;
     // every live Store of this engine (compaction of the persistent arena, gc())
     std::shared_ptr<std::unordered_set<Store*>> live = std::make_shared<std::unordered_set<Store*>>();
-    bool in_pair = false;
     double gc_next = 0.6;  // compaction threshold (fraction of a semi-space)
     int gc_count = 0;
     std::vector<void*> dev_allocs;  // plan arrays etc.
@@ -339,6 +351,9 @@ struct Engine {
         s->V = s->U + nk;
         s->rank = (int*)(s->V + nk);
         cudaStream_t stream = main_st();
+        // defined (empty) low-rank tables until the store's leaves are written: the
+        // compaction (gc) reads the ranks of every live store, including outputs in progress
+        if (nk) CK(cudaMemsetAsync(s->U, 0, nk * 20, stream));
         live->insert(s.get());
         return StoreP(s.get(), [s, stream, reg = live](Store*) mutable {
             reg->erase(s.get());
@@ -713,8 +728,9 @@ struct Engine {
             if (adaptive) {
                 if (P->pp_gb < 0 || P->pp_level != level_tag) {
                     measure = true;
-                    // new plan, or a new level (ranks grew): measure on a conservative batch
-                    chunk = P->pp_gb < 0 ? 1 : batch_for(3.0 * P->pp_gb);
+                    // new plan, or a new level (ranks grew, by more than 10x for the root
+                    // products): measure on a single plane
+                    chunk = 1;
                 } else {
                     chunk = batch_for(P->pp_gb);
                 }
@@ -765,9 +781,8 @@ struct Engine {
     // ~100 GB, ~4x the live low-rank data (temporaries of invert_node, superseded leaf
     // factors).  For C5-sized planes, when the current semi-space passes gc_next, every live
     // store's U/V is copied into the other semi-space (k_compact, repointing the store's
-    // tables) and allocation continues there.  Safe point: entry of a mult_add outside
-    // pair() with both lanes drained -- no product slot or in-flight kernel holds an arena
-    // pointer.  Results are unchanged (copies are bitwise).  Only one factorization may be in
+    // tables) and allocation continues there.  Safe point: entry of a mult_add with both
+    // lanes drained -- no product slot or in-flight kernel holds an arena pointer.  Results are unchanged (copies are bitwise).  Only one factorization may be in
     // progress on the context (in-process ranks share it, so they never compact).
     // ACRGPU_GC_FORCE=<fraction>: compact at any size once the semi-space is that full
     // (tests: 0 compacts at every safe point); ACRGPU_NO_GC disables compaction.
@@ -775,8 +790,11 @@ struct Engine {
         if (ctx->factoring != 1 || getenv("ACRGPU_NO_GC")) return false;
         return S.dim > 4096 || getenv("ACRGPU_GC_FORCE");
     }
+    // Safe point at every mult_add entry (also inside pair(): all lanes are drained first, and
+    // the host holds no arena pointer between mult_adds), so at most one batched mult_add's
+    // flush outputs are allocated between two checks.
     void gc_check() {
-        if (in_pair || ctx->cur != 0 || !gc_enabled()) return;
+        if (!gc_enabled()) return;
         for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.st));
         unsigned long long used = 0;
         CK(cudaMemcpy(&used, ctx->persist.ctr, sizeof(used), cudaMemcpyDeviceToHost));
@@ -849,7 +867,7 @@ struct Engine {
         ctx->swap_space();
         ++gc_count;
         const double live_frac = (double)total / (double)ctx->persist.cap;
-        gc_next = std::min(0.9, std::max(0.6, live_frac + 0.3));
+        gc_next = std::min(0.85, std::max(0.6, live_frac + 0.25));
         if (getenv("ACRGPU_VERBOSE"))
             fprintf(stderr, "[acrgpu] compaction %d (level %d): %zu stores, live %.2f GB of %.2f GB semi-space\n", gc_count,
                     level_tag, live->size(), total * 8.0 / 1e9, ctx->persist.cap * 8.0 / 1e9);
@@ -884,14 +902,11 @@ struct Engine {
             f1();
             return;
         }
-        gc_check();  // safe point before both lanes start
         ctx->depend(1, 0);
-        in_pair = true;
         f0();
         ctx->cur = 1;
         f1();
         ctx->cur = 0;
-        in_pair = false;
         ctx->depend(0, 1);
     }
 
@@ -1688,7 +1703,20 @@ static void factor_finish(PartRun& R) {
         R.lev_ev.clear();
     }
     check_device_errors(F);
-    compact_factor(F);
+    if (E.gc_enabled()) {
+        // compaction mode (C5-sized planes): every live low-rank factor is already in the
+        // current semi-space; the factorization takes that buffer over instead of copying
+        // ~30 GB into a new allocation the device no longer has room for.  The context
+        // allocates a fresh semi-space at its next factorization.
+        CK(cudaDeviceSynchronize());
+        if (F->ubuf) cudaFree(F->ubuf);
+        unsigned long long used = 0;
+        CK(cudaMemcpy(&used, E.ctx->persist.ctr, sizeof(used), cudaMemcpyDeviceToHost));
+        F->ubuf = E.ctx->take_space();
+        F->ubuf_doubles = (long)used;
+    } else {
+        compact_factor(F);
+    }
     cudaEvent_t e2;
     CK(cudaEventCreate(&e2));
     CK(cudaEventRecord(e2, E.st()));

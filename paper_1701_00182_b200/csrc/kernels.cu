@@ -412,8 +412,10 @@ __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, cons
     __syncthreads();
 }
 
-template <int DMAX, int RPCAP, int NTH>
-__global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews bv) {
+// QR = false: dense route only (the <= 64 class never takes the QR route); without the
+// blocked-QR code the kernel fits 128 registers per thread, so two CTAs share an SM.
+template <int DMAX, int RPCAP, int NTH, bool QR = true>
+__global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, BatchViews bv) {
     constexpr int NWH = NTH / 32;
     extern __shared__ double smem[];
     __shared__ double red[NWH];
@@ -506,6 +508,9 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
     }
 
     // ---------------- QR route
+    if constexpr (!QR) {
+        __trap();  // size class routing error: a block above DMAX reached the dense-only kernel
+    } else {
     // workspace: Uc (m x K) | Vc (n x K) | tau_u (K) | tau_v (K) | [core engine work if too big for smem]
     const int pmax = ku > kv ? ku : kv;
     const bool core_in_smem = pmax <= DMAX;
@@ -619,6 +624,7 @@ __global__ void __launch_bounds__(NTH, 1) k_truncate(TruncArgs args, BatchViews 
         add_flops(args.flops, F_GEQRF, fqr);
         add_flops(args.flops, F_GEMM, fgemm);
     }
+    }  // QR
 }
 
 // ------------------------------------------------------------------ dense * dense product
@@ -639,6 +645,30 @@ __global__ void __launch_bounds__(NT, 1) k_dd_product(DDArgs args, BatchViews bv
     const int m = task.m, k = task.k, n = task.n;
     const double* Ad = bv.a[b].dense + task.da;
     const double* Bd = bv.b[b].dense + task.db;
+    {  // zero operand (off-diagonal leaves of the diagonal level-0 couplings): rank-0 product
+        int nz = 0;
+        for (int e = threadIdx.x; e < m * k; e += NT) nz |= Ad[e] != 0.0;
+        int nzb = 0;
+        for (int e = threadIdx.x; e < k * n; e += NT) nzb |= Bd[e] != 0.0;
+        nz = __syncthreads_or(nz);
+        nzb = __syncthreads_or(nzb);
+        if (!nz || !nzb) {
+            if (threadIdx.x == 0) {
+                Slot& s = args.slots[(size_t)task.prod * args.B + b];
+                s.rank = 0;
+                s.U = nullptr;
+                s.V = nullptr;
+                s.ldu = m;
+                s.ldv = n;
+                double fsvd = 0, fqr = 0, fgemm = fl_gemm(m, n, k);
+                fl_svd(m, n, fsvd, fqr, fgemm);
+                add_flops(args.flops, F_SVD, fsvd);
+                add_flops(args.flops, F_GEQRF, fqr);
+                add_flops(args.flops, F_GEMM, fgemm);
+            }
+            return;
+        }
+    }
     CtaSvdWork w = cta_smem_work(smem, DENSE_MAX, DENSE_MAX);
     double* M = w.A;
     w.lda = m;
@@ -1524,6 +1554,27 @@ __global__ void __launch_bounds__(64) k_small32(TruncArgs targs, DDArgs dargs, i
     } else {
         const double* Ad = bv.a[b].dense + dt.da;
         const double* Bd = bv.b[b].dense + dt.db;
+        // A zero operand (the off-diagonal dense leaves of the diagonal level-0 couplings E/F)
+        // gives a zero product, whose truncation is rank 0: skip the GEMM and the SVD.
+        bool nzA = false, nzB = false;
+        for (int e = lane; e < m * dt.k; e += 32) nzA |= Ad[e] != 0.0;
+        for (int e = lane; e < dt.k * n; e += 32) nzB |= Bd[e] != 0.0;
+        if (!__any_sync(0xffffffffu, nzA) || !__any_sync(0xffffffffu, nzB)) {
+            if (lane == 0) {
+                Slot& s = dargs.slots[(size_t)dt.prod * dargs.B + b];
+                s.rank = 0;
+                s.U = nullptr;
+                s.V = nullptr;
+                s.ldu = m;
+                s.ldv = n;
+                double fsvd = 0, fqr = 0, fgemm = fl_gemm(m, n, dt.k);  // nominal work of the reference
+                fl_svd(m, n, fsvd, fqr, fgemm);
+                add_flops(dargs.flops, F_SVD, fsvd);
+                add_flops(dargs.flops, F_GEQRF, fqr);
+                add_flops(dargs.flops, F_GEMM, fgemm);
+            }
+            return;
+        }
         warp_accumulate32(a, SmallTaskIO::dd_part(Ad, Bd, m, dt.k, n, true), sm);
     }
     // pivot threshold 1e-3 below the cutoff (values-only: sigma_1 to ~1e-10)
@@ -1755,7 +1806,7 @@ static size_t trunc_smem_big() {
 }
 
 void setup_kernels() {
-    cudaFuncSetAttribute(k_truncate<64, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
+    cudaFuncSetAttribute(k_truncate<64, 64, 256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
     cudaFuncSetAttribute(k_truncate<BIG_DMAX, BIG_RPCAP, BIG_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_big());
     cudaFuncSetAttribute(k_dd_product, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
     cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1782,7 +1833,7 @@ void launch_trunc_small(cudaStream_t st, int nc, int ntasks, const TruncTask* ta
     DDArgs d{};
     ProfScope _ps(st, name, (long)ntasks * B);
     if (nc == 32) k_small32<0><<<dim3((ntasks + 1) / 2, B), 64, 0, st>>>(a, d, ntasks, bv);
-    else k_truncate<64, 64, 256><<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
+    else k_truncate<64, 64, 256, false><<<dim3(ntasks, B), NT, trunc_smem(), st>>>(a, bv);
 }
 
 void launch_dd_small(cudaStream_t st, int nc, int ntasks, const DDTask* tasks, Slot* slots, int B, double eps,

@@ -11,7 +11,10 @@ namespace acrgpu {
 
 constexpr int DENSE_MAX = 64;
 constexpr int MAX_KERNELS = 32;             // per-kernel flop ledgers               // dense route / dense leaf limit
-constexpr size_t SMEM_TRUNC = 112 * 1024;   // dynamic smem of k_truncate / k_dd_product
+// dynamic smem of the 64-class kernels (k_truncate<64,..>, k_dd_product, k_sigma1_dense):
+// one cta_smem_work(64, 64) = A, W, J (3 x 64 x 64) + tau/nrm/sig (3 x 64) doubles + perm/order
+// (2 x 64) ints.  Sized exactly so that two CTAs fit on one SM.
+constexpr size_t SMEM_TRUNC = (3 * 64 * 64 + 3 * 64) * 8 + 2 * 64 * 4 + 64;
 
 struct ScatterLaunch {
     const int* rows;

@@ -58,6 +58,20 @@ def test_baseline_configs_small_n(acr, oracle, k):
         assert np.linalg.norm(ug - uo) <= 1e-3 * np.linalg.norm(uo)
 
 
+@pytest.mark.parametrize("n", [16, 32])
+def test_config5_operator_leaf64_multi_rhs(acr, oracle, n):
+    """BASELINE config 5 (vardiff, leaf 64, eps 1e-6, 16 RHS) at reduced plane counts: the
+    64x64 dense-leaf kernels (k_dd_product, k_lu_inverse at 64, mid64/d128/QR truncation
+    classes) against the oracle, all 16 right-hand sides in one solve."""
+    c = P.CONFIGS[5]
+    sysm = P.config_system(5, n=n)
+    assert sysm.rhs.shape[0] == 16
+    g, o, ug, uo, rg, ro, sg, so = compare(acr, oracle, sysm, c["eps"], c["leaf"], threads=16)
+    assert_parity(rg, ro, sg, so, g.level_info(), o.level_info())
+    assert np.linalg.norm(ug - uo) <= 1e-3 * np.linalg.norm(uo)
+    assert abs(g.factor_bytes() - so["factor_bytes"]) <= 0.02 * so["factor_bytes"]
+
+
 def test_config1_full_size(acr, oracle):
     """C1 at its BASELINE size (n=32, N=32768, eps 1e-6): residual, ranks, bytes."""
     sysm = P.config_system(1)

@@ -9,7 +9,7 @@ from collections import defaultdict
 
 NAMES = {  # template instantiations -> the launch names bench.py reports
     r"k_small32<0>": "k_trunc_small32", r"k_small32<1>": "k_dd_small32",
-    r"k_truncate<64, 64, 256>": "k_trunc_mid64", r"k_truncate<128, 56, 512>": "k_trunc_d128|k_trunc_qr",
+    r"k_truncate<64, 64, 256": "k_trunc_mid64", r"k_truncate<128, 56, 512": "k_trunc_d128|k_trunc_qr",
 }
 
 
