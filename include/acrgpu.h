@@ -56,6 +56,8 @@ enum {
     ACRGPU_E_LEAFMEM = 3,
     ACRGPU_E_USAGE = 4,
     ACRGPU_E_DEVICE = 5,
+    ACRGPU_E_INDEFINITE = 6,   /* IndefiniteError (pcg: nonpositive curvature) */
+    ACRGPU_E_DIVERGENCE = 7,   /* DivergenceError (iterative refinement) */
     ACRGPU_E_INTERNAL = 9
 };
 
@@ -191,6 +193,30 @@ int acrgpu_factor_partitioned(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_s
 /* Same, on a system already uploaded with acrgpu_system_upload. */
 int acrgpu_factor_partitioned_resident(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_dsystem* sys,
                                        const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err);
+
+/* ---- Krylov drivers with the GPU factorization as preconditioner
+ * (core/include/acr/krylov.hpp:8-35, core/src/krylov.cpp:38-133).  One right-hand side
+ * f_dev and solution u_dev ([n][dim], device memory, original ordering) on an uploaded
+ * system; the operator is applied as one CSR SpMV built from the system's COO blocks on
+ * first use.  residual_history (host, may be NULL) receives the true relative residual
+ * ||f - A u|| / ||f|| of every iteration (up to max_iterations entries).
+ *   acrgpu_pcg     <- acr::pcg(system, precond, tol, max_iterations); precond may be NULL
+ *                     (plain CG).  ACRGPU_E_INDEFINITE when p^T A p <= 0.
+ *   acrgpu_refine  <- acr::iterative_refinement(system, precond, tol, max_iterations).
+ *                     ACRGPU_E_DIVERGENCE after three consecutive residual increases.
+ * Nonconvergence is reported in the trace (converged = 0), not as an error.  The
+ * preconditioner must be a single-GPU factorization of a system of the same shape. */
+typedef struct acrgpu_trace {
+    int converged;
+    int iterations;
+    double apply_time;             /* mean seconds per preconditioner application (device events) */
+    double total_time;             /* seconds */
+} acrgpu_trace;
+int acrgpu_pcg(acrgpu_ctx* ctx, const acrgpu_dsystem* sys, acrgpu_fact* precond, double tol, int max_iterations,
+               const double* f_dev, double* u_dev, double* residual_history, acrgpu_trace* trace, acrgpu_error* err);
+int acrgpu_refine(acrgpu_ctx* ctx, const acrgpu_dsystem* sys, acrgpu_fact* precond, double tol, int max_iterations,
+                  const double* f_dev, double* u_dev, double* residual_history, acrgpu_trace* trace,
+                  acrgpu_error* err);
 
 /* Library build identification (sm arch, version). */
 const char* acrgpu_version(void);

@@ -52,6 +52,14 @@ class LeafMemoryError(Error):
     pass
 
 
+class IndefiniteError(Error):
+    """pcg: nonpositive search-direction curvature (errors.hpp:45-48)."""
+
+
+class DivergenceError(Error):
+    """iterative_refinement: three consecutive residual increases (errors.hpp:51-54)."""
+
+
 class UsageError(Error):
     pass
 
@@ -131,6 +139,11 @@ class _Level(C.Structure):
                 ("largest_rank", C.c_int), ("average_rank", C.c_double)]
 
 
+class _Trace(C.Structure):
+    _fields_ = [("converged", C.c_int), ("iterations", C.c_int), ("apply_time", C.c_double),
+                ("total_time", C.c_double)]
+
+
 class _Timing(C.Structure):
     _fields_ = [("lift_ms", C.c_double), ("factor_ms", C.c_double), ("solve_ms", C.c_double),
                 ("flops_nominal", C.c_double), ("flops_svd", C.c_double), ("flops_qr", C.c_double),
@@ -165,6 +178,10 @@ SYMBOLS = {
                                             C.POINTER(C.c_void_p), C.POINTER(_Err)]),
     "acrgpu_factor_partitioned_resident": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_Cfg),
                                                      C.POINTER(C.c_void_p), C.POINTER(_Err)]),
+    "acrgpu_pcg": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
+                             C.POINTER(C.c_double), C.POINTER(_Trace), C.POINTER(_Err)]),
+    "acrgpu_refine": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
+                                C.POINTER(C.c_double), C.POINTER(_Trace), C.POINTER(_Err)]),
 }
 
 COMM_ID_BYTES = 128
@@ -198,6 +215,10 @@ def _raise(err: _Err):
         raise LeafMemoryError(msg)
     if code == 4:
         raise UsageError(msg)
+    if code == 6:
+        raise IndefiniteError(msg)
+    if code == 7:
+        raise DivergenceError(msg)
     if code == 5:
         raise DeviceError(msg)
     raise Error(msg or f"acrgpu error {code}")
@@ -472,3 +493,55 @@ def structure(coords, leaf_size=32, eta=2.0, weak=False):
     lib().acrgpu_structure(dim, _p(coords, C.c_double), leaf_size, eta, 1 if weak else 0, _p(perm, C.c_int),
                            _p(leaves, C.c_int), n, C.byref(err))
     return perm, leaves
+
+
+# ---------------------------------------------------------------- Krylov drivers
+@dataclasses.dataclass
+class IterationTrace:
+    """acr::IterationTrace (krylov.hpp:8-14)."""
+    converged: bool = False
+    iterations: int = 0
+    residual_history: list = dataclasses.field(default_factory=list)
+    apply_time: float = 0.0
+    total_time: float = 0.0
+
+
+@dataclasses.dataclass
+class KrylovResult:
+    """acr::KrylovResult (krylov.hpp:16-19): u is (n, dim)."""
+    u: np.ndarray
+    trace: IterationTrace
+
+
+def _krylov(entry, system, precond, tol, max_iterations):
+    import torch  # device buffers only (plumbing); the iteration runs in libacrgpu
+    dsys = system if isinstance(system, DeviceSystem) else DeviceSystem(system, precond._ctx if precond else None)
+    host = dsys.system
+    f = np.ascontiguousarray(np.asarray(host.rhs, np.float64).reshape(-1, host.n, host.dim)[0])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f_d = torch.from_numpy(f).to(dev)
+    u_d = torch.empty_like(f_d)
+    hist = np.zeros(max(1, max_iterations))
+    tr = _Trace()
+    err = _Err()
+    torch.cuda.synchronize()
+    rc = getattr(lib(), entry)(dsys.ctx.h, dsys.h, precond.h if precond is not None else None, float(tol),
+                               int(max_iterations), C.c_void_p(f_d.data_ptr()), C.c_void_p(u_d.data_ptr()),
+                               _p(hist, C.c_double), C.byref(tr), C.byref(err))
+    if rc:
+        _raise(err)
+    u = u_d.cpu().numpy()
+    return KrylovResult(u, IterationTrace(bool(tr.converged), int(tr.iterations),
+                                          [float(x) for x in hist[:tr.iterations]], tr.apply_time, tr.total_time))
+
+
+def pcg(system, precond: AcrFactorization | None, tol: float, max_iterations: int) -> KrylovResult:
+    """acr::pcg (krylov.cpp:38-90): preconditioned CG with true-residual stopping on the
+    system's first right-hand side; precond None runs plain CG.  Raises IndefiniteError."""
+    return _krylov("acrgpu_pcg", system, precond, tol, max_iterations)
+
+
+def iterative_refinement(system, precond: AcrFactorization, tol: float, max_iterations: int) -> KrylovResult:
+    """acr::iterative_refinement (krylov.cpp:92-131): u += M^{-1}(f - A u).  Raises
+    DivergenceError after three consecutive residual increases."""
+    return _krylov("acrgpu_refine", system, precond, tol, max_iterations)

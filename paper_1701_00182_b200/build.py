@@ -12,7 +12,7 @@ LIB = os.path.join(HERE, "libacrgpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
-SOURCES = ["structure.cpp", "kernels.cu", "engine.cu"]
+SOURCES = ["structure.cpp", "kernels.cu", "krylov.cu", "engine.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh"))) + [os.path.join("..", "..", "include", "acrgpu.h")]
 
 

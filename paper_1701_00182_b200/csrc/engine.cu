@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1156,8 +1157,12 @@ struct DSys {
     double* d_vals = nullptr;
     long* d_off = nullptr;
     int device = 0;
+    // whole operator as CSR over [n][dim] rows (Krylov drivers; built on first use)
+    long* csr_ptr = nullptr;
+    int* csr_col = nullptr;
+    double* csr_val = nullptr;
     ~DSys() {
-        for (void* p : std::initializer_list<void*>{d_rows, d_cols, d_vals, d_off})
+        for (void* p : std::initializer_list<void*>{d_rows, d_cols, d_vals, d_off, csr_ptr, csr_col, csr_val})
             if (p) cudaFree(p);
     }
 };
@@ -2407,6 +2412,202 @@ static HostStats store_stats(Engine& E, const SP& s) {
     return h;
 }
 
+// ------------------------------------------------------------------ Krylov drivers
+// pcg / iterative_refinement (core/src/krylov.cpp:38-133) on the device: the operator
+// y_j = E_j u_{j-1} + D_j u_j + F_j u_{j+1} (block.cpp:89-107) as one CSR SpMV, the
+// preconditioner as one solve against the factorization, scalars read back per step.
+static void ensure_csr(DSys& ds, cudaStream_t st) {
+    if (ds.csr_ptr) return;
+    const int n = ds.n, dim = ds.dim;
+    const long N = (long)n * dim;
+    std::vector<std::vector<std::pair<int, double>>> rows(N);
+    auto add_block = [&](int b, int pout, int pin) {
+        for (long e = ds.off[b]; e < ds.off[b + 1]; ++e)
+            rows[(long)pout * dim + ds.rows[e]].push_back({pin * dim + ds.cols[e], ds.vals[e]});
+    };
+    for (int j = 0; j < n; ++j) {
+        if (j > 0) add_block(n + j - 1, j, j - 1);        // E(j): plane j <- plane j-1
+        add_block(j, j, j);                               // D(j)
+        if (j + 1 < n) add_block(2 * n - 1 + j, j, j + 1);  // F(j): plane j <- plane j+1
+    }
+    std::vector<long> ptr(N + 1, 0);
+    std::vector<int> col;
+    std::vector<double> val;
+    for (long i = 0; i < N; ++i) {
+        auto& r = rows[i];
+        std::stable_sort(r.begin(), r.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (size_t q = 0; q < r.size(); ++q) {
+            if (q > 0 && r[q].first == r[q - 1].first) {
+                val.back() += r[q].second;
+                continue;
+            }
+            col.push_back(r[q].first);
+            val.push_back(r[q].second);
+        }
+        ptr[i + 1] = (long)col.size();
+    }
+    ds.csr_ptr = upload(ptr, st);
+    ds.csr_col = upload(col, st);
+    ds.csr_val = upload(val, st);
+    CK(cudaStreamSynchronize(st));
+}
+
+struct Krylov {
+    DSys& ds;
+    acrgpu_fact* M;
+    cudaStream_t st;
+    long N;
+    double *r = nullptr, *z = nullptr, *p = nullptr, *ap = nullptr, *t = nullptr, *part = nullptr, *sc = nullptr;
+    double apply_ms = 0;
+    int applies = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    Krylov(DSys& d, acrgpu_fact* pre, cudaStream_t s) : ds(d), M(pre), st(s), N((long)d.n * d.dim) {
+        r = dmalloc<double>(5 * N + KRY_G + 8);
+        z = r + N;
+        p = z + N;
+        ap = p + N;
+        t = ap + N;
+        part = t + N;
+        sc = part + KRY_G;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        ensure_csr(ds, st);
+    }
+    ~Krylov() {
+        cudaFree(r);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    double dot(const double* x, const double* y) {
+        launch_dot(st, x, y, N, part, sc);
+        double h = 0;
+        CK(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return h;
+    }
+    void spmv(const double* x, const double* b, double* y) {
+        launch_csr_spmv(st, ds.csr_ptr, ds.csr_col, ds.csr_val, x, b, y, N);
+    }
+    // z = M^{-1} v (identity without a preconditioner)
+    void precond(const double* v, double* zz) {
+        if (!M) {
+            CK(cudaMemcpyAsync(zz, v, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            return;
+        }
+        CK(cudaEventRecord(e0, st));
+        do_solve(M, 1, v, zz);
+        CK(cudaEventRecord(e1, st));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        apply_ms += ms;
+        ++applies;
+    }
+    double true_residual(const double* b, const double* x, double bnorm) {
+        spmv(x, b, t);  // t = b - A x
+        return std::sqrt(dot(t, t)) / bnorm;
+    }
+};
+
+static void krylov_check(acrgpu_ctx* ctx, const DSys* ds, acrgpu_fact* pre, int max_iterations, const double* f,
+                         double* u) {
+    if (!ctx || !ds || !f || !u) throw AcrError{ACRGPU_E_USAGE, "null argument"};
+    if (max_iterations < 0) throw AcrError{ACRGPU_E_USAGE, "max_iterations must be >= 0"};
+    if (pre) {
+        if (!pre->eng || pre->comm || !pre->vparts.empty())
+            throw AcrError{ACRGPU_E_USAGE, "preconditioner must be a single-GPU factorization"};
+        if (pre->n != ds->n || pre->dim != ds->dim)
+            throw AcrError{ACRGPU_E_DIMENSION, "preconditioner and system shapes differ"};
+    }
+}
+
+// acr::pcg (krylov.cpp:38-90)
+static acrgpu_trace run_pcg(DSys& ds, acrgpu_fact* pre, cudaStream_t st, double tol, int maxit, const double* b,
+                            double* x, double* hist) {
+    const auto t_start = std::chrono::steady_clock::now();
+    acrgpu_trace tr{};
+    Krylov K(ds, pre, st);
+    const long N = K.N;
+    CK(cudaMemsetAsync(x, 0, N * sizeof(double), st));
+    const double bnorm = std::sqrt(K.dot(b, b));
+    if (bnorm == 0.0) {
+        tr.converged = 1;
+        return tr;
+    }
+    CK(cudaMemcpyAsync(K.r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    K.precond(K.r, K.z);
+    CK(cudaMemcpyAsync(K.p, K.z, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    double rz = K.dot(K.r, K.z);
+    for (int k = 1; k <= maxit; ++k) {
+        K.spmv(K.p, nullptr, K.ap);
+        const double pAp = K.dot(K.p, K.ap);
+        if (!(pAp > 0)) {
+            char buf[160];
+            std::snprintf(buf, sizeof(buf), "conjugate gradient: nonpositive curvature p^T A p = %g", pAp);
+            throw AcrError{ACRGPU_E_INDEFINITE, buf};
+        }
+        const double alpha = rz / pAp;
+        launch_cg_update(st, x, K.r, K.p, K.ap, alpha, N);
+        // stop on the recomputed residual, not the recurrence residual
+        const double true_res = K.true_residual(b, x, bnorm);
+        if (hist) hist[k - 1] = true_res;
+        tr.iterations = k;
+        if (true_res <= tol) {
+            tr.converged = 1;
+            break;
+        }
+        K.precond(K.r, K.z);
+        const double rz_next = K.dot(K.r, K.z);
+        launch_xpby(st, K.p, K.z, rz_next / rz, N);
+        rz = rz_next;
+    }
+    CK(cudaStreamSynchronize(st));
+    tr.total_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    if (K.applies > 0) tr.apply_time = K.apply_ms / 1000.0 / K.applies;
+    return tr;
+}
+
+// acr::iterative_refinement (krylov.cpp:92-131)
+static acrgpu_trace run_refine(DSys& ds, acrgpu_fact* pre, cudaStream_t st, double tol, int maxit, const double* b,
+                               double* x, double* hist) {
+    const auto t_start = std::chrono::steady_clock::now();
+    acrgpu_trace tr{};
+    Krylov K(ds, pre, st);
+    const long N = K.N;
+    CK(cudaMemsetAsync(x, 0, N * sizeof(double), st));
+    const double bnorm = std::sqrt(K.dot(b, b));
+    if (bnorm == 0.0) {
+        tr.converged = 1;
+        return tr;
+    }
+    double prev = 1.0;  // residual of the zero initial guess
+    int growth_streak = 0;
+    for (int k = 1; k <= maxit; ++k) {
+        K.spmv(x, b, K.r);  // r = b - A x
+        K.precond(K.r, K.z);
+        launch_vadd(st, x, K.z, N);
+        const double res = K.true_residual(b, x, bnorm);
+        if (hist) hist[k - 1] = res;
+        tr.iterations = k;
+        if (res <= tol) {
+            tr.converged = 1;
+            break;
+        }
+        growth_streak = res > prev ? growth_streak + 1 : 0;
+        if (growth_streak >= 3) {
+            char buf[200];
+            std::snprintf(buf, sizeof(buf),
+                          "iterative refinement: residual grew over three consecutive corrections (last %g)", res);
+            throw AcrError{ACRGPU_E_DIVERGENCE, buf};
+        }
+        prev = res;
+    }
+    CK(cudaStreamSynchronize(st));
+    tr.total_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    if (tr.iterations > 0) tr.apply_time = K.apply_ms / 1000.0 / tr.iterations;
+    return tr;
+}
+
 }  // namespace acrgpu
 
 // ================================================================== C-ABI
@@ -2446,6 +2647,7 @@ static void clear_err(acrgpu_error* err) {
 extern "C" {
 
 const char* acrgpu_version(void) { return "acrgpu 0.1 sm_100a fp64"; }
+
 
 long acrgpu_profile_report(char* buf, long cap, int reset) {
     const std::string r = prof_report(reset != 0);
@@ -2955,6 +3157,32 @@ long acrgpu_structure(int dim, const double* coords, int leaf_size, double eta, 
         fill_err(err, AcrError{e.code, e.msg});
         return -e.code;
     }
+}
+
+int acrgpu_pcg(acrgpu_ctx* ctx, const acrgpu_dsystem* sys, acrgpu_fact* precond, double tol, int max_iterations,
+               const double* f_dev, double* u_dev, double* residual_history, acrgpu_trace* trace, acrgpu_error* err) {
+    ABI_TRY({
+        krylov_check(ctx, sys ? sys->d.get() : nullptr, precond, max_iterations, f_dev, u_dev);
+        cudaStream_t st = precond ? fact_stream(precond) : ctx->c.st;
+        const acrgpu_trace tr = run_pcg(*sys->d, precond, st, tol, max_iterations, f_dev, u_dev, residual_history);
+        if (trace) *trace = tr;
+        launches_take();
+        return 0;
+    })
+}
+
+int acrgpu_refine(acrgpu_ctx* ctx, const acrgpu_dsystem* sys, acrgpu_fact* precond, double tol, int max_iterations,
+                  const double* f_dev, double* u_dev, double* residual_history, acrgpu_trace* trace,
+                  acrgpu_error* err) {
+    ABI_TRY({
+        if (!precond) throw AcrError{ACRGPU_E_USAGE, "iterative_refinement: a factorization is required"};
+        krylov_check(ctx, sys ? sys->d.get() : nullptr, precond, max_iterations, f_dev, u_dev);
+        const acrgpu_trace tr =
+            run_refine(*sys->d, precond, fact_stream(precond), tol, max_iterations, f_dev, u_dev, residual_history);
+        if (trace) *trace = tr;
+        launches_take();
+        return 0;
+    })
 }
 
 }  // extern "C"

@@ -1712,35 +1712,29 @@ static bool prof_on() {
     if (g_prof_on < 0) g_prof_on = getenv("ACRGPU_PROFILE") ? 1 : 0;
     return g_prof_on == 1;
 }
-struct ProfScope {
-    cudaStream_t st;
-    const char* name;
-    long ctas;
-    cudaEvent_t a = nullptr;
-    ProfScope(cudaStream_t s, const char* n, long c) : st(s), name(n), ctas(c) {
-        ++g_launches;
-        if (prof_on()) {
-            a = ev_get();
-            cudaEventRecord(a, st);
+ProfScope::ProfScope(cudaStream_t s, const char* n, long c) : st(s), name(n), ctas(c) {
+    ++g_launches;
+    if (prof_on()) {
+        a = ev_get();
+        cudaEventRecord(a, st);
+    }
+}
+ProfScope::~ProfScope() {
+    static const bool dbg = getenv("ACRGPU_DEBUG_SYNC") != nullptr;
+    if (dbg) {  // debugging aid: attribute launch / execution errors to the kernel
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            fprintf(stderr, "[acrgpu] %s (%ld CTAs): %s\n", name, ctas, cudaGetErrorString(e));
+            abort();
         }
     }
-    ~ProfScope() {
-        static const bool dbg = getenv("ACRGPU_DEBUG_SYNC") != nullptr;
-        if (dbg) {  // debugging aid: attribute launch / execution errors to the kernel
-            cudaError_t e = cudaGetLastError();
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) {
-                fprintf(stderr, "[acrgpu] %s (%ld CTAs): %s\n", name, ctas, cudaGetErrorString(e));
-                abort();
-            }
-        }
-        if (a) {
-            cudaEvent_t b = ev_get();
-            cudaEventRecord(b, st);
-            g_prof.push_back({name, a, b, ctas});
-        }
+    if (a) {
+        cudaEvent_t b = ev_get();
+        cudaEventRecord(b, st);
+        g_prof.push_back({name, a, b, ctas});
     }
-};
+}
 static std::vector<std::tuple<float, std::string, long>> g_top;  // slowest launches
 void prof_flush() {
     if (g_prof.empty()) return;

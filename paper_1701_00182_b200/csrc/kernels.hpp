@@ -56,6 +56,26 @@ struct ImageFix {
 };
 void launch_image_fix(cudaStream_t st, const ImageFix& a);
 
+// Launch accounting (every launch) and, with ACRGPU_PROFILE=1, CUDA events around it on
+// the launching stream (per-kernel device time in prof_report).
+struct ProfScope {
+    cudaStream_t st;
+    const char* name;
+    long ctas;
+    cudaEvent_t a = nullptr;
+    ProfScope(cudaStream_t s, const char* n, long c);
+    ~ProfScope();
+};
+
+// Krylov vector kernels (krylov.cu)
+constexpr int KRY_G = 296;  // partial sums per dot product (2 x 148 SMs)
+void launch_csr_spmv(cudaStream_t st, const long* ptr, const int* col, const double* val, const double* x,
+                     const double* b, double* y, long nrows);
+void launch_dot(cudaStream_t st, const double* x, const double* y, long n, double* part, double* out);
+void launch_cg_update(cudaStream_t st, double* x, double* r, const double* p, const double* ap, double alpha, long n);
+void launch_xpby(cudaStream_t st, double* p, const double* z, double beta, long n);
+void launch_vadd(cudaStream_t st, double* x, const double* z, long n);
+
 void setup_kernels();
 long launches_take();
 std::string prof_report(bool reset);
