@@ -99,6 +99,7 @@ struct Ctx {
     DevError* err = nullptr;
     FlopLedger* flops = nullptr;
     double* scratch = nullptr;  // sigma / abs-cut scratch (main lane only)
+    unsigned long long* h_zero = nullptr;  // pinned 0: arena counters are reset by the copy engine
     size_t scratch_cap = 0;
     unsigned long long call_id = 0;
     std::vector<std::pair<int, std::vector<int>>> call_planes;  // call id -> (level, planes)
@@ -131,6 +132,8 @@ struct Ctx {
         persist_sp[1] = dmalloc<double>(persist_half);
         trans_base = dmalloc<double>(NLANES * tbytes / 8);
         ctrs = dmalloc<unsigned long long>(1 + NLANES);
+        CK(cudaMallocHost(&h_zero, sizeof(unsigned long long)));
+        *h_zero = 0;
         overflow = dmalloc<int>(1 + NLANES);
         err = dmalloc<DevError>(1);
         flops = dmalloc<FlopLedger>(MAX_KERNELS);
@@ -142,6 +145,11 @@ struct Ctx {
         reset_all();
     }
     Lane& lane() { return lanes[cur]; }
+    // stream-ordered reset of a device arena counter through the copy engine (a one-thread
+    // kernel would wait for a free SM behind the other lane's 1-CTA-per-SM kernels)
+    void reset_ctr(cudaStream_t s, unsigned long long* ctr) {
+        CK(cudaMemcpyAsync(ctr, h_zero, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    }
     // lane `to` waits for the work issued so far on lane `from`
     void depend(int to, int from) {
         CK(cudaEventRecord(lanes[from].ev, lanes[from].st));
@@ -203,6 +211,8 @@ struct Ctx {
             if (l.st) cudaStreamSynchronize(l.st);
         for (void* p : std::initializer_list<void*>{persist_sp[0], persist_sp[1], trans_base, ctrs, overflow, err, flops, scratch})
             if (p) cudaFree(p);
+        if (h_zero) cudaFreeHost(h_zero);
+        h_zero = nullptr;
         for (auto& l : lanes) {
             if (l.slots) cudaFree(l.slots);
             if (l.ev) cudaEventDestroy(l.ev);
@@ -745,7 +755,7 @@ struct Engine {
             }
             Slot* slots = ctx->get_slots((size_t)std::max(1, P->nprod + P->ntt) * nb);
             const Arena tr = ctx->lane().trans;
-            launch_reset_counter(st(), tr.ctr);
+            ctx->reset_ctr(st(), tr.ctr);
             launch_alloc_apply(st(), P->nalloc, P->allocs, slots, nb, tr, bv);
             launch_apply_t(st(), P->ntt, P->tts, slots, P->nprod, nb, tr, ctx->flops, bv);
             launch_apply(st(), P->napply, P->applies, P->aleaves, P->x_ld, slots, P->nprod, nb, ctx->flops, bv);
@@ -990,7 +1000,7 @@ struct Engine {
             launch_sigma1_small(st(), S.max_dense_dim <= 32 ? 32 : 64, nd, d_doff, d_dm, d_dn, nb, sig_d, ctx->flops, bv);
             Slot* slots = ctx->get_slots(1);
             // sigma_1 per Rk leaf (values only); per-class task lists index sig_k by class offset
-            launch_reset_counter(st(), ctx->lane().trans.ctr);
+            ctx->reset_ctr(st(), ctx->lane().trans.ctr);
             for (int c = 0; c < NCLASS; ++c)
                 if (leaf_cls.n[c]) {
                     Classed<TruncTask> one;
@@ -1000,7 +1010,7 @@ struct Engine {
                               ctx->persist, bv);
                 }
             launch_scale_reduce(st(), sig_d, nd, sig_k, nk, nb, cfg.eps, cut);
-            launch_reset_counter(st(), ctx->lane().trans.ctr);
+            ctx->reset_ctr(st(), ctx->lane().trans.ctr);
             run_trunc(leaf_cls, leaf_parts, slots, nb, 0.0, cut, nullptr, false, ctx->persist, bv);
         }
     }

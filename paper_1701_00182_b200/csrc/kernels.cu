@@ -783,13 +783,12 @@ __device__ __forceinline__ void ap_accumulate(double (&acc)[2][4], const double*
 }
 
 // T = In^T X (rank x k) for one Rk leaf, once per (leaf, plane).
-__global__ void __launch_bounds__(NT) k_apply_t(ApplyTArgs args, BatchViews bv) {
+__device__ __forceinline__ void apply_t_item(const ApplyTArgs& args, const BatchViews& bv, const int ti, const int b) {
     __shared__ double As[64 * AP_LDA];  // In^T chunk: 64 ranks x 32 contracted
     __shared__ double Bs[32 * AP_LDB];  // X chunk: 32 contracted x 32 columns
     __shared__ double* sh_T;
-    const ApplyTTask task = args.tasks[blockIdx.x];
-    const int b = blockIdx.y;
-    Slot& out = args.slots[(size_t)(args.nprod + blockIdx.x) * args.B + b];
+    const ApplyTTask task = args.tasks[ti];
+    Slot& out = args.slots[(size_t)(args.nprod + ti) * args.B + b];
     const Slot s = args.slots[(size_t)task.prod * args.B + b];
     const int k = s.rank;
     const bool trans = task.kind == P_RK_LEFT;
@@ -840,20 +839,29 @@ __global__ void __launch_bounds__(NT) k_apply_t(ApplyTArgs args, BatchViews bv) 
     if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, 2.0 * rr * L * k);
 }
 
+// Grid-stride over (task, plane) items (see item_grid: capped for k_apply_t, whose many
+// rank-0 items return at once; one CTA per item for the others).
+__global__ void __launch_bounds__(NT) k_apply_t(const ApplyTArgs args, const __grid_constant__ BatchViews bv, const int ntasks) {
+    const long total = (long)ntasks * args.B;
+    for (long w = blockIdx.x; w < total; w += gridDim.x) {
+        __syncthreads();  // shared staging of the previous item is no longer read
+        apply_t_item(args, bv, (int)(w / args.B), (int)(w % args.B));
+    }
+}
+
 // One output slab (<= 64 rows, all k columns): Y = sum over dense leaves of D (or D^T) X
 // plus sum over Rk leaves of Out T, operands staged through shared memory.
-__global__ void __launch_bounds__(NT) k_apply(ApplyArgs args, BatchViews bv) {
+__device__ __forceinline__ void apply_item(const ApplyArgs& args, const BatchViews& bv, const int ti, const int b) {
     __shared__ double As[64 * AP_LDA];
     __shared__ double Bs[32 * AP_LDB];
-    const ApplyTask task = args.tasks[blockIdx.x];
-    const int b = blockIdx.y;
+    const ApplyTask task = args.tasks[ti];
     const Slot s = args.slots[(size_t)task.prod * args.B + b];
     const int k = s.rank;
     if (k == 0) return;
     const bool trans = task.kind == P_RK_LEFT;
     const HView& H = trans ? bv.b[b] : bv.a[b];
     const double* X = trans ? bv.a[b].V[task.kx] : bv.b[b].U[task.kx];
-    const int ldx = args.x_ld[blockIdx.x];
+    const int ldx = args.x_ld[ti];
     double* Y = trans ? s.V : s.U;
     const int ldy = trans ? s.ldv : s.ldu;
     const int r0 = task.r0, nr = task.r1 - task.r0;
@@ -932,6 +940,16 @@ __global__ void __launch_bounds__(NT) k_apply(ApplyArgs args, BatchViews bv) {
     if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, fl);
 }
 
+// Grid-stride over (task, plane) items (see item_grid: capped for k_apply_t, whose many
+// rank-0 items return at once; one CTA per item for the others).
+__global__ void __launch_bounds__(NT) k_apply(const ApplyArgs args, const __grid_constant__ BatchViews bv, const int ntasks) {
+    const long total = (long)ntasks * args.B;
+    for (long w = blockIdx.x; w < total; w += gridDim.x) {
+        __syncthreads();  // shared staging of the previous item is no longer read
+        apply_item(args, bv, (int)(w / args.B), (int)(w % args.B));
+    }
+}
+
 // ------------------------------------------------------------------ dense-target deposits
 struct DepArgs {
     const DepTask* tasks;
@@ -941,9 +959,8 @@ struct DepArgs {
     FlopLedger* flops;
 };
 
-__global__ void __launch_bounds__(NT) k_deposit(DepArgs args, BatchViews bv) {
-    const DepTask task = args.tasks[blockIdx.x];
-    const int b = blockIdx.y;
+__device__ __forceinline__ void deposit_item(const DepArgs& args, const BatchViews& bv, const int ti, const int b) {
+    const DepTask task = args.tasks[ti];
     double* Cd = bv.c[b].dense + task.doff;
     const int m = task.m, n = task.n;
     double fl = 0;
@@ -973,6 +990,16 @@ __global__ void __launch_bounds__(NT) k_deposit(DepArgs args, BatchViews bv) {
         Cd[e] = c;
     }
     if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, fl);
+}
+
+// Grid-stride over (task, plane) items (see item_grid: capped for k_apply_t, whose many
+// rank-0 items return at once; one CTA per item for the others).
+__global__ void __launch_bounds__(NT) k_deposit(const DepArgs args, const __grid_constant__ BatchViews bv, const int ntasks) {
+    const long total = (long)ntasks * args.B;
+    for (long w = blockIdx.x; w < total; w += gridDim.x) {
+        __syncthreads();  // shared staging of the previous item is no longer read
+        deposit_item(args, bv, (int)(w / args.B), (int)(w % args.B));
+    }
 }
 
 // ------------------------------------------------------------------ dense leaf inversion
@@ -1851,6 +1878,13 @@ void launch_sigma1_small(cudaStream_t st, int nc, int nleaf, const long* doff, c
     else k_sigma1_dense<<<dim3(nleaf, B), NT, trunc_smem(), st>>>(a, bv);
 }
 
+// Grid of a grid-stride item kernel: `per_sm` resident CTAs on each of the 148 SMs, four
+// rounds of them, never more CTAs than items (per_sm 0: one CTA per item).
+static unsigned item_grid(long items, int per_sm) {
+    const long cap = per_sm > 0 ? 148L * per_sm * 4 : items;
+    return (unsigned)(items < cap ? (items > 0 ? items : 1) : cap);
+}
+
 void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slot* slots, int B, Arena arena,
                         const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
@@ -1865,7 +1899,7 @@ void launch_apply_t(cudaStream_t st, int ntasks, const ApplyTTask* tasks, Slot* 
     if (ntasks == 0 || B == 0) return;
     ApplyTArgs a{tasks, slots, B, nprod, arena, ledger(flops, "k_apply_t")};
     ProfScope _ps(st, "k_apply_t", (long)ntasks * B);
-    k_apply_t<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
+    k_apply_t<<<item_grid((long)ntasks * B, 3), NT, 0, st>>>(a, bv, ntasks);
 }
 
 void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
@@ -1873,7 +1907,8 @@ void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const App
     if (ntasks == 0 || B == 0) return;
     ApplyArgs a{tasks, leaves, slots, B, nprod, x_ld, ledger(flops, "k_apply")};
     ProfScope _ps(st, "k_apply", (long)((ntasks)*(B)));
-    k_apply<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
+    // one CTA per item: the slab products vary too much in cost for a static stride (measured)
+    k_apply<<<item_grid((long)ntasks * B, 0), NT, 0, st>>>(a, bv, ntasks);
 }
 
 void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Part* parts, const Slot* slots, int B,
@@ -1881,7 +1916,7 @@ void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Par
     if (ntasks == 0 || B == 0) return;
     DepArgs a{tasks, parts, slots, B, ledger(flops, "k_deposit")};
     ProfScope _ps(st, "k_deposit", (long)((ntasks)*(B)));
-    k_deposit<<<dim3(ntasks, B), NT, 0, st>>>(a, bv);
+    k_deposit<<<item_grid((long)ntasks * B, 0), NT, 0, st>>>(a, bv, ntasks);
 }
 
 void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, unsigned long long call_id,

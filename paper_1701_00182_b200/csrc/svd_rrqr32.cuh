@@ -105,17 +105,18 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
             sm.tau[k] = tau;
         }
         tau = __shfl_sync(FULL, tau, k);
-        double vv[32];
-#pragma unroll
-        for (int i = k + 1; i < 32; ++i) vv[i] = __shfl_sync(FULL, a[i], k);
+        __syncwarp();  // reflector k (sm.H[k][k+1..31], written by lane k) visible to the warp
         if (lane > k && tau != 0.0) {
+            // the reflector is read from shared memory (broadcast) rather than shuffled into
+            // 31 registers: keeps the engine under 170 registers (6 CTAs per SM)
+            const volatile double* hk = sm.H[k];
             double s = a[k];
 #pragma unroll
-            for (int i = k + 1; i < 32; ++i) s = fma(vv[i], a[i], s);
+            for (int i = k + 1; i < 32; ++i) s = fma(hk[i], a[i], s);
             s *= tau;
             a[k] -= s;
 #pragma unroll
-            for (int i = k + 1; i < 32; ++i) a[i] = fma(-s, vv[i], a[i]);
+            for (int i = k + 1; i < 32; ++i) a[i] = fma(-s, hk[i], a[i]);
         }
         rp = k + 1;
     }
@@ -205,19 +206,25 @@ __device__ __forceinline__ void warp_sigma_pos32(const double (&a)[32], int rp, 
 // Phase 3: write U' (m x r) = Q [J Sigma; 0] and V' (n x r) = P W Sigma^{-1}.
 // J Sigma is recovered as R W Sigma^{-1} (R = J W^T), with R^T still staged in sm.T,
 // so the Jacobi sweeps never accumulate J.
-__device__ void warp_write32(const double (&a)[32], int m, int n, int rp, double sig, int pos, int r, Warp32Smem& sm,
+__device__ void warp_write32(double (&a)[32], int m, int n, int rp, double sig, int pos, int r, Warp32Smem& sm,
                              double* Uo, double* Vo) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
     if (lane < rp && pos < r) {
         const double inv = 1.0 / sig;
-        double x[32];
+        double* w = Vo + (size_t)pos * n;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < n) w[sm.perm[j]] = a[j] * inv;
+        // x = R W_c / sigma in place over a[]: R is upper triangular (R[i][j] = T[j][i] = 0
+        // for j < i), so x[i] only needs a[j >= i], which are not yet overwritten
+        double (&x)[32] = a;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             double acc = 0.0;
             if (i < rp) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) acc = fma(sm.T[j][i], a[j], acc);  // R[i][j] = T[j][i]
+                for (int j = i; j < 32; ++j) acc = fma(sm.T[j][i], a[j], acc);  // R[i][j] = T[j][i]
             }
             x[i] = acc * inv;
         }
@@ -240,10 +247,6 @@ __device__ void warp_write32(const double (&a)[32], int m, int n, int rp, double
 #pragma unroll
         for (int i = 0; i < 32; ++i)
             if (i < m) u[i] = x[i];
-        double* w = Vo + (size_t)pos * n;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < n) w[sm.perm[j]] = a[j] * inv;
     }
     __syncwarp();
 }
