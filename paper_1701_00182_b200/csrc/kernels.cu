@@ -1022,8 +1022,7 @@ __global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
     double* Out = bv.c[b].dense + task.doff;
     double* LU = smem;                 // n x n
     double* Ao = LU + n * n;           // original (for the 1-norm)
-    double* vx = Ao + n * n;           // work vectors
-    double* vz = vx + n;
+    double* vx = Ao + n * n;           // work vector (permutations of the condition estimate)
     for (int e = threadIdx.x; e < n * n; e += NT) {
         LU[e] = A[e];
         Ao[e] = A[e];
@@ -1067,89 +1066,140 @@ __global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
         }
         __syncthreads();
     }
-    // Hager / Higham 1-norm condition estimate (one warp, sequential solves)
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
+    // Row permutation of the pivoting: (P b)[i] = b[perm[i]] (the swaps piv[0..n) in order).
+    __shared__ int perm[DENSE_MAX];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) perm[i] = i;
+        for (int k = 0; k < n; ++k) {
+            const int t = perm[k];
+            perm[k] = perm[piv[k]];
+            perm[piv[k]] = t;
+        }
+    }
+    zero_pivot = false;
+    for (int k = 0; k < n; ++k) zero_pivot |= (LU[k + k * n] == 0.0);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+    // Warp-parallel triangular solves: lane owns rows lane and lane + 32 (y0, y1); each step
+    // broadcasts the finished entry k from its owner lane.  Per element the updates run in
+    // the same order as the sequential column-oriented substitution.
+    auto own = [&](int k, double y0, double y1) { return __shfl_sync(FULL, k < 32 ? y0 : y1, k & 31); };
+    auto lsolve = [&](double& y0, double& y1) {  // L y = y (unit lower)
+        for (int k = 0; k < n - 1; ++k) {
+            const double xk = own(k, y0, y1);
+            if (lane > k && lane < n) y0 = fma(-LU[lane + k * n], xk, y0);
+            if (lane + 32 > k && lane + 32 < n) y1 = fma(-LU[lane + 32 + k * n], xk, y1);
+        }
+    };
+    auto usolve = [&](double& y0, double& y1) {  // U y = y
+        for (int k = n - 1; k >= 0; --k) {
+            if (lane == (k & 31)) {
+                if (k < 32) y0 /= LU[k + k * n];
+                else y1 /= LU[k + k * n];
+            }
+            const double xk = own(k, y0, y1);
+            if (lane < k) y0 = fma(-LU[lane + k * n], xk, y0);
+            if (lane + 32 < k) y1 = fma(-LU[lane + 32 + k * n], xk, y1);
+        }
+    };
+    if (warp == 0) {
+        // Hager / Higham 1-norm condition estimate (rcond of Eigen's PartialPivLU), warp 0
         double anorm = 0;
         for (int c = 0; c < n; ++c) {
-            double s = 0;
-            for (int i = lane; i < n; i += 32) s += fabs(Ao[i + c * n]);
-            s = warp_sum(s);
-            anorm = fmax(anorm, s);
+            double s2 = 0;
+            for (int i = lane; i < n; i += 32) s2 += fabs(Ao[i + c * n]);
+            s2 = warp_sum(s2);
+            anorm = fmax(anorm, s2);
         }
-        auto solve = [&](double* x) {  // A x = b in place
+        const bool r0 = lane < n, r1 = lane + 32 < n;
+        auto solve = [&](double& y0, double& y1) {  // A x = b: x = U^-1 L^-1 P b
             __syncwarp();
-            if (lane == 0) {
-                for (int k = 0; k < n; ++k) { const double t = x[k]; x[k] = x[piv[k]]; x[piv[k]] = t; }
-                for (int k = 0; k < n; ++k)
-                    for (int i = k + 1; i < n; ++i) x[i] -= LU[i + k * n] * x[k];
-                for (int k = n - 1; k >= 0; --k) {
-                    x[k] /= LU[k + k * n];
-                    for (int i = 0; i < k; ++i) x[i] -= LU[i + k * n] * x[k];
-                }
-            }
+            if (r0) vx[lane] = y0;
+            if (r1) vx[lane + 32] = y1;
             __syncwarp();
+            y0 = r0 ? vx[perm[lane]] : 0.0;
+            y1 = r1 ? vx[perm[lane + 32]] : 0.0;
+            lsolve(y0, y1);
+            usolve(y0, y1);
         };
-        auto solve_t = [&](double* x) {  // A^T x = b in place
-            __syncwarp();
-            if (lane == 0) {
-                for (int k = 0; k < n; ++k) {
-                    for (int i = 0; i < k; ++i) x[k] -= LU[i + k * n] * x[i];
-                    x[k] /= LU[k + k * n];
+        auto solve_t = [&](double& y0, double& y1) {  // A^T x = b: x = P^T L^-T U^-T b
+            for (int k = 0; k < n; ++k) {  // U^T w = b (forward, column-oriented)
+                if (lane == (k & 31)) {
+                    if (k < 32) y0 /= LU[k + k * n];
+                    else y1 /= LU[k + k * n];
                 }
-                for (int k = n - 1; k >= 0; --k)
-                    for (int i = k + 1; i < n; ++i) x[k] -= LU[i + k * n] * x[i];
-                for (int k = n - 1; k >= 0; --k) { const double t = x[k]; x[k] = x[piv[k]]; x[piv[k]] = t; }
+                const double xk = own(k, y0, y1);
+                if (lane > k && r0) y0 = fma(-LU[k + lane * n], xk, y0);
+                if (lane + 32 > k && r1) y1 = fma(-LU[k + (lane + 32) * n], xk, y1);
+            }
+            for (int k = n - 1; k > 0; --k) {  // L^T v = w (unit upper)
+                const double xk = own(k, y0, y1);
+                if (lane < k) y0 = fma(-LU[k + lane * n], xk, y0);
+                if (lane + 32 < k) y1 = fma(-LU[k + (lane + 32) * n], xk, y1);
             }
             __syncwarp();
+            if (r0) vx[perm[lane]] = y0;
+            if (r1) vx[perm[lane + 32]] = y1;
+            __syncwarp();
+            y0 = r0 ? vx[lane] : 0.0;
+            y1 = r1 ? vx[lane + 32] : 0.0;
         };
         double rc = 0.0;
-        bool zp = false;
-        for (int k = 0; k < n; ++k) zp |= (LU[k + k * n] == 0.0);
-        if (anorm > 0 && !zp) {
+        if (anorm > 0 && !zero_pivot) {
             double est = 0;
-            for (int i = lane; i < n; i += 32) vx[i] = 1.0 / n;
+            double x0 = r0 ? 1.0 / n : 0.0, x1 = r1 ? 1.0 / n : 0.0;  // current probe vector
             for (int it = 0; it < 5; ++it) {
-                __syncwarp();
-                for (int i = lane; i < n; i += 32) vz[i] = vx[i];
-                solve(vz);
-                double ny = 0;
-                for (int i = lane; i < n; i += 32) ny += fabs(vz[i]);
-                ny = warp_sum(ny);
+                double z0 = x0, z1 = x1;
+                solve(z0, z1);
+                const double ny = warp_sum(fabs(z0) + fabs(z1));
                 if (it > 0 && ny <= est) break;
                 est = ny;
-                __syncwarp();
-                for (int i = lane; i < n; i += 32) vz[i] = vz[i] >= 0 ? 1.0 : -1.0;
-                solve_t(vz);
-                double zmax = -1;
-                int jmax = 0;
-                if (lane == 0)
-                    for (int i = 0; i < n; ++i)
-                        if (fabs(vz[i]) > zmax) { zmax = fabs(vz[i]); jmax = i; }
-                zmax = __shfl_sync(0xffffffffu, zmax, 0);
-                jmax = __shfl_sync(0xffffffffu, jmax, 0);
-                double ztx = 0;
-                for (int i = lane; i < n; i += 32) ztx += vz[i] * vx[i];
-                ztx = warp_sum(ztx);
+                z0 = r0 ? (z0 >= 0 ? 1.0 : -1.0) : 0.0;
+                z1 = r1 ? (z1 >= 0 ? 1.0 : -1.0) : 0.0;
+                solve_t(z0, z1);
+                // first index of max |z|
+                double zmax = fmax(r0 ? fabs(z0) : -1.0, r1 ? fabs(z1) : -1.0);
+                int jmax = (r1 && fabs(z1) > (r0 ? fabs(z0) : -1.0)) ? lane + 32 : lane;
+                for (int o = 16; o; o >>= 1) {
+                    const double ob = __shfl_xor_sync(FULL, zmax, o);
+                    const int oj = __shfl_xor_sync(FULL, jmax, o);
+                    if (ob > zmax || (ob == zmax && oj < jmax)) {
+                        zmax = ob;
+                        jmax = oj;
+                    }
+                }
+                const double ztx = warp_sum(z0 * x0 + z1 * x1);
                 if (it > 0 && zmax <= ztx) break;
-                __syncwarp();
-                for (int i = lane; i < n; i += 32) vx[i] = (i == jmax) ? 1.0 : 0.0;
+                x0 = (lane == jmax) ? 1.0 : 0.0;
+                x1 = (lane + 32 == jmax) ? 1.0 : 0.0;
             }
-            __syncwarp();
-            for (int i = lane; i < n; i += 32) vz[i] = ((i % 2) ? -1.0 : 1.0) * (1.0 + double(i) / (n > 1 ? n - 1 : 1));
-            solve(vz);
-            double na = 0;
-            for (int i = lane; i < n; i += 32) na += fabs(vz[i]);
-            na = warp_sum(na);
+            auto alt = [&](int i) { return ((i % 2) ? -1.0 : 1.0) * (1.0 + double(i) / (n > 1 ? n - 1 : 1)); };
+            double z0 = r0 ? alt(lane) : 0.0, z1 = r1 ? alt(lane + 32) : 0.0;
+            solve(z0, z1);
+            const double na = warp_sum(fabs(z0) + fabs(z1));
             est = fmax(est, 2.0 * na / (3.0 * n));
             rc = (est > 0 && isfinite(est)) ? 1.0 / (anorm * est) : 0.0;
         }
         if (lane == 0) sh_rcond = rc;
+    } else {
+        // inverse, warps 1..NT/32-1: column c of A^{-1} = U^-1 L^-1 P e_c
+        for (int c = warp - 1; c < n; c += NT / 32 - 1) {
+            double* x = Out + (size_t)c * n;
+            if (zero_pivot) {
+                for (int i = lane; i < n; i += 32) x[i] = 0.0;
+                continue;
+            }
+            double y0 = (lane < n && perm[lane] == c) ? 1.0 : 0.0;
+            double y1 = (lane + 32 < n && perm[lane + 32] == c) ? 1.0 : 0.0;
+            lsolve(y0, y1);
+            usolve(y0, y1);
+            if (lane < n) x[lane] = y0;
+            if (lane + 32 < n) x[lane + 32] = y1;
+        }
     }
     __syncthreads();
     const double rcond = sh_rcond;
-    zero_pivot = false;
-    for (int k = 0; k < n; ++k) zero_pivot |= (LU[k + k * n] == 0.0);
     if (!(rcond > 1e-14)) {
         if (threadIdx.x == 0) {
             const unsigned long long key = (args.call_id << 16) | (unsigned long long)b;
@@ -1161,24 +1211,6 @@ __global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
                 args.err->rcond = rcond;
             }
         }
-    }
-    // inverse: column c of A^{-1} solves A x = e_c (thread per column)
-    for (int c = threadIdx.x; c < n; c += NT) {
-        double* x = Out + (size_t)c * n;
-        if (zero_pivot) {
-            for (int i = 0; i < n; ++i) x[i] = 0.0;
-            continue;
-        }
-        double xr[DENSE_MAX];
-        for (int i = 0; i < n; ++i) xr[i] = (i == c) ? 1.0 : 0.0;
-        for (int k = 0; k < n; ++k) { const double t = xr[k]; xr[k] = xr[piv[k]]; xr[piv[k]] = t; }
-        for (int k = 0; k < n; ++k)
-            for (int i = k + 1; i < n; ++i) xr[i] -= LU[i + k * n] * xr[k];
-        for (int k = n - 1; k >= 0; --k) {
-            xr[k] /= LU[k + k * n];
-            for (int i = 0; i < k; ++i) xr[i] -= LU[i + k * n] * xr[k];
-        }
-        for (int i = 0; i < n; ++i) x[i] = xr[i];
     }
     if (threadIdx.x == 0) add_flops(args.flops, F_LU, 2.0 * n * n * n);
 }
