@@ -23,6 +23,8 @@
  *                        <- acr::execute_parallel_factor(system, plan, config)
  *                           core/include/acr/parallel.hpp:60-61, core/src/parallel.cpp:96-297;
  *                           plane ownership = plan_schedule(n, p) (parallel.cpp:383-405)
+ *   acrgpu_messages      <- ParallelRun::ledger records (MessageLedger, parallel.hpp:24-48,
+ *                           parallel.cpp:142-161,356-378)
  *
  * Errors map 1:1 onto the reference exception classes (core/include/acr/errors.hpp:10-60):
  *   ACRGPU_E_DIMENSION  DimensionError(plane)        ACRGPU_E_SINGULAR  SingularBlockError(level, plane)
@@ -193,6 +195,20 @@ int acrgpu_factor_partitioned(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_s
 /* Same, on a system already uploaded with acrgpu_system_upload. */
 int acrgpu_factor_partitioned_resident(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_dsystem* sys,
                                        const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err);
+/* Cross-rank elimination payloads of a partitioned factorization (MessageRecord,
+ * core/include/acr/parallel.hpp:24-30; recorded as in parallel.cpp:142-161): one record per
+ * (eliminated plane, destination rank), bytes = memory_footprint of {Dinv, E, F} as sent
+ * (before the stored-inverse trim) + 8*dim for the plane right-hand side.  Records of all
+ * ranks held by this handle (every rank for an in-process communicator, this rank's own
+ * sends for NCCL).  Returns the record count (written up to cap); 0 for acrgpu_factor. */
+typedef struct acrgpu_message {
+    int level;
+    int from_plane;
+    int to_plane;
+    int solve_phase;               /* always 0 here; solve-phase {u} records follow from the plan */
+    long bytes;
+} acrgpu_message;
+long acrgpu_messages(acrgpu_fact* f, acrgpu_message* out, long cap);
 
 /* ---- Krylov drivers with the GPU factorization as preconditioner
  * (core/include/acr/krylov.hpp:8-35, core/src/krylov.cpp:38-133).  One right-hand side

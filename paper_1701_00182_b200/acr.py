@@ -151,6 +151,11 @@ class _Timing(C.Structure):
                 ("solve_launches", C.c_long)]
 
 
+class _Msg(C.Structure):
+    _fields_ = [("level", C.c_int), ("from_plane", C.c_int), ("to_plane", C.c_int), ("solve_phase", C.c_int),
+                ("bytes", C.c_long)]
+
+
 SYMBOLS = {
     "acrgpu_version": (C.c_char_p, []),
     "acrgpu_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p), C.POINTER(_Err)]),
@@ -167,6 +172,7 @@ SYMBOLS = {
     "acrgpu_level_info": (C.c_int, [C.c_void_p, C.POINTER(_Level), C.c_int]),
     "acrgpu_dinv_ranks": (C.c_long, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_long]),
     "acrgpu_timing_get": (C.c_int, [C.c_void_p, C.POINTER(_Timing)]),
+    "acrgpu_messages": (C.c_long, [C.c_void_p, C.POINTER(_Msg), C.c_long]),
     "acrgpu_profile_report": (C.c_long, [C.c_char_p, C.c_long, C.c_int]),
     "acrgpu_structure": (C.c_long, [C.c_int, C.POINTER(C.c_double), C.c_int, C.c_double, C.c_int,
                                      C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_long, C.POINTER(_Err)]),
@@ -340,6 +346,14 @@ class AcrFactorization:
         lib().acrgpu_dinv_ranks(self.h, level, plane, _p(out, C.c_int), n)
         return out
 
+    def messages(self) -> list:
+        """Elimination-payload records of a partitioned factorization (MessageRecord,
+        parallel.hpp:24-30); empty for a single-rank factorization."""
+        k = lib().acrgpu_messages(self.h, None, 0)
+        arr = (_Msg * max(k, 1))()
+        k = lib().acrgpu_messages(self.h, arr, k)
+        return [MessageRecord(a.level, a.from_plane, a.to_plane, int(a.bytes), bool(a.solve_phase)) for a in arr[:k]]
+
     def timing(self) -> dict:
         t = _Timing()
         lib().acrgpu_timing_get(self.h, C.byref(t))
@@ -465,6 +479,75 @@ def acr_factor_partitioned(system, comm: Comm, config: AcrConfig | None = None, 
     f = AcrFactorization(h, system, config, ctx)
     f._comm = comm  # keep the communicator alive
     return f
+
+
+@dataclasses.dataclass
+class MessageRecord:
+    """parallel.hpp:24-30."""
+    level: int
+    from_plane: int
+    to_plane: int
+    bytes: int
+    solve_phase: bool = False
+
+
+@dataclasses.dataclass
+class LevelTraffic:
+    """parallel.hpp:32-38."""
+    level: int = 0
+    messages: int = 0
+    bytes: int = 0
+    active_workers: int = 0
+    idle_workers: int = 0
+
+
+@dataclasses.dataclass
+class MessageLedger:
+    """parallel.hpp:40-48: cross-worker traffic per level, factor and solve phases."""
+    factor: list
+    solve: list
+    records: list
+
+    def total_messages(self) -> int:
+        return len(self.records)
+
+    def total_bytes(self) -> int:
+        return sum(r.bytes for r in self.records)
+
+
+def message_ledger(fact: AcrFactorization, plan) -> MessageLedger:
+    """Aggregate a partitioned factorization's records the way run_parallel does
+    (parallel.cpp:356-378).  Factor-phase records come from the device run; the solve
+    phase moves one plane vector u_j (8*dim bytes) from the owner of each retained plane
+    to the owner of each eliminated neighbour held elsewhere (parallel.cpp:264-274),
+    which depends only on the plan."""
+    from .plan import eliminated_positions
+    levels = len(fact.level_info()) - 1
+    factor = [LevelTraffic(level=i) for i in range(levels)]
+    solve = [LevelTraffic(level=i) for i in range(levels)]
+    for i in range(levels):
+        active = len(set(plan.assignment[i]))
+        for part in (factor[i], solve[i]):
+            part.active_workers = active
+            part.idle_workers = plan.p - active
+    records = list(fact.messages())
+    for i in range(levels):
+        own = plan.assignment[i]
+        m = len(own)
+        is_elim = [False] * m
+        for e in eliminated_positions(m):
+            is_elim[e] = True
+        for j in range(m):
+            if is_elim[j]:
+                continue
+            for nb in (j - 1, j + 1):
+                if 0 <= nb < m and is_elim[nb] and own[nb] != own[j]:
+                    records.append(MessageRecord(i, j, nb, 8 * fact.dim, True))
+    for r in records:
+        part = solve[r.level] if r.solve_phase else factor[r.level]
+        part.messages += 1
+        part.bytes += r.bytes
+    return MessageLedger(factor, solve, records)
 
 
 def acr_solve(fact: AcrFactorization, f):

@@ -1091,6 +1091,12 @@ struct Engine {
 };
 
 // ------------------------------------------------------------------ factorization object
+struct HostStats {
+    long rank_sum = 0;
+    int largest = 0, ndense = 0, nrk = 0;
+    long bytes = 0;
+};
+
 struct Level {
     int plane_count = 0;
     std::vector<int> elim, ret;
@@ -1133,6 +1139,7 @@ struct acrgpu_fact {
     int rank = 0;
     std::vector<std::vector<int>> owners;  // per level: plane position -> rank
     std::vector<acrgpu_fact*> vparts;      // in-process ranks of a local communicator (owned)
+    std::vector<acrgpu_message> msgs;      // elimination payloads this rank sent (ledger)
 };
 
 struct acrgpu_comm {
@@ -1539,6 +1546,11 @@ static void mark_level(PartRun& R) {
                 R.rank, R.lev_ev.size(), used * 8.0 / 1e9, E.ctx->persist.cap * 8.0 / 1e9, E.peak_transient_gb, fr / 1e9);
     }
     if (!verbose_levels()) return;
+    static const bool per_level_kernels = getenv("ACRGPU_PROFILE") != nullptr;
+    if (per_level_kernels) {  // kernel totals since the previous mark (synchronises)
+        const std::string rep = prof_report(true);
+        fprintf(stderr, "[acrgpu] kernels before mark %zu:\n%s", R.lev_ev.size(), rep.c_str());
+    }
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
     CK(cudaEventRecord(e, R.F->eng->main_st()));
@@ -1844,6 +1856,8 @@ static ImageLayout image_layout(size_t nk, size_t dsize, size_t lr) {
 
 static void ensure_kmn(Engine& E) { E.ensure_kmn_tables(); }
 
+static HostStats store_stats(Engine& E, const SP& s);
+
 static StoreImage pack_store(Engine& E, const SP& s) {
     cudaStream_t st = E.main_st();
     ensure_kmn(E);
@@ -2083,11 +2097,20 @@ static void factor_partitioned(std::vector<PartRun>& runs, const std::vector<std
             const int me = runs[r].rank;
             for (int e : elim) {
                 if (ow[e] != me) continue;
-                std::vector<int> dests;
+                std::vector<int> dests, dest_plane;
                 for (int nb : {e - 1, e + 1})
                     if (nb >= 0 && nb < m && !is_elim[nb] && ow[nb] != me &&
-                        std::find(dests.begin(), dests.end(), ow[nb]) == dests.end())
+                        std::find(dests.begin(), dests.end(), ow[nb]) == dests.end()) {
                         dests.push_back(ow[nb]);
+                        dest_plane.push_back(nb);
+                    }
+                if (!dests.empty()) {  // ledger record per destination (parallel.cpp:150-155)
+                    CK(cudaStreamSynchronize(E.main_st()));
+                    long bytes = 8L * sys.dim + store_stats(E, Ls[r].Dinv[e]).bytes;
+                    if (SP s = at(Ls[r].E, e)) bytes += store_stats(E, s).bytes;
+                    if (SP s = at(Ls[r].F, e)) bytes += store_stats(E, s).bytes;
+                    for (int nb : dest_plane) runs[r].F->msgs.push_back(acrgpu_message{lvl, e, nb, 0, bytes});
+                }
                 for (int d : dests)
                     for (int kind = 0; kind < 3; ++kind) {
                         SP s = kind == 0 ? Ls[r].Dinv[e] : (kind == 1 ? at(Ls[r].E, e) : at(Ls[r].F, e));
@@ -2395,12 +2418,6 @@ static void do_solve(acrgpu_fact* F, int nrhs, const double* f_dev, double* u_de
 }
 
 // ------------------------------------------------------------------ stats
-struct HostStats {
-    long rank_sum = 0;
-    int largest = 0, ndense = 0, nrk = 0;
-    long bytes = 0;
-};
-
 static HostStats store_stats(Engine& E, const SP& s) {
     HostStats h;
     if (!s) return h;
@@ -2986,6 +3003,16 @@ long acrgpu_dinv_ranks(acrgpu_fact* f, int li, int j, int* out, long cap) {
         return n;
     }
     return -1;
+}
+
+long acrgpu_messages(acrgpu_fact* f, acrgpu_message* out, long cap) {
+    long n = 0;
+    for (acrgpu_fact* p : parts_of(f))
+        for (const acrgpu_message& m : p->msgs) {
+            if (out && n < cap) out[n] = m;
+            ++n;
+        }
+    return n;
 }
 
 int acrgpu_timing_get(acrgpu_fact* f, acrgpu_timing* out) {

@@ -12,6 +12,9 @@ flattened.  Right-hand sides are ``rhs[r, j, i]`` (RHS r, plane j, point i).
 Generators:
   poisson(n)            reference assemble_poisson   (proj/core/src/discretize.cpp:46-71)
   poisson2d_block(n)    reference poisson2d_block    (discretize.cpp:227-242)
+  convdiff_vortex(n, alpha, a)  reference assemble_convdiff (discretize.cpp:73-174)
+  helmholtz_fem(n, kappa)       reference assemble_helmholtz (discretize.cpp:176-214)
+  assemble(kind, n, ...)        reference assemble(ProblemSpec) (discretize.hpp:55)
   config_system(k)      BASELINE.json configs[k-1] with the builder decisions of
                         SURVEY.md §8(d) (documented in DESIGN.md §2).
 The portable RNG is splitmix64 -> 53-bit doubles; Box-Muller for
@@ -296,6 +299,189 @@ def helmholtz7(n: int, seed: int, omega: float = 2 * math.pi * 6.4, nrhs: int = 
     rhs[:, c, c * n + c] += 1.0
     return _constant_coeff(n, 6.0 - omega * omega * h * h, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, rhs,
                            f"helmholtz{n}")
+
+
+# ----------------------------------------------------------------------------
+# The reference's own generators behind acr::assemble (discretize.hpp:10-55)
+# ----------------------------------------------------------------------------
+
+PROBLEM_KINDS = ("poisson", "convdiff", "helmholtz")
+
+
+def parse_problem_kind(name: str) -> str:
+    """discretize.cpp:25-30 (UsageError on unknown names is raised by the caller's layer)."""
+    if name not in PROBLEM_KINDS:
+        raise ValueError(f"unknown problem kind: {name}")
+    return name
+
+
+def helmholtz_kappa_for(n: int) -> float:
+    """~12 points per wavelength (discretize.cpp:41-44)."""
+    return n / 2.0
+
+
+def _plane_block(entries_r, entries_c, entries_v):
+    """PlaneBlock construction (block.cpp:7-29): sort by (row, col) -- stable, so
+    duplicates keep their insertion order -- then sum duplicates left to right."""
+    r = np.concatenate(entries_r).astype(np.int64)
+    c = np.concatenate(entries_c).astype(np.int64)
+    v = np.concatenate(entries_v).astype(np.float64)
+    order = np.lexsort((c, r))  # lexsort is stable
+    r, c, v = r[order], c[order], v[order]
+    if len(r) == 0:
+        return r.astype(np.int32), c.astype(np.int32), v
+    new = np.ones(len(r), bool)
+    new[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+    starts = np.flatnonzero(new)
+    out_v = np.add.reduceat(v, starts)  # runs of <= 8 duplicates sum left to right
+    return r[starts].astype(np.int32), c[starts].astype(np.int32), out_v
+
+
+def convdiff_vortex(n: int, alpha: float, a: float = 1.0) -> System:
+    """Reference assemble_convdiff (discretize.cpp:73-174): 7-point diffusion plus
+    alpha * b(x).grad u with the three-component vortex field b and first-order upwind
+    differences, h^2-scaled; the right-hand side is A applied to the sampled reference
+    solution sum_d sin(pi x_d) + sin(3 pi x_d), which is returned as ``exact``."""
+    if alpha < 0:
+        raise ValueError("assemble_convdiff: alpha must be nonnegative")
+    if n < 2:
+        raise ValueError("GridSpec: n must be >= 2")
+    h = 1.0 / (n + 1)
+    m = n * n
+    jj, ii = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    i = ii.ravel()
+    j = jj.ravel()
+    r = j * n + i
+    x = (i + 1) * h
+    y = (j + 1) * h
+    t = 2.0 * math.pi * a
+    Dblocks, Eblocks, Fblocks = [], [], []
+    for z in range(n):
+        zc = (z + 1) * h
+        # per-row insertion order of the reference: centre, W, E, S, N, then E/F -1,
+        # then the three upwind terms.  Stable sorting keeps that order within a row,
+        # so build columns of (row, insertion slot) and sort once.
+        dr, dc, dv, ds = [], [], [], []
+        er, ec, ev = [], [], []
+        fr, fc, fv = [], [], []
+
+        def add(lst, rows, cols, vals, slot):
+            lst[0].append(rows)
+            lst[1].append(cols)
+            lst[2].append(np.broadcast_to(np.asarray(vals, np.float64), rows.shape).copy())
+            if len(lst) > 3:
+                lst[3].append(np.full(rows.shape, slot))
+
+        D = (dr, dc, dv, ds)
+        add(D, r, r, 6.0, 0)
+        msk = i > 0
+        add(D, r[msk], r[msk] - 1, -1.0, 1)
+        msk = i < n - 1
+        add(D, r[msk], r[msk] + 1, -1.0, 2)
+        msk = j > 0
+        add(D, r[msk], r[msk] - n, -1.0, 3)
+        msk = j < n - 1
+        add(D, r[msk], r[msk] + n, -1.0, 4)
+        er.append(r)
+        ec.append(r)
+        ev.append(np.full(m, -1.0))
+        fr.append(r)
+        fc.append(r)
+        fv.append(np.full(m, -1.0))
+        if alpha != 0.0:
+            b1 = np.sin(t * x) * np.sin(t * (0.125 + y)) + np.sin(t * (0.125 + zc)) * np.sin(t * x)
+            b2 = np.cos(t * x) * np.cos(t * (0.125 + y)) + np.cos(t * (0.125 + y)) * np.cos(t * zc)
+            b3 = np.cos(t * x) * np.cos(t * (0.125 + zc)) + np.sin(t * (0.125 + y)) * np.sin(t * zc)
+            slot = 5
+            for bd, lo_in, hi_in, off, axis in ((b1, i > 0, i < n - 1, 1, 0), (b2, j > 0, j < n - 1, n, 1),
+                                                (b3, None, None, 0, 2)):
+                c = alpha * h * bd
+                nz = c != 0.0
+                pos = nz & (bd > 0)
+                neg = nz & ~(bd > 0)
+                # diagonal: +c when bd > 0, -c otherwise (both inserted into D)
+                add(D, r[pos], r[pos], c[pos], slot)
+                add(D, r[neg], r[neg], -c[neg], slot)
+                if axis < 2:
+                    lo = pos & lo_in
+                    add(D, r[lo], r[lo] - off, -c[lo], slot + 1)
+                    hi = neg & hi_in
+                    add(D, r[hi], r[hi] + off, c[hi], slot + 1)
+                else:
+                    if z > 0:
+                        er.append(r[pos])
+                        ec.append(r[pos])
+                        ev.append(-c[pos])
+                    if z < n - 1:
+                        fr.append(r[neg])
+                        fc.append(r[neg])
+                        fv.append(c[neg])
+                slot += 2
+        # reference order within a row: insertion order; rows interleave, so sort by
+        # (row, slot) first to reproduce it, then the PlaneBlock sort/merge
+        R = np.concatenate(dr)
+        S = np.concatenate(ds)
+        o = np.lexsort((S, R))
+        Dblocks.append(_plane_block([R[o]], [np.concatenate(dc)[o]], [np.concatenate(dv)[o]]))
+        Eblocks.append(_plane_block(er, ec, ev))
+        Fblocks.append(_plane_block(fr, fc, fv))
+    u = np.empty((n, m))
+    for z in range(n):
+        zc = (z + 1) * h
+        u[z] = (np.sin(math.pi * x) + np.sin(math.pi * y) + math.sin(math.pi * zc) +
+                np.sin(3 * math.pi * x) + np.sin(3 * math.pi * y) + math.sin(3 * math.pi * zc))
+    blocks = Dblocks + Eblocks[1:] + Fblocks[:-1]
+    sysm = _assemble(n, m, plane_coords(n), blocks, np.zeros((1, n, m)), f"convdiff_vortex{n}")
+    sysm.rhs = sysm.apply(u[None])
+    sysm.exact = u
+    return sysm
+
+
+def helmholtz_fem(n: int, kappa: float) -> System:
+    """Reference assemble_helmholtz (discretize.cpp:176-214): 27-point trilinear FEM
+    K - kappa^2 M from 1D stiffness/mass stencils; D/E/F are 9-point plane blocks;
+    f = h^3."""
+    if n < 2:
+        raise ValueError("GridSpec: n must be >= 2")
+    h = 1.0 / (n + 1)
+    m = n * n
+    k1 = (-1.0 / h, 2.0 / h, -1.0 / h)
+    m1 = (h / 6.0, 4.0 * h / 6.0, h / 6.0)
+    w = np.zeros((3, 3, 3))
+    for dz in range(3):
+        for dy in range(3):
+            for dx in range(3):
+                w[dx, dy, dz] = (k1[dx] * m1[dy] * m1[dz] + m1[dx] * k1[dy] * m1[dz] + m1[dx] * m1[dy] * k1[dz]
+                                 - kappa * kappa * m1[dx] * m1[dy] * m1[dz])
+    jj, ii = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    i = ii.ravel()
+    j = jj.ravel()
+    r = j * n + i
+    out = {0: ([], [], []), 1: ([], [], []), 2: ([], [], [])}
+    for dy in (-1, 0, 1):
+        for dx in (-1, 0, 1):
+            ok = (i + dx >= 0) & (i + dx < n) & (j + dy >= 0) & (j + dy < n)
+            c = (j + dy) * n + (i + dx)
+            for dz in range(3):
+                out[dz][0].append(r[ok])
+                out[dz][1].append(c[ok])
+                out[dz][2].append(np.full(int(ok.sum()), w[dx + 1, dy + 1, dz]))
+    D = _plane_block(*out[1])
+    E = _plane_block(*out[0])
+    F = _plane_block(*out[2])
+    blocks = [D] * n + [E] * (n - 1) + [F] * (n - 1)
+    return _assemble(n, m, plane_coords(n), blocks, np.full((1, n, m), h ** 3), f"helmholtz_fem{n}")
+
+
+def assemble(kind: str, n: int, alpha: float = 0.0, a: float = 1.0, kappa: float = 0.0) -> System:
+    """acr::assemble(ProblemSpec) (discretize.hpp:55; report.cpp:333-339 passes kappa
+    through, 0 meaning helmholtz_kappa_for(n) at the CLI)."""
+    kind = parse_problem_kind(kind)
+    if kind == "poisson":
+        return poisson(n)
+    if kind == "convdiff":
+        return convdiff_vortex(n, alpha, a)
+    return helmholtz_fem(n, kappa if kappa > 0 else helmholtz_kappa_for(n))
 
 
 def first_planes(sysm: System, k: int) -> System:
