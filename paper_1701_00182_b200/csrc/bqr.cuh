@@ -325,6 +325,18 @@ __device__ void wy_update(double* A, int lda, int h, int nc, const double* V, in
     // 2. W <- -op(T) (sum of slices): thread per (column, output row), in place by
     // column-disjoint chunks; T staged with ld 17 (conflict-free for both transposes)
     for (int e = threadIdx.x; e < BQR_NB * BQR_NB; e += NT) Tpad[(e % BQR_NB) + (e / BQR_NB) * (BQR_NB + 1)] = T[e];
+    // fold the row-slice partial sums into slice 0 first (same summation order as summing
+    // them inside the product below; keeps the unrolled product free of a runtime loop,
+    // which the compiler had expanded to ~40k instructions)
+    if (nsp > 1) {
+        for (int e = threadIdx.x; e < nct * 8 * BQR_NB; e += NT) {
+            const int k = e % BQR_NB, c = e / BQR_NB;
+            double wk = Ws[k + (size_t)c * BQR_LDW];
+#pragma unroll 1
+            for (int sp = 1; sp < nsp; ++sp) wk += Ws[(size_t)sp * slice + k + (size_t)c * BQR_LDW];
+            Ws[k + (size_t)c * BQR_LDW] = wk;
+        }
+    }
     __syncthreads();
     {
         const int tot = nct * 8 * BQR_NB;
@@ -339,8 +351,7 @@ __device__ void wy_update(double* A, int lda, int h, int nc, const double* V, in
                     double s = 0;
 #pragma unroll
                     for (int k = 0; k < BQR_NB; ++k) {
-                        double wk = Ws[k + (size_t)c * BQR_LDW];
-                        for (int sp = 1; sp < nsp; ++sp) wk += Ws[(size_t)sp * slice + k + (size_t)c * BQR_LDW];
+                        const double wk = Ws[k + (size_t)c * BQR_LDW];
                         s = fma(trans ? Tpad[k + i * (BQR_NB + 1)] : Tpad[i + k * (BQR_NB + 1)], wk, s);
                     }
                     y[q] = -s;

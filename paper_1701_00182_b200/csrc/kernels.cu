@@ -28,6 +28,18 @@
 #include "kernels.hpp"
 #include "structure.hpp"
 #include "svd_small.cuh"
+namespace acrgpu {
+// warp-engine phase timing (clock64 deltas of lane 0 per task): diagnostics only
+__device__ unsigned long long g_w32_cyc[8];
+__device__ unsigned long long g_w32_cnt;
+__device__ __forceinline__ void w32_mark(int i, unsigned long long& t0) {
+    if ((threadIdx.x & 31) == 0) {
+        const unsigned long long t = clock64();
+        atomicAdd(&g_w32_cyc[i], t - t0);
+        t0 = t;
+    }
+}
+}  // namespace acrgpu
 #include "svd_rrqr32.cuh"
 
 namespace acrgpu {
@@ -1560,7 +1572,7 @@ constexpr int W32_TC = 16;
 // mode 0: truncation task list (TruncArgs); mode 1: dense*dense products (DDArgs).
 // Two warps per CTA, one task per warp (rank-revealing QR + Jacobi, svd_rrqr32.cuh).
 template <int MODE>
-__global__ void __launch_bounds__(64) k_small32(TruncArgs targs, DDArgs dargs, int ntasks, BatchViews bv) {
+__global__ void __launch_bounds__(64, 6) k_small32(TruncArgs targs, DDArgs dargs, int ntasks, BatchViews bv) {
     __shared__ Warp32Smem smem[2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ti = blockIdx.x * 2 + warp;
@@ -1600,6 +1612,8 @@ __global__ void __launch_bounds__(64) k_small32(TruncArgs targs, DDArgs dargs, i
         K = dt.k;
         eps = dargs.eps;
     }
+    unsigned long long wt = clock64();
+    if (lane == 0) atomicAdd(&g_w32_cnt, 1ull);
     double a[32], v[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) a[i] = 0.0;
@@ -1614,11 +1628,10 @@ __global__ void __launch_bounds__(64) k_small32(TruncArgs targs, DDArgs dargs, i
         const double* Ad = bv.a[b].dense + dt.da;
         const double* Bd = bv.b[b].dense + dt.db;
         // A zero operand (the off-diagonal dense leaves of the diagonal level-0 couplings E/F)
-        // gives a zero product, whose truncation is rank 0: skip the GEMM and the SVD.
-        bool nzA = false, nzB = false;
-        for (int e = lane; e < m * dt.k; e += 32) nzA |= Ad[e] != 0.0;
-        for (int e = lane; e < dt.k * n; e += 32) nzB |= Bd[e] != 0.0;
-        if (!__any_sync(0xffffffffu, nzA) || !__any_sync(0xffffffffu, nzB)) {
+        // gives a zero product, whose truncation is rank 0: skip the SVD.  The staging of the
+        // product sees every entry of A (m x k) and B (k x n), so it doubles as the check.
+        const int nz = warp_accumulate32(a, SmallTaskIO::dd_part(Ad, Bd, m, dt.k, n, true), sm);
+        if (!__any_sync(0xffffffffu, nz & 1) || !__any_sync(0xffffffffu, nz & 2)) {
             if (lane == 0) {
                 Slot& s = dargs.slots[(size_t)dt.prod * dargs.B + b];
                 s.rank = 0;
@@ -1634,12 +1647,12 @@ __global__ void __launch_bounds__(64) k_small32(TruncArgs targs, DDArgs dargs, i
             }
             return;
         }
-        warp_accumulate32(a, SmallTaskIO::dd_part(Ad, Bd, m, dt.k, n, true), sm);
     }
     // pivot threshold 1e-3 below the cutoff (values-only: sigma_1 to ~1e-10)
     const double drel = values_only ? 1e-10 : 1.8e-4 * eps;
     const double dabs = values_only ? 0.0 : 1.8e-4 * abs_cut;
-    const int rp = warp_rrqr_jacobi32(a, v, m, n, drel, dabs, !values_only, sm);
+    w32_mark(0, wt);
+    const int rp = warp_rrqr_jacobi32(a, v, m, n, drel, dabs, !values_only, sm, &wt);
     double sig, smax;
     int pos, r;
     warp_sigma_pos32(a, rp, values_only ? 0.0 : eps, abs_cut, sig, pos, r, smax);
@@ -1654,7 +1667,9 @@ __global__ void __launch_bounds__(64) k_small32(TruncArgs targs, DDArgs dargs, i
     if (lane == 0 && r > 0) out = arena_alloc(MODE == 0 ? targs.out_arena : dargs.out_arena, (unsigned long long)(m + n) * r);
     out = (double*)__shfl_sync(0xffffffffu, (unsigned long long)out, 0);
     if (out == nullptr) r = 0;
+    w32_mark(3, wt);
     if (r > 0) warp_write32(a, m, n, rp, sig, pos, r, sm, out, out + (size_t)m * r);
+    w32_mark(4, wt);
     if (lane == 0) {
         if (MODE == 0) {
             SmallTaskIO::write_out(targs, task, b, C, r, out, out ? out + (size_t)m * r : nullptr);
@@ -1833,7 +1848,17 @@ std::string prof_report(bool reset) {
                  cnt ? (double)ph[6] / cnt : 0.0, cnt ? (double)ph[7] / cnt : 0.0, ph[8], ph[9], ph[10] / 1e9,
                  ph[11] / 1e9, ph[12] / 1e9);
         out += buf;
+        unsigned long long w[8], wc = 0;
+        cudaMemcpyFromSymbol(w, g_w32_cyc, sizeof(w));
+        cudaMemcpyFromSymbol(&wc, g_w32_cnt, sizeof(wc));
+        const double d = wc ? (double)wc : 1.0;
+        snprintf(buf, sizeof(buf), "#phase warp32 tasks %llu (cycles per task): load %.0f qr %.0f jacobi %.0f sigma %.0f "
+                 "write %.0f | sweeps %.2f rp %.2f\n", wc, w[0] / d, w[1] / d, w[2] / d, w[3] / d, w[4] / d, w[6] / d, w[7] / d);
+        out += buf;
         if (reset) {
+            const unsigned long long z8[8] = {};
+            cudaMemcpyToSymbol(g_w32_cyc, z8, sizeof(z8));
+            cudaMemcpyToSymbol(g_w32_cnt, z8, sizeof(unsigned long long));
             const unsigned long long z[16] = {};
             cudaMemcpyToSymbol(g_phase_cyc, z, sizeof(z));
             cudaMemcpyToSymbol(g_phase_cnt, z, sizeof(unsigned long long));

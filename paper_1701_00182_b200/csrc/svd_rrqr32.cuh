@@ -42,7 +42,7 @@ __device__ __forceinline__ int rr_partner(int x, int r, int P) {
 // lane c < rp holds column c of W = R^T J in a[0..n); sm.H / sm.tau / sm.perm describe
 // Q and P, sm.T holds R^T.  (v / want_v: unused, kept for call-site compatibility.)
 __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n, double delta_rel,
-                                  double abs_delta, bool want_v, Warp32Smem& sm) {
+                                  double abs_delta, bool want_v, Warp32Smem& sm, unsigned long long* wt = nullptr) {
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu;
     int perm_j = lane;
@@ -57,13 +57,21 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
     const double delta2 = fmax(d1 * d1, abs_delta * abs_delta);
     const int kmax = m < n ? m : n;
     int rp = 0;
-    // ---- QR with column pivoting, stopped at the numerical rank
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        if (k >= kmax) break;
+    // ---- QR with column pivoting, stopped at the numerical rank.
+    // The step loop is rolled (one copy of the code for every k): a fully unrolled
+    // 32-step loop is ~40k SASS instructions, and a warp running it alone (the top
+    // cyclic-reduction levels, a handful of tasks per launch) stalls on instruction
+    // fetch.  Per-k register indexing becomes masks over the unrolled i loops; every
+    // FMA sequence is the one of the unrolled form (leading terms are exact zeros or
+    // ones), so the results are bitwise unchanged.
+#pragma unroll 1
+    for (int k = 0; k < kmax; ++k) {
         double nr = 0;
 #pragma unroll
-        for (int i = k; i < 32; ++i) nr = fma(a[i], a[i], nr);
+        for (int i = 0; i < 32; ++i) {
+            const double ai = i >= k ? a[i] : 0.0;
+            nr = fma(ai, ai, nr);
+        }
         double best = (lane >= k && lane < n) ? nr : -1.0;
         int bidx = lane;
 #pragma unroll
@@ -82,41 +90,52 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
             for (int i = 0; i < 32; ++i) a[i] = __shfl_sync(FULL, a[i], src);
             perm_j = __shfl_sync(FULL, perm_j, src);
         }
-        double tau = 0.0;
+        // lane k publishes its column; every lane derives the reflector from it
         if (lane == k) {
-            double tail = 0;
 #pragma unroll
-            for (int i = k + 1; i < 32; ++i) tail = fma(a[i], a[i], tail);
-            const double c0 = a[k];
-            if (tail > 2.2250738585072014e-308) {
-                double beta = sqrt(c0 * c0 + tail);
-                if (c0 >= 0) beta = -beta;
-                const double inv = 1.0 / (c0 - beta);
-                tau = (beta - c0) / beta;
-#pragma unroll
-                for (int i = k + 1; i < 32; ++i) a[i] *= inv;
-                a[k] = beta;
-            } else {
-#pragma unroll
-                for (int i = k + 1; i < 32; ++i) a[i] = 0.0;
-            }
-#pragma unroll
-            for (int i = k + 1; i < 32; ++i) sm.H[k][i] = a[i];
-            sm.tau[k] = tau;
+            for (int i = 0; i < 32; ++i) sm.H[k][i] = a[i];
         }
-        tau = __shfl_sync(FULL, tau, k);
-        __syncwarp();  // reflector k (sm.H[k][k+1..31], written by lane k) visible to the warp
+        __syncwarp();
+        const double* hk = sm.H[k];
+        double tail = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const double h = i > k ? hk[i] : 0.0;
+            tail = fma(h, h, tail);
+        }
+        const double c0 = hk[k];
+        double tau = 0.0, inv = 0.0, beta = c0;
+        if (tail > 2.2250738585072014e-308) {
+            beta = sqrt(c0 * c0 + tail);
+            if (c0 >= 0) beta = -beta;
+            inv = 1.0 / (c0 - beta);
+            tau = (beta - c0) / beta;
+        }
         if (lane > k && tau != 0.0) {
-            // the reflector is read from shared memory (broadcast) rather than shuffled into
-            // 31 registers: keeps the engine under 170 registers (6 CTAs per SM)
-            const volatile double* hk = sm.H[k];
-            double s = a[k];
+            // v = [0 (i < k); 1; hk[i] * inv (i > k)]
+            double s = 0.0;
 #pragma unroll
-            for (int i = k + 1; i < 32; ++i) s = fma(hk[i], a[i], s);
+            for (int i = 0; i < 32; ++i) {
+                const double vi = i > k ? hk[i] * inv : (i == k ? 1.0 : 0.0);
+                s = fma(vi, a[i], s);
+            }
             s *= tau;
-            a[k] -= s;
 #pragma unroll
-            for (int i = k + 1; i < 32; ++i) a[i] = fma(-s, hk[i], a[i]);
+            for (int i = 0; i < 32; ++i) {
+                const double vi = i > k ? hk[i] * inv : (i == k ? 1.0 : 0.0);
+                a[i] = fma(-s, vi, a[i]);
+            }
+        } else if (lane == k) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (i == k) a[i] = beta;
+        }
+        __syncwarp();  // all lanes read the raw column before lane k stores the reflector
+        if (lane == k) {
+            // the stored reflector (Q for the write phase): [0; 1; v] in full length
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sm.H[k][i] = i > k ? (tau != 0.0 ? hk[i] * inv : 0.0) : (i == k ? 1.0 : 0.0);
+            sm.tau[k] = tau;
         }
         rp = k + 1;
     }
@@ -128,6 +147,10 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
 #pragma unroll
     for (int j = 0; j < 32; ++j) a[j] = lane < rp ? sm.T[j][lane] : 0.0;
     __syncwarp();
+    if (wt) {
+        w32_mark(1, *wt);
+        if (lane == 0) atomicAdd(&g_w32_cyc[7], (unsigned long long)rp);
+    }
     if (rp < 2) return rp;
     // ---- one-sided Jacobi on the rp columns of A'
     const int P = rp + (rp & 1);
@@ -175,8 +198,10 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
                 for (int i = 0; i < 32; ++i) a[i] = fma(sl, pa[i], c * a[i]);
             }
         }
+        if (wt && lane == 0) atomicAdd(&g_w32_cyc[6], 1ull);
         if (!any) break;
     }
+    if (wt) w32_mark(2, *wt);
     return rp;
 }
 
@@ -228,19 +253,17 @@ __device__ void warp_write32(double (&a)[32], int m, int n, int rp, double sig, 
             }
             x[i] = acc * inv;
         }
+#pragma unroll 1
+        for (int k = rp - 1; k >= 0; --k) {
+            const double tk = sm.tau[k];
+            if (tk != 0.0) {
+                const double* hk = sm.H[k];  // [0 (i < k); 1; v]
+                double s = 0.0;
 #pragma unroll
-        for (int k = 31; k >= 0; --k) {
-            if (k < rp) {
-                const double tk = sm.tau[k];
-                if (tk != 0.0) {
-                    double s = x[k];
+                for (int i = 0; i < 32; ++i) s = fma(hk[i], x[i], s);
+                s *= tk;
 #pragma unroll
-                    for (int i = k + 1; i < 32; ++i) s = fma(sm.H[k][i], x[i], s);
-                    s *= tk;
-                    x[k] -= s;
-#pragma unroll
-                    for (int i = k + 1; i < 32; ++i) x[i] = fma(-s, sm.H[k][i], x[i]);
-                }
+                for (int i = 0; i < 32; ++i) x[i] = fma(-s, hk[i], x[i]);
             }
         }
         double* u = Uo + (size_t)pos * m;
@@ -252,31 +275,43 @@ __device__ void warp_write32(double (&a)[32], int m, int n, int rp, double sig, 
 }
 
 // Column-per-lane formation: M[i, j] += alpha sum_t P(i,t) Q(j,t), i in [pd, pd+pr), j in [qd, qd+qr).
-// P chunks are staged through sm.T (rows x TC); lane j reads its own Q(j, t).
-__device__ void warp_accumulate32(double (&a)[32], const RowPart& p, Warp32Smem& sm) {
+// Each 32-column chunk of P is staged through sm.T (T[t][i]) and of Q through sm.H (H[t][j]) by
+// fully unrolled predicated loads, so a lane has all of its chunk's loads in flight at once
+// (a rolled load-then-use loop waits one L2 round trip per column).  Returns, per lane,
+// whether any staged P / Q value was nonzero (nzP | 2 nzQ).  The FMA order is unchanged.
+__device__ int warp_accumulate32(double (&a)[32], const RowPart& p, Warp32Smem& sm) {
     const int lane = threadIdx.x & 31;
     constexpr int TC = 32;
     const int jr = lane - p.qd;
     const bool own = jr >= 0 && jr < p.qr;
+    const int ir = lane - p.pd;
+    const bool prow = ir >= 0 && ir < p.pr;
+    bool nzP = false, nzQ = false;
     for (int t0 = 0; t0 < p.k; t0 += TC) {
         const int tn = min(TC, p.k - t0);
         __syncwarp();
-        // stage P rows [0,32) x chunk (zero outside [pd, pd+pr))
-        for (int t = 0; t < tn; ++t) {
-            const int i = lane;
-            const int ir = i - p.pd;
-            sm.T[t][i] = (ir >= 0 && ir < p.pr) ? p.alpha * p.P[ir * p.ps + (long)(t0 + t) * p.pt] : 0.0;
+#pragma unroll
+        for (int t = 0; t < TC; ++t) {
+            if (t < tn) {
+                const double x = prow ? p.alpha * p.P[ir * p.ps + (long)(t0 + t) * p.pt] : 0.0;
+                const double y = own ? p.Q[jr * p.qs + (long)(t0 + t) * p.qt] : 0.0;
+                nzP |= x != 0.0;
+                nzQ |= y != 0.0;
+                sm.T[t][lane] = x;
+                sm.H[t][lane] = y;
+            }
         }
         __syncwarp();
         if (own) {
             for (int t = 0; t < tn; ++t) {
-                const double q = p.Q[jr * p.qs + (long)(t0 + t) * p.qt];
+                const double q = sm.H[t][lane];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) a[i] = fma(sm.T[t][i], q, a[i]);
             }
         }
     }
     __syncwarp();
+    return (nzP ? 1 : 0) | (nzQ ? 2 : 0);
 }
 
 }  // namespace acrgpu
