@@ -111,30 +111,25 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
             inv = 1.0 / (c0 - beta);
             tau = (beta - c0) / beta;
         }
+        // v = [0 (i < k); 1; hk[i] * inv (i > k)], formed once (v[] is free during the QR)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = i > k ? (tau != 0.0 ? hk[i] * inv : 0.0) : (i == k ? 1.0 : 0.0);
         if (lane > k && tau != 0.0) {
-            // v = [0 (i < k); 1; hk[i] * inv (i > k)]
             double s = 0.0;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const double vi = i > k ? hk[i] * inv : (i == k ? 1.0 : 0.0);
-                s = fma(vi, a[i], s);
-            }
+            for (int i = 0; i < 32; ++i) s = fma(v[i], a[i], s);
             s *= tau;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const double vi = i > k ? hk[i] * inv : (i == k ? 1.0 : 0.0);
-                a[i] = fma(-s, vi, a[i]);
-            }
-        } else if (lane == k) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (i == k) a[i] = beta;
+            for (int i = 0; i < 32; ++i) a[i] = fma(-s, v[i], a[i]);
         }
         __syncwarp();  // all lanes read the raw column before lane k stores the reflector
         if (lane == k) {
             // the stored reflector (Q for the write phase): [0; 1; v] in full length
 #pragma unroll
-            for (int i = 0; i < 32; ++i) sm.H[k][i] = i > k ? (tau != 0.0 ? hk[i] * inv : 0.0) : (i == k ? 1.0 : 0.0);
+            for (int i = 0; i < 32; ++i) {
+                sm.H[k][i] = v[i];
+                if (i == k) a[i] = beta;
+            }
             sm.tau[k] = tau;
         }
         rp = k + 1;
@@ -165,8 +160,13 @@ __device__ int warp_rrqr_jacobi32(double (&a)[32], double (&v)[32], int m, int n
     const double zthr = fro * (16.0 * JEPS * JEPS);
     for (int sweep = 0; sweep < 40; ++sweep) {
         bool any = false;
+        // circle-method partner (rr_partner) stepped incrementally: no integer modulo per round
+        const int y = lane - 1;
+        int yp = y <= 0 ? 0 : (P - 1) - y;
         for (int round = 0; round < P - 1; ++round) {
-            const int p = lane < P ? rr_partner(lane, round, P) : lane;
+            const int p = lane >= P ? lane : (lane == 0 ? 1 + round : (yp == y ? 0 : 1 + yp));
+            yp += 2;
+            if (yp >= P - 1) yp -= P - 1;
             const bool low = lane < p;
             double pa[32];
 #pragma unroll
