@@ -392,13 +392,34 @@ __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, cons
     for (int t0 = 0; t0 < k; t0 += KC) {
         const int kc = min(KC, k - t0);
         __syncthreads();
-        for (int e = threadIdx.x; e < RA * kc; e += NTH) {
-            const int i = e % RA, t = e / RA;
-            As[i + t * RA] = (i < ru && (!TRI || ra0 + i <= t0 + t)) ? A[i + (size_t)(t0 + t) * lda] : 0.0;
+        // groups of 8 loads are issued before their shared-memory stores (a load-store loop
+        // pays one memory round trip per iteration: the compiler cannot reorder across the
+        // generic smem store)
+        for (int e0 = threadIdx.x; e0 < RA * kc; e0 += 8 * NTH) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * NTH, i = e % RA, t = e / RA;
+                v[u] = (e < RA * kc && i < ru && (!TRI || ra0 + i <= t0 + t)) ? A[i + (size_t)(t0 + t) * lda] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * NTH;
+                if (e < RA * kc) As[(e % RA) + (e / RA) * RA] = v[u];
+            }
         }
-        for (int e = threadIdx.x; e < RB * kc; e += NTH) {
-            const int i = e % RB, t = e / RB;
-            Bs[i + t * RB] = (i < rv && (!TRI || rb0 + i <= t0 + t)) ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
+        for (int e0 = threadIdx.x; e0 < RB * kc; e0 += 8 * NTH) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * NTH, i = e % RB, t = e / RB;
+                v[u] = (e < RB * kc && i < rv && (!TRI || rb0 + i <= t0 + t)) ? B[i + (size_t)(t0 + t) * ldb] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * NTH;
+                if (e < RB * kc) Bs[(e % RB) + (e / RB) * RB] = v[u];
+            }
         }
         __syncthreads();
         for (int t = 0; t < kc; ++t) {

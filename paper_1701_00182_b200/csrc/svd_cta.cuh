@@ -241,9 +241,8 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
         for (int sweep = 0; sweep < 40; ++sweep) {
             int rotated = 0;
             for (int r = 0; r < P - 1; ++r) {
-                // pairs (pi, pi + NW) per warp iteration: independent reductions interleave;
-                // the per-pair arithmetic is the one of the single-pair loop
-                auto pair_of = [&](int pi, int& p, int& q) {
+                for (int pi = warp; pi < P / 2; pi += NW) {
+                    int p, q;
                     if (pi == 0) {
                         p = 0;
                         q = 1 + r;
@@ -256,65 +255,30 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
                         q = 1 + b;
                     }
                     if (p > q) { const int t = p; p = q; q = t; }
-                };
-                for (int pi = warp; pi < P / 2; pi += 2 * NW) {
-                    int p0, q0, p1 = 0, q1 = 0;
-                    pair_of(pi, p0, q0);
-                    const bool has1 = pi + NW < P / 2;
-                    if (has1) pair_of(pi + NW, p1, q1);
-                    const bool ok0 = q0 < cols, ok1 = has1 && q1 < cols;
-                    if (!ok0 && !ok1) continue;
-                    double* ap = W + (size_t)(ok0 ? p0 : p1) * ldw;
-                    double* aq = W + (size_t)(ok0 ? q0 : q1) * ldw;
-                    double* bp = W + (size_t)(ok1 ? p1 : p0) * ldw;
-                    double* bq = W + (size_t)(ok1 ? q1 : q0) * ldw;
-                    double al = 0, be = 0, ga = 0, al1 = 0, be1 = 0, ga1 = 0;
+                    if (q >= cols) continue;
+                    double* ap = W + (size_t)p * ldw;
+                    double* aq = W + (size_t)q * ldw;
+                    double al = 0, be = 0, ga = 0;
                     #pragma unroll 4
                     for (int e = lane; e < rows; e += 32) {
                         const double x = ap[e], y = aq[e];
                         al = fma(x, x, al);
                         be = fma(y, y, be);
                         ga = fma(x, y, ga);
-                        if (ok0 && ok1) {
-                            const double x1 = bp[e], y1 = bq[e];
-                            al1 = fma(x1, x1, al1);
-                            be1 = fma(y1, y1, be1);
-                            ga1 = fma(x1, y1, ga1);
-                        }
                     }
-#pragma unroll
-                    for (int o = 16; o; o >>= 1) {
-                        al += __shfl_xor_sync(0xffffffffu, al, o);
-                        be += __shfl_xor_sync(0xffffffffu, be, o);
-                        ga += __shfl_xor_sync(0xffffffffu, ga, o);
-                        al1 += __shfl_xor_sync(0xffffffffu, al1, o);
-                        be1 += __shfl_xor_sync(0xffffffffu, be1, o);
-                        ga1 += __shfl_xor_sync(0xffffffffu, ga1, o);
-                    }
-                    // (ap, aq) is the first valid pair; (bp, bq) the second when both are valid
-                    double c, s, c1 = 1.0, s1 = 0.0;
-                    const bool rot0 = jacobi_params(al, be, ga, tol2, zthr, c, s);
-                    const bool rot1 = ok0 && ok1 && jacobi_params(al1, be1, ga1, tol2, zthr, c1, s1);
-                    if (rot0 || rot1) {
-                        #pragma unroll 4
-                        for (int e = lane; e < rows; e += 32) {
-                            if (rot0) rot2(ap[e], aq[e], c, s);
-                            if (rot1) rot2(bp[e], bq[e], c1, s1);
-                        }
-                        rotated = 1;
-                    }
+                    al = warp_sum(al);
+                    be = warp_sum(be);
+                    ga = warp_sum(ga);
+                    double c, s;
+                    if (!jacobi_params(al, be, ga, tol2, zthr, c, s)) continue;
+                    #pragma unroll 4
+                    for (int e = lane; e < rows; e += 32) rot2(ap[e], aq[e], c, s);
                     if (J) {
-                        if (rot0) {
-                            double* vp = J + (size_t)(ok0 ? p0 : p1) * ldj;
-                            double* vq = J + (size_t)(ok0 ? q0 : q1) * ldj;
-                            for (int e = lane; e < cols; e += 32) rot2(vp[e], vq[e], c, s);
-                        }
-                        if (rot1) {
-                            double* vp = J + (size_t)p1 * ldj;
-                            double* vq = J + (size_t)q1 * ldj;
-                            for (int e = lane; e < cols; e += 32) rot2(vp[e], vq[e], c1, s1);
-                        }
+                        double* vp = J + (size_t)p * ldj;
+                        double* vq = J + (size_t)q * ldj;
+                        for (int e = lane; e < cols; e += 32) rot2(vp[e], vq[e], c, s);
                     }
+                    rotated = 1;
                 }
                 __syncthreads();
             }

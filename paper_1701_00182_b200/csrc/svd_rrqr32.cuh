@@ -290,15 +290,28 @@ __device__ int warp_accumulate32(double (&a)[32], const RowPart& p, Warp32Smem& 
     for (int t0 = 0; t0 < p.k; t0 += TC) {
         const int tn = min(TC, p.k - t0);
         __syncwarp();
+        // loads of a group are issued before any of its shared-memory stores: the compiler
+        // cannot move a global load above a store through the (generic) smem reference, so a
+        // load-store-load sequence would pay one memory round trip per column
 #pragma unroll
-        for (int t = 0; t < TC; ++t) {
-            if (t < tn) {
-                const double x = prow ? p.alpha * p.P[ir * p.ps + (long)(t0 + t) * p.pt] : 0.0;
-                const double y = own ? p.Q[jr * p.qs + (long)(t0 + t) * p.qt] : 0.0;
-                nzP |= x != 0.0;
-                nzQ |= y != 0.0;
-                sm.T[t][lane] = x;
-                sm.H[t][lane] = y;
+        for (int t8 = 0; t8 < TC; t8 += 8) {
+            if (t8 < tn) {
+                double xv[8], yv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int t = t8 + u;
+                    xv[u] = (t < tn && prow) ? p.alpha * p.P[ir * p.ps + (long)(t0 + t) * p.pt] : 0.0;
+                    yv[u] = (t < tn && own) ? p.Q[jr * p.qs + (long)(t0 + t) * p.qt] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (t8 + u < tn) {
+                        nzP |= xv[u] != 0.0;
+                        nzQ |= yv[u] != 0.0;
+                        sm.T[t8 + u][lane] = xv[u];
+                        sm.H[t8 + u][lane] = yv[u];
+                    }
+                }
             }
         }
         __syncwarp();
