@@ -992,35 +992,64 @@ struct DepArgs {
     FlopLedger* flops;
 };
 
+// Per group of 4 elements per thread (1024 elements: one group for a 32 x 32 leaf, four for
+// 64 x 64), parts outermost and the elements' partial sums in registers: the part and slot
+// records are read once per part and group rather than once per element, and the
+// elements' operand loads overlap.  Each element still adds its contributions in part
+// order, so the result is bitwise that of the element loop.
+constexpr int DEP_E = 4;
 __device__ __forceinline__ void deposit_item(const DepArgs& args, const BatchViews& bv, const int ti, const int b) {
     const DepTask task = args.tasks[ti];
     double* Cd = bv.c[b].dense + task.doff;
     const int m = task.m, n = task.n;
+    const int nel = m * n;
     double fl = 0;
-    for (int e = threadIdx.x; e < m * n; e += NT) {
-        const int i = e % m, j = e / m;
-        double c = Cd[e];
+    for (int g0 = 0; g0 < nel; g0 += DEP_E * NT) {
+        double c[DEP_E];
+#pragma unroll
+        for (int q = 0; q < DEP_E; ++q) {
+            const int e = g0 + threadIdx.x + q * NT;
+            c[q] = e < nel ? Cd[e] : 0.0;
+        }
         for (int pi = task.pbeg; pi < task.pend; ++pi) {
             const Part p = args.parts[pi];
             if (p.src == S_GEMM) {
                 const double* A = bv.a[b].dense + p.da;
                 const double* Bm = bv.b[b].dense + p.db;
-                double a = 0;
-                for (int t = 0; t < p.gk; ++t) a = fma(A[i + (size_t)t * m], Bm[t + (size_t)j * p.gk], a);
-                c += p.alpha * a;
-                if (e == 0) fl += 2.0 * m * n * p.gk;
+#pragma unroll
+                for (int q = 0; q < DEP_E; ++q) {
+                    const int e = g0 + threadIdx.x + q * NT;
+                    if (e < nel) {
+                        const int i = e % m, j = e / m;
+                        double a = 0;
+                        for (int t = 0; t < p.gk; ++t) a = fma(A[i + (size_t)t * m], Bm[t + (size_t)j * p.gk], a);
+                        c[q] += p.alpha * a;
+                    }
+                }
+                if (g0 == 0) fl += 2.0 * m * n * p.gk;
             } else {
                 const Slot s = args.slots[(size_t)p.id * args.B + b];
                 if (s.rank == 0) continue;
                 const double* U = s.U + p.u_src;
                 const double* V = s.V + p.v_src;
-                double a = 0;
-                for (int t = 0; t < s.rank; ++t) a = fma(p.alpha * U[i + (size_t)t * s.ldu], V[j + (size_t)t * s.ldv], a);
-                c += a;
-                if (e == 0) fl += 2.0 * m * n * s.rank;
+#pragma unroll
+                for (int q = 0; q < DEP_E; ++q) {
+                    const int e = g0 + threadIdx.x + q * NT;
+                    if (e < nel) {
+                        const int i = e % m, j = e / m;
+                        double a = 0;
+                        for (int t = 0; t < s.rank; ++t) a = fma(p.alpha * U[i + (size_t)t * s.ldu], V[j + (size_t)t * s.ldv], a);
+                        c[q] += a;
+                    }
+                }
+                if (g0 == 0) fl += 2.0 * m * n * s.rank;
             }
         }
-        Cd[e] = c;
+#pragma unroll
+        for (int q = 0; q < DEP_E; ++q) {
+            const int e = g0 + threadIdx.x + q * NT;
+            if (e < nel) Cd[e] = c[q];
+        }
     }
     if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, fl);
 }
