@@ -156,12 +156,6 @@ static Mat matmul(const Mat& A, const Mat& B, bool ta = false, bool tb = false) 
     return C;
 }
 
-static double fro(const Mat& A) {
-    double s = 0;
-    for (double v : A.a) s += v * v;
-    return std::sqrt(s);
-}
-
 // ---------------------------------------------------------------- Householder QR
 // Unpivoted Householder QR of A (m x K): R = top ku rows (upper trapezoidal,
 // ku x K), Q = explicit thin factor (m x ku), ku = min(m, K).

@@ -449,9 +449,7 @@ __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, cons
 // blocked-QR code the kernel fits 128 registers per thread, so two CTAs share an SM.
 template <int DMAX, int RPCAP, int NTH, bool QR = true>
 __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, BatchViews bv) {
-    constexpr int NWH = NTH / 32;
     extern __shared__ double smem[];
-    __shared__ double red[NWH];
     __shared__ int sh_K;
     __shared__ double* sh_ws;
     const TruncTask task = args.tasks[blockIdx.x];
@@ -495,8 +493,6 @@ __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, Ba
 
     const int ku = m < K ? m : K, kv = n < K ? n : K;
     double fsvd = 0, fqr = 0, fgemm = 0;
-    __shared__ int sh_rp;
-    __shared__ double sh_smax;
     __shared__ double* sh_out;
 
     if (m <= DMAX && n <= DMAX) {
@@ -1616,9 +1612,7 @@ struct SmallTaskIO {
     }
 };
 
-// ---- blocks <= 32 x 32: one warp per task, four tasks per CTA
-constexpr int W32_TC = 16;
-
+// ---- blocks <= 32 x 32: one warp per task
 // mode 0: truncation task list (TruncArgs); mode 1: dense*dense products (DDArgs).
 // Two warps per CTA, one task per warp (rank-revealing QR + Jacobi, svd_rrqr32.cuh).
 template <int MODE>
