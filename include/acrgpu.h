@@ -169,6 +169,9 @@ long acrgpu_structure(int dim, const double* coords, int leaf_size, double eta, 
 /* Per-kernel device time accumulated while ACRGPU_PROFILE=1 is set in the environment:
  * lines "kernel total_ms launches ctas".  Returns the length written (NUL-terminated). */
 long acrgpu_profile_report(char* buf, long cap, int reset);
+/* Select which launches are timed (overrides ACRGPU_PROFILE): NULL / "" / "0" none, "1" / "*"
+ * every kernel, else a comma-separated list of kernel names (e.g. "k_trunc_qr"). */
+void acrgpu_profile_select(const char* filter);
 
 /* ---- Plane partition over several GPUs (execute_parallel_factor, parallel.cpp:96-297).
  * Rank w owns the planes plan_schedule(n, p) assigns it (contiguous blocks at level 0;

@@ -174,6 +174,7 @@ SYMBOLS = {
     "acrgpu_timing_get": (C.c_int, [C.c_void_p, C.POINTER(_Timing)]),
     "acrgpu_messages": (C.c_long, [C.c_void_p, C.POINTER(_Msg), C.c_long]),
     "acrgpu_profile_report": (C.c_long, [C.c_char_p, C.c_long, C.c_int]),
+    "acrgpu_profile_select": (None, [C.c_char_p]),
     "acrgpu_structure": (C.c_long, [C.c_int, C.POINTER(C.c_double), C.c_int, C.c_double, C.c_int,
                                      C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_long, C.POINTER(_Err)]),
     "acrgpu_comm_unique_id": (C.c_int, [C.c_char_p, C.POINTER(_Err)]),
@@ -554,8 +555,15 @@ def acr_solve(fact: AcrFactorization, f):
     return fact.solve(f)
 
 
+def profile_select(names: str | None) -> None:
+    """Time these kernels' launches with CUDA events on their streams: None/"" none, "*" all,
+    else a comma-separated list of kernel names (overrides ACRGPU_PROFILE)."""
+    lib().acrgpu_profile_select((names or "").encode())
+
+
 def profile_report(reset: bool = True) -> str:
-    """Per-kernel device totals collected when ACRGPU_PROFILE=1 (name -> ms, launches, CTAs)."""
+    """Per-kernel device totals of the launches selected by profile_select / ACRGPU_PROFILE
+    (name -> ms, launches, CTAs, nominal flops)."""
     n = lib().acrgpu_profile_report(None, 0, 0)
     buf = C.create_string_buffer(n + 1)
     lib().acrgpu_profile_report(buf, n + 1, 1 if reset else 0)

@@ -35,12 +35,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if force or _stale(o, [s] + hdrs):
             cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
             if src.endswith(".cpp"):
-                cmd = [NVCC, *FLAGS, "-x", "c++", "-c", s, "-o", o]
+                cmd = [NVCC, *ARCH, *FLAGS, "-x", "c++", "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static" if False else "-cudart=static"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart=static"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

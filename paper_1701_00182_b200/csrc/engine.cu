@@ -304,6 +304,8 @@ struct Engine {
     SlabTask* slabs = nullptr;        // matvec slabs of the root
     ApplyLeaf* slab_leaves = nullptr;
     int nslabs = 0;
+    MvLeaf* mv_rk = nullptr;          // matvec phase 1: every Rk leaf of the root
+    int n_mv_rk = 0;
 
     ~Engine() {
         for (void* p : dev_allocs) cudaFree(p);
@@ -1087,6 +1089,13 @@ struct Engine {
         nslabs = (int)sl.size();
         slabs = up(sl);
         slab_leaves = up(al);
+        std::vector<MvLeaf> rk;
+        for (int k = 0; k < S.n_rk(); ++k) {
+            const SNode& L = S.node(S.k_node[k]);
+            rk.push_back(MvLeaf{k, L.cb, L.cols(), L.rows()});
+        }
+        n_mv_rk = (int)rk.size();
+        mv_rk = up(rk);
     }
 };
 
@@ -1818,7 +1827,8 @@ static void matvec(Engine& E, const std::vector<MV>& items, int nrhs) {
             mb.base[b] = it.base;
             mb.y[b] = it.y;
         }
-        launch_matvec(E.st(), E.nslabs, E.slabs, E.slab_leaves, nrhs, E.S.dim, E.ctx->flops, mb);
+        launch_matvec(E.st(), E.nslabs, E.slabs, E.slab_leaves, E.mv_rk, E.n_mv_rk, nrhs, E.S.dim, E.ctx->lane().trans,
+                      E.ctx->flops, mb);
     }
 }
 
@@ -2675,6 +2685,8 @@ extern "C" {
 
 const char* acrgpu_version(void) { return "acrgpu 0.1 sm_100a fp64"; }
 
+
+void acrgpu_profile_select(const char* filter) { prof_select(filter); }
 
 long acrgpu_profile_report(char* buf, long cap, int reset) {
     const std::string r = prof_report(reset != 0);

@@ -45,22 +45,8 @@ __device__ __forceinline__ void w32_mark(int i, unsigned long long& t0) {
 namespace acrgpu {
 
 constexpr int NT = 256;
-constexpr int NW = NT / 32;
-constexpr double DEPS = 2.2204460492503131e-16;
 
 // ------------------------------------------------------------------ helpers
-
-// block-wide sum (all threads get the result); red: >= NW doubles of smem
-__device__ double block_sum(double v, double* red) {
-    v = warp_sum(v);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    double s = 0;
-    for (int i = 0; i < NW; ++i) s += red[i];
-    return s;
-}
 
 __device__ double* arena_alloc(const Arena& a, unsigned long long n) {
     n = (n + 15ull) & ~15ull;  // 128-byte granules
@@ -106,133 +92,6 @@ __device__ void fl_svd(double r, double c, double& fsvd, double& fqr, double& fg
     fgemm += fl_gemm(q, p, p);
 }
 
-// ------------------------------------------------------------------ one-sided Jacobi SVD
-// Columns of A (rows x cols, ld lda, rows >= cols) are orthogonalised by plane
-// rotations in round-robin (tournament) order; each pair is handled by one warp.
-// V (cols x cols, ld ldv) accumulates the right rotations when non-null.  On exit
-// column j of A = sigma_j u_j and sig[j] = ||a_j||.  Works on shared or global memory.
-// Equivalent algorithm class to the reference's JacobiSVD (hmatrix.cpp:67,89).
-__device__ void jacobi_svd(double* A, int lda, int rows, int cols, double* V, int ldv, double* sig) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (V)
-        for (int e = threadIdx.x; e < cols * cols; e += NT) {
-            const int i = e % cols, j = e / cols;
-            V[i + (size_t)j * ldv] = (i == j) ? 1.0 : 0.0;
-        }
-    __syncthreads();
-    __shared__ double sh_fro;
-    {
-        double f = 0;
-        for (size_t e = threadIdx.x; e < (size_t)rows * cols; e += NT) {
-            const double x = A[(e % rows) + (e / rows) * (size_t)lda];
-            f = fma(x, x, f);
-        }
-        __shared__ double redf[NW];
-        f = warp_sum(f);
-        if (lane == 0) redf[warp] = f;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0;
-            for (int i = 0; i < NW; ++i) t += redf[i];
-            sh_fro = t;
-        }
-        __syncthreads();
-    }
-    const double zthr = sh_fro * (16.0 * DEPS * DEPS);
-    if (cols > 1) {
-        const int P = cols + (cols & 1);
-        const int npairs = P / 2, rounds = P - 1;
-        const double tol = (double)(rows > 1 ? rows : 1) * DEPS;
-        for (int sweep = 0; sweep < 60; ++sweep) {
-            int rotated = 0;
-            for (int r = 0; r < rounds; ++r) {
-                for (int i = warp; i < npairs; i += NW) {
-                    int p, q;
-                    if (i == 0) {
-                        p = 0;
-                        q = 1 + r;
-                    } else {
-                        p = 1 + (r + i) % (P - 1);
-                        q = 1 + (r - i + P - 1) % (P - 1);
-                    }
-                    if (p > q) { const int t = p; p = q; q = t; }
-                    if (q >= cols) continue;
-                    double* ap = A + (size_t)p * lda;
-                    double* aq = A + (size_t)q * lda;
-                    double al = 0, be = 0, ga = 0;
-                    #pragma unroll 4
-                    for (int e = lane; e < rows; e += 32) {
-                        const double x = ap[e], y = aq[e];
-                        al = fma(x, x, al);
-                        be = fma(y, y, be);
-                        ga = fma(x, y, ga);
-                    }
-                    al = warp_sum(al);
-                    be = warp_sum(be);
-                    ga = warp_sum(ga);
-                    if (!(fabs(ga) > tol * sqrt(al) * sqrt(be)) || !(al > zthr) || !(be > zthr)) continue;
-                    const double zeta = (be - al) / (2.0 * ga);
-                    double t;
-                    if (fabs(zeta) > 1e150) t = 0.5 / zeta;
-                    else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-                    #pragma unroll 4
-                    for (int e = lane; e < rows; e += 32) {
-                        const double x = ap[e], y = aq[e];
-                        ap[e] = c * x - s * y;
-                        aq[e] = s * x + c * y;
-                    }
-                    if (V) {
-                        double* vp = V + (size_t)p * ldv;
-                        double* vq = V + (size_t)q * ldv;
-                        for (int e = lane; e < cols; e += 32) {
-                            const double x = vp[e], y = vq[e];
-                            vp[e] = c * x - s * y;
-                            vq[e] = s * x + c * y;
-                        }
-                    }
-                    rotated = 1;
-                }
-                __syncthreads();
-            }
-            if (!__syncthreads_or(rotated)) break;
-        }
-    }
-    for (int j = warp; j < cols; j += NW) {
-        const double* aj = A + (size_t)j * lda;
-        double s = 0;
-        #pragma unroll 4
-        for (int e = lane; e < rows; e += 32) s = fma(aj[e], aj[e], s);
-        s = warp_sum(s);
-        if (lane == 0) sig[j] = sqrt(s);
-    }
-    __syncthreads();
-}
-
-// order[t] = index of the t-th largest sig (ties by index); returns via smem.
-__device__ void sort_desc(const double* sig, int n, int* order) {
-    for (int j = threadIdx.x; j < n; j += NT) {
-        const double v = sig[j];
-        int pos = 0;
-        for (int i = 0; i < n; ++i) {
-            const double w = sig[i];
-            pos += (w > v) || (w == v && i < j);
-        }
-        order[pos] = j;
-    }
-    __syncthreads();
-}
-
-__device__ int rank_of(const double* sig, const int* order, int n, double eps, double abs_cut) {
-    if (n == 0) return 0;
-    const double s0 = sig[order[0]];
-    if (!(s0 > 0.0)) return 0;
-    const double cut = fmax(eps * s0, abs_cut);
-    int r = 0;
-    while (r < n && sig[order[r]] > cut) ++r;
-    return r;
-}
-
 // ------------------------------------------------------------------ part resolution
 struct PartRes {
     const double* U;
@@ -260,76 +119,6 @@ __device__ __forceinline__ PartRes resolve_part(const Part& p, const Slot* slots
             r.ldv = p.rows_v;
         }
     }
-    return r;
-}
-
-// ------------------------------------------------------------------ dense-route SVD truncation
-// M (m x n, ld m) in smem.  Computes the truncated SVD and writes outputs
-// U' = U_r Sigma_r (m x r) and V' = V_r (n x r) into one arena allocation.
-// work: >= n*n + (m<n ? n*m + m*m - n*n : 0) doubles of smem; sig/order: >= max(m,n).
-// Returns r (block-uniform); *out_ptr receives the allocation (nullptr if r == 0).
-__device__ int svd_truncate_dense(double* M, int m, int n, double eps, double abs_cut, double* work, double* sig,
-                                  int* order, const Arena& arena, double** out_ptr, double* sig_max_out,
-                                  bool values_only) {
-    __shared__ double* sh_out;
-    __shared__ int sh_r;
-    const bool tall = m >= n;
-    double *A, *Vw;
-    int rows, cols;
-    if (tall) {
-        A = M;
-        rows = m;
-        cols = n;
-        Vw = values_only ? nullptr : work;
-    } else {  // work on M^T (n x m)
-        A = work;
-        rows = n;
-        cols = m;
-        for (int e = threadIdx.x; e < m * n; e += NT) {
-            const int i = e % m, j = e / m;
-            A[j + (size_t)i * n] = M[e];
-        }
-        Vw = values_only ? nullptr : work + (size_t)n * m;
-        __syncthreads();
-    }
-    jacobi_svd(A, rows, rows, cols, Vw, cols, sig);
-    sort_desc(sig, cols, order);
-    if (threadIdx.x == 0) {
-        sh_r = rank_of(sig, order, cols, eps, abs_cut);
-        if (sig_max_out) *sig_max_out = cols > 0 ? sig[order[0]] : 0.0;
-        sh_out = nullptr;
-        if (!values_only && sh_r > 0) sh_out = arena_alloc(arena, (unsigned long long)(m + n) * sh_r);
-    }
-    __syncthreads();
-    const int r = sh_r;
-    double* out = sh_out;
-    if (out_ptr) *out_ptr = out;
-    if (values_only || r == 0 || out == nullptr) return r;
-    double* Uo = out;
-    double* Vo = out + (size_t)m * r;
-    if (tall) {
-        for (int e = threadIdx.x; e < m * r; e += NT) {
-            const int i = e % m, t = e / m;
-            Uo[e] = A[i + (size_t)order[t] * rows];
-        }
-        for (int e = threadIdx.x; e < n * r; e += NT) {
-            const int i = e % n, t = e / n;
-            Vo[e] = Vw[i + (size_t)order[t] * cols];
-        }
-    } else {
-        // M^T J = W  =>  M = J W^T = (J Sigma)(W Sigma^{-1})^T
-        for (int e = threadIdx.x; e < m * r; e += NT) {
-            const int i = e % m, t = e / m;
-            const int j = order[t];
-            Uo[e] = Vw[i + (size_t)j * cols] * sig[j];
-        }
-        for (int e = threadIdx.x; e < n * r; e += NT) {
-            const int i = e % n, t = e / n;
-            const int j = order[t];
-            Vo[e] = A[i + (size_t)j * rows] / sig[j];
-        }
-    }
-    __syncthreads();
     return r;
 }
 
@@ -795,8 +584,6 @@ struct ApplyTArgs {
 // tr + 32 i (i < 2) and columns tc + 8 j (j < 4); the k-dimension is staged in shared
 // memory in chunks of 32 (A: 64 x 32, ld 65; B: 32 x 32, ld 33).
 constexpr int AP_LDA = 65, AP_LDB = 33;
-constexpr int APPLY_ROWS = 64;  // max slab rows (matvec)
-constexpr int APPLY_TR = 64;    // Rk ranks per inner pass (matvec)
 __device__ __forceinline__ void ap_accumulate(double (&acc)[2][4], const double* As, const double* Bs, int kc) {
     const int tr = threadIdx.x & 31, tc = threadIdx.x >> 5;
 #pragma unroll 8
@@ -1325,17 +1112,118 @@ __global__ void k_scale_reduce(const double* sig_d, int nd, const double* sig_k,
 }
 
 // ------------------------------------------------------------------ solve: batched H-matvec
+// happly / node_apply in the solve (hmatrix.cpp:695-706; acr.cpp:180-229): y = base - H x
+// for a batch of (H, x, base, y) items, x and y plane vectors in tree order with nrhs
+// columns (ld dim).  HBM-bound: every stored entry of H is read exactly once.
+//   phase 1 (k_mv_t):    T_k = V_k^T X[cols of leaf k] (rank x nrhs) once per (Rk leaf, item),
+//                        into the transient arena; pointer table [item][leaf] at the arena base.
+//   phase 2 (k_mv_slab): per <= 64-row output slab, y = base - sum_dense D X - sum_Rk U_k T_k.
+// Per right-hand-side column the arithmetic is a fixed sequence (independent of nrhs and
+// of the batch), so multi-RHS solves are bitwise equal to single-RHS ones.
 struct MatvecArgs {
     const SlabTask* tasks;
     const ApplyLeaf* leaves;
+    const MvLeaf* rk;     // Rk leaves of the root (phase 1)
+    int nrk;
     int nrhs;
     int dim;
+    Arena arena;          // transient: [count x nrk T pointers | T blocks]
     FlopLedger* flops;
 };
+constexpr int MV_ROWS = 64;     // rows per phase-1 chunk / per slab
+constexpr int MV_TC = 64;       // rank columns per phase-1 pass
+constexpr int MV_RHS = 16;      // right-hand sides per pass
+constexpr int MV_LD = MV_ROWS + 1;
 
-// y[slab] = base[slab] - (H x)[slab]  (base null: y = H x).  Leaves in DFS order.
-__global__ void __launch_bounds__(NT) k_matvec(MatvecArgs args, MatvecBatch mb) {
-    __shared__ double T[APPLY_TR * 16];
+__device__ __forceinline__ double** mv_tptr(const MatvecArgs& a) { return (double**)a.arena.base; }
+
+// T = V^T X: thread (t = tid & 63, column group tid >> 6) accumulates T[t][cg + 4 q] over the
+// chunk's rows in row order; V chunk (64 rows x 64 rank columns) and X chunk (64 rows x 16
+// columns) are staged through shared memory with coalesced loads.
+__global__ void __launch_bounds__(NT) k_mv_t(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
+    __shared__ double Vs[MV_TC * MV_LD];
+    __shared__ double Xs[MV_RHS * MV_LD];
+    __shared__ double* sh_T;
+    const long total = (long)args.nrk * mb.count;
+    const int t = threadIdx.x & 63, cg = threadIdx.x >> 6;
+    double fl = 0;
+    for (long w = blockIdx.x; w < total; w += gridDim.x) {
+        const int b = (int)(w % mb.count), li = (int)(w / mb.count);
+        const MvLeaf L = args.rk[li];
+        const HView& H = mb.h[b];
+        const int rr = H.rank[L.k];
+        __syncthreads();  // previous item's staging and sh_T are no longer read
+        if (threadIdx.x == 0) {
+            double* T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)rr * args.nrhs) : nullptr;
+            mv_tptr(args)[(size_t)b * args.nrk + li] = T;
+            sh_T = T;
+        }
+        __syncthreads();
+        double* T = sh_T;
+        if (T == nullptr) continue;
+        const double* V = H.V[L.k];
+        const double* X = mb.x[b] + L.in_off;
+        const int n = L.n;
+        for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
+            const int nc = min(MV_RHS, args.nrhs - c0);
+            for (int t0 = 0; t0 < rr; t0 += MV_TC) {
+                const int nt = min(MV_TC, rr - t0);
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int j0 = 0; j0 < n; j0 += MV_ROWS) {
+                    const int jc = min(MV_ROWS, n - j0);
+                    double v[16], x[4];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {  // V chunk: row fastest (coalesced)
+                        const int e = threadIdx.x + u * NT, j = e & 63, tt = e >> 6;
+                        v[u] = (j < jc && tt < nt) ? V[(j0 + j) + (size_t)(t0 + tt) * n] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = threadIdx.x + u * NT, j = e & 63, c = e >> 6;
+                        x[u] = (j < jc && c < nc) ? X[(j0 + j) + (size_t)(c0 + c) * args.dim] : 0.0;
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const int e = threadIdx.x + u * NT;
+                        Vs[(e >> 6) * MV_LD + (e & 63)] = v[u];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = threadIdx.x + u * NT;
+                        Xs[(e >> 6) * MV_LD + (e & 63)] = x[u];
+                    }
+                    __syncthreads();
+                    if (t < nt) {
+#pragma unroll 4
+                        for (int j = 0; j < jc; ++j) {
+                            const double vj = Vs[t * MV_LD + j];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) acc[q] = fma(vj, Xs[(cg + 4 * q) * MV_LD + j], acc[q]);
+                        }
+                    }
+                }
+                if (t < nt)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = cg + 4 * q;
+                        if (c < nc) T[(t0 + t) + (size_t)(c0 + c) * rr] = acc[q];
+                    }
+            }
+        }
+        if (threadIdx.x == 0) fl += 2.0 * rr * n * args.nrhs;
+    }
+    if (threadIdx.x == 0 && fl > 0) add_flops(args.flops, F_APPLY, fl);
+}
+
+// One output slab (<= 64 rows) of one item.  Thread (row i = tid & 63, group g = tid >> 6)
+// accumulates, for every right-hand side, the contracted indices j = g (mod 4) of every
+// leaf in leaf order (dense: D[i, j] x[j]; Rk: U[i, t] T[t]); the four group partials are
+// added in group order at the end.  Operand rows are read coalesced straight from HBM,
+// the x / T chunks are broadcast from shared memory.
+__global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
+    __shared__ double Xs[MV_RHS * MV_LD];
+    __shared__ double red[4 * MV_RHS * MV_ROWS];
     const SlabTask task = args.tasks[blockIdx.x];
     const int b = blockIdx.y;
     const HView& H = mb.h[b];
@@ -1344,77 +1232,83 @@ __global__ void __launch_bounds__(NT) k_matvec(MatvecArgs args, MatvecBatch mb) 
     double* Y = mb.y[b];
     const int ld = args.dim;
     const int nr = task.r1 - task.r0;
+    const int i = threadIdx.x & 63, g = threadIdx.x >> 6;
+    const int row = task.r0 + i;
+    double* const* Tp = mv_tptr(args) + (size_t)b * args.nrk;
     double fl = 0;
-    for (int c0 = 0; c0 < args.nrhs; c0 += 16) {
-        const int nc = min(16, args.nrhs - c0);
-        constexpr int PER = (APPLY_ROWS * 16) / NT;  // 4
-        double acc[PER];
+    for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
+        const int nc = min(MV_RHS, args.nrhs - c0);
+        double acc[MV_RHS];
 #pragma unroll
-        for (int q = 0; q < PER; ++q) acc[q] = 0.0;
+        for (int c = 0; c < MV_RHS; ++c) acc[c] = 0.0;
         for (int li = task.lbeg; li < task.lend; ++li) {
             const ApplyLeaf L = args.leaves[li];
             const int o0 = max(task.r0, L.out_off), o1 = min(task.r1, L.out_off + L.m);
             if (o0 >= o1) continue;
+            const bool mine = row >= o0 && row < o1;
+            const int lr = row - L.out_off;
+            const double* A;   // operand column j at A + j * lda (this thread's row)
+            const double* Xin; // contracted vector chunk source, column c at Xin + c * ldx
+            int len, lda, ldx;
             if (L.kind == K_DENSE) {
-                const double* D = H.dense + L.doff;
-#pragma unroll
-                for (int q = 0; q < PER; ++q) {
-                    const int e = threadIdx.x + q * NT;
-                    const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
-                    const int row = task.r0 + i;
-                    if (i >= nr || c >= nc || row < o0 || row >= o1) continue;
-                    const int lr = row - L.out_off;
-                    const double* x = X + L.in_off + (size_t)(c0 + c) * ld;
-                    double a = 0;
-                    for (int j = 0; j < L.n; ++j) a = fma(D[lr + (size_t)j * L.m], x[j], a);
-                    acc[q] += a;
-                }
-                if (threadIdx.x == 0) fl += 2.0 * (o1 - o0) * L.n * nc;
+                A = H.dense + L.doff + lr;
+                lda = L.m;
+                len = L.n;
+                Xin = X + L.in_off + (size_t)c0 * ld;
+                ldx = ld;
             } else {
                 const int rr = H.rank[L.id];
-                if (rr == 0) continue;
-                const double* Vk = H.V[L.id];
-                const double* Uk = H.U[L.id];
-                for (int t0 = 0; t0 < rr; t0 += APPLY_TR) {
-                    const int nt = min(APPLY_TR, rr - t0);
-                    __syncthreads();
-                    for (int e = threadIdx.x; e < nt * nc; e += NT) {
-                        const int t = e % nt, c = e / nt;
-                        const double* v = Vk + (size_t)(t0 + t) * L.n;
-                        const double* x = X + L.in_off + (size_t)(c0 + c) * ld;
-                        double a = 0;
-                        for (int j = 0; j < L.n; ++j) a = fma(v[j], x[j], a);
-                        T[t + c * APPLY_TR] = a;
-                    }
-                    __syncthreads();
+                const double* T = rr > 0 ? Tp[L.id] : nullptr;
+                if (T == nullptr) continue;
+                A = H.U[L.id] + lr;
+                lda = L.m;
+                len = rr;
+                Xin = T + (size_t)c0 * rr;
+                ldx = rr;
+            }
+            for (int j0 = 0; j0 < len; j0 += MV_ROWS) {
+                const int jc = min(MV_ROWS, len - j0);
+                __syncthreads();
 #pragma unroll
-                    for (int q = 0; q < PER; ++q) {
-                        const int e = threadIdx.x + q * NT;
-                        const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
-                        const int row = task.r0 + i;
-                        if (i >= nr || c >= nc || row < o0 || row >= o1) continue;
-                        const int lr = row - L.out_off;
-                        double a = 0;
-                        for (int t = 0; t < nt; ++t) a = fma(Uk[lr + (size_t)(t0 + t) * L.m], T[t + c * APPLY_TR], a);
-                        acc[q] += a;
+                for (int u = 0; u < 4; ++u) {
+                    const int e = threadIdx.x + u * NT, j = e & 63, c = e >> 6;
+                    Xs[c * MV_LD + j] = (j < jc && c < nc) ? Xin[(j0 + j) + (size_t)c * ldx] : 0.0;
+                }
+                __syncthreads();
+                if (mine) {
+                    int j = g;
+                    for (; j + 12 < jc; j += 16) {  // four operand loads in flight per thread
+                        double d[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) d[q] = A[(size_t)(j0 + j + 4 * q) * lda];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+#pragma unroll
+                            for (int c = 0; c < MV_RHS; ++c)
+                                if (c < nc) acc[c] = fma(d[q], Xs[c * MV_LD + j + 4 * q], acc[c]);
+                    }
+                    for (; j < jc; j += 4) {
+                        const double d = A[(size_t)(j0 + j) * lda];
+#pragma unroll
+                        for (int c = 0; c < MV_RHS; ++c)
+                            if (c < nc) acc[c] = fma(d, Xs[c * MV_LD + j], acc[c]);
                     }
                 }
-                if (threadIdx.x == 0) {
-                    fl += 2.0 * (o1 - o0) * rr * nc;
-                    if (L.out_off >= task.r0 && L.out_off < task.r1) fl += 2.0 * rr * L.n * nc;
-                }
             }
-        }
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            const int e = threadIdx.x + q * NT;
-            const int i = e % APPLY_ROWS, c = e / APPLY_ROWS;
-            if (i < nr && c < nc) {
-                const size_t o = (task.r0 + i) + (size_t)(c0 + c) * ld;
-                Y[o] = base ? base[o] - acc[q] : acc[q];
-            }
+            if (threadIdx.x == 0 && c0 == 0) fl += 2.0 * (o1 - o0) * len * args.nrhs;
         }
         __syncthreads();
+#pragma unroll
+        for (int c = 0; c < MV_RHS; ++c) red[(g * MV_RHS + c) * MV_ROWS + i] = acc[c];
+        __syncthreads();
+        for (int e = threadIdx.x; e < MV_ROWS * nc; e += NT) {
+            const int r = e & 63, c = e >> 6;
+            if (r >= nr) continue;
+            const double s = ((red[(0 * MV_RHS + c) * MV_ROWS + r] + red[(1 * MV_RHS + c) * MV_ROWS + r]) +
+                              red[(2 * MV_RHS + c) * MV_ROWS + r]) + red[(3 * MV_RHS + c) * MV_ROWS + r];
+            const size_t o = (task.r0 + r) + (size_t)(c0 + c) * ld;
+            Y[o] = base ? base[o] - s : s;
+        }
     }
     if (threadIdx.x == 0) add_flops(args.flops, F_APPLY, fl);
 }
@@ -1506,6 +1400,7 @@ __global__ void k_scatter(ScatterArgs a, BatchViews bv) {
 }
 
 __global__ void k_reset_counter(unsigned long long* ctr) { *ctr = 0; }
+__global__ void k_set_counter(unsigned long long* ctr, unsigned long long v) { *ctr = v; }
 
 // Factor compaction: copy every low-rank leaf (U then V) of a batch of stores into
 // one exact-size buffer at host-computed offsets and repoint the leaf tables.
@@ -1825,14 +1720,42 @@ void fold_ledger() {
     cudaMemset(g_report_ledger, 0, MAX_KERNELS * sizeof(FlopLedger));
 }
 static std::map<std::string, std::tuple<double, long, long>> g_prof_acc;  // ms, launches, ctas
+// -1: not yet read from ACRGPU_PROFILE; 0 off; 1 every kernel; 2 only the kernels in
+// g_prof_sel (ACRGPU_PROFILE=name[,name...] or prof_select): events around the selected
+// launches only, so a timed region can carry the dominant kernel's timing without
+// paying two event records on every other launch.
 static int g_prof_on = -1;
-static bool prof_on() {
-    if (g_prof_on < 0) g_prof_on = getenv("ACRGPU_PROFILE") ? 1 : 0;
-    return g_prof_on == 1;
+static std::vector<std::string> g_prof_sel;
+void prof_select(const char* filter) {
+    g_prof_sel.clear();
+    if (!filter || !*filter || std::string(filter) == "0") {
+        g_prof_on = 0;
+        return;
+    }
+    const std::string f(filter);
+    if (f == "1" || f == "*") {
+        g_prof_on = 1;
+        return;
+    }
+    size_t a = 0;
+    while (a <= f.size()) {
+        size_t b = f.find(',', a);
+        if (b == std::string::npos) b = f.size();
+        if (b > a) g_prof_sel.push_back(f.substr(a, b - a));
+        a = b + 1;
+    }
+    g_prof_on = g_prof_sel.empty() ? 0 : 2;
+}
+static bool prof_on(const char* name) {
+    if (g_prof_on < 0) prof_select(getenv("ACRGPU_PROFILE"));
+    if (g_prof_on != 2) return g_prof_on == 1;
+    for (const auto& s : g_prof_sel)
+        if (s == name) return true;
+    return false;
 }
 ProfScope::ProfScope(cudaStream_t s, const char* n, long c) : st(s), name(n), ctas(c) {
     ++g_launches;
-    if (prof_on()) {
+    if (prof_on(n)) {
         a = ev_get();
         cudaEventRecord(a, st);
     }
@@ -2036,14 +1959,23 @@ void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const dou
     k_scale_reduce<<<B, 256, 0, st>>>(sig_d, nd, sig_k, nk, B, eps, abs_cut);
 }
 
-void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, int nrhs, int dim,
-                   FlopLedger* flops, const MatvecBatch& mb) {
+void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, const MvLeaf* rk,
+                   int nrk, int nrhs, int dim, Arena arena, FlopLedger* flops, const MatvecBatch& mb) {
     if (ntasks == 0 || mb.count == 0) return;
-    MatvecArgs a{tasks, leaves, nrhs, dim, ledger(flops, "k_matvec")};
-    ProfScope _ps(st, "k_matvec", (long)((ntasks)*(mb.count)));
-    k_matvec<<<dim3(ntasks, mb.count), NT, 0, st>>>(a, mb);
+    MatvecArgs a{tasks, leaves, rk, nrk, nrhs, dim, arena, ledger(flops, "k_mv_t")};
+    {
+        // T pointer table [count][nrk] at the arena base, T blocks bump-allocated after it
+        ProfScope _ps(st, "k_set_counter", 1);
+        k_set_counter<<<1, 1, 0, st>>>(arena.ctr, ((unsigned long long)mb.count * nrk + 15ull) & ~15ull);
+    }
+    if (nrk > 0) {
+        ProfScope _ps(st, "k_mv_t", (long)nrk * mb.count);
+        k_mv_t<<<item_grid((long)nrk * mb.count, 5), NT, 0, st>>>(a, mb);
+    }
+    a.flops = ledger(flops, "k_mv_slab");
+    ProfScope _ps(st, "k_mv_slab", (long)ntasks * mb.count);
+    k_mv_slab<<<dim3(ntasks, mb.count), NT, 0, st>>>(a, mb);
 }
-
 void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
     ProfScope _ps(st, "k_permute_in", (long)(1184));
     k_permute_in<<<1184, 256, 0, st>>>(in, out, perm, n, dim, nrhs);

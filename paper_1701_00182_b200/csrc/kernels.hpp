@@ -79,6 +79,7 @@ void launch_vadd(cudaStream_t st, double* x, const double* z, long n);
 void setup_kernels();
 long launches_take();
 std::string prof_report(bool reset);
+void prof_select(const char* filter);
 void set_report_ledger(FlopLedger* l);
 void fold_ledger();
 int kernel_id(const char* name);
@@ -107,8 +108,10 @@ void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, 
                FlopLedger* flops, const BatchViews& bv, int maxm);
 void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,
                          double* abs_cut);
-void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, int nrhs, int dim,
-                   FlopLedger* flops, const MatvecBatch& mb);
+// Batched solve matvec y = base - H x (two phases, see kernels.cu).  arena: transient
+// workspace (reset by the call) for the per-leaf V^T x blocks.
+void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, const MvLeaf* rk,
+                   int nrk, int nrhs, int dim, Arena arena, FlopLedger* flops, const MatvecBatch& mb);
 void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs);
 void launch_permute_out(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs);
 void launch_zero_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk);

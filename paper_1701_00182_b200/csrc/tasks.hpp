@@ -153,6 +153,11 @@ struct SlabTask {      // output rows [r0, r1) of the tree-ordered plane vector
     int r0, r1;
     int lbeg, lend;    // ApplyLeaf range (non-transposed, in_off = leaf col, out_off = leaf row)
 };
+struct MvLeaf {         // Rk leaf k of the root: columns [in_off, in_off + n), rows m
+    int k;
+    int in_off;
+    int n, m;
+};
 struct MatvecBatch {
     int count;
     HView h[MAXB];
