@@ -364,6 +364,23 @@ def run_ours(args):
                 "whole_factor_achieved_tflops": flops / (sum(t_fac) / len(t_fac) / 1000.0) / 1e12 if t_fac else None,
                 "kernels": warm_rows[:10]}
 
+    # solve against the HBM roofline (k_mv_t + k_mv_slab of the profiled warm-up step): every
+    # stored entry of every applied H-matrix is read once and takes part in 2*nrhs flops
+    solve_roof = None
+    mv = [r for r in warm_rows if r["kernel"] in ("k_mv_t", "k_mv_slab")]
+    if mv:
+        peak_gbs = None
+        try:
+            peak_gbs = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except Exception:
+            peak_gbs = 6442.2
+        mv_ms = sum(r["ms"] for r in mv)
+        mv_bytes = 8.0 * sum(r["flops"] for r in mv) / (2.0 * nrhs)
+        ach = mv_bytes / (mv_ms / 1e3) / 1e9 if mv_ms > 0 else 0.0
+        solve_roof = {"bound": "hbm", "kernels": ["k_mv_t", "k_mv_slab"], "achieved": ach, "peak": peak_gbs,
+                      "unit": "GB/s", "frac": ach / peak_gbs, "bytes_per_solve": mv_bytes, "kernel_ms": mv_ms,
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
     # end-to-end through the public API with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
@@ -421,7 +438,7 @@ def run_ours(args):
                 "nominal_flops_per_step": flops, "gpu_launches": launches // max(1, args.steps),
                 "levels": [{"level": l.level, "planes": l.plane_count, "largest_rank": l.largest_rank,
                             "average_rank": round(l.average_rank, 3)} for l in lv],
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks}
+                "roofline": roof, "solve_roofline": solve_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

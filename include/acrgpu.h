@@ -192,6 +192,17 @@ typedef struct acrgpu_comm acrgpu_comm;
 int acrgpu_comm_unique_id(unsigned char* id /* ACRGPU_COMM_ID_BYTES */, acrgpu_error* err);
 int acrgpu_comm_create(const unsigned char* id, int nranks, int rank, acrgpu_comm** out, acrgpu_error* err);
 int acrgpu_comm_create_local(int nranks, acrgpu_comm** out, acrgpu_error* err);
+/* Host-staged multi-process communicator (no NCCL): every wire image is copied to host memory
+ * and moved by `fn`, called once per exchange phase with all of this rank's sends (to rank
+ * dst[i], sbytes[i] bytes at sbuf[i]) and receives (from rank src[j] into rbuf[j], rbytes[j]
+ * bytes).  Messages between one pair of ranks are posted in the same order on both sides, so
+ * a point-to-point channel that keeps per-pair order (e.g. torch.distributed isend/irecv over
+ * gloo) delivers them correctly.  Returns nonzero to abort the factorization (ACRGPU_E_DEVICE).
+ * Used to run the partitioned data path across real processes without NVLink/NCCL. */
+typedef int (*acrgpu_exchange_fn)(void* user, int nsend, const int* dst, const void* const* sbuf, const long* sbytes,
+                                  int nrecv, const int* src, void* const* rbuf, const long* rbytes);
+int acrgpu_comm_create_host(acrgpu_exchange_fn fn, void* user, int nranks, int rank, acrgpu_comm** out,
+                            acrgpu_error* err);
 void acrgpu_comm_destroy(acrgpu_comm* comm);
 int acrgpu_factor_partitioned(acrgpu_ctx* ctx, acrgpu_comm* comm, const acrgpu_system* sys,
                               const acrgpu_config* cfg, acrgpu_fact** out, acrgpu_error* err);

@@ -180,6 +180,8 @@ SYMBOLS = {
     "acrgpu_comm_unique_id": (C.c_int, [C.c_char_p, C.POINTER(_Err)]),
     "acrgpu_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(_Err)]),
     "acrgpu_comm_create_local": (C.c_int, [C.c_int, C.POINTER(C.c_void_p), C.POINTER(_Err)]),
+    "acrgpu_comm_create_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                          C.POINTER(_Err)]),
     "acrgpu_comm_destroy": (None, [C.c_void_p]),
     "acrgpu_factor_partitioned": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Sys), C.POINTER(_Cfg),
                                             C.POINTER(C.c_void_p), C.POINTER(_Err)]),
@@ -413,6 +415,41 @@ def acr_factor(system, config: AcrConfig | None = None, ctx: Context | None = No
     return AcrFactorization(h, host, config, ctx)
 
 
+_EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p),
+                          C.POINTER(C.c_long), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.POINTER(C.c_long))
+
+
+def torch_exchange(group=None):
+    """Exchange callable for ``Comm.host`` over torch.distributed point-to-point (any backend
+    with CPU tensors, e.g. gloo): per peer, the k-th send matches the peer's k-th receive
+    (tag k)."""
+    import torch
+    import torch.distributed as dist
+
+    def exchange(sends, recvs):
+        reqs, keep, tags = [], [], {}
+        for dst, mv in sends:
+            k = tags.get(("s", dst), 0)
+            tags[("s", dst)] = k + 1
+            t = torch.frombuffer(bytearray(mv), dtype=torch.uint8) if len(mv) else torch.zeros(0, dtype=torch.uint8)
+            keep.append(t)
+            reqs.append(dist.isend(t, dst, group=group, tag=k))
+        outs = []
+        for src, mv in recvs:
+            k = tags.get(("r", src), 0)
+            tags[("r", src)] = k + 1
+            t = torch.empty(len(mv), dtype=torch.uint8)
+            outs.append((mv, t))
+            reqs.append(dist.irecv(t, src, group=group, tag=k))
+        for r in reqs:
+            r.wait()
+        for mv, t in outs:
+            if len(mv):
+                mv[:] = t.numpy().tobytes()  # mv: unsigned-byte view of the library's host buffer
+
+    return exchange
+
+
 class Comm:
     """Plane-partition communicator (execute_parallel_factor, parallel.hpp:60-61).
 
@@ -439,6 +476,36 @@ class Comm:
         if lib().acrgpu_comm_create_local(nranks, C.byref(h), C.byref(err)):
             _raise(err)
         return cls(h, nranks, 0, True)
+
+    @classmethod
+    def host(cls, exchange, nranks: int, rank: int) -> "Comm":
+        """Host-staged communicator: ``exchange(sends, recvs)`` moves the wire images of one
+        phase -- ``sends`` a list of (dst rank, memoryview), ``recvs`` a list of (src rank,
+        writable memoryview); messages between one pair of ranks must be matched in list
+        order (``torch_exchange`` does it with torch.distributed isend/irecv)."""
+
+        def fn(user, nsend, dst, sbuf, sbytes, nrecv, src, rbuf, rbytes):
+            try:
+                def view(addr, n):
+                    return memoryview((C.c_ubyte * n).from_address(addr)).cast("B") if n else memoryview(bytearray(0))
+
+                sends = [(dst[i], view(sbuf[i], sbytes[i])) for i in range(nsend)]
+                recvs = [(src[i], view(rbuf[i], rbytes[i])) for i in range(nrecv)]
+                exchange(sends, recvs)
+                return 0
+            except Exception:  # pragma: no cover - surfaced as ACRGPU_E_DEVICE
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        cb = _EXCHANGE_FN(fn)
+        h = C.c_void_p()
+        err = _Err()
+        if lib().acrgpu_comm_create_host(cb, None, nranks, rank, C.byref(h), C.byref(err)):
+            _raise(err)
+        c = cls(h, nranks, rank, False)
+        c._cb = cb  # keep the trampoline alive as long as the communicator
+        return c
 
     @classmethod
     def nccl(cls, uid: bytes, nranks: int, rank: int) -> "Comm":

@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <functional>
 #include <map>
 #include <memory>
@@ -75,8 +76,15 @@ static T* upload(const std::vector<T>& v, cudaStream_t st) {
 // mult_adds of one recursion step (T12 || T21, C12 || C21 in invert_node; the
 // E'/F' couplings beside the D updates) run concurrently on the GPU.
 constexpr int NLANES = 2;
+// Inside one mult_add the launches of independent task lists (apply vs dense*dense products,
+// the size classes of one truncation phase, dense deposits vs the Rk flush) fork onto NSUB
+// side streams of the lane and join back before the next dependent phase.
+constexpr int NSUB = 3;
 struct Lane {
     cudaStream_t st = nullptr;
+    cudaStream_t sub[NSUB] = {};
+    cudaEvent_t fork_ev = nullptr;
+    cudaEvent_t join_ev[NSUB] = {};
     Arena trans{};
     Slot* slots = nullptr;
     size_t slots_cap = 0;
@@ -110,6 +118,11 @@ struct Ctx {
         for (auto& l : lanes) {
             CK(cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&l.ev, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&l.fork_ev, cudaEventDisableTiming));
+            for (int i = 0; i < NSUB; ++i) {
+                CK(cudaStreamCreateWithFlags(&l.sub[i], cudaStreamNonBlocking));
+                CK(cudaEventCreateWithFlags(&l.join_ev[i], cudaEventDisableTiming));
+            }
         }
         st = lanes[0].st;
         setup_kernels();
@@ -155,6 +168,22 @@ struct Ctx {
         CK(cudaEventRecord(lanes[from].ev, lanes[from].st));
         CK(cudaStreamWaitEvent(lanes[to].st, lanes[from].ev, 0));
     }
+    // the lane's side streams i < k wait for everything issued so far on the lane's stream
+    void fork(int k) {
+        Lane& l = lane();
+        CK(cudaEventRecord(l.fork_ev, l.st));
+        for (int i = 0; i < k && i < NSUB; ++i) CK(cudaStreamWaitEvent(l.sub[i], l.fork_ev, 0));
+    }
+    // the lane's stream waits for side streams i < k
+    void join(int k) {
+        Lane& l = lane();
+        for (int i = 0; i < k && i < NSUB; ++i) {
+            CK(cudaEventRecord(l.join_ev[i], l.sub[i]));
+            CK(cudaStreamWaitEvent(l.st, l.join_ev[i], 0));
+        }
+    }
+    // stream q of the current fork: 0 = the lane's stream, 1..NSUB = side streams
+    cudaStream_t fstream(int q) { return q == 0 ? lane().st : lane().sub[(q - 1) % NSUB]; }
     void reset_all() {
         for (auto& l : lanes) CK(cudaStreamSynchronize(l.st));
         persist.base = space_ptr(space);
@@ -216,6 +245,12 @@ struct Ctx {
         for (auto& l : lanes) {
             if (l.slots) cudaFree(l.slots);
             if (l.ev) cudaEventDestroy(l.ev);
+            if (l.fork_ev) cudaEventDestroy(l.fork_ev);
+            for (int i = 0; i < NSUB; ++i) {
+                if (l.sub[i]) cudaStreamSynchronize(l.sub[i]);
+                if (l.sub[i]) cudaStreamDestroy(l.sub[i]);
+                if (l.join_ev[i]) cudaEventDestroy(l.join_ev[i]);
+            }
             if (l.st) cudaStreamDestroy(l.st);
             l = Lane{};
         }
@@ -308,6 +343,7 @@ struct Engine {
     int n_mv_rk = 0;
 
     ~Engine() {
+        gc_release_all();
         for (void* p : dev_allocs) cudaFree(p);
     }
     template <class T>
@@ -337,17 +373,38 @@ struct Engine {
         return c;
     }
 
-    void run_trunc(const Classed<TruncTask>& tl, const Part* parts, Slot* slots, int nb, double eps,
-                   const double* abs_cut, double* sig_out, bool values_only, Arena out, const BatchViews& bv) {
+    // One truncation phase: the size classes are independent task lists.  q0: first stream
+    // of the current fork to use (the classes go to q0, q0 + 1, ...); returns the next free one.
+    int run_trunc(const Classed<TruncTask>& tl, const Part* parts, Slot* slots, int nb, double eps,
+                  const double* abs_cut, double* sig_out, bool values_only, Arena out, const BatchViews& bv,
+                  int q0 = -1) {
         const Arena tr = ctx->lane().trans;
-        if (tl.n[0]) launch_trunc_small(st(), 32, tl.n[0], tl.p[0], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
+        int q = q0;
+        auto sq = [&]() { return q0 < 0 ? st() : ctx->fstream(q++); };
+        if (tl.n[0]) launch_trunc_small(sq(), 32, tl.n[0], tl.p[0], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
                                         tr, ctx->flops, bv);
-        if (tl.n[1]) launch_trunc_small(st(), 64, tl.n[1], tl.p[1], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
+        if (tl.n[1]) launch_trunc_small(sq(), 64, tl.n[1], tl.p[1], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
                                         tr, ctx->flops, bv);
-        if (tl.n[2]) launch_truncate(st(), tl.n[2], tl.p[2], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
+        if (tl.n[2]) launch_truncate(sq(), tl.n[2], tl.p[2], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
                                      tr, ctx->flops, bv, "k_trunc_d128");
-        if (tl.n[3]) launch_truncate(st(), tl.n[3], tl.p[3], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
+        if (tl.n[3]) launch_truncate(sq(), tl.n[3], tl.p[3], parts, slots, nb, eps, abs_cut, sig_out, values_only, out,
                                      tr, ctx->flops, bv, "k_trunc_qr");
+        return q;
+    }
+    static int nclasses(const Classed<TruncTask>& tl) {
+        return (tl.n[0] > 0) + (tl.n[1] > 0) + (tl.n[2] > 0) + (tl.n[3] > 0);
+    }
+    // run_trunc with the classes on parallel streams of the lane (fork / join around it)
+    void run_trunc_par(const Classed<TruncTask>& tl, const Part* parts, Slot* slots, int nb, double eps,
+                       const double* abs_cut, double* sig_out, bool values_only, Arena out, const BatchViews& bv) {
+        const int k = nclasses(tl);
+        if (k <= 1) {
+            run_trunc(tl, parts, slots, nb, eps, abs_cut, sig_out, values_only, out, bv);
+            return;
+        }
+        ctx->fork(k - 1);
+        run_trunc(tl, parts, slots, nb, eps, abs_cut, sig_out, values_only, out, bv, 0);
+        ctx->join(k - 1);
     }
 
     // -------------------------------------------------------------- storage
@@ -739,13 +796,20 @@ struct Engine {
             int chunk = MAXB;
             bool measure = false;
             if (adaptive) {
-                if (P->pp_gb < 0 || P->pp_level != level_tag) {
-                    measure = true;
-                    // new plan, or a new level (ranks grew, by more than 10x for the root
-                    // products): measure on a single plane
-                    chunk = 1;
-                } else {
+                const int left = (int)(C.size() - i0);
+                if (left == 1) {
+                    chunk = 1;  // a single plane left: nothing to size
+                } else if (P->pp_gb >= 0 && P->pp_level == level_tag) {
                     chunk = batch_for(P->pp_gb);
+                } else if (P->pp_gb >= 0 && batch_for(std::max(4.0 * P->pp_gb, 1e-4)) >= left) {
+                    // measured at an earlier level and small: even 4x rank growth fits every
+                    // remaining plane in one batch (most plans; no host round trip)
+                    chunk = left;
+                } else {
+                    // new plan, or one whose growth could overflow the arena: measure on a
+                    // single plane (root products grow by more than 10x over the levels)
+                    measure = true;
+                    chunk = 1;
                 }
             }
             const int nb = (int)std::min<size_t>(chunk, C.size() - i0);
@@ -758,15 +822,33 @@ struct Engine {
             Slot* slots = ctx->get_slots((size_t)std::max(1, P->nprod + P->ntt) * nb);
             const Arena tr = ctx->lane().trans;
             ctx->reset_ctr(st(), tr.ctr);
-            launch_alloc_apply(st(), P->nalloc, P->allocs, slots, nb, tr, bv);
-            launch_apply_t(st(), P->ntt, P->tts, slots, P->nprod, nb, tr, ctx->flops, bv);
-            launch_apply(st(), P->napply, P->applies, P->aleaves, P->x_ld, slots, P->nprod, nb, ctx->flops, bv);
-            if (P->dds.n[0]) launch_dd_small(st(), 32, P->dds.n[0], P->dds.p[0], slots, nb, eps, tr, ctx->flops, bv);
-            if (P->dds.n[1]) launch_dd_small(st(), 64, P->dds.n[1], P->dds.p[1], slots, nb, eps, tr, ctx->flops, bv);
             if (P->dds.n[2] || P->dds.n[3]) throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64"};
-            for (auto& ph : P->bb) run_trunc(ph, P->parts, slots, nb, eps, nullptr, nullptr, false, tr, bv);
-            launch_deposit(st(), P->ndep, P->deps, P->parts, slots, nb, ctx->flops, bv);
-            run_trunc(P->flush, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->persist, bv);
+            // products: the apply chain on the lane's stream, the dense*dense classes beside it
+            {
+                const int kdd = (P->dds.n[0] > 0) + (P->dds.n[1] > 0);
+                ctx->fork(kdd);
+                int q = 1;
+                if (P->dds.n[0]) launch_dd_small(ctx->fstream(q++), 32, P->dds.n[0], P->dds.p[0], slots, nb, eps, tr, ctx->flops, bv);
+                if (P->dds.n[1]) launch_dd_small(ctx->fstream(q++), 64, P->dds.n[1], P->dds.p[1], slots, nb, eps, tr, ctx->flops, bv);
+                launch_alloc_apply(st(), P->nalloc, P->allocs, slots, nb, tr, bv);
+                launch_apply_t(st(), P->ntt, P->tts, slots, P->nprod, nb, tr, ctx->flops, bv);
+                launch_apply(st(), P->napply, P->applies, P->aleaves, P->x_ld, slots, P->nprod, nb, ctx->flops, bv);
+                ctx->join(kdd);
+            }
+            // Branch*Branch agglomerations, bottom-up: the classes of a phase in parallel
+            for (auto& ph : P->bb) run_trunc_par(ph, P->parts, slots, nb, eps, nullptr, nullptr, false, tr, bv);
+            // dense-target deposits and the Rk flush write disjoint leaves of C: in parallel
+            {
+                const int kf = nclasses(P->flush);
+                const int tasks = (P->ndep > 0 ? 1 : 0) + kf;
+                const int k = std::min(NSUB, std::max(0, tasks - 1));  // side streams used
+                if (k > 0) ctx->fork(k);
+                int q = 0;  // stream 0 = the lane's own
+                if (P->ndep > 0) launch_deposit(ctx->fstream(q++), P->ndep, P->deps, P->parts, slots, nb, ctx->flops, bv);
+                if (kf) run_trunc(P->flush, P->parts, slots, nb, eps, nullptr, nullptr, false, ctx->persist, bv, k > 0 ? q : -1);
+                if (k > 0) ctx->join(k);
+            }
+            gc_mark();
             if (measure) {
                 unsigned long long used = 0;
                 CK(cudaStreamSynchronize(st()));
@@ -803,17 +885,86 @@ struct Engine {
         if (ctx->factoring != 1 || getenv("ACRGPU_NO_GC")) return false;
         return S.dim > 4096 || getenv("ACRGPU_GC_FORCE");
     }
-    // Safe point at every mult_add entry (also inside pair(): all lanes are drained first, and
-    // the host holds no arena pointer between mult_adds), so at most one batched mult_add's
-    // flush outputs are allocated between two checks.
+    // Safe point at every mult_add entry (also inside pair(): the host holds no arena pointer
+    // between mult_adds).  The fill level is watched without host round trips: every
+    // mult_add ends with an 8-byte copy of the arena counter into pinned memory plus an
+    // event (copy engine, no SM slot), and the check reads the newest completed copies.
+    // The value is a lower bound; the mult_adds still in flight are bounded by the largest
+    // growth seen between two completed marks, and the host waits for the oldest of them
+    // only when that bound could reach the end of the semi-space (or more than 16 are
+    // pending).  Compaction itself drains both lanes as before.
+    struct GcMark {
+        cudaEvent_t ev = nullptr;
+        unsigned long long* slot = nullptr;
+    };
+    std::deque<GcMark> gc_marks;  // issue order
+    std::vector<GcMark> gc_free;
+    std::vector<unsigned long long*> gc_slabs;  // pinned slot blocks
+    unsigned long long gc_known = 0;  // newest completed counter value (doubles)
+    double gc_growth = 0;             // largest growth between two completed marks (doubles)
+    GcMark gc_take() {
+        if (gc_free.empty()) {
+            unsigned long long* blk = nullptr;
+            CK(cudaMallocHost(&blk, 64 * sizeof(unsigned long long)));
+            gc_slabs.push_back(blk);
+            for (int i = 0; i < 64; ++i) {
+                GcMark m;
+                CK(cudaEventCreateWithFlags(&m.ev, cudaEventDisableTiming));
+                m.slot = blk + i;
+                gc_free.push_back(m);
+            }
+        }
+        GcMark m = gc_free.back();
+        gc_free.pop_back();
+        return m;
+    }
+    void gc_release_all() {
+        for (auto& m : gc_free) cudaEventDestroy(m.ev);
+        for (auto& m : gc_marks) cudaEventDestroy(m.ev);
+        for (auto* b : gc_slabs) cudaFreeHost(b);
+        gc_free.clear();
+        gc_marks.clear();
+        gc_slabs.clear();
+    }
+    void gc_mark() {
+        if (!gc_enabled()) return;
+        GcMark m = gc_take();
+        CK(cudaMemcpyAsync(m.slot, ctx->persist.ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st()));
+        CK(cudaEventRecord(m.ev, st()));
+        gc_marks.push_back(m);
+    }
+    void gc_poll(bool wait_oldest) {
+        if (wait_oldest && !gc_marks.empty()) CK(cudaEventSynchronize(gc_marks.front().ev));
+        for (auto it = gc_marks.begin(); it != gc_marks.end();) {
+            const cudaError_t q = cudaEventQuery(it->ev);
+            if (q == cudaErrorNotReady) {
+                ++it;
+                continue;
+            }
+            CK(q);
+            const unsigned long long v = *it->slot;
+            if (v > gc_known) {
+                gc_growth = std::max(gc_growth, (double)(v - gc_known));
+                gc_known = v;
+            }
+            gc_free.push_back(*it);
+            it = gc_marks.erase(it);
+        }
+    }
     void gc_check() {
         if (!gc_enabled()) return;
-        for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.st));
-        unsigned long long used = 0;
-        CK(cudaMemcpy(&used, ctx->persist.ctr, sizeof(used), cudaMemcpyDeviceToHost));
+        const double cap = (double)ctx->persist.cap;
+        const double g = std::max(gc_growth, 0.01 * cap);
+        gc_poll(false);
+        // worst case once the next mult_add is issued: every pending one (and it) grows by 1.5 g
+        while (!gc_marks.empty() &&
+               (gc_marks.size() > 16 || (double)gc_known + 1.5 * g * (double)(gc_marks.size() + 1) > 0.92 * cap))
+            gc_poll(true);
         const char* force = getenv("ACRGPU_GC_FORCE");
         const double at = force ? atof(force) : gc_next;
-        if (used == 0 || (double)used < at * (double)ctx->persist.cap) return;
+        if (gc_known == 0 || (double)gc_known < at * cap) return;
+        for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.st));
+        gc_poll(false);
         gc();
     }
     void gc() {
@@ -878,6 +1029,7 @@ struct Engine {
         CK(cudaStreamSynchronize(s0));
         for (void* p : tmp) cudaFree(p);
         ctx->swap_space();
+        gc_known = total;
         ++gc_count;
         const double live_frac = (double)total / (double)ctx->persist.cap;
         gc_next = std::min(0.85, std::max(0.6, live_frac + 0.25));
@@ -1155,6 +1307,8 @@ struct acrgpu_comm {
     int nranks = 1, rank = 0;
     bool local = true;
     void* nccl = nullptr;  // ncclComm_t
+    acrgpu_exchange_fn host_fn = nullptr;  // host-staged transport (acrgpu_comm_create_host)
+    void* host_user = nullptr;
 };
 
 namespace acrgpu {
@@ -2077,6 +2231,107 @@ struct NcclTransport : Transport {
     }
 };
 
+// One rank per process, images staged through host memory and moved by a caller-supplied
+// exchange callback (e.g. torch.distributed over gloo): the same two phases as NCCL (sizes,
+// then images), each one callback with every send and receive of the phase.  Messages
+// between a pair of ranks are posted in (peer, key) order on both sides.
+struct HostTransport : Transport {
+    acrgpu_exchange_fn fn = nullptr;
+    void* user = nullptr;
+    cudaStream_t st = nullptr;
+    void call(std::vector<int>& dst, std::vector<const void*>& sb, std::vector<long>& sn, std::vector<int>& src,
+              std::vector<void*>& rb, std::vector<long>& rn) {
+        const int rc = fn(user, (int)dst.size(), dst.data(), sb.data(), sn.data(), (int)src.size(), src.data(), rb.data(),
+                          rn.data());
+        if (rc != 0) throw AcrError{ACRGPU_E_DEVICE, "host transport: exchange callback failed (" + std::to_string(rc) + ")"};
+    }
+    std::vector<Msg> exchange(std::vector<Msg>& out, const std::vector<Expect>& expect) override {
+        std::vector<size_t> oi(out.size()), ei(expect.size());
+        std::iota(oi.begin(), oi.end(), 0);
+        std::iota(ei.begin(), ei.end(), 0);
+        std::sort(oi.begin(), oi.end(), [&](size_t a, size_t b) {
+            return out[a].dst != out[b].dst ? out[a].dst < out[b].dst : out[a].key < out[b].key;
+        });
+        std::sort(ei.begin(), ei.end(), [&](size_t a, size_t b) {
+            return expect[a].src != expect[b].src ? expect[a].src < expect[b].src : expect[a].key < expect[b].key;
+        });
+        const size_t no = out.size(), ne = expect.size();
+        std::vector<long long> ssz(no), rsz(ne, 0);
+        std::vector<int> dst(no), src(ne);
+        std::vector<const void*> sb(no);
+        std::vector<void*> rb(ne);
+        std::vector<long> sn(no, 8), rn(ne, 8);
+        for (size_t i = 0; i < no; ++i) {
+            ssz[i] = (long long)out[oi[i]].im.n;
+            dst[i] = out[oi[i]].dst;
+            sb[i] = &ssz[i];
+        }
+        for (size_t i = 0; i < ne; ++i) {
+            src[i] = expect[ei[i]].src;
+            rb[i] = &rsz[i];
+        }
+        call(dst, sb, sn, src, rb, rn);
+        // images: device -> host, exchange, host -> device
+        CK(cudaStreamSynchronize(st));
+        // (empty images -- absent couplings -- are known to both sides and not sent)
+        std::vector<std::vector<double>> hs(no), hr(ne);
+        std::vector<int> dst2, src2;
+        std::vector<const void*> sb2;
+        std::vector<void*> rb2;
+        std::vector<long> sn2, rn2;
+        for (size_t i = 0; i < no; ++i) {
+            const Msg& m = out[oi[i]];
+            if (!m.im.n) continue;
+            hs[i].resize(m.im.n);
+            CK(cudaMemcpy(hs[i].data(), m.im.buf, m.im.n * sizeof(double), cudaMemcpyDeviceToHost));
+            dst2.push_back(dst[i]);
+            sb2.push_back(hs[i].data());
+            sn2.push_back((long)(m.im.n * sizeof(double)));
+        }
+        for (size_t i = 0; i < ne; ++i) {
+            if (!rsz[i]) continue;
+            hr[i].resize((size_t)rsz[i]);
+            src2.push_back(src[i]);
+            rb2.push_back(hr[i].data());
+            rn2.push_back((long)(rsz[i] * sizeof(double)));
+        }
+        call(dst2, sb2, sn2, src2, rb2, rn2);
+        std::vector<Msg> in(ne);
+        for (size_t i = 0; i < ne; ++i) {
+            const Expect& x = expect[ei[i]];
+            Msg& m = in[ei[i]];
+            m.src = x.src;
+            m.dst = x.dst;
+            m.key = x.key;
+            m.im.n = (size_t)rsz[i];
+            if (m.im.n) {
+                CK(cudaMallocAsync((void**)&m.im.buf, m.im.n * sizeof(double), st));
+                CK(cudaMemcpyAsync(m.im.buf, hr[i].data(), m.im.n * sizeof(double), cudaMemcpyHostToDevice, st));
+            }
+        }
+        CK(cudaStreamSynchronize(st));
+        for (auto& m : out)
+            if (m.im.buf) CK(cudaFreeAsync(m.im.buf, st));
+        out.clear();
+        return in;
+    }
+};
+
+// transport of a multi-process communicator (NCCL or host-staged)
+static std::unique_ptr<Transport> make_transport(acrgpu_comm* comm, cudaStream_t st) {
+    if (comm->host_fn) {
+        auto t = std::make_unique<HostTransport>();
+        t->fn = comm->host_fn;
+        t->user = comm->host_user;
+        t->st = st;
+        return t;
+    }
+    auto t = std::make_unique<NcclTransport>();
+    t->comm = (ncclComm_t)comm->nccl;
+    t->st = st;
+    return t;
+}
+
 // ------------------------------------------------------------------ partitioned factor
 static void factor_partitioned(std::vector<PartRun>& runs, const std::vector<std::vector<int>>& own, Transport& T,
                                const DSys& sys) {
@@ -2859,10 +3114,8 @@ int acrgpu_solve_device(acrgpu_fact* f, int nrhs, const double* f_dev, double* u
             std::vector<SolveRun> runs(1);
             runs[0].F = f;
             runs[0].rank = f->rank;
-            NcclTransport T;
-            T.comm = (ncclComm_t)f->comm->nccl;
-            T.st = st;
-            solve_runs(runs, &f->owners, &T, nrhs, f_dev, u_dev);
+            auto T = make_transport(f->comm, st);
+            solve_runs(runs, &f->owners, T.get(), nrhs, f_dev, u_dev);
         } else {
             do_solve(f, nrhs, f_dev, u_dev);
         }
@@ -3079,6 +3332,23 @@ int acrgpu_comm_create(const unsigned char* id, int nranks, int rank, acrgpu_com
     })
 }
 
+int acrgpu_comm_create_host(acrgpu_exchange_fn fn, void* user, int nranks, int rank, acrgpu_comm** out,
+                            acrgpu_error* err) {
+    ABI_TRY({
+        *out = nullptr;
+        if (!fn) throw AcrError{ACRGPU_E_USAGE, "comm: null exchange callback"};
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw AcrError{ACRGPU_E_USAGE, "comm: bad rank / size"};
+        auto* cm = new acrgpu_comm;
+        cm->nranks = nranks;
+        cm->rank = rank;
+        cm->local = false;
+        cm->host_fn = fn;
+        cm->host_user = user;
+        *out = cm;
+        return 0;
+    })
+}
+
 int acrgpu_comm_create_local(int nranks, acrgpu_comm** out, acrgpu_error* err) {
     ABI_TRY({
         *out = nullptr;
@@ -3147,10 +3417,8 @@ static int factor_partitioned_impl(acrgpu_ctx* ctx, acrgpu_comm* comm, const DSy
                 LocalTransport T;
                 factor_partitioned(runs, own, T, *ds);
             } else {
-                NcclTransport T;
-                T.comm = (ncclComm_t)comm->nccl;
-                T.st = ctx->c.st;
-                factor_partitioned(runs, own, T, *ds);
+                auto T = make_transport(comm, ctx->c.st);
+                factor_partitioned(runs, own, *T, *ds);
             }
         } catch (...) {
             for (auto& p : parts) {

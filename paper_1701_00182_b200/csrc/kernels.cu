@@ -1130,100 +1130,86 @@ struct MatvecArgs {
     Arena arena;          // transient: [count x nrk T pointers | T blocks]
     FlopLedger* flops;
 };
-constexpr int MV_ROWS = 64;     // rows per phase-1 chunk / per slab
-constexpr int MV_TC = 64;       // rank columns per phase-1 pass
-constexpr int MV_RHS = 16;      // right-hand sides per pass
-constexpr int MV_LD = MV_ROWS + 1;
+constexpr int MV_RHS = 16;      // right-hand sides per pass (fixed register slots)
 
 __device__ __forceinline__ double** mv_tptr(const MatvecArgs& a) { return (double**)a.arena.base; }
 
-// T = V^T X: thread (t = tid & 63, column group tid >> 6) accumulates T[t][cg + 4 q] over the
-// chunk's rows in row order; V chunk (64 rows x 64 rank columns) and X chunk (64 rows x 16
-// columns) are staged through shared memory with coalesced loads.
-__global__ void __launch_bounds__(NT) k_mv_t(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
-    __shared__ double Vs[MV_TC * MV_LD];
-    __shared__ double Xs[MV_RHS * MV_LD];
-    __shared__ double* sh_T;
+// T = V^T X for one (item, Rk leaf) per WARP (eight units per CTA, no barriers): lanes walk
+// the leaf's rows (V coalesced from HBM; X from L2/L1 -- work units are item-major, so the
+// warps in flight share one item's X), two rank columns at a time with every right-hand
+// side in registers; the 32 lane partials are combined by a fixed shuffle tree.  Rank-0
+// leaves (most level-0 couplings) cost one metadata round trip.
+__global__ void __launch_bounds__(NT, 2) k_mv_t(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
+    const int lane = threadIdx.x & 31;
     const long total = (long)args.nrk * mb.count;
-    const int t = threadIdx.x & 63, cg = threadIdx.x >> 6;
+    const long stride = (long)gridDim.x * (NT / 32);
     double fl = 0;
-    for (long w = blockIdx.x; w < total; w += gridDim.x) {
-        const int b = (int)(w % mb.count), li = (int)(w / mb.count);
+    for (long w = (long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); w < total; w += stride) {
+        const int b = (int)(w / args.nrk), li = (int)(w % args.nrk);
         const MvLeaf L = args.rk[li];
         const HView& H = mb.h[b];
         const int rr = H.rank[L.k];
-        __syncthreads();  // previous item's staging and sh_T are no longer read
-        if (threadIdx.x == 0) {
-            double* T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)rr * args.nrhs) : nullptr;
+        double* T = nullptr;
+        if (lane == 0) {
+            T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)rr * args.nrhs) : nullptr;
             mv_tptr(args)[(size_t)b * args.nrk + li] = T;
-            sh_T = T;
         }
-        __syncthreads();
-        double* T = sh_T;
+        T = (double*)__shfl_sync(0xffffffffu, (unsigned long long)T, 0);
         if (T == nullptr) continue;
         const double* V = H.V[L.k];
         const double* X = mb.x[b] + L.in_off;
-        const int n = L.n;
+        const int n = L.n, ld = args.dim;
         for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
             const int nc = min(MV_RHS, args.nrhs - c0);
-            for (int t0 = 0; t0 < rr; t0 += MV_TC) {
-                const int nt = min(MV_TC, rr - t0);
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                for (int j0 = 0; j0 < n; j0 += MV_ROWS) {
-                    const int jc = min(MV_ROWS, n - j0);
-                    double v[16], x[4];
+            const double* Xc = X + (size_t)c0 * ld;
+            for (int t0 = 0; t0 < rr; t0 += 2) {
+                const bool two = t0 + 1 < rr;
+                const double* v0p = V + (size_t)t0 * n;
+                const double* v1p = V + (size_t)(two ? t0 + 1 : t0) * n;
+                double a0[MV_RHS], a1[MV_RHS];
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) {  // V chunk: row fastest (coalesced)
-                        const int e = threadIdx.x + u * NT, j = e & 63, tt = e >> 6;
-                        v[u] = (j < jc && tt < nt) ? V[(j0 + j) + (size_t)(t0 + tt) * n] : 0.0;
-                    }
+                for (int c = 0; c < MV_RHS; ++c) a0[c] = a1[c] = 0.0;
+                for (int j = lane; j < n; j += 32) {
+                    const double v0 = v0p[j], v1 = two ? v1p[j] : 0.0;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = threadIdx.x + u * NT, j = e & 63, c = e >> 6;
-                        x[u] = (j < jc && c < nc) ? X[(j0 + j) + (size_t)(c0 + c) * args.dim] : 0.0;
-                    }
-                    __syncthreads();
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        const int e = threadIdx.x + u * NT;
-                        Vs[(e >> 6) * MV_LD + (e & 63)] = v[u];
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = threadIdx.x + u * NT;
-                        Xs[(e >> 6) * MV_LD + (e & 63)] = x[u];
-                    }
-                    __syncthreads();
-                    if (t < nt) {
-#pragma unroll 4
-                        for (int j = 0; j < jc; ++j) {
-                            const double vj = Vs[t * MV_LD + j];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) acc[q] = fma(vj, Xs[(cg + 4 * q) * MV_LD + j], acc[q]);
-                        }
+                    for (int c = 0; c < MV_RHS; ++c) {
+                        const double x = c < nc ? Xc[j + (size_t)c * ld] : 0.0;
+                        a0[c] = fma(v0, x, a0[c]);
+                        a1[c] = fma(v1, x, a1[c]);
                     }
                 }
-                if (t < nt)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int c = cg + 4 * q;
-                        if (c < nc) T[(t0 + t) + (size_t)(c0 + c) * rr] = acc[q];
-                    }
+                const double p0 = reduce_scatter16(a0, lane);
+                const double p1 = reduce_scatter16(a1, lane);
+                if (lane < nc) {
+                    T[t0 + (size_t)(c0 + lane) * rr] = p0;
+                    if (two) T[t0 + 1 + (size_t)(c0 + lane) * rr] = p1;
+                }
             }
         }
-        if (threadIdx.x == 0) fl += 2.0 * rr * n * args.nrhs;
+        if (lane == 0) fl += 2.0 * rr * n * args.nrhs;
     }
-    if (threadIdx.x == 0 && fl > 0) add_flops(args.flops, F_APPLY, fl);
+    if (lane == 0 && fl > 0) add_flops(args.flops, F_APPLY, fl);
 }
 
-// One output slab (<= 64 rows) of one item.  Thread (row i = tid & 63, group g = tid >> 6)
-// accumulates, for every right-hand side, the contracted indices j = g (mod 4) of every
-// leaf in leaf order (dense: D[i, j] x[j]; Rk: U[i, t] T[t]); the four group partials are
-// added in group order at the end.  Operand rows are read coalesced straight from HBM,
-// the x / T chunks are broadcast from shared memory.
+// One output slab (<= 64 rows) of one item.  The slab's leaf records (operand base, contracted
+// vector, lengths) are resolved once into shared memory, then the leaves are taken in groups
+// whose contracted vectors (x chunk or T block, all right-hand sides) are staged together:
+// one barrier pair per group instead of a chain of dependent metadata loads per leaf.
+// Thread (row i = tid & 63, group g = tid >> 6) accumulates, per right-hand side, the
+// contracted indices j = g (mod 4) of every leaf in leaf order; the four partials are added
+// in group order at the end.
+constexpr int MV_META = 96;       // leaf records resolved per pass
+constexpr int MV_STAGE = 256;     // staged contracted entries per group (x 16 right-hand sides)
+struct MvMeta {
+    const double* A;    // operand column 0 at row 0 of the leaf (ld lda)
+    const double* xin;  // contracted vector, column c at xin + c * ldx
+    int len, lda, ldx, o0, o1, out_off;
+};
 __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
-    __shared__ double Xs[MV_RHS * MV_LD];
-    __shared__ double red[4 * MV_RHS * MV_ROWS];
+    static_assert(4 * MV_RHS * 64 == MV_RHS * MV_STAGE, "red aliases Xs");
+    __shared__ double Xs[MV_RHS * MV_STAGE];  // staged vectors; the final reduction reuses it
+    __shared__ MvMeta meta[MV_META];
+    double* red = Xs;
     const SlabTask task = args.tasks[blockIdx.x];
     const int b = blockIdx.y;
     const HView& H = mb.h[b];
@@ -1241,71 +1227,93 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
         double acc[MV_RHS];
 #pragma unroll
         for (int c = 0; c < MV_RHS; ++c) acc[c] = 0.0;
-        for (int li = task.lbeg; li < task.lend; ++li) {
-            const ApplyLeaf L = args.leaves[li];
-            const int o0 = max(task.r0, L.out_off), o1 = min(task.r1, L.out_off + L.m);
-            if (o0 >= o1) continue;
-            const bool mine = row >= o0 && row < o1;
-            const int lr = row - L.out_off;
-            const double* A;   // operand column j at A + j * lda (this thread's row)
-            const double* Xin; // contracted vector chunk source, column c at Xin + c * ldx
-            int len, lda, ldx;
-            if (L.kind == K_DENSE) {
-                A = H.dense + L.doff + lr;
-                lda = L.m;
-                len = L.n;
-                Xin = X + L.in_off + (size_t)c0 * ld;
-                ldx = ld;
-            } else {
-                const int rr = H.rank[L.id];
-                const double* T = rr > 0 ? Tp[L.id] : nullptr;
-                if (T == nullptr) continue;
-                A = H.U[L.id] + lr;
-                lda = L.m;
-                len = rr;
-                Xin = T + (size_t)c0 * rr;
-                ldx = rr;
-            }
-            for (int j0 = 0; j0 < len; j0 += MV_ROWS) {
-                const int jc = min(MV_ROWS, len - j0);
-                __syncthreads();
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = threadIdx.x + u * NT, j = e & 63, c = e >> 6;
-                    Xs[c * MV_LD + j] = (j < jc && c < nc) ? Xin[(j0 + j) + (size_t)c * ldx] : 0.0;
-                }
-                __syncthreads();
-                if (mine) {
-                    int j = g;
-                    for (; j + 12 < jc; j += 16) {  // four operand loads in flight per thread
-                        double d[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) d[q] = A[(size_t)(j0 + j + 4 * q) * lda];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-#pragma unroll
-                            for (int c = 0; c < MV_RHS; ++c)
-                                if (c < nc) acc[c] = fma(d[q], Xs[c * MV_LD + j + 4 * q], acc[c]);
-                    }
-                    for (; j < jc; j += 4) {
-                        const double d = A[(size_t)(j0 + j) * lda];
-#pragma unroll
-                        for (int c = 0; c < MV_RHS; ++c)
-                            if (c < nc) acc[c] = fma(d, Xs[c * MV_LD + j], acc[c]);
+        for (int l0 = task.lbeg; l0 < task.lend; l0 += MV_META) {
+            const int nl = min(MV_META, task.lend - l0);
+            __syncthreads();
+            if (threadIdx.x < nl) {
+                const ApplyLeaf L = args.leaves[l0 + threadIdx.x];
+                MvMeta m{nullptr, nullptr, 0, L.m, 0, max(task.r0, L.out_off), min(task.r1, L.out_off + L.m), L.out_off};
+                if (m.o0 < m.o1) {
+                    if (L.kind == K_DENSE) {
+                        m.A = H.dense + L.doff;
+                        m.len = L.n;
+                        m.xin = X + L.in_off + (size_t)c0 * ld;
+                        m.ldx = ld;
+                    } else {
+                        const int rr = H.rank[L.id];
+                        const double* T = rr > 0 ? Tp[L.id] : nullptr;
+                        if (T) {
+                            m.A = H.U[L.id];
+                            m.len = rr;
+                            m.xin = T + (size_t)c0 * rr;
+                            m.ldx = rr;
+                        }
                     }
                 }
+                meta[threadIdx.x] = m;
             }
-            if (threadIdx.x == 0 && c0 == 0) fl += 2.0 * (o1 - o0) * len * args.nrhs;
+            __syncthreads();
+            int q0 = 0;
+            while (q0 < nl) {
+                // group [q0, q1): staged lengths fit MV_STAGE (a longer leaf is its own group, chunked)
+                int q1 = q0, tot = 0;
+                while (q1 < nl && (q1 == q0 || tot + meta[q1].len <= MV_STAGE)) tot += meta[q1++].len;
+                for (int j0 = 0; j0 < max(tot, 1); j0 += MV_STAGE) {
+                    const int jn = min(MV_STAGE, tot - j0);
+                    __syncthreads();
+                    // stage entries [j0, j0 + jn) of the group's concatenated contracted vectors
+                    for (int e = threadIdx.x; e < MV_STAGE * MV_RHS; e += NT) {
+                        const int p = e % MV_STAGE, c = e / MV_STAGE;
+                        double v = 0.0;
+                        if (p < jn && c < nc) {
+                            int q = q0, pos = j0 + p;
+                            while (pos >= meta[q].len) pos -= meta[q++].len;
+                            v = meta[q].xin[pos + (size_t)c * meta[q].ldx];
+                        }
+                        Xs[c * MV_STAGE + p] = v;
+                    }
+                    __syncthreads();
+                    int off = 0;  // offset of leaf q's entries in the concatenation
+                    for (int q = q0; q < q1; off += meta[q].len, ++q) {
+                        const MvMeta& m = meta[q];
+                        const int lo = max(off, j0), hi = min(off + m.len, j0 + jn);
+                        if (lo >= hi || row < m.o0 || row >= m.o1) continue;
+                        const double* A = m.A + (row - m.out_off);
+                        // local indices j in [lo - off, hi - off), j = g (mod 4)
+                        int j = lo - off;
+                        j += (g - j % 4 + 4) % 4;
+                        const int je = hi - off;
+                        const double* xs = Xs + (off - j0);
+                        for (; j + 12 < je; j += 16) {
+                            double d[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) d[u] = A[(size_t)(j + 4 * u) * m.lda];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                for (int c = 0; c < MV_RHS; ++c) acc[c] = fma(d[u], xs[c * MV_STAGE + j + 4 * u], acc[c]);
+                        }
+                        for (; j < je; j += 4) {
+                            const double d = A[(size_t)j * m.lda];
+#pragma unroll
+                            for (int c = 0; c < MV_RHS; ++c) acc[c] = fma(d, xs[c * MV_STAGE + j], acc[c]);
+                        }
+                    }
+                }
+                if (threadIdx.x == 0 && c0 == 0)
+                    for (int q = q0; q < q1; ++q) fl += 2.0 * (meta[q].o1 - meta[q].o0) * meta[q].len * args.nrhs;
+                q0 = q1;
+            }
         }
         __syncthreads();
 #pragma unroll
-        for (int c = 0; c < MV_RHS; ++c) red[(g * MV_RHS + c) * MV_ROWS + i] = acc[c];
+        for (int c = 0; c < MV_RHS; ++c) red[(g * MV_RHS + c) * 64 + i] = acc[c];
         __syncthreads();
-        for (int e = threadIdx.x; e < MV_ROWS * nc; e += NT) {
+        for (int e = threadIdx.x; e < 64 * nc; e += NT) {
             const int r = e & 63, c = e >> 6;
             if (r >= nr) continue;
-            const double s = ((red[(0 * MV_RHS + c) * MV_ROWS + r] + red[(1 * MV_RHS + c) * MV_ROWS + r]) +
-                              red[(2 * MV_RHS + c) * MV_ROWS + r]) + red[(3 * MV_RHS + c) * MV_ROWS + r];
+            const double s = ((red[(0 * MV_RHS + c) * 64 + r] + red[(1 * MV_RHS + c) * 64 + r]) +
+                              red[(2 * MV_RHS + c) * 64 + r]) + red[(3 * MV_RHS + c) * 64 + r];
             const size_t o = (task.r0 + r) + (size_t)(c0 + c) * ld;
             Y[o] = base ? base[o] - s : s;
         }
@@ -1970,7 +1978,7 @@ void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const App
     }
     if (nrk > 0) {
         ProfScope _ps(st, "k_mv_t", (long)nrk * mb.count);
-        k_mv_t<<<item_grid((long)nrk * mb.count, 5), NT, 0, st>>>(a, mb);
+        k_mv_t<<<item_grid((long)nrk * mb.count, 4), NT, 0, st>>>(a, mb);
     }
     a.flops = ledger(flops, "k_mv_slab");
     ProfScope _ps(st, "k_mv_slab", (long)ntasks * mb.count);

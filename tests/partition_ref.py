@@ -1,4 +1,5 @@
-"""Plane-partitioned cyclic reduction: the multi-worker orchestration of the
+"""TEST SCAFFOLDING (not the product path): a dense numpy restatement of the plane-partitioned
+cyclic reduction, the multi-worker orchestration of the
 reference's execute_parallel_factor (proj/core/src/parallel.cpp:96-297), with
 the block arithmetic abstracted behind a kernel and the mailbox replaced by a
 point-to-point transport (torch.distributed: gloo on CPU in the tests, NCCL for GPU ranks).
@@ -18,7 +19,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .plan import eliminated_positions, plan_schedule, retained_positions
+from paper_1701_00182_b200.plan import eliminated_positions, plan_schedule, retained_positions
 
 
 class DenseKernel:

@@ -59,3 +59,25 @@ def test_structure_errors():
 def test_dense_mode_rejected():
     with pytest.raises(acr.UsageError):
         acr._cfg(acr.AcrConfig(mode=acr.ArithmeticMode.Dense))
+
+
+SHIM = os.path.join(os.path.dirname(os.path.abspath(__file__)), "shim", "acr_shim_check.cpp")
+
+
+def build_shim(out):
+    """INTEGRATION.md §2's reference-side C++ shim, compiled against include/acrgpu.h and
+    linked with libacrgpu.so (stand-ins for the Eigen-based reference types)."""
+    import subprocess
+    from paper_1701_00182_b200 import build as B
+    lib = B.build()
+    libdir = os.path.dirname(lib)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-Wno-misleading-indentation", "-Werror",
+                    "-I", os.path.join(root, "include"), SHIM, "-L", libdir, "-lacrgpu",
+                    f"-Wl,-rpath,{libdir}", "-o", out], check=True)
+    return out
+
+
+def test_cpp_shim_compiles_and_links(tmp_path):
+    exe = build_shim(str(tmp_path / "acr_shim_check"))
+    assert os.path.exists(exe)

