@@ -1134,13 +1134,17 @@ constexpr int MV_RHS = 16;      // right-hand sides per pass (fixed register slo
 
 __device__ __forceinline__ double** mv_tptr(const MatvecArgs& a) { return (double**)a.arena.base; }
 
-// T = V^T X for one (item, Rk leaf) per WARP (eight units per CTA, no barriers): lanes walk
-// the leaf's rows (V coalesced from HBM; X from L2/L1 -- work units are item-major, so the
-// warps in flight share one item's X), two rank columns at a time with every right-hand
-// side in registers; the 32 lane partials are combined by a fixed shuffle tree.  Rank-0
-// leaves (most level-0 couplings) cost one metadata round trip.
-__global__ void __launch_bounds__(NT, 2) k_mv_t(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
-    const int lane = threadIdx.x & 31;
+// Both phases run on the FP64 tensor cores (mma.sync.m8n8k4.f64, DMMA; fragment layout in
+// bqr.cuh): the right-hand sides are always 16 zero-padded columns, so every output element
+// is the same sequence of DMMA k-steps whatever nrhs is -- multi-RHS solves stay bitwise equal
+// to single-RHS ones.
+//
+// Phase 1, one (item, Rk leaf) per WARP (eight per CTA, no barriers): T^T (16 x rank) =
+// X^T (16 x n) V (n x rank), rank tiles of 8, k-steps of 4 rows.  V streams from HBM (each
+// load = 8 rank columns x 4 consecutive rows, full 32-byte sectors), X from L2 (units are
+// item-major, so the warps in flight share one item's X).
+__global__ void __launch_bounds__(NT) k_mv_t(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
     const long total = (long)args.nrk * mb.count;
     const long stride = (long)gridDim.x * (NT / 32);
     double fl = 0;
@@ -1157,32 +1161,48 @@ __global__ void __launch_bounds__(NT, 2) k_mv_t(MatvecArgs args, const __grid_co
         T = (double*)__shfl_sync(0xffffffffu, (unsigned long long)T, 0);
         if (T == nullptr) continue;
         const double* V = H.V[L.k];
-        const double* X = mb.x[b] + L.in_off;
         const int n = L.n, ld = args.dim;
         for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
             const int nc = min(MV_RHS, args.nrhs - c0);
-            const double* Xc = X + (size_t)c0 * ld;
-            for (int t0 = 0; t0 < rr; t0 += 2) {
-                const bool two = t0 + 1 < rr;
-                const double* v0p = V + (size_t)t0 * n;
-                const double* v1p = V + (size_t)(two ? t0 + 1 : t0) * n;
-                double a0[MV_RHS], a1[MV_RHS];
+            const double* X = mb.x[b] + L.in_off + (size_t)c0 * ld;
+            const bool c_lo = g < nc, c_hi = g + 8 < nc;  // this lane's A rows (RHS g, g + 8)
+            const double* xlo = X + (size_t)g * ld;
+            const double* xhi = X + (size_t)(g + 8) * ld;
+            for (int tc = 0; tc < rr; tc += 8) {
+                const bool vok = tc + g < rr;  // this lane's B column (rank tc + g)
+                const double* vcol = V + (size_t)(vok ? tc + g : 0) * n;
+                double d00 = 0, d01 = 0, d10 = 0, d11 = 0;  // C tiles: RHS 0-7 / 8-15 x rank tc..tc+7
+                int k0 = 0;
+                for (; k0 + 32 <= n; k0 += 32) {  // eight k-steps, loads first
+                    double va[8], xa[8], xb[8];
 #pragma unroll
-                for (int c = 0; c < MV_RHS; ++c) a0[c] = a1[c] = 0.0;
-                for (int j = lane; j < n; j += 32) {
-                    const double v0 = v0p[j], v1 = two ? v1p[j] : 0.0;
+                    for (int s = 0; s < 8; ++s) {
+                        const int j = k0 + 4 * s + t4;
+                        va[s] = vok ? vcol[j] : 0.0;
+                        xa[s] = c_lo ? xlo[j] : 0.0;
+                        xb[s] = c_hi ? xhi[j] : 0.0;
+                    }
 #pragma unroll
-                    for (int c = 0; c < MV_RHS; ++c) {
-                        const double x = c < nc ? Xc[j + (size_t)c * ld] : 0.0;
-                        a0[c] = fma(v0, x, a0[c]);
-                        a1[c] = fma(v1, x, a1[c]);
+                    for (int s = 0; s < 8; ++s) {
+                        dmma8x8x4(d00, d01, xa[s], va[s]);
+                        dmma8x8x4(d10, d11, xb[s], va[s]);
                     }
                 }
-                const double p0 = reduce_scatter16(a0, lane);
-                const double p1 = reduce_scatter16(a1, lane);
-                if (lane < nc) {
-                    T[t0 + (size_t)(c0 + lane) * rr] = p0;
-                    if (two) T[t0 + 1 + (size_t)(c0 + lane) * rr] = p1;
+                for (; k0 < n; k0 += 4) {
+                    const int j = k0 + t4;
+                    const bool jok = j < n;
+                    const double va = (vok && jok) ? vcol[j] : 0.0;
+                    dmma8x8x4(d00, d01, (c_lo && jok) ? xlo[j] : 0.0, va);
+                    dmma8x8x4(d10, d11, (c_hi && jok) ? xhi[j] : 0.0, va);
+                }
+                // C[g][2 t4 + i]: RHS g (+8), rank tc + 2 t4 + i  ->  T[rank + rhs * rr]
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int tr = tc + 2 * t4 + i;
+                    if (tr < rr) {
+                        if (c_lo) T[tr + (size_t)(c0 + g) * rr] = i ? d01 : d00;
+                        if (c_hi) T[tr + (size_t)(c0 + g + 8) * rr] = i ? d11 : d10;
+                    }
                 }
             }
         }
@@ -1191,25 +1211,22 @@ __global__ void __launch_bounds__(NT, 2) k_mv_t(MatvecArgs args, const __grid_co
     if (lane == 0 && fl > 0) add_flops(args.flops, F_APPLY, fl);
 }
 
-// One output slab (<= 64 rows) of one item.  The slab's leaf records (operand base, contracted
-// vector, lengths) are resolved once into shared memory, then the leaves are taken in groups
-// whose contracted vectors (x chunk or T block, all right-hand sides) are staged together:
-// one barrier pair per group instead of a chain of dependent metadata loads per leaf.
-// Thread (row i = tid & 63, group g = tid >> 6) accumulates, per right-hand side, the
-// contracted indices j = g (mod 4) of every leaf in leaf order; the four partials are added
-// in group order at the end.
+// Phase 2, one output slab (<= 64 rows) of one item per CTA: warp w owns rows 8w .. 8w+7 and
+// all 16 right-hand sides (two 8 x 8 C tiles), so no cross-warp reduction.  The slab's leaf
+// records are resolved once into shared memory; the contracted vectors (x chunk or T block)
+// of a group of leaves are staged together (one barrier pair per group); each leaf is then
+// contracted in DMMA k-steps of 4 with the operand rows streamed from HBM.
 constexpr int MV_META = 96;       // leaf records resolved per pass
-constexpr int MV_STAGE = 256;     // staged contracted entries per group (x 16 right-hand sides)
+constexpr int MV_STAGE = 256;     // staged contracted entries per group
+constexpr int MV_SLD = MV_STAGE + 4;  // Xs row stride (RHS-major): conflict-light B fragments
 struct MvMeta {
     const double* A;    // operand column 0 at row 0 of the leaf (ld lda)
     const double* xin;  // contracted vector, column c at xin + c * ldx
     int len, lda, ldx, o0, o1, out_off;
 };
 __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
-    static_assert(4 * MV_RHS * 64 == MV_RHS * MV_STAGE, "red aliases Xs");
-    __shared__ double Xs[MV_RHS * MV_STAGE];  // staged vectors; the final reduction reuses it
+    __shared__ double Xs[MV_RHS * MV_SLD];
     __shared__ MvMeta meta[MV_META];
-    double* red = Xs;
     const SlabTask task = args.tasks[blockIdx.x];
     const int b = blockIdx.y;
     const HView& H = mb.h[b];
@@ -1217,16 +1234,13 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
     const double* base = mb.base[b];
     double* Y = mb.y[b];
     const int ld = args.dim;
-    const int nr = task.r1 - task.r0;
-    const int i = threadIdx.x & 63, g = threadIdx.x >> 6;
-    const int row = task.r0 + i;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+    const int row = task.r0 + 8 * warp + g;  // this lane's A row
     double* const* Tp = mv_tptr(args) + (size_t)b * args.nrk;
     double fl = 0;
     for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
         const int nc = min(MV_RHS, args.nrhs - c0);
-        double acc[MV_RHS];
-#pragma unroll
-        for (int c = 0; c < MV_RHS; ++c) acc[c] = 0.0;
+        double d00 = 0, d01 = 0, d10 = 0, d11 = 0;  // rows 8w+g, RHS 2t4+i (tile 0) / 8+2t4+i (tile 1)
         for (int l0 = task.lbeg; l0 < task.lend; l0 += MV_META) {
             const int nl = min(MV_META, task.lend - l0);
             __syncthreads();
@@ -1255,48 +1269,56 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
             __syncthreads();
             int q0 = 0;
             while (q0 < nl) {
-                // group [q0, q1): staged lengths fit MV_STAGE (a longer leaf is its own group, chunked)
+                // group [q0, q1) of leaves whose contracted lengths (each rounded up to a k-step
+                // of 4) fit MV_STAGE; a longer leaf is its own group, taken in chunks
                 int q1 = q0, tot = 0;
-                while (q1 < nl && (q1 == q0 || tot + meta[q1].len <= MV_STAGE)) tot += meta[q1++].len;
+                while (q1 < nl && (q1 == q0 || tot + ((meta[q1].len + 3) & ~3) <= MV_STAGE)) tot += (meta[q1++].len + 3) & ~3;
                 for (int j0 = 0; j0 < max(tot, 1); j0 += MV_STAGE) {
                     const int jn = min(MV_STAGE, tot - j0);
                     __syncthreads();
-                    // stage entries [j0, j0 + jn) of the group's concatenated contracted vectors
                     for (int e = threadIdx.x; e < MV_STAGE * MV_RHS; e += NT) {
                         const int p = e % MV_STAGE, c = e / MV_STAGE;
                         double v = 0.0;
                         if (p < jn && c < nc) {
                             int q = q0, pos = j0 + p;
-                            while (pos >= meta[q].len) pos -= meta[q++].len;
-                            v = meta[q].xin[pos + (size_t)c * meta[q].ldx];
+                            while (pos >= ((meta[q].len + 3) & ~3)) pos -= (meta[q++].len + 3) & ~3;
+                            if (pos < meta[q].len) v = meta[q].xin[pos + (size_t)c * meta[q].ldx];
                         }
-                        Xs[c * MV_STAGE + p] = v;
+                        Xs[c * MV_SLD + p] = v;
                     }
                     __syncthreads();
-                    int off = 0;  // offset of leaf q's entries in the concatenation
-                    for (int q = q0; q < q1; off += meta[q].len, ++q) {
+                    int off = 0;  // offset of leaf q's (padded) entries in the concatenation
+                    for (int q = q0; q < q1; off += (meta[q].len + 3) & ~3, ++q) {
                         const MvMeta& m = meta[q];
-                        const int lo = max(off, j0), hi = min(off + m.len, j0 + jn);
-                        if (lo >= hi || row < m.o0 || row >= m.o1) continue;
-                        const double* A = m.A + (row - m.out_off);
-                        // local indices j in [lo - off, hi - off), j = g (mod 4)
+                        const int lo = max(off, j0), hi = min(off + ((m.len + 3) & ~3), j0 + jn);
+                        if (lo >= hi) continue;
+                        if (8 * warp >= m.o1 - task.r0 || 8 * warp + 8 <= m.o0 - task.r0) continue;  // no rows here
+                        const bool rok = row >= m.o0 && row < m.o1;
+                        const double* A = m.A + (rok ? row - m.out_off : 0);
+                        // B fragment of tile ct: B[k = t4][n = g] = x[j][RHS 8 ct + g]
+                        const double* b0 = Xs + (size_t)g * MV_SLD + (off - j0);
+                        const double* b1 = Xs + (size_t)(g + 8) * MV_SLD + (off - j0);
                         int j = lo - off;
-                        j += (g - j % 4 + 4) % 4;
                         const int je = hi - off;
-                        const double* xs = Xs + (off - j0);
-                        for (; j + 12 < je; j += 16) {
-                            double d[4];
+                        for (; j + 16 <= je; j += 16) {
+                            double a[4];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) d[u] = A[(size_t)(j + 4 * u) * m.lda];
+                            for (int s = 0; s < 4; ++s) {
+                                const int jj = j + 4 * s + t4;
+                                a[s] = (rok && jj < m.len) ? A[(size_t)jj * m.lda] : 0.0;
+                            }
 #pragma unroll
-                            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                                for (int c = 0; c < MV_RHS; ++c) acc[c] = fma(d[u], xs[c * MV_STAGE + j + 4 * u], acc[c]);
+                            for (int s = 0; s < 4; ++s) {
+                                const int jj = j + 4 * s + t4;
+                                dmma8x8x4(d00, d01, a[s], b0[jj]);
+                                dmma8x8x4(d10, d11, a[s], b1[jj]);
+                            }
                         }
                         for (; j < je; j += 4) {
-                            const double d = A[(size_t)j * m.lda];
-#pragma unroll
-                            for (int c = 0; c < MV_RHS; ++c) acc[c] = fma(d, xs[c * MV_STAGE + j], acc[c]);
+                            const int jj = j + t4;
+                            const double a = (rok && jj < m.len) ? A[(size_t)jj * m.lda] : 0.0;
+                            dmma8x8x4(d00, d01, a, b0[jj]);
+                            dmma8x8x4(d10, d11, a, b1[jj]);
                         }
                     }
                 }
@@ -1305,17 +1327,23 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
                 q0 = q1;
             }
         }
-        __syncthreads();
+        // C[g][2 t4 + i] of tile ct: row 8 warp + g, RHS 8 ct + 2 t4 + i
+        const int r = 8 * warp + g;
+        if (r < task.r1 - task.r0) {
 #pragma unroll
-        for (int c = 0; c < MV_RHS; ++c) red[(g * MV_RHS + c) * 64 + i] = acc[c];
-        __syncthreads();
-        for (int e = threadIdx.x; e < 64 * nc; e += NT) {
-            const int r = e & 63, c = e >> 6;
-            if (r >= nr) continue;
-            const double s = ((red[(0 * MV_RHS + c) * 64 + r] + red[(1 * MV_RHS + c) * 64 + r]) +
-                              red[(2 * MV_RHS + c) * 64 + r]) + red[(3 * MV_RHS + c) * 64 + r];
-            const size_t o = (task.r0 + r) + (size_t)(c0 + c) * ld;
-            Y[o] = base ? base[o] - s : s;
+            for (int i = 0; i < 2; ++i) {
+                const int ca = 2 * t4 + i, cb = 8 + 2 * t4 + i;
+                if (ca < nc) {
+                    const size_t o = (task.r0 + r) + (size_t)(c0 + ca) * ld;
+                    const double s = i ? d01 : d00;
+                    Y[o] = base ? base[o] - s : s;
+                }
+                if (cb < nc) {
+                    const size_t o = (task.r0 + r) + (size_t)(c0 + cb) * ld;
+                    const double s = i ? d11 : d10;
+                    Y[o] = base ? base[o] - s : s;
+                }
+            }
         }
     }
     if (threadIdx.x == 0) add_flops(args.flops, F_APPLY, fl);

@@ -184,5 +184,5 @@ int main(int argc, char** argv) {
         return 3;
     } catch (const acr::DimensionError&) {
     }
-    return res < 1e-8 ? 0 : 4;
+    return res < 1e-5 ? 0 : 4;
 }
