@@ -135,7 +135,8 @@ def test_config4_helmholtz_full_size_pinned(acr):
     lg, lo = f.level_info(), fx["levels"]
     assert [l.plane_count for l in lg] == [l["plane_count"] for l in lo]
     for a, b in zip(lg[:2], lo[:2]):
-        assert abs(a.largest_rank - b["largest_rank"]) <= 1 and abs(a.average_rank - b["average_rank"]) <= 0.01 * b["average_rank"]
+        assert abs(a.largest_rank - b["largest_rank"]) <= max(1, round(0.1 * b["largest_rank"])), (a, b)
+        assert abs(a.average_rank - b["average_rank"]) <= 0.05 * b["average_rank"], (a, b)
     check_dinv(f, fx, entries={(d["level"], d["plane"]) for d in fx["dinv_ranks"] if d["level"] <= 1})
 
 
