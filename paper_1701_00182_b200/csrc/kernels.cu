@@ -158,6 +158,7 @@ struct TruncArgs {
     Arena out_arena;        // persistent (flush) or transient (products)
     Arena work;             // transient workspace
     FlopLedger* flops;
+    int dense_min_k;        // blocks <= DMAX take the dense route only when K >= this (else the QR route)
 };
 
 // C (ru x rv, ld ldc; shared memory) += alpha * A (ru x k) * B^T (rv x k), A/B column-major
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, Ba
     double fsvd = 0, fqr = 0, fgemm = 0;
     __shared__ double* sh_out;
 
-    if (m <= DMAX && n <= DMAX) {
+    if (m <= DMAX && n <= DMAX && (!QR || K >= args.dense_min_k)) {
         // ---------------- dense route: M = sum alpha U V^T in shared memory, rank-revealing SVD
         CtaSvdWork w = cta_smem_work(smem, DMAX, RPCAP);
         double* M = w.A;
@@ -463,44 +464,71 @@ __global__ void __launch_bounds__(NT, 1) k_dd_product(DDArgs args, BatchViews bv
     const int m = task.m, k = task.k, n = task.n;
     const double* Ad = bv.a[b].dense + task.da;
     const double* Bd = bv.b[b].dense + task.db;
-    {  // zero operand (off-diagonal leaves of the diagonal level-0 couplings): rank-0 product
-        int nz = 0;
-        for (int e = threadIdx.x; e < m * k; e += NT) nz |= Ad[e] != 0.0;
-        int nzb = 0;
-        for (int e = threadIdx.x; e < k * n; e += NT) nzb |= Bd[e] != 0.0;
-        nz = __syncthreads_or(nz);
-        nzb = __syncthreads_or(nzb);
-        if (!nz || !nzb) {
-            if (threadIdx.x == 0) {
-                Slot& s = args.slots[(size_t)task.prod * args.B + b];
-                s.rank = 0;
-                s.U = nullptr;
-                s.V = nullptr;
-                s.ldu = m;
-                s.ldv = n;
-                double fsvd = 0, fqr = 0, fgemm = fl_gemm(m, n, k);
-                fl_svd(m, n, fsvd, fqr, fgemm);
-                add_flops(args.flops, F_SVD, fsvd);
-                add_flops(args.flops, F_GEQRF, fqr);
-                add_flops(args.flops, F_GEMM, fgemm);
-            }
-            return;
-        }
-    }
     CtaSvdWork w = cta_smem_work(smem, DENSE_MAX, DENSE_MAX);
     double* M = w.A;
     w.lda = m;
-    // operands staged in the (not yet used) W / J areas
+    // operands staged in the (not yet used) W / J areas; a zero operand (off-diagonal leaves
+    // of the diagonal level-0 couplings) is detected while staging and gives a rank-0 product
     double* As = w.W;
     double* Bs = w.J;
-    for (int e = threadIdx.x; e < m * k; e += NT) As[e] = Ad[e];
-    for (int e = threadIdx.x; e < k * n; e += NT) Bs[e] = Bd[e];
-    __syncthreads();
-    for (int e = threadIdx.x; e < m * n; e += NT) {
-        const int i = e % m, j = e / m;
-        double acc = 0;
-        for (int p = 0; p < k; ++p) acc = fma(As[i + (size_t)p * m], Bs[p + (size_t)j * k], acc);
-        M[e] = acc;
+    auto zero_product = [&]() {
+        if (threadIdx.x == 0) {
+            Slot& s = args.slots[(size_t)task.prod * args.B + b];
+            s.rank = 0;
+            s.U = nullptr;
+            s.V = nullptr;
+            s.ldu = m;
+            s.ldv = n;
+            double fsvd = 0, fqr = 0, fgemm = fl_gemm(m, n, k);
+            fl_svd(m, n, fsvd, fqr, fgemm);
+            add_flops(args.flops, F_SVD, fsvd);
+            add_flops(args.flops, F_GEQRF, fqr);
+            add_flops(args.flops, F_GEMM, fgemm);
+        }
+    };
+    {
+        int nz = 0;
+        for (int e = threadIdx.x; e < m * k; e += NT) {
+            const double v = Ad[e];
+            nz |= v != 0.0;
+            As[e] = v;
+        }
+        if (!__syncthreads_or(nz)) {
+            zero_product();
+            return;
+        }
+        nz = 0;
+        for (int e = threadIdx.x; e < k * n; e += NT) {
+            const double v = Bd[e];
+            nz |= v != 0.0;
+            Bs[e] = v;
+        }
+        if (!__syncthreads_or(nz)) {
+            zero_product();
+            return;
+        }
+    }
+    // M = A B on the FP64 tensor cores: 8 x 8 output tiles over the warps, k-steps of 4
+    // (mma.sync.m8n8k4.f64; fragment layout in bqr.cuh), operands from shared memory
+    {
+        const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+        const int tm = (m + 7) >> 3, tn = (n + 7) >> 3;
+        for (int tile = threadIdx.x >> 5; tile < tm * tn; tile += NT / 32) {
+            const int ti = tile % tm, tj = tile / tm;
+            const int ra = 8 * ti + g, cb = 8 * tj + g;
+            double d0 = 0.0, d1 = 0.0;
+            for (int k0 = 0; k0 < k; k0 += 4) {
+                const int kk = k0 + t;
+                const double a = (ra < m && kk < k) ? As[ra + (size_t)kk * m] : 0.0;
+                const double bb = (cb < n && kk < k) ? Bs[kk + (size_t)cb * k] : 0.0;
+                dmma8x8x4(d0, d1, a, bb);
+            }
+            const int c0 = 8 * tj + 2 * t;
+            if (ra < m) {
+                if (c0 < n) M[ra + (size_t)c0 * m] = d0;
+                if (c0 + 1 < n) M[ra + (size_t)(c0 + 1) * m] = d1;
+            }
+        }
     }
     __syncthreads();
     int rp;
@@ -580,29 +608,17 @@ struct ApplyTArgs {
     FlopLedger* flops;
 };
 
-// Register tile of the apply kernels: a 64 x 32 output block, thread (tr, tc) owns rows
-// tr + 32 i (i < 2) and columns tc + 8 j (j < 4); the k-dimension is staged in shared
-// memory in chunks of 32 (A: 64 x 32, ld 65; B: 32 x 32, ld 33).
-constexpr int AP_LDA = 65, AP_LDB = 33;
-__device__ __forceinline__ void ap_accumulate(double (&acc)[2][4], const double* As, const double* Bs, int kc) {
-    const int tr = threadIdx.x & 31, tc = threadIdx.x >> 5;
-#pragma unroll 8
-    for (int t = 0; t < kc; ++t) {
-        const double a0 = As[tr + t * AP_LDA], a1 = As[tr + 32 + t * AP_LDA];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const double bb = Bs[t + (tc + 8 * j) * AP_LDB];
-            acc[0][j] = fma(a0, bb, acc[0][j]);
-            acc[1][j] = fma(a1, bb, acc[1][j]);
-        }
-    }
-}
+// The apply products run on the FP64 tensor cores (mma.sync.m8n8k4.f64, DMMA; fragment layout
+// in bqr.cuh), ONE WARP PER (task, plane) ITEM: a CTA holds eight items and strides over the
+// grid, so the many rank-0 items of the level-0 couplings cost one slot read each instead of
+// a CTA launch.  Operand fragments (8 rows x 4 columns) are read straight from L2/HBM with
+// four k-steps of loads in flight; per output element the sum runs over the leaves in DFS
+// order and over k-steps of 4 in order, whatever the batch.
 
-// T = In^T X (rank x k) for one Rk leaf, once per (leaf, plane).
-__device__ __forceinline__ void apply_t_item(const ApplyTArgs& args, const BatchViews& bv, const int ti, const int b) {
-    __shared__ double As[64 * AP_LDA];  // In^T chunk: 64 ranks x 32 contracted
-    __shared__ double Bs[32 * AP_LDB];  // X chunk: 32 contracted x 32 columns
-    __shared__ double* sh_T;
+// T = In^T X (rank x k) for one Rk leaf, once per (leaf, plane): 8 x 8 tiles of T per warp.
+__device__ __forceinline__ void apply_t_item(const ApplyTArgs& args, const BatchViews& bv, const int ti, const int b,
+                                             double& fl) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
     const ApplyTTask task = args.tasks[ti];
     Slot& out = args.slots[(size_t)(args.nprod + ti) * args.B + b];
     const Slot s = args.slots[(size_t)task.prod * args.B + b];
@@ -611,65 +627,61 @@ __device__ __forceinline__ void apply_t_item(const ApplyTArgs& args, const Batch
     const HView& H = trans ? bv.b[b] : bv.a[b];
     const int rr = k ? H.rank[task.id] : 0;
     if (rr == 0) {
-        if (threadIdx.x == 0) out.U = nullptr;
+        if (lane == 0) out.U = nullptr;
         return;
     }
-    if (threadIdx.x == 0) sh_T = arena_alloc(args.arena, (unsigned long long)rr * k);
-    __syncthreads();
-    double* T = sh_T;
-    if (threadIdx.x == 0) {
+    double* T = nullptr;
+    if (lane == 0) {
+        T = arena_alloc(args.arena, (unsigned long long)rr * k);
         out.U = T;
         out.rank = rr;
     }
+    T = (double*)__shfl_sync(0xffffffffu, (unsigned long long)T, 0);
     if (!T) return;  // arena exhausted: flagged; the slabs skip this leaf
     const double* In = trans ? H.U[task.id] : H.V[task.id];
     const double* X = (trans ? bv.a[b].V[task.kx] : bv.b[b].U[task.kx]) + task.in_off;
     const int L = task.in_len, ldx = task.x_ld;
-    const int tr = threadIdx.x & 31, tc = threadIdx.x >> 5;
-    for (int t0 = 0; t0 < rr; t0 += 64)
-        for (int c0 = 0; c0 < k; c0 += 32) {
-            const int nt = min(64, rr - t0), nc = min(32, k - c0);
-            double acc[2][4] = {};
-            for (int j0 = 0; j0 < L; j0 += 32) {
-                const int jc = min(32, L - j0);
-                __syncthreads();
-                for (int e = threadIdx.x; e < 64 * 32; e += NT) {  // contracted index fastest: coalesced
-                    const int j = e & 31, t = e >> 5;
-                    As[t + j * AP_LDA] = (j < jc && t < nt) ? In[(j0 + j) + (size_t)(t0 + t) * L] : 0.0;
-                }
-                for (int e = threadIdx.x; e < 32 * 32; e += NT) {
-                    const int j = e & 31, c = e >> 5;
-                    Bs[j + c * AP_LDB] = (j < jc && c < nc) ? X[(j0 + j) + (size_t)(c0 + c) * ldx] : 0.0;
-                }
-                __syncthreads();
-                ap_accumulate(acc, As, Bs, jc);
+    const int nti = (rr + 7) >> 3, ntj = (k + 7) >> 3;
+    for (int tile = 0; tile < nti * ntj; ++tile) {
+        const int t0 = 8 * (tile % nti), c0 = 8 * (tile / nti);
+        const bool aok = t0 + g < rr, bok = c0 + g < k;
+        const double* ap = In + (size_t)(aok ? t0 + g : 0) * L;   // A[g][t] = In[j + (t0 + g) L]
+        const double* bp = X + (size_t)(bok ? c0 + g : 0) * ldx;  // B[t][g] = X[j + (c0 + g) ldx]
+        double d0 = 0.0, d1 = 0.0;
+        for (int j0 = 0; j0 < L; j0 += 16) {
+            double av[4], bw[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = j0 + 4 * q + t4;
+                av[q] = (aok && j < L) ? ap[j] : 0.0;
+                bw[q] = (bok && j < L) ? bp[j] : 0.0;
             }
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int t = tr + 32 * i, c = tc + 8 * j;
-                    if (t < nt && c < nc) T[(t0 + t) + (size_t)(c0 + c) * rr] = acc[i][j];
-                }
+            for (int q = 0; q < 4; ++q)
+                if (j0 + 4 * q < L) dmma8x8x4(d0, d1, av[q], bw[q]);
         }
-    if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, 2.0 * rr * L * k);
+        const int tr = t0 + g, tc = c0 + 2 * t4;
+        if (tr < rr) {
+            if (tc < k) T[tr + (size_t)tc * rr] = d0;
+            if (tc + 1 < k) T[tr + (size_t)(tc + 1) * rr] = d1;
+        }
+    }
+    if (lane == 0) fl += 2.0 * rr * L * k;
 }
 
-// Grid-stride over (task, plane) items (see item_grid: capped for k_apply_t, whose many
-// rank-0 items return at once; one CTA per item for the others).
 __global__ void __launch_bounds__(NT) k_apply_t(const ApplyTArgs args, const __grid_constant__ BatchViews bv, const int ntasks) {
     const long total = (long)ntasks * args.B;
-    for (long w = blockIdx.x; w < total; w += gridDim.x) {
-        __syncthreads();  // shared staging of the previous item is no longer read
-        apply_t_item(args, bv, (int)(w / args.B), (int)(w % args.B));
-    }
+    double fl = 0;
+    for (long w = (long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); w < total; w += (long)gridDim.x * (NT / 32))
+        apply_t_item(args, bv, (int)(w / args.B), (int)(w % args.B), fl);
+    if ((threadIdx.x & 31) == 0 && fl > 0) add_flops(args.flops, F_GEMM, fl);
 }
 
-// One output slab (<= 64 rows, all k columns): Y = sum over dense leaves of D (or D^T) X
-// plus sum over Rk leaves of Out T, operands staged through shared memory.
-__device__ __forceinline__ void apply_item(const ApplyArgs& args, const BatchViews& bv, const int ti, const int b) {
-    __shared__ double As[64 * AP_LDA];
-    __shared__ double Bs[32 * AP_LDB];
+// One output slab (<= 64 rows, all k columns) per warp: Y = sum over dense leaves of D (or D^T)
+// X plus sum over Rk leaves of Out T, as 8 x 8 tiles of Y accumulated in DMMA fragments.
+__device__ __forceinline__ void apply_item(const ApplyArgs& args, const BatchViews& bv, const int ti, const int b,
+                                           double& fl) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
     const ApplyTask task = args.tasks[ti];
     const Slot s = args.slots[(size_t)task.prod * args.B + b];
     const int k = s.rank;
@@ -681,89 +693,66 @@ __device__ __forceinline__ void apply_item(const ApplyArgs& args, const BatchVie
     double* Y = trans ? s.V : s.U;
     const int ldy = trans ? s.ldv : s.ldu;
     const int r0 = task.r0, nr = task.r1 - task.r0;
-    const int tr = threadIdx.x & 31, tc = threadIdx.x >> 5;
-    double fl = 0;
-    for (int c0 = 0; c0 < k; c0 += 32) {
-        const int nc = min(32, k - c0);
-        double acc[2][4] = {};
+    const int nti = (nr + 7) >> 3, ntj = (k + 7) >> 3;
+    for (int tile = 0; tile < nti * ntj; ++tile) {
+        const int rt = 8 * (tile % nti), c0 = 8 * (tile / nti);
+        const int row = r0 + rt + g;  // this lane's A row (slab output space)
+        const bool bok = c0 + g < k;
+        double d0 = 0.0, d1 = 0.0;
         for (int li = task.lbeg; li < task.lend; ++li) {
             const ApplyLeaf L = args.leaves[li];
             const int out_len = trans ? L.n : L.m;
-            const int in_len = trans ? L.m : L.n;
-            const int o0 = max(r0, L.out_off), o1 = min(task.r1, L.out_off + out_len);
-            if (o0 >= o1) continue;
+            const int o0 = max(r0 + rt, L.out_off), o1 = min(min(task.r1, r0 + rt + 8), L.out_off + out_len);
+            if (o0 >= o1) continue;  // leaf misses this row tile
+            const bool rok = row >= o0 && row < o1;
+            const int lr = rok ? row - L.out_off : 0;
+            const double* A;   // A[g][t] = A_(row, j) at A + j * ja (+ row offset folded in)
+            long ja;
+            const double* Bp;  // B[t][g] = contracted (j, column c0 + g) at Bp + j
+            int len;
             if (L.kind == K_DENSE) {
                 const double* D = H.dense + L.doff;
-                for (int j0 = 0; j0 < in_len; j0 += 32) {
-                    const int jc = min(32, in_len - j0);
-                    __syncthreads();
-                    if (!trans) {
-                        for (int e = threadIdx.x; e < 64 * 32; e += NT) {  // output row fastest: coalesced
-                            const int i = e & 63, j = e >> 6;
-                            const int row = r0 + i;
-                            As[i + j * AP_LDA] = (row >= o0 && row < o1 && j < jc)
-                                                     ? D[(row - L.out_off) + (size_t)(j0 + j) * L.m] : 0.0;
-                        }
-                    } else {
-                        for (int e = threadIdx.x; e < 64 * 32; e += NT) {  // contracted index fastest
-                            const int j = e & 31, i = e >> 5;
-                            const int row = r0 + i;
-                            As[i + j * AP_LDA] = (row >= o0 && row < o1 && j < jc)
-                                                     ? D[(j0 + j) + (size_t)(row - L.out_off) * L.m] : 0.0;
-                        }
-                    }
-                    for (int e = threadIdx.x; e < 32 * 32; e += NT) {
-                        const int j = e & 31, c = e >> 5;
-                        Bs[j + c * AP_LDB] = (j < jc && c < nc) ? X[L.in_off + j0 + j + (size_t)(c0 + c) * ldx] : 0.0;
-                    }
-                    __syncthreads();
-                    ap_accumulate(acc, As, Bs, jc);
-                }
-                fl += 2.0 * (o1 - o0) * in_len * nc;
+                len = trans ? L.m : L.n;
+                if (!trans) { A = D + lr; ja = L.m; }
+                else { A = D + (size_t)lr * L.m; ja = 1; }
+                Bp = X + L.in_off + (size_t)(bok ? c0 + g : 0) * ldx;
             } else {
                 const Slot ts = args.slots[(size_t)(args.nprod + L.tl) * args.B + b];
                 const double* T = ts.U;
                 if (!T) continue;
-                const int rr = ts.rank;
-                const double* Out = trans ? H.V[L.id] : H.U[L.id];
-                for (int t0 = 0; t0 < rr; t0 += 32) {
-                    const int tcn = min(32, rr - t0);
-                    __syncthreads();
-                    for (int e = threadIdx.x; e < 64 * 32; e += NT) {
-                        const int i = e & 63, t = e >> 6;
-                        const int row = r0 + i;
-                        As[i + t * AP_LDA] = (row >= o0 && row < o1 && t < tcn)
-                                                 ? Out[(row - L.out_off) + (size_t)(t0 + t) * out_len] : 0.0;
-                    }
-                    for (int e = threadIdx.x; e < 32 * 32; e += NT) {
-                        const int t = e & 31, c = e >> 5;
-                        Bs[t + c * AP_LDB] = (t < tcn && c < nc) ? T[(t0 + t) + (size_t)(c0 + c) * rr] : 0.0;
-                    }
-                    __syncthreads();
-                    ap_accumulate(acc, As, Bs, tcn);
+                len = ts.rank;
+                A = (trans ? H.V[L.id] : H.U[L.id]) + lr;
+                ja = out_len;
+                Bp = T + (size_t)(bok ? c0 + g : 0) * len;
+            }
+            for (int j0 = 0; j0 < len; j0 += 16) {
+                double av[4], bw[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = j0 + 4 * q + t4;
+                    av[q] = (rok && j < len) ? A[(size_t)j * ja] : 0.0;
+                    bw[q] = (bok && j < len) ? Bp[j] : 0.0;
                 }
-                fl += 2.0 * (o1 - o0) * rr * nc;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (j0 + 4 * q < len) dmma8x8x4(d0, d1, av[q], bw[q]);
             }
+            if (lane == 0 && c0 == 0) fl += 2.0 * (o1 - o0) * len * k;
         }
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int r = tr + 32 * i, c = tc + 8 * j;
-                if (r < nr && c < nc) Y[(r0 + r) + (size_t)(c0 + c) * ldy] = acc[i][j];
-            }
+        const int yc = c0 + 2 * t4;
+        if (rt + g < nr) {
+            if (yc < k) Y[(row) + (size_t)yc * ldy] = d0;
+            if (yc + 1 < k) Y[(row) + (size_t)(yc + 1) * ldy] = d1;
+        }
     }
-    if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, fl);
 }
 
-// Grid-stride over (task, plane) items (see item_grid: capped for k_apply_t, whose many
-// rank-0 items return at once; one CTA per item for the others).
 __global__ void __launch_bounds__(NT) k_apply(const ApplyArgs args, const __grid_constant__ BatchViews bv, const int ntasks) {
     const long total = (long)ntasks * args.B;
-    for (long w = blockIdx.x; w < total; w += gridDim.x) {
-        __syncthreads();  // shared staging of the previous item is no longer read
-        apply_item(args, bv, (int)(w / args.B), (int)(w % args.B));
-    }
+    double fl = 0;
+    for (long w = (long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); w < total; w += (long)gridDim.x * (NT / 32))
+        apply_item(args, bv, (int)(w / args.B), (int)(w % args.B), fl);
+    if ((threadIdx.x & 31) == 0 && fl > 0) add_flops(args.flops, F_GEMM, fl);
 }
 
 // ------------------------------------------------------------------ dense-target deposits
@@ -775,64 +764,66 @@ struct DepArgs {
     FlopLedger* flops;
 };
 
-// Per group of 4 elements per thread (1024 elements: one group for a 32 x 32 leaf, four for
-// 64 x 64), parts outermost and the elements' partial sums in registers: the part and slot
-// records are read once per part and group rather than once per element, and the
-// elements' operand loads overlap.  Each element still adds its contributions in part
-// order, so the result is bitwise that of the element loop.
-constexpr int DEP_E = 4;
+// Dense-target deposit on the FP64 tensor cores: warp per 8 x 8 tile of the target leaf (tile
+// w, w + 8, ... of the leaf's tile grid), the tile held in DMMA accumulator fragments while every
+// part is added in part order -- alpha U V^T as k-steps of 4 over the part's rank
+// (mma.sync.m8n8k4.f64; alpha = +-1 is applied exactly to the U fragment), exact dense
+// products A B likewise over their inner dimension.  U / V / A / B fragments come straight
+// from L2 (8 rows x 4 columns per load).
 __device__ __forceinline__ void deposit_item(const DepArgs& args, const BatchViews& bv, const int ti, const int b) {
     const DepTask task = args.tasks[ti];
     double* Cd = bv.c[b].dense + task.doff;
     const int m = task.m, n = task.n;
-    const int nel = m * n;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int tm = (m + 7) >> 3, tn = (n + 7) >> 3;
     double fl = 0;
-    for (int g0 = 0; g0 < nel; g0 += DEP_E * NT) {
-        double c[DEP_E];
-#pragma unroll
-        for (int q = 0; q < DEP_E; ++q) {
-            const int e = g0 + threadIdx.x + q * NT;
-            c[q] = e < nel ? Cd[e] : 0.0;
-        }
+    for (int tile = threadIdx.x >> 5; tile < tm * tn; tile += NT / 32) {
+        const int ri = 8 * (tile % tm) + g;          // A-fragment row of this lane
+        const int cj = 8 * (tile / tm) + g;          // B-fragment column of this lane
+        const int c0 = 8 * (tile / tm) + 2 * t;      // accumulator columns c0, c0 + 1 (row ri)
+        const bool rok = ri < m, cok = cj < n;
+        double d0 = (rok && c0 < n) ? Cd[ri + (size_t)c0 * m] : 0.0;
+        double d1 = (rok && c0 + 1 < n) ? Cd[ri + (size_t)(c0 + 1) * m] : 0.0;
         for (int pi = task.pbeg; pi < task.pend; ++pi) {
             const Part p = args.parts[pi];
+            const double* A;
+            const double* Bt;  // B fragment source: element (k, col) at Bt[k * bk + col * bc]
+            long lda, bk, bc;
+            int kk;
+            double alpha = p.alpha;
             if (p.src == S_GEMM) {
-                const double* A = bv.a[b].dense + p.da;
-                const double* Bm = bv.b[b].dense + p.db;
-#pragma unroll
-                for (int q = 0; q < DEP_E; ++q) {
-                    const int e = g0 + threadIdx.x + q * NT;
-                    if (e < nel) {
-                        const int i = e % m, j = e / m;
-                        double a = 0;
-                        for (int t = 0; t < p.gk; ++t) a = fma(A[i + (size_t)t * m], Bm[t + (size_t)j * p.gk], a);
-                        c[q] += p.alpha * a;
-                    }
-                }
-                if (g0 == 0) fl += 2.0 * m * n * p.gk;
+                A = bv.a[b].dense + p.da;
+                lda = m;
+                Bt = bv.b[b].dense + p.db;
+                bk = 1;
+                bc = p.gk;
+                kk = p.gk;
             } else {
                 const Slot s = args.slots[(size_t)p.id * args.B + b];
                 if (s.rank == 0) continue;
-                const double* U = s.U + p.u_src;
-                const double* V = s.V + p.v_src;
-#pragma unroll
-                for (int q = 0; q < DEP_E; ++q) {
-                    const int e = g0 + threadIdx.x + q * NT;
-                    if (e < nel) {
-                        const int i = e % m, j = e / m;
-                        double a = 0;
-                        for (int t = 0; t < s.rank; ++t) a = fma(p.alpha * U[i + (size_t)t * s.ldu], V[j + (size_t)t * s.ldv], a);
-                        c[q] += a;
-                    }
-                }
-                if (g0 == 0) fl += 2.0 * m * n * s.rank;
+                A = s.U + p.u_src;
+                lda = s.ldu;
+                Bt = s.V + p.v_src;  // V^T: element (k, col) = V[col + k ldv]
+                bk = s.ldv;
+                bc = 1;
+                kk = s.rank;
             }
-        }
+            for (int k0 = 0; k0 < kk; k0 += 16) {  // four k-steps, fragment loads first
+                double av[4], bw[4];
 #pragma unroll
-        for (int q = 0; q < DEP_E; ++q) {
-            const int e = g0 + threadIdx.x + q * NT;
-            if (e < nel) Cd[e] = c[q];
+                for (int s = 0; s < 4; ++s) {
+                    const int q = k0 + 4 * s + t;
+                    av[s] = (rok && q < kk) ? alpha * A[ri + (size_t)q * lda] : 0.0;
+                    bw[s] = (cok && q < kk) ? Bt[(size_t)q * bk + (size_t)cj * bc] : 0.0;
+                }
+#pragma unroll
+                for (int s = 0; s < 4; ++s)
+                    if (k0 + 4 * s < kk) dmma8x8x4(d0, d1, av[s], bw[s]);
+            }
+            if (tile == 0 && lane == 0) fl += 2.0 * m * n * kk;
         }
+        if (rok && c0 < n) Cd[ri + (size_t)c0 * m] = d0;
+        if (rok && c0 + 1 < n) Cd[ri + (size_t)(c0 + 1) * m] = d1;
     }
     if (threadIdx.x == 0) add_flops(args.flops, F_GEMM, fl);
 }
@@ -1851,6 +1842,13 @@ std::string prof_report(bool reset) {
                  cnt ? (double)ph[6] / cnt : 0.0, cnt ? (double)ph[7] / cnt : 0.0, ph[8], ph[9], ph[10] / 1e9,
                  ph[11] / 1e9, ph[12] / 1e9);
         out += buf;
+        unsigned long long cc[8];
+        cudaMemcpyFromSymbol(cc, g_cta_cyc, sizeof(cc));
+        const double cn = cc[0] ? (double)cc[0] : 1.0;
+        snprintf(buf, sizeof(buf), "#phase cta-engine tasks %llu (cycles per task): rrqr %.0f jacobi %.0f write %.0f | "
+                 "rp %.2f cols %.2f sweeps %.2f\n", cc[0], cc[1] / cn, cc[2] / cn, cc[3] / cn, cc[4] / cn, cc[5] / cn,
+                 cc[6] / cn);
+        out += buf;
         unsigned long long w[8], wc = 0;
         cudaMemcpyFromSymbol(w, g_w32_cyc, sizeof(w));
         cudaMemcpyFromSymbol(&wc, g_w32_cnt, sizeof(wc));
@@ -1865,6 +1863,7 @@ std::string prof_report(bool reset) {
             const unsigned long long z[16] = {};
             cudaMemcpyToSymbol(g_phase_cyc, z, sizeof(z));
             cudaMemcpyToSymbol(g_phase_cnt, z, sizeof(unsigned long long));
+            cudaMemcpyToSymbol(g_cta_cyc, z8, sizeof(z8));
         }
     }
     for (auto& [ms, name, ctas] : g_top) {
@@ -1899,8 +1898,9 @@ void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const 
                      double eps, const double* abs_cut, double* sig_out, bool values_only, Arena out_arena,
                      Arena work, FlopLedger* flops, const BatchViews& bv, const char* name) {
     if (ntasks == 0 || B == 0) return;
+    static const int dense_min_k = getenv("ACRGPU_DENSE_MIN_K") ? atoi(getenv("ACRGPU_DENSE_MIN_K")) : 0;
     TruncArgs a{tasks, parts, slots, B, eps, abs_cut, sig_out, values_only ? 1 : 0, out_arena, work,
-                ledger(flops, name)};
+                ledger(flops, name), dense_min_k};
     ProfScope _ps(st, name, (long)ntasks * B);
     k_truncate<BIG_DMAX, BIG_RPCAP, BIG_NT><<<dim3(ntasks, B), BIG_NT, trunc_smem_big(), st>>>(a, bv);
 }
@@ -1945,6 +1945,14 @@ static unsigned item_grid(long items, int per_sm) {
     return (unsigned)(items < cap ? (items > 0 ? items : 1) : cap);
 }
 
+// Grid of a warp-per-item kernel: one warp per item up to 8 resident CTAs of 8 warps on each of
+// the 148 SMs (items beyond that are strided).
+static unsigned warp_grid(long items) {
+    const long ctas = (items + NT / 32 - 1) / (NT / 32);
+    const long cap = 148L * 8;
+    return (unsigned)(ctas < 1 ? 1 : (ctas < cap ? ctas : cap));
+}
+
 void launch_alloc_apply(cudaStream_t st, int ntasks, const AllocTask* tasks, Slot* slots, int B, Arena arena,
                         const BatchViews& bv) {
     if (ntasks == 0 || B == 0) return;
@@ -1959,7 +1967,7 @@ void launch_apply_t(cudaStream_t st, int ntasks, const ApplyTTask* tasks, Slot* 
     if (ntasks == 0 || B == 0) return;
     ApplyTArgs a{tasks, slots, B, nprod, arena, ledger(flops, "k_apply_t")};
     ProfScope _ps(st, "k_apply_t", (long)ntasks * B);
-    k_apply_t<<<item_grid((long)ntasks * B, 3), NT, 0, st>>>(a, bv, ntasks);
+    k_apply_t<<<warp_grid((long)ntasks * B), NT, 0, st>>>(a, bv, ntasks);
 }
 
 void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const ApplyLeaf* leaves, const int* x_ld,
@@ -1967,8 +1975,7 @@ void launch_apply(cudaStream_t st, int ntasks, const ApplyTask* tasks, const App
     if (ntasks == 0 || B == 0) return;
     ApplyArgs a{tasks, leaves, slots, B, nprod, x_ld, ledger(flops, "k_apply")};
     ProfScope _ps(st, "k_apply", (long)((ntasks)*(B)));
-    // one CTA per item: the slab products vary too much in cost for a static stride (measured)
-    k_apply<<<item_grid((long)ntasks * B, 0), NT, 0, st>>>(a, bv, ntasks);
+    k_apply<<<warp_grid((long)ntasks * B), NT, 0, st>>>(a, bv, ntasks);
 }
 
 void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Part* parts, const Slot* slots, int B,

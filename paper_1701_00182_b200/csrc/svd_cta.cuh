@@ -10,6 +10,10 @@
 #pragma once
 // (included inside namespace acrgpu by kernels.cu, after arena_alloc)
 
+// CTA-engine phase timing (clock64 deltas of thread 0, summed over tasks): diagnostics only.
+// [0] tasks [1] rrqr [2] jacobi [3] write [4] sum rp [5] sum cols [6] jacobi sweeps
+__device__ unsigned long long g_cta_cyc[8];
+
 struct CtaSvdWork {
     double* A;      // rows x cols (ld = lda): input, then R + reflectors
     int lda;
@@ -282,6 +286,7 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
                 }
                 __syncthreads();
             }
+            if (threadIdx.x == 0) atomicAdd(&g_cta_cyc[6], 1ull);
             if (!__syncthreads_or(rotated)) break;
         }
     }
@@ -326,8 +331,17 @@ __device__ int cta_trunc_svd(CtaSvdWork& w, int rows, int cols, double eps, doub
     const double dabs = values_only ? 0.0 : 1.8e-4 * abs_cut;
     const double d1 = drel * sqrt(cm);
     const double delta2 = fmax(d1 * d1, dabs * dabs);
+    unsigned long long ct0 = clock64();
     const int rp = cta_rrqr<NT>(w, rows, cols, delta2);
     *rp_out = rp;
+    if (threadIdx.x == 0) {
+        const unsigned long long t = clock64();
+        atomicAdd(&g_cta_cyc[0], 1ull);
+        atomicAdd(&g_cta_cyc[1], t - ct0);
+        atomicAdd(&g_cta_cyc[4], (unsigned long long)rp);
+        atomicAdd(&g_cta_cyc[5], (unsigned long long)cols);
+        ct0 = t;
+    }
     if (rp == 0) {
         *smax_out = 0.0;
         return 0;
@@ -371,6 +385,7 @@ __device__ int cta_trunc_svd(CtaSvdWork& w, int rows, int cols, double eps, doub
         }
         sh_r = r;
         sh_smax = s0;
+        atomicAdd(&g_cta_cyc[2], clock64() - ct0);
     }
     __syncthreads();
     *smax_out = sh_smax;
@@ -383,6 +398,7 @@ __device__ void cta_trunc_write(const CtaSvdWork& w, int rows, int cols, int rp,
                                 int ldv) {
     constexpr int NW = NT / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned long long wt0 = clock64();
     // J_r Sigma_r = R W_r Sigma_r^{-1}  (R = J W^T: the rp x cols upper rows of the pivoted QR)
     for (int e = threadIdx.x; e < rows * r; e += NT) {
         const int i = e % rows, t = e / rows;
@@ -417,6 +433,7 @@ __device__ void cta_trunc_write(const CtaSvdWork& w, int rows, int cols, int rp,
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&g_cta_cyc[3], clock64() - wt0);
 }
 
 
