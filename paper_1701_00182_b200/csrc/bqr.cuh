@@ -17,7 +17,7 @@
 
 constexpr int BQR_NB = 16;
 constexpr int BQR_LDW = 20;  // W (16 x ncol) leading dimension: == 4 mod 16 -> conflict-free fragments
-constexpr int BQR_SCRATCH = 32 * 16 + 16 + 32;  // panel_qr_reg reduction scratch (<= 32 warps)
+constexpr int BQR_SCRATCH = 2 * 32 * 16 + 32;  // panel_qr_reg reduction scratch (<= 32 warps, double-buffered)
 
 // smem leading dimension of an h-row panel: == 4 (mod 16) doubles, so the DMMA
 // fragment loads (8 rows x 4 columns or 4 rows x 8 columns) hit 16 distinct banks.
@@ -28,11 +28,6 @@ __host__ __device__ inline size_t bqr_smem_doubles(int rows, int cols) {
     return BQR_SCRATCH + (size_t)bqr_ldp(rows) * BQR_NB + 2 * BQR_NB * BQR_NB + (size_t)BQR_LDW * (((cols + 7) / 8) * 8) + 64;
 }
 
-__device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
 
 // Unblocked Householder on a smem panel P (h x nb, ld ldp); tau[nb].  One barrier per
 // column: every thread derives (beta, tau, 1/(c0-beta)) from the column's tail norm,
@@ -115,14 +110,13 @@ __device__ void panel_qr(double* P, int h, int ldp, int nb, double* tau) {
 // reflector scalars itself and updates its rows.  The panel is read from and
 // written back to W (global, rows j0.., columns j0..j0+nb), and the explicit
 // reflector block V (h x 16, zero columns past nb) is left in smem P (ld ldp).
-// scratch: >= NW * 16 + 16 + 32 doubles of shared memory.
+// scratch: >= 2 * NW * 16 + 32 doubles of shared memory.
 template <int NT, int RPT>
 __device__ void panel_qr_reg(double* Wp, int ld, int h, int nb, double* tau, double* P, int ldp, double* scratch) {
     constexpr int NW = NT / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* red = scratch;            // NW x 16 warp partials
-    double* fin = red + NW * 16;      // 16 totals
-    double* rowj = fin + 16;          // 2 x 16: row j of the panel (double-buffered)
+    double* red = scratch;            // 2 x NW x 16 warp partials (double-buffered by column parity)
+    double* rowj = red + 2 * NW * 16;  // 2 x 16: row j of the panel (double-buffered)
     double x[RPT][BQR_NB];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
@@ -152,14 +146,17 @@ __device__ void panel_qr_reg(double* Wp, int ld, int h, int nb, double* tau, dou
             }
         }
         const double part = reduce_scatter16(v, lane);
-        if (lane < 16) red[warp * 16 + lane] = part;
+        double* rb = red + (j & 1) * NW * 16;
+        if (lane < 16) rb[warp * 16 + lane] = part;
         __syncthreads();
-        if (threadIdx.x < 16) {
-            double s = 0;
-            for (int w = 0; w < NW; ++w) s += red[w * 16 + threadIdx.x];
-            fin[threadIdx.x] = s;
-        }
-        __syncthreads();
+        // every warp forms the 16 column totals itself (lane l < 16 sums slot l over the warps,
+        // in warp order) and shares them by shuffles: one barrier per column instead of two
+        double tot = 0;
+        if (lane < 16)
+            for (int w = 0; w < NW; ++w) tot += rb[w * 16 + lane];
+        double fin[BQR_NB];
+#pragma unroll
+        for (int c = 0; c < BQR_NB; ++c) fin[c] = __shfl_sync(0xffffffffu, tot, c);
         const double* rj = rowj + (j & 1) * 16;
         const double tail = fin[j], c0 = rj[j];
         double beta, tj, inv;

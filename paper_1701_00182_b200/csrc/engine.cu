@@ -91,6 +91,8 @@ struct Lane {
     cudaEvent_t ev = nullptr;
 };
 
+struct PlanCache;
+
 struct Ctx {
     int device = 0;
     cudaStream_t st = nullptr;  // == lanes[0].st (main stream)
@@ -111,6 +113,7 @@ struct Ctx {
     size_t scratch_cap = 0;
     unsigned long long call_id = 0;
     std::vector<std::pair<int, std::vector<int>>> call_planes;  // call id -> (level, planes)
+    std::shared_ptr<PlanCache> plan_cache;  // compiled plans of the last structure
 
     void init(int dev) {
         if (dev >= 0) CK(cudaSetDevice(dev));
@@ -168,14 +171,21 @@ struct Ctx {
         CK(cudaEventRecord(lanes[from].ev, lanes[from].st));
         CK(cudaStreamWaitEvent(lanes[to].st, lanes[from].ev, 0));
     }
+    // ACRGPU_NO_FORK=1: every launch on the lane's own stream (A/B switch)
+    static bool no_fork() {
+        static const bool v = getenv("ACRGPU_NO_FORK") != nullptr;
+        return v;
+    }
     // the lane's side streams i < k wait for everything issued so far on the lane's stream
     void fork(int k) {
+        if (no_fork()) return;
         Lane& l = lane();
         CK(cudaEventRecord(l.fork_ev, l.st));
         for (int i = 0; i < k && i < NSUB; ++i) CK(cudaStreamWaitEvent(l.sub[i], l.fork_ev, 0));
     }
     // the lane's stream waits for side streams i < k
     void join(int k) {
+        if (no_fork()) return;
         Lane& l = lane();
         for (int i = 0; i < k && i < NSUB; ++i) {
             CK(cudaEventRecord(l.join_ev[i], l.sub[i]));
@@ -183,7 +193,7 @@ struct Ctx {
         }
     }
     // stream q of the current fork: 0 = the lane's stream, 1..NSUB = side streams
-    cudaStream_t fstream(int q) { return q == 0 ? lane().st : lane().sub[(q - 1) % NSUB]; }
+    cudaStream_t fstream(int q) { return (q == 0 || no_fork()) ? lane().st : lane().sub[(q - 1) % NSUB]; }
     void reset_all() {
         for (auto& l : lanes) CK(cudaStreamSynchronize(l.st));
         persist.base = space_ptr(space);
@@ -238,6 +248,7 @@ struct Ctx {
     void destroy() {
         for (auto& l : lanes)
             if (l.st) cudaStreamSynchronize(l.st);
+        plan_cache.reset();
         for (void* p : std::initializer_list<void*>{persist_sp[0], persist_sp[1], trans_base, ctrs, overflow, err, flops, scratch})
             if (p) cudaFree(p);
         if (h_zero) cudaFreeHost(h_zero);
@@ -310,6 +321,19 @@ struct Plan {
     int pp_level = -1;
 };
 
+// Compiled plans depend only on the structure (cluster tree + block tree) and on the exact
+// dense-product flag, so they are kept in the context across factorizations of systems with
+// the same structure (the bench and every repeated factorization skip ~10^3 plan builds and
+// their device uploads).  Keyed by the structure's parameters and a hash of the coordinates.
+struct PlanCache {
+    std::string key;
+    std::map<std::tuple<int, int, int, int>, std::unique_ptr<Plan>> plans;
+    std::vector<void*> dev;  // device arrays of the plans
+    ~PlanCache() {
+        for (void* p : dev) cudaFree(p);
+    }
+};
+
 struct Engine {
     Ctx* ctx = nullptr;
     Structure S;
@@ -317,12 +341,12 @@ struct Engine {
     bool exact_dd = false;
     double peak_transient_gb = 0, peak_transient_per_plane_gb = 0;  // ACRGPU_ARENA_STATS
     int level_tag = 0;  // current cyclic-reduction level (adaptive batching)
-    std::map<std::tuple<int, int, int, int>, std::unique_ptr<Plan>> plans;
+    std::shared_ptr<PlanCache> pc;  // shared with the context (see PlanCache)
     // every live Store of this engine (compaction of the persistent arena, gc())
     std::shared_ptr<std::unordered_set<Store*>> live = std::make_shared<std::unordered_set<Store*>>();
     double gc_next = 0.6;  // compaction threshold (fraction of a semi-space)
     int gc_count = 0;
-    std::vector<void*> dev_allocs;  // plan arrays etc.
+    std::vector<void*> dev_allocs;  // per-factorization device tables (structure, lifted leaves)
 
     // structure-wide device tables
     int* d_perm = nullptr;
@@ -361,14 +385,22 @@ struct Engine {
     cudaStream_t st() const { return ctx->lanes[ctx->cur].st; }
     cudaStream_t main_st() const { return ctx->st; }
 
+    // plan arrays: owned by the plan cache (they outlive this engine)
     template <class T>
-    Classed<T> up_classed(const std::vector<T>& v) {
+    T* upc(const std::vector<T>& v) {
+        T* p = dmalloc<T>(v.size());
+        if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+        pc->dev.push_back((void*)p);
+        return p;
+    }
+    template <class T>
+    Classed<T> up_classed(const std::vector<T>& v, bool cached = false) {
         Classed<T> c;
         std::vector<T> parts[NCLASS];
         for (const T& t : v) parts[size_class(t.m, t.n)].push_back(t);
         for (int k = 0; k < NCLASS; ++k) {
             c.n[k] = (int)parts[k].size();
-            if (c.n[k]) c.p[k] = up(parts[k]);
+            if (c.n[k]) c.p[k] = cached ? upc(parts[k]) : up(parts[k]);
         }
         return c;
     }
@@ -723,8 +755,8 @@ struct Engine {
 
     Plan* plan(int c, int a, int b, double alpha) {
         const auto key = std::make_tuple(c, a, b, alpha > 0 ? 1 : -1);
-        auto it = plans.find(key);
-        if (it != plans.end()) return it->second.get();
+        auto it = pc->plans.find(key);
+        if (it != pc->plans.end()) return it->second.get();
         PlanBuild pb;
         mult_rec(pb, c, a, b, alpha, c, a, b);
         const SNode& CR = S.node(c);
@@ -763,19 +795,19 @@ struct Engine {
         P->nalloc = (int)pb.allocs.size();
         P->napply = (int)pb.applies.size();
         P->ntt = (int)pb.tts.size();
-        P->tts = up(pb.tts);
+        P->tts = upc(pb.tts);
         P->ndep = (int)pb.deps.size();
-        P->allocs = up(pb.allocs);
-        P->applies = up(pb.applies);
-        P->aleaves = up(pb.aleaves);
-        P->x_ld = up(pb.x_ld);
-        P->dds = up_classed(pb.dds);
-        for (auto& ph : pb.bb) P->bb.push_back(up_classed(ph));
-        P->flush = up_classed(pb.flush);
-        P->deps = up(pb.deps);
-        P->parts = up(pb.parts);
+        P->allocs = upc(pb.allocs);
+        P->applies = upc(pb.applies);
+        P->aleaves = upc(pb.aleaves);
+        P->x_ld = upc(pb.x_ld);
+        P->dds = up_classed(pb.dds, true);
+        for (auto& ph : pb.bb) P->bb.push_back(up_classed(ph, true));
+        P->flush = up_classed(pb.flush, true);
+        P->deps = upc(pb.deps);
+        P->parts = upc(pb.parts);
         Plan* raw = P.get();
-        plans[key] = std::move(P);
+        pc->plans[key] = std::move(P);
         return raw;
     }
 
@@ -1088,13 +1120,13 @@ struct Engine {
             if (n.rows() != n.cols() || n.rows() > DENSE_MAX)
                 throw AcrError{ACRGPU_E_USAGE, "GPU path: dense diagonal leaf larger than 64"};
             auto key = std::make_tuple(node, -1000, -1000, 0);
-            auto it = plans.find(key);
+            auto it = pc->plans.find(key);
             Plan* P;
-            if (it == plans.end()) {
+            if (it == pc->plans.end()) {
                 auto np = std::make_unique<Plan>();
-                np->deps = (DepTask*)up(std::vector<LuTask>{t});
+                np->deps = (DepTask*)upc(std::vector<LuTask>{t});
                 P = np.get();
-                plans[key] = std::move(np);
+                pc->plans[key] = std::move(np);
             } else {
                 P = it->second.get();
             }
@@ -1291,6 +1323,7 @@ struct acrgpu_fact {
     std::vector<acrgpu::Level> levels;
     std::vector<acrgpu::StoreP> apexDinv, apexE, apexF;
     acrgpu_timing timing{};
+    double timing_host_enqueue_ms = 0;  // host time to issue the factorization (diagnostics)
     double* fbuf = nullptr;  // solve workspace
     size_t fbuf_cap = 0;
     double* ubuf = nullptr;  // compacted low-rank factors of the stored blocks
@@ -1644,6 +1677,7 @@ struct PartRun {
     std::vector<SP> D, Ev, Fv;
     std::vector<cudaEvent_t> lev_ev;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    std::chrono::steady_clock::time_point host_t0;
 };
 
 // plan_schedule (parallel.cpp:383-405): contiguous plane blocks at level 0; retained
@@ -1884,6 +1918,7 @@ static void factor_finish(PartRun& R) {
     }
     if (verbose_levels()) {
         CK(cudaDeviceSynchronize());
+        fprintf(stderr, "[acrgpu] rank %d host enqueue %.1f ms\n", R.rank, F->timing_host_enqueue_ms);
         for (size_t i = 1; i < R.lev_ev.size(); ++i) {
             float ms = 0;
             cudaEventElapsedTime(&ms, R.lev_ev[i - 1], R.lev_ev[i]);
@@ -1946,6 +1981,7 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
     FactoringScope fs(F->eng->ctx);
     PartRun R;
     R.F = F;
+    R.host_t0 = std::chrono::steady_clock::now();
     factor_begin(R, sys, nullptr);
     const int stop = F->eng->cfg.stop_planes;
     int lvl = 0;
@@ -1959,6 +1995,7 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
         ++lvl;
     }
     factor_apex(R, lvl);
+    F->timing_host_enqueue_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - R.host_t0).count();
     factor_finish(R);
 }
 
@@ -3044,6 +3081,21 @@ static std::unique_ptr<acrgpu_fact> make_part(acrgpu_ctx* ctx, const DSys& ds, c
         throw AcrError{ACRGPU_E_USAGE, "GPU path: dense leaves above 64 rows are not supported"};
     if (!E.S.balanced)
         throw AcrError{ACRGPU_E_USAGE, "GPU path: unbalanced cluster trees (mixed dense/branch products) are not supported"};
+    {
+        // plan cache key: structure parameters + FNV-1a hash of the coordinates
+        unsigned long long h = 1469598103934665603ull;
+        const unsigned char* c = (const unsigned char*)ds.coords.data();
+        for (size_t i = 0; i < ds.coords.size() * sizeof(double); ++i) h = (h ^ c[i]) * 1099511628211ull;
+        char key[256];
+        std::snprintf(key, sizeof(key), "%d:%d:%.17g:%d:%d:%llx", ds.dim, cfg->leaf_size, cfg->eta, cfg->weak,
+                      (int)E.exact_dd, h);
+        auto& cache = ctx->c.plan_cache;
+        if (!cache || cache->key != key) {
+            cache = std::make_shared<PlanCache>();
+            cache->key = key;
+        }
+        E.pc = cache;
+    }
     E.prepare_structure();
     ++ctx->refs;
     return F;

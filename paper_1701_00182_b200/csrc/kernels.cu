@@ -1518,20 +1518,6 @@ struct SmallTaskIO {
         }
         return rp;
     }
-    __device__ static RowPart dd_part(const double* Ad, const double* Bd, int m, int k, int n, bool tall) {
-        RowPart rp;
-        rp.k = k;
-        rp.upper = 0;
-        rp.alpha = 1.0;
-        if (tall) {  // A[i,j] = sum_t Ad(i,t) Bd(t,j)
-            rp.P = Ad; rp.ps = 1; rp.pt = m; rp.pd = 0; rp.pr = m;
-            rp.Q = Bd; rp.qs = k; rp.qt = 1; rp.qd = 0; rp.qr = n;
-        } else {     // A = M^T: A[i,j] = sum_t Bd(t,i) Ad(j,t)
-            rp.P = Bd; rp.ps = k; rp.pt = 1; rp.pd = 0; rp.pr = n;
-            rp.Q = Ad; rp.qs = 1; rp.qt = m; rp.qd = 0; rp.qr = m;
-        }
-        return rp;
-    }
 };
 
 // ---- blocks <= 32 x 32: one warp per task
@@ -1584,19 +1570,25 @@ __global__ void __launch_bounds__(64, 6) k_small32(TruncArgs targs, DDArgs dargs
 #pragma unroll
     for (int i = 0; i < 32; ++i) a[i] = 0.0;
     if (MODE == 0) {
+        double cf[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cf[i][j][0] = cf[i][j][1] = 0.0;
         for (int pi = task.pbeg; pi < task.pend; ++pi) {
             const Part p = targs.parts[pi];
             const PartRes pr = resolve_part(p, targs.slots, b, targs.B, C);
             if (pr.rank == 0) continue;
-            warp_accumulate32(a, SmallTaskIO::row_part(p, pr, true), sm);
+            warp_accumulate32_mma(cf, SmallTaskIO::row_part(p, pr, true), sm);
         }
+        warp_frags_to_cols(cf, a, sm);
     } else {
         const double* Ad = bv.a[b].dense + dt.da;
         const double* Bd = bv.b[b].dense + dt.db;
         // A zero operand (the off-diagonal dense leaves of the diagonal level-0 couplings E/F)
         // gives a zero product, whose truncation is rank 0: skip the SVD.  The staging of the
         // product sees every entry of A (m x k) and B (k x n), so it doubles as the check.
-        const int nz = warp_accumulate32(a, SmallTaskIO::dd_part(Ad, Bd, m, dt.k, n, true), sm);
+        const int nz = warp_dd32_mma(a, Ad, Bd, m, dt.k, n, sm);
         if (!__any_sync(0xffffffffu, nz & 1) || !__any_sync(0xffffffffu, nz & 2)) {
             if (lane == 0) {
                 Slot& s = dargs.slots[(size_t)dt.prod * dargs.B + b];

@@ -274,13 +274,72 @@ __device__ void warp_write32(double (&a)[32], int m, int n, int rp, double sig, 
     __syncwarp();
 }
 
-// Column-per-lane formation: M[i, j] += alpha sum_t P(i,t) Q(j,t), i in [pd, pd+pr), j in [qd, qd+qr).
-// Each 32-column chunk of P is staged through sm.T (T[t][i]) and of Q through sm.H (H[t][j]) by
-// fully unrolled predicated loads, so a lane has all of its chunk's loads in flight at once
-// (a rolled load-then-use loop waits one L2 round trip per column).  Returns, per lane,
-// whether any staged P / Q value was nonzero (nzP | 2 nzQ).  The FMA order is unchanged.
-__device__ int warp_accumulate32(double (&a)[32], const RowPart& p, Warp32Smem& sm) {
-    const int lane = threadIdx.x & 31;
+// Dense * dense formation on the FP64 tensor cores: M = Ad (m x k, ld m) * Bd (k x n, ld k),
+// m, n, k <= 32, returned column per lane (a[i] = M[i][lane]).  Ad is staged as T[t][i] and Bd
+// as H[t][j] (coalesced predicated loads, all in flight), the 4 x 4 tiles of M are accumulated
+// in DMMA fragments (mma.sync.m8n8k4.f64, 16 per k-step of 4), and the fragments are turned
+// into columns through sm.T.  Returns the zero-operand flags like warp_accumulate32.
+__device__ int warp_dd32_mma(double (&a)[32], const double* Ad, const double* Bd, int m, int k, int n, Warp32Smem& sm) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+    bool nzP = false, nzQ = false;
+    __syncwarp();
+#pragma unroll
+    for (int t8 = 0; t8 < 32; t8 += 8) {
+        double xv[8], yv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = t8 + u;
+            xv[u] = (t < k && lane < m) ? Ad[lane + (long)t * m] : 0.0;  // Ad[i = lane][t]
+            yv[u] = (t < k && lane < n) ? Bd[t + (long)lane * k] : 0.0;  // Bd[t][j = lane]
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            nzP |= xv[u] != 0.0;
+            nzQ |= yv[u] != 0.0;
+            sm.T[t8 + u][lane] = xv[u];
+            sm.H[t8 + u][lane] = yv[u];
+        }
+    }
+    __syncwarp();
+    double c[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+    for (int k0 = 0; k0 < k; k0 += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            af[i] = sm.T[k0 + t4][8 * i + g];  // A[g][t4] of row tile i
+            bf[i] = sm.H[k0 + t4][8 * i + g];  // B[t4][g] of column tile i
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma8x8x4(c[i][j][0], c[i][j][1], af[i], bf[j]);
+    }
+    __syncwarp();
+    // C[g][2 t4 + q] of tile (i, j) = M[8 i + g][8 j + 2 t4 + q] -> sm.T[col][row]
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            sm.T[8 * j + 2 * t4][8 * i + g] = c[i][j][0];
+            sm.T[8 * j + 2 * t4 + 1][8 * i + g] = c[i][j][1];
+        }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = (i < m && lane < n) ? sm.T[lane][i] : 0.0;
+    __syncwarp();
+    return (nzP ? 1 : 0) | (nzQ ? 2 : 0);
+}
+
+// Truncation-task formation on the FP64 tensor cores: M += alpha P Q^T for one part, staged
+// like warp_accumulate32 (T[t][i] = alpha P(i, t), H[t][j] = Q(j, t), zero outside the part's
+// rows / columns) and accumulated into the 4 x 4 tiles of DMMA fragments c (kept across the
+// parts of a task); warp_frags_to_cols turns them into columns once at the end.
+__device__ int warp_accumulate32_mma(double (&c)[4][4][2], const RowPart& p, Warp32Smem& sm) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
     constexpr int TC = 32;
     const int jr = lane - p.qd;
     const bool own = jr >= 0 && jr < p.qr;
@@ -290,9 +349,6 @@ __device__ int warp_accumulate32(double (&a)[32], const RowPart& p, Warp32Smem& 
     for (int t0 = 0; t0 < p.k; t0 += TC) {
         const int tn = min(TC, p.k - t0);
         __syncwarp();
-        // loads of a group are issued before any of its shared-memory stores: the compiler
-        // cannot move a global load above a store through the (generic) smem reference, so a
-        // load-store-load sequence would pay one memory round trip per column
 #pragma unroll
         for (int t8 = 0; t8 < TC; t8 += 8) {
             if (t8 < tn) {
@@ -305,26 +361,46 @@ __device__ int warp_accumulate32(double (&a)[32], const RowPart& p, Warp32Smem& 
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    if (t8 + u < tn) {
-                        nzP |= xv[u] != 0.0;
-                        nzQ |= yv[u] != 0.0;
-                        sm.T[t8 + u][lane] = xv[u];
-                        sm.H[t8 + u][lane] = yv[u];
-                    }
+                    nzP |= xv[u] != 0.0;
+                    nzQ |= yv[u] != 0.0;
+                    sm.T[t8 + u][lane] = xv[u];
+                    sm.H[t8 + u][lane] = yv[u];
                 }
             }
         }
         __syncwarp();
-        if (own) {
-            for (int t = 0; t < tn; ++t) {
-                const double q = sm.H[t][lane];
+        for (int k0 = 0; k0 < tn; k0 += 4) {
+            const bool kok = k0 + t4 < tn;
+            double af[4], bf[4];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) a[i] = fma(sm.T[t][i], q, a[i]);
+            for (int i = 0; i < 4; ++i) {
+                af[i] = kok ? sm.T[k0 + t4][8 * i + g] : 0.0;
+                bf[i] = kok ? sm.H[k0 + t4][8 * i + g] : 0.0;
             }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma8x8x4(c[i][j][0], c[i][j][1], af[i], bf[j]);
         }
     }
     __syncwarp();
     return (nzP ? 1 : 0) | (nzQ ? 2 : 0);
+}
+
+__device__ void warp_frags_to_cols(const double (&c)[4][4][2], double (&a)[32], Warp32Smem& sm) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            sm.T[8 * j + 2 * t4][8 * i + g] = c[i][j][0];
+            sm.T[8 * j + 2 * t4 + 1][8 * i + g] = c[i][j][1];
+        }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = sm.T[lane][i];
+    __syncwarp();
 }
 
 }  // namespace acrgpu

@@ -13,6 +13,15 @@ namespace acrgpu {
 
 constexpr double JEPS = 2.2204460492503131e-16;
 
+// FP64 tensor-core step D += A B, mma.sync.aligned.m8n8k4 (DMMA; tcgen05 has no f64 kind).
+// Fragment layout (checked by tools/dmma_layout.cu): lane = 4 g + t;  A (8x4): A[g][t];
+// B (4x8): B[t][g];  C/D (8x8): lane holds C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
