@@ -132,68 +132,72 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
         // apply reflector k to the remaining columns; refresh norms; warp-local pivot candidates
         double wb = -1.0;
         int wi = cols;
-        // two columns per warp iteration (j, j + NW): their reductions are independent, so
+        // RQ columns per warp iteration (j, j + NW, ...): their reductions are independent, so
         // the shuffle trees interleave; per-column arithmetic and pivot order are unchanged
-        for (int j = k + 1 + warp; j < cols; j += 2 * NW) {
-            const int j1 = j + NW;
-            const bool two = j1 < cols;
-            double* cj = A + (size_t)j * lda;
-            double* cj1 = A + (size_t)(two ? j1 : j) * lda;
-            double s = 0, s1 = 0;
+        constexpr int RQ = 4;
+        for (int j = k + 1 + warp; j < cols; j += RQ * NW) {
+            double* cq[RQ];
+            bool has[RQ];
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+                has[q] = j + q * NW < cols;
+                cq[q] = A + (size_t)(has[q] ? j + q * NW : j) * lda;
+            }
+            double sq[RQ];
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) sq[q] = 0.0;
             if (tk != 0.0) {
-#pragma unroll 4
+#pragma unroll 2
                 for (int i = k + 1 + lane; i < rows; i += 32) {
-                    s = fma(ck[i], cj[i], s);
-                    if (two) s1 = fma(ck[i], cj1[i], s1);
+                    const double v = ck[i];
+#pragma unroll
+                    for (int q = 0; q < RQ; ++q)
+                        if (has[q]) sq[q] = fma(v, cq[q][i], sq[q]);
                 }
 #pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    s += __shfl_xor_sync(0xffffffffu, s, o);
-                    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-                }
-                s = fma(s, inv, cj[k]) * tk;
-                s1 = two ? fma(s1, inv, cj1[k]) * tk : 0.0;
+                for (int o = 16; o; o >>= 1)
+#pragma unroll
+                    for (int q = 0; q < RQ; ++q) sq[q] += __shfl_xor_sync(0xffffffffu, sq[q], o);
+#pragma unroll
+                for (int q = 0; q < RQ; ++q) sq[q] = has[q] ? fma(sq[q], inv, cq[q][k]) * tk : 0.0;
             }
-            const double si = s * inv, si1 = s1 * inv;
-            double nn = 0, tl = 0, nn1 = 0, tl1 = 0;
-#pragma unroll 4
+            double nn[RQ], tl[RQ];
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) nn[q] = tl[q] = 0.0;
+#pragma unroll 2
             for (int i = k + 1 + lane; i < rows; i += 32) {
-                const double v = fma(-si, ck[i], cj[i]);
-                cj[i] = v;
-                nn = fma(v, v, nn);
-                if (i > k + 1) tl = fma(v, v, tl);
-                if (two) {
-                    const double v1 = fma(-si1, ck[i], cj1[i]);
-                    cj1[i] = v1;
-                    nn1 = fma(v1, v1, nn1);
-                    if (i > k + 1) tl1 = fma(v1, v1, tl1);
-                }
+                const double ci = ck[i];
+#pragma unroll
+                for (int q = 0; q < RQ; ++q)
+                    if (has[q]) {
+                        const double v = fma(-(sq[q] * inv), ci, cq[q][i]);
+                        cq[q][i] = v;
+                        nn[q] = fma(v, v, nn[q]);
+                        if (i > k + 1) tl[q] = fma(v, v, tl[q]);
+                    }
             }
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                nn += __shfl_xor_sync(0xffffffffu, nn, o);
-                tl += __shfl_xor_sync(0xffffffffu, tl, o);
-                nn1 += __shfl_xor_sync(0xffffffffu, nn1, o);
-                tl1 += __shfl_xor_sync(0xffffffffu, tl1, o);
-            }
-            if (lane == 0) {
-                cj[k] -= s;
-                w.nrm[j] = nn;
-                tail[j] = tl;
-                if (two) {
-                    cj1[k] -= s1;
-                    w.nrm[j1] = nn1;
-                    tail[j1] = tl1;
+            for (int o = 16; o; o >>= 1)
+#pragma unroll
+                for (int q = 0; q < RQ; ++q) {
+                    nn[q] += __shfl_xor_sync(0xffffffffu, nn[q], o);
+                    tl[q] += __shfl_xor_sync(0xffffffffu, tl[q], o);
                 }
+            if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < RQ; ++q)
+                    if (has[q]) {
+                        cq[q][k] -= sq[q];
+                        w.nrm[j + q * NW] = nn[q];
+                        tail[j + q * NW] = tl[q];
+                    }
             }
-            if (nn > wb) {
-                wb = nn;
-                wi = j;
-            }
-            if (two && nn1 > wb) {
-                wb = nn1;
-                wi = j1;
-            }
+#pragma unroll
+            for (int q = 0; q < RQ; ++q)
+                if (has[q] && nn[q] > wb) {
+                    wb = nn[q];
+                    wi = j + q * NW;
+                }
         }
         p_inv = inv;
         p_beta = beta;
