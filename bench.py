@@ -240,7 +240,7 @@ def parse_profile(text):
         p = line.split()
         if len(p) >= 5:
             rows.append({"kernel": p[0], "ms": float(p[1]), "launches": int(p[2]), "ctas": int(p[3]),
-                         "flops": float(p[4])})
+                         "flops": float(p[4]), "executed_flops": float(p[5]) if len(p) > 5 else float(p[4])})
     rows.sort(key=lambda r: -r["ms"])
     return rows
 
@@ -382,6 +382,7 @@ def run_ours(args):
         avg_ms = dom["ms"] / max(1, dom["launches"])
         fl_launch = dom["flops"] / max(1, dom["launches"])
         ach = fl_launch / (avg_ms / 1000.0) / 1e12 if avg_ms > 0 else 0.0
+        ach_exec = dom["executed_flops"] / max(1, dom["launches"]) / (avg_ms / 1000.0) / 1e12 if avg_ms > 0 else 0.0
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
@@ -391,6 +392,7 @@ def run_ours(args):
                 traffic = None
         roof = {"bound": "fp64", "kernel": dom["kernel"], "achieved": ach, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "achieved_executed": ach_exec, "frac_executed": ach_exec / FP64_PEAK_TFLOPS,
                 "share_of_step": (next(r["ms"] for r in warm_rows if r["kernel"] == dom_name) / tot_ms),
                 "share_source": "per-kernel event times of the last warm-up step (every launch timed)",
                 "peak_source": "measured FP64 DMMA mma.sync.m8n8k4 (profiles/r01_fp64_peak.txt); "

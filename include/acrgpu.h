@@ -166,8 +166,10 @@ int acrgpu_timing_get(acrgpu_fact* f, acrgpu_timing* out);
 long acrgpu_structure(int dim, const double* coords, int leaf_size, double eta, int weak,
                       int* perm, int* leaves, long cap, acrgpu_error* err);
 
-/* Per-kernel device time accumulated while ACRGPU_PROFILE=1 is set in the environment:
- * lines "kernel total_ms launches ctas".  Returns the length written (NUL-terminated). */
+/* Per-kernel device time of the launches selected by acrgpu_profile_select / ACRGPU_PROFILE:
+ * lines "kernel total_ms launches ctas nominal_flops executed_flops" (nominal = the reference
+ * algorithm's count; executed = nominal minus the part the kernel skipped: zero-operand
+ * products, the QRs the dense route replaces).  Returns the length written (NUL-terminated). */
 long acrgpu_profile_report(char* buf, long cap, int reset);
 /* Select which launches are timed (overrides ACRGPU_PROFILE): NULL / "" / "0" none, "1" / "*"
  * every kernel, else a comma-separated list of kernel names (e.g. "k_trunc_qr"). */

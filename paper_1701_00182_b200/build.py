@@ -23,8 +23,11 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    objdir = os.path.join(HERE, "build")
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str | None = None) -> str:
+    """Compile csrc/ into LIB (or `lib`, with extra -D `defines`: kernel-variant A/B builds,
+    selected at run time by ACRGPU_LIB)."""
+    objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
+    out = lib or LIB
     os.makedirs(objdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []
@@ -33,18 +36,19 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            dflags = [f"-D{d}" for d in defines]
+            cmd = [NVCC, *ARCH, *FLAGS, *dflags, "-c", s, "-o", o]
             if src.endswith(".cpp"):
-                cmd = [NVCC, *ARCH, *FLAGS, "-x", "c++", "-c", s, "-o", o]
+                cmd = [NVCC, *ARCH, *FLAGS, *dflags, "-x", "c++", "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.run(cmd, check=True)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart=static"]
+    if force or _stale(out, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-cudart=static"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -318,10 +318,13 @@ __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, Ba
                 fqr += fl_orgqr(m, ku) + fl_orgqr(n, kv);
                 fgemm += fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
             }
+            const double qr_nominal = fqr;
             fl_svd(ku, kv, fsvd, fqr, fgemm);
             add_flops(args.flops, F_SVD, fsvd);
             add_flops(args.flops, F_GEQRF, fqr);
             add_flops(args.flops, F_GEMM, fgemm);
+            // the dense route forms M (2 m n K) instead of the two QRs
+            add_flops(args.flops, F_SKIP, fmax(0.0, qr_nominal - fl_gemm(m, n, K)));
         }
         return;
     }
@@ -484,6 +487,7 @@ __global__ void __launch_bounds__(NT, 1) k_dd_product(DDArgs args, BatchViews bv
             add_flops(args.flops, F_SVD, fsvd);
             add_flops(args.flops, F_GEQRF, fqr);
             add_flops(args.flops, F_GEMM, fgemm);
+            add_flops(args.flops, F_SKIP, fsvd + fqr + fgemm);
         }
     };
     {
@@ -1499,10 +1503,13 @@ struct SmallTaskIO {
             fqr = fl_geqrf(m, K) + fl_orgqr(m, ku) + fl_geqrf(n, K) + fl_orgqr(n, kv);
             fgemm = fl_gemm(ku, kv, K) + fl_gemm(m, r, ku) + fl_gemm(n, r, kv);
         }
+        const double qr_nominal = fqr;
         fl_svd(ku, kv, fsvd, fqr, fgemm);
         add_flops(args.flops, F_SVD, fsvd);
         add_flops(args.flops, F_GEQRF, fqr);
         add_flops(args.flops, F_GEMM, fgemm);
+        // the warp engine forms M (2 m n K) instead of the two QRs
+        add_flops(args.flops, F_SKIP, fmax(0.0, qr_nominal - fl_gemm(m, n, K)));
     }
     __device__ static RowPart row_part(const Part& p, const PartRes& pr, bool tall) {
         RowPart rp;
@@ -1602,6 +1609,7 @@ __global__ void __launch_bounds__(64, 6) k_small32(TruncArgs targs, DDArgs dargs
                 add_flops(dargs.flops, F_SVD, fsvd);
                 add_flops(dargs.flops, F_GEQRF, fqr);
                 add_flops(dargs.flops, F_GEMM, fgemm);
+                add_flops(dargs.flops, F_SKIP, fsvd + fqr + fgemm);  // not executed
             }
             return;
         }
@@ -1725,6 +1733,7 @@ static FlopLedger* ledger(FlopLedger* base, const char* name) {
 }
 void set_report_ledger(FlopLedger* l) { g_report_ledger = l; }
 static std::map<std::string, double> g_flop_acc;  // folded per-kernel nominal flops
+static std::map<std::string, double> g_skip_acc;  // folded per-kernel nominal flops not executed
 // Fold the device ledgers into the host accumulators (called before every ledger reset
 // and by prof_report), so totals survive across factorizations.
 void fold_ledger() {
@@ -1735,6 +1744,7 @@ void fold_ledger() {
         double fl = 0;
         for (int c = 0; c < F_NCLASS; ++c) fl += led[id].f[c];
         g_flop_acc[g_kernel_names[id]] += fl;
+        g_skip_acc[g_kernel_names[id]] += led[id].f[F_SKIP];
     }
     cudaMemset(g_report_ledger, 0, MAX_KERNELS * sizeof(FlopLedger));
 }
@@ -1821,7 +1831,9 @@ std::string prof_report(bool reset) {
     char buf[320];
     for (auto& [k, v] : g_prof_acc) {
         const double fl = g_flop_acc.count(k) ? g_flop_acc[k] : 0.0;
-        snprintf(buf, sizeof(buf), "%s %.3f %ld %ld %.6e\n", k.c_str(), std::get<0>(v), std::get<1>(v), std::get<2>(v), fl);
+        const double sk = g_skip_acc.count(k) ? g_skip_acc[k] : 0.0;
+        snprintf(buf, sizeof(buf), "%s %.3f %ld %ld %.6e %.6e\n", k.c_str(), std::get<0>(v), std::get<1>(v), std::get<2>(v), fl,
+                 fl - sk);
         out += buf;
     }
     {
@@ -1865,6 +1877,7 @@ std::string prof_report(bool reset) {
     if (reset) {
         g_prof_acc.clear();
         g_flop_acc.clear();
+        g_skip_acc.clear();
         g_top.clear();
     }
     return out;

@@ -134,7 +134,10 @@ __device__ int cta_rrqr(const CtaSvdWork& w, int rows, int cols, double delta2) 
         int wi = cols;
         // RQ columns per warp iteration (j, j + NW, ...): their reductions are independent, so
         // the shuffle trees interleave; per-column arithmetic and pivot order are unchanged
-        constexpr int RQ = 4;
+#ifndef ACRGPU_RRQR_Q
+#define ACRGPU_RRQR_Q 4
+#endif
+        constexpr int RQ = ACRGPU_RRQR_Q;
         for (int j = k + 1 + warp; j < cols; j += RQ * NW) {
             double* cq[RQ];
             bool has[RQ];

@@ -143,9 +143,13 @@ struct DevError {
 };
 
 // Nominal FLOP ledger (SURVEY §8(d) formulas; same as oracle/acr_oracle.cpp).
-enum FlopClass : int { F_GEMM = 0, F_GEQRF, F_ORGQR, F_SVD, F_LU, F_APPLY, F_NCLASS };
+// Nominal FLOPs of the reference algorithm by class (SURVEY §8(d) formulas), plus F_SKIP: the
+// part of the nominal count a kernel did not execute (zero-operand products detected on the
+// device; the two QRs the dense route replaces by forming M, net of that formation GEMM).
+// executed = nominal - F_SKIP.
+enum FlopClass : int { F_GEMM = 0, F_GEQRF, F_ORGQR, F_SVD, F_LU, F_APPLY, F_NCLASS, F_SKIP = F_NCLASS };
 struct FlopLedger {
-    double f[F_NCLASS];
+    double f[F_NCLASS + 1];
 };
 
 // Solve: batched H-matvec  y = base - H x  (or y = H x when base == nullptr).
