@@ -36,6 +36,9 @@ import sys
 import threading
 import time
 
+# libacrgpu uses 16 streams (4 lanes x 4); must be set before the CUDA context exists
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -23,6 +23,8 @@ import os
 
 import numpy as np
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # libacrgpu's 16 streams; read at context creation
+
 from . import problems
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

@@ -75,7 +75,16 @@ static T* upload(const std::vector<T>& v, cudaStream_t st) {
 // Two execution lanes (stream + transient arena + product slots): independent
 // mult_adds of one recursion step (T12 || T21, C12 || C21 in invert_node; the
 // E'/F' couplings beside the D updates) run concurrently on the GPU.
-constexpr int NLANES = 2;
+// 4 lanes x (1 + NSUB) streams: more hardware work queues than the default 8, or streams
+// of different lanes share a queue and serialise (read when the CUDA context is created;
+// an explicit setting of the caller's wins).
+static const int g_max_connections_set = setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+
+constexpr int NLANES = 4;
+// Lanes come in groups of two.  Group 0 (lanes 0, 1; high-priority streams) runs the
+// latency-bound invert_node chain of a level; group 1 (lanes 2, 3; low priority) runs the
+// throughput-bound Schur updates the next level's chain does not depend on (do_factor).
+constexpr int NGROUPS = NLANES / 2;
 // Inside one mult_add the launches of independent task lists (apply vs dense*dense products,
 // the size classes of one truncation phase, dense deposits vs the Rk flush) fork onto NSUB
 // side streams of the lane and join back before the next dependent phase.
@@ -98,6 +107,11 @@ struct Ctx {
     cudaStream_t st = nullptr;  // == lanes[0].st (main stream)
     Lane lanes[NLANES];
     int cur = 0;                // active lane
+    int base = 0;               // first lane of the active group (pair() uses base, base + 1)
+    int carved = 0;             // lanes the transient arena is currently split into
+    size_t trans_doubles = 0;   // whole transient arena
+    cudaEvent_t group_ev[NGROUPS][2] = {};
+    cudaEvent_t aux_ev = nullptr;
     Arena persist{};
     double* persist_sp[2] = {nullptr, nullptr};  // two semi-spaces of persist_half doubles each
     size_t persist_half = 0;
@@ -118,15 +132,22 @@ struct Ctx {
     void init(int dev) {
         if (dev >= 0) CK(cudaSetDevice(dev));
         CK(cudaGetDevice(&device));
-        for (auto& l : lanes) {
-            CK(cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking));
+        int prio_lo = 0, prio_hi = 0;  // numerically lowest = greatest priority
+        CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        for (int li = 0; li < NLANES; ++li) {
+            Lane& l = lanes[li];
+            const int prio = li < 2 ? prio_hi : prio_lo;
+            CK(cudaStreamCreateWithPriority(&l.st, cudaStreamNonBlocking, prio));
             CK(cudaEventCreateWithFlags(&l.ev, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&l.fork_ev, cudaEventDisableTiming));
             for (int i = 0; i < NSUB; ++i) {
-                CK(cudaStreamCreateWithFlags(&l.sub[i], cudaStreamNonBlocking));
+                CK(cudaStreamCreateWithPriority(&l.sub[i], cudaStreamNonBlocking, prio));
                 CK(cudaEventCreateWithFlags(&l.join_ev[i], cudaEventDisableTiming));
             }
         }
+        for (auto& g : group_ev)
+            for (auto& e : g) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&aux_ev, cudaEventDisableTiming));
         st = lanes[0].st;
         setup_kernels();
         size_t freeb = 0, total = 0;
@@ -142,11 +163,12 @@ struct Ctx {
             return (f > 0.0 && f < 0.9) ? f : dflt;
         };
         const size_t pbytes = ((size_t)(freeb * frac("ACRGPU_PERSIST_FRAC", 0.50)) / 2) & ~(size_t)4095;
-        const size_t tbytes = ((size_t)(freeb * frac("ACRGPU_TRANS_FRAC", 0.22)) / NLANES) & ~(size_t)4095;
+        const size_t tbytes = ((size_t)(freeb * frac("ACRGPU_TRANS_FRAC", 0.22))) & ~(size_t)4095;
         persist_half = pbytes / 8;
         persist_sp[0] = dmalloc<double>(persist_half);
         persist_sp[1] = dmalloc<double>(persist_half);
-        trans_base = dmalloc<double>(NLANES * tbytes / 8);
+        trans_doubles = tbytes / 8;
+        trans_base = dmalloc<double>(trans_doubles);
         ctrs = dmalloc<unsigned long long>(1 + NLANES);
         CK(cudaMallocHost(&h_zero, sizeof(unsigned long long)));
         *h_zero = 0;
@@ -156,9 +178,31 @@ struct Ctx {
         set_report_ledger(flops);
         space = 0;
         persist = Arena{persist_sp[0], persist_half, ctrs, overflow};
-        for (int l = 0; l < NLANES; ++l)
-            lanes[l].trans = Arena{trans_base + (size_t)l * (tbytes / 8), tbytes / 8, ctrs + 1 + l, overflow + 1 + l};
+        carve(NLANES);
         reset_all();
+    }
+    // Split the transient arena over the first nl lanes (the others get nothing).  Planes up
+    // to C2 size use all four lanes (pipelined levels); C5-sized planes run both groups'
+    // work on lanes 0, 1 with twice the arena each.  Only between factorizations.
+    void carve(int nl) {
+        if (nl == carved) return;
+        for (auto& l : lanes) CK(cudaStreamSynchronize(l.st));
+        const size_t per = (trans_doubles / nl) & ~(size_t)511;
+        for (int l = 0; l < NLANES; ++l)
+            lanes[l].trans = Arena{trans_base + (size_t)(l < nl ? l : 0) * per, l < nl ? per : 0, ctrs + 1 + l, overflow + 1 + l};
+        carved = nl;
+    }
+    // select the lane group the following operations are issued on
+    void set_group(int g) {
+        base = 2 * g;
+        cur = base;
+    }
+    // group `to` (both lanes) waits for everything issued so far on group `from`
+    void group_depend(int to, int from) {
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventRecord(group_ev[from][i], lanes[2 * from + i].st));
+            for (int j = 0; j < 2; ++j) CK(cudaStreamWaitEvent(lanes[2 * to + j].st, group_ev[from][i], 0));
+        }
     }
     Lane& lane() { return lanes[cur]; }
     // stream-ordered reset of a device arena counter through the copy engine (a one-thread
@@ -209,6 +253,7 @@ struct Ctx {
         call_id = 0;
         call_planes.clear();
         cur = 0;
+        base = 0;
     }
     // semi-space `i`, allocated again if a factorization took it over (take_space)
     double* space_ptr(int i) {
@@ -265,6 +310,13 @@ struct Ctx {
             if (l.st) cudaStreamDestroy(l.st);
             l = Lane{};
         }
+        for (auto& g : group_ev)
+            for (auto& e : g) {
+                if (e) cudaEventDestroy(e);
+                e = nullptr;
+            }
+        if (aux_ev) cudaEventDestroy(aux_ev);
+        aux_ev = nullptr;
         st = nullptr;
     }
 };
@@ -1094,21 +1146,42 @@ struct Engine {
     // after everything already queued on lane 0; lane 0 continues after both).
     template <class F0, class F1>
     void pair(F0&& f0, F1&& f1) {
-        if (NLANES < 2 || ctx->cur != 0) {
+        const int b = ctx->base;
+        if (ctx->cur != b) {
             f0();
             f1();
             return;
         }
-        ctx->depend(1, 0);
+        ctx->depend(b + 1, b);
         f0();
-        ctx->cur = 1;
+        ctx->cur = b + 1;
         f1();
-        ctx->cur = 0;
-        ctx->depend(0, 1);
+        ctx->cur = b;
+        ctx->depend(b, b + 1);
     }
 
     // out = inverse(in) (reference invert_node, hmatrix.cpp:483-534); out views pre-allocated
+    // ACRGPU_TIME_INVERT=1 (diagnostic, synchronises): inclusive wall time of the invert_node
+    // recursion per node size, printed per level under ACRGPU_VERBOSE.
+    std::map<int, std::pair<double, int>> invert_time;  // rows -> (ms, calls)
+    static bool time_invert() {
+        static const bool v = getenv("ACRGPU_TIME_INVERT") != nullptr;
+        return v;
+    }
     void invert(const std::vector<View>& out, const std::vector<View>& in, int level, const std::vector<int>& planes) {
+        if (!time_invert()) {
+            invert_impl(out, in, level, planes);
+            return;
+        }
+        for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.st));
+        const auto t0 = std::chrono::steady_clock::now();
+        invert_impl(out, in, level, planes);
+        for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.st));
+        auto& rec = invert_time[S.node(in[0].node).rows()];
+        rec.first += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        rec.second += 1;
+    }
+    void invert_impl(const std::vector<View>& out, const std::vector<View>& in, int level, const std::vector<int>& planes) {
         const int node = in[0].node;
         const SNode& n = S.node(node);
         if (n.kind == K_DENSE) {
@@ -1580,8 +1653,13 @@ static void check_device_errors(acrgpu_fact* F) {
     CK(cudaGetLastError());
     DevError de;
     CK(cudaMemcpy(&de, C.err, sizeof(de), cudaMemcpyDeviceToHost));
-    int ovf[2];
-    CK(cudaMemcpy(ovf, C.overflow, sizeof(ovf), cudaMemcpyDeviceToHost));
+    int ovf[2] = {0, 0};
+    {
+        int all[1 + NLANES];
+        CK(cudaMemcpy(all, C.overflow, sizeof(all), cudaMemcpyDeviceToHost));
+        ovf[0] = all[0];
+        for (int l = 0; l < NLANES; ++l) ovf[1] |= all[1 + l];
+    }
     if (de.key != ~0ull) {
         const unsigned long long cid = de.key >> 16;
         const int b = (int)(de.key & 0xffff);
@@ -1743,6 +1821,13 @@ static void mark_level(PartRun& R) {
                 R.rank, R.lev_ev.size(), used * 8.0 / 1e9, E.ctx->persist.cap * 8.0 / 1e9, E.peak_transient_gb, fr / 1e9);
     }
     if (!verbose_levels()) return;
+    if (Engine::time_invert()) {
+        Engine& E = *R.F->eng;
+        fprintf(stderr, "[acrgpu] invert_node inclusive ms (rows: ms calls) before mark %zu:", R.lev_ev.size());
+        for (auto& [rows, rec] : E.invert_time) fprintf(stderr, " %d: %.2f %d |", rows, rec.first, rec.second);
+        fprintf(stderr, "\n");
+        E.invert_time.clear();
+    }
     static const bool per_level_kernels = getenv("ACRGPU_PROFILE") != nullptr;
     if (per_level_kernels) {  // kernel totals since the previous mark (synchronises)
         const std::string rep = prof_report(true);
@@ -1788,85 +1873,169 @@ static Level level_invert(PartRun& R, int lvl, const std::vector<char>& mine_pos
 // (eliminate_around, acr.hpp:78-107), then the stored inverses trimmed to full
 // tolerance (acr.cpp:116-118).  Eliminated neighbours owned elsewhere must already
 // be present in L (received).
-static void level_update(PartRun& R, Level& L, const std::vector<char>& mine_pos) {
+//
+// The update is split in two parts so that the single-GPU driver can pipeline levels:
+// part 1 updates the diagonal blocks of the retained planes in `first` (the planes the
+// NEXT level eliminates: its invert_node chain needs nothing else), part 2 does the rest
+// (the other diagonal blocks, every new coupling block, recompression of this level's
+// stored inverses).  Per-plane arithmetic does not depend on the batch composition, so
+// any split gives bitwise the results of the one-pass update.
+struct LevelUpdate {
+    int mn = 0;
+    std::vector<SP> Dn, En, Fn;
+    std::vector<int> keepE, keepF;  // retained indices whose coupling is carried over unchanged
+    struct Side {
+        std::vector<int> t;              // retained index of each entry
+        std::vector<SP> Ts;
+        std::vector<View> Tv, Cpl, Dnb;  // T = Cpl * Dnb
+        std::vector<View> dc, db;        // D -= T * x   (null store: no such product)
+        std::vector<View> nc, nb;        // new coupling = -T * y
+        std::vector<char> has_d, has_n;
+    } side[2];
+};
+
+// allocate every output / temporary store of the level's update (on the main stream)
+static LevelUpdate update_begin(PartRun& R, Level& L, const std::vector<char>& mine_pos) {
     Engine& E = *R.F->eng;
     const int m = L.plane_count;
     std::vector<char> is_elim(m, 0);
     for (int e : L.elim) is_elim[e] = 1;
-    const int mn = (int)L.ret.size();
-    std::vector<SP> Dn(mn), En(mn), Fn(mn);
+    LevelUpdate U;
+    const int mn = U.mn = (int)L.ret.size();
+    U.Dn.assign(mn, nullptr);
+    U.En.assign(mn, nullptr);
+    U.Fn.assign(mn, nullptr);
     for (int t = 0; t < mn; ++t)
-        if (mine_pos[L.ret[t]]) Dn[t] = R.D[L.ret[t]];
+        if (mine_pos[L.ret[t]]) U.Dn[t] = R.D[L.ret[t]];
     auto at = [&](const std::vector<SP>& v, int j) -> SP { return (j < 0 || j >= (int)v.size()) ? nullptr : v[j]; };
     // Per side (lo: eliminated j-1, hi: eliminated j+1) three batched mult_adds:
     //   T = E_j Dinv_{j-1};  D_j -= T F_{j-1};  E' = -T E_{j-1}      (mirrored for hi).
-    // Schedule over the two lanes: T_lo || T_hi, then {D_lo; D_hi} on lane 0 (same D_j,
-    // reference order lo then hi) || {E'; F'} on lane 1.
-    struct SideOps {
-        std::vector<SP> Ts;
-        std::vector<View> Tv, Cpl, Dnb;  // T = Cpl * Dnb
-        std::vector<View> dc, da, db;    // D -= T * x
-        std::vector<View> nc, na, nb;    // new coupling = -T * y
-    } ops[2];
-    for (int side = 0; side < 2; ++side) {
-        SideOps& o = ops[side];
+    for (int sd = 0; sd < 2; ++sd) {
+        LevelUpdate::Side& o = U.side[sd];
         for (int t = 0; t < mn; ++t) {
             const int j = L.ret[t];
             if (!mine_pos[j]) continue;
-            const int nbp = side == 0 ? j - 1 : j + 1;
+            const int nbp = sd == 0 ? j - 1 : j + 1;
             if (!(nbp >= 0 && nbp < m && is_elim[nbp])) continue;
             if (!L.Dinv[nbp]) throw AcrError{ACRGPU_E_INTERNAL, "missing eliminated neighbour"};
+            o.t.push_back(t);
             o.Ts.push_back(E.new_store(0));
             const View T = root_view(o.Ts.back());
             o.Tv.push_back(T);
-            SP cpl = side == 0 ? at(L.E, j) : at(L.F, j);
+            SP cpl = sd == 0 ? at(L.E, j) : at(L.F, j);
             if (!cpl) throw AcrError{ACRGPU_E_INTERNAL, "missing coupling block"};
             o.Cpl.push_back(root_view(cpl));
             o.Dnb.push_back(root_view(L.Dinv[nbp]));
-            if (SP x = side == 0 ? at(L.F, nbp) : at(L.E, nbp)) {
-                o.dc.push_back(root_view(Dn[t]));
-                o.da.push_back(T);
-                o.db.push_back(root_view(x));
+            SP x = sd == 0 ? at(L.F, nbp) : at(L.E, nbp);
+            o.has_d.push_back(x ? 1 : 0);
+            o.dc.push_back(root_view(U.Dn[t]));
+            o.db.push_back(root_view(x));
+            SP y = sd == 0 ? at(L.E, nbp) : at(L.F, nbp);
+            o.has_n.push_back(y ? 1 : 0);
+            SP nw = nullptr;
+            if (y) {
+                nw = E.new_store(0);
+                (sd == 0 ? U.En : U.Fn)[t] = nw;
             }
-            if (SP y = side == 0 ? at(L.E, nbp) : at(L.F, nbp)) {
-                SP nw = E.new_store(0);
-                (side == 0 ? En : Fn)[t] = nw;
-                o.nc.push_back(root_view(nw));
-                o.na.push_back(T);
-                o.nb.push_back(root_view(y));
-            }
+            o.nc.push_back(root_view(nw));
+            o.nb.push_back(root_view(y));
         }
-        E.zero(o.Tv);
-        E.zero(o.nc);
     }
-    E.pair([&] { E.mult_add(ops[0].Tv, ops[0].Cpl, ops[0].Dnb, 1.0); },
-           [&] { E.mult_add(ops[1].Tv, ops[1].Cpl, ops[1].Dnb, 1.0); });
-    E.ctx->depend(0, 1);  // both T batches visible to both lanes
-    E.pair(
-        [&] {
-            E.mult_add(ops[0].dc, ops[0].da, ops[0].db, -1.0);
-            E.mult_add(ops[1].dc, ops[1].da, ops[1].db, -1.0);
-        },
-        [&] {
-            E.mult_add(ops[0].nc, ops[0].na, ops[0].nb, -1.0);
-            E.mult_add(ops[1].nc, ops[1].na, ops[1].nb, -1.0);
-        });
-    // adjacent retained planes keep their coupling (acr.cpp:104-111)
+    // adjacent retained planes keep their coupling (acr.cpp:104-111): copies made in update_finish
     for (int t = 0; t < mn; ++t) {
         const int j = L.ret[t];
         if (!mine_pos[j]) continue;
-        if (!En[t] && t > 0 && L.ret[t - 1] == j - 1 && at(L.E, j)) {
-            En[t] = E.new_store(0);
-            E.copy({root_view(En[t])}, {root_view(L.E[j])});
+        if (!U.En[t] && t > 0 && L.ret[t - 1] == j - 1 && at(L.E, j)) {
+            U.En[t] = E.new_store(0);
+            U.keepE.push_back(t);
         }
-        if (!Fn[t] && t + 1 < mn && L.ret[t + 1] == j + 1 && at(L.F, j)) {
-            Fn[t] = E.new_store(0);
-            E.copy({root_view(Fn[t])}, {root_view(L.F[j])});
+        if (!U.Fn[t] && t + 1 < mn && L.ret[t + 1] == j + 1 && at(L.F, j)) {
+            U.Fn[t] = E.new_store(0);
+            U.keepF.push_back(t);
         }
     }
-    R.D = std::move(Dn);
-    R.Ev = std::move(En);
-    R.Fv = std::move(Fn);
+    return U;
+}
+
+// Pieces of the update on the active lane group, over the retained planes t with
+// sel[t] == which (couplings: optionally of every plane).
+struct UpdOps {
+    std::vector<View> c, a, b;
+};
+// T = E_j Dinv_{j-1} (lo) || T = F_j Dinv_{j+1} (hi) on the two lanes of the group
+static void update_T(PartRun& R, LevelUpdate& U, const std::vector<char>& sel, char which) {
+    Engine& E = *R.F->eng;
+    UpdOps ops[2];
+    for (int sd = 0; sd < 2; ++sd) {
+        const LevelUpdate::Side& o = U.side[sd];
+        for (size_t i = 0; i < o.t.size(); ++i)
+            if (sel[o.t[i]] == which) {
+                ops[sd].c.push_back(o.Tv[i]);
+                ops[sd].a.push_back(o.Cpl[i]);
+                ops[sd].b.push_back(o.Dnb[i]);
+            }
+        E.zero(ops[sd].c);
+    }
+    E.pair([&] { E.mult_add(ops[0].c, ops[0].a, ops[0].b, 1.0); }, [&] { E.mult_add(ops[1].c, ops[1].a, ops[1].b, 1.0); });
+    E.ctx->depend(E.ctx->base + 1, E.ctx->base);  // both T batches visible to both lanes (pair: base waited already)
+}
+// selected operand lists: D_j -= T x (diag) or new coupling = -T y
+static void update_ops(const LevelUpdate& U, const std::vector<char>& sel, char which, bool all, bool diag, UpdOps (&ops)[2]) {
+    for (int sd = 0; sd < 2; ++sd) {
+        const LevelUpdate::Side& o = U.side[sd];
+        for (size_t i = 0; i < o.t.size(); ++i) {
+            if (!(all || sel[o.t[i]] == which)) continue;
+            if (!(diag ? o.has_d[i] : o.has_n[i])) continue;
+            ops[sd].c.push_back(diag ? o.dc[i] : o.nc[i]);
+            ops[sd].a.push_back(o.Tv[i]);
+            ops[sd].b.push_back(diag ? o.db[i] : o.nb[i]);
+        }
+    }
+}
+// {D_lo; D_hi} (same D_j: reference order lo then hi) || {E'; F'} on the two lanes
+static void update_DN(PartRun& R, LevelUpdate& U, const std::vector<char>& sel, char which, bool couplings_of_all) {
+    Engine& E = *R.F->eng;
+    UpdOps d[2], n[2];
+    update_ops(U, sel, which, false, true, d);
+    update_ops(U, sel, which, couplings_of_all, false, n);
+    E.zero(n[0].c);
+    E.zero(n[1].c);
+    E.pair(
+        [&] {
+            E.mult_add(d[0].c, d[0].a, d[0].b, -1.0);
+            E.mult_add(d[1].c, d[1].a, d[1].b, -1.0);
+        },
+        [&] {
+            E.mult_add(n[0].c, n[0].a, n[0].b, -1.0);
+            E.mult_add(n[1].c, n[1].a, n[1].b, -1.0);
+        });
+}
+// diagonal updates only, the selected planes split in two halves over the two lanes
+static void update_D_split(PartRun& R, LevelUpdate& U, const std::vector<char>& sel, char which) {
+    Engine& E = *R.F->eng;
+    std::vector<int> ts;
+    for (int t = 0; t < U.mn; ++t)
+        if (sel[t] == which) ts.push_back(t);
+    std::vector<char> half[2] = {std::vector<char>(U.mn, 0), std::vector<char>(U.mn, 0)};
+    for (size_t i = 0; i < ts.size(); ++i) half[i < (ts.size() + 1) / 2 ? 0 : 1][ts[i]] = 1;
+    UpdOps d[2][2];
+    update_ops(U, half[0], 1, false, true, d[0]);
+    update_ops(U, half[1], 1, false, true, d[1]);
+    auto run = [&](UpdOps (&q)[2]) {
+        E.mult_add(q[0].c, q[0].a, q[0].b, -1.0);
+        E.mult_add(q[1].c, q[1].a, q[1].b, -1.0);
+    };
+    E.pair([&] { run(d[0]); }, [&] { run(d[1]); });
+}
+
+// copies of kept couplings, hand-over of the new level's blocks, recompression
+static void update_finish(PartRun& R, Level& L, LevelUpdate& U, const std::vector<char>& mine_pos) {
+    Engine& E = *R.F->eng;
+    for (int t : U.keepE) E.copy({root_view(U.En[t])}, {root_view(L.E[L.ret[t]])});
+    for (int t : U.keepF) E.copy({root_view(U.Fn[t])}, {root_view(L.F[L.ret[t]])});
+    R.D = std::move(U.Dn);
+    R.Ev = std::move(U.En);
+    R.Fv = std::move(U.Fn);
     {
         std::vector<View> dv;
         for (int e : L.elim)
@@ -1882,8 +2051,16 @@ static void level_update(PartRun& R, Level& L, const std::vector<char>& mine_pos
         }
 }
 
+static void level_update(PartRun& R, Level& L, const std::vector<char>& mine_pos) {
+    LevelUpdate U = update_begin(R, L, mine_pos);
+    const std::vector<char> sel(U.mn, 1);
+    update_T(R, U, sel, 1);
+    update_DN(R, U, sel, 1, false);
+    update_finish(R, L, U, mine_pos);
+}
+
 // factor_apex (acr.cpp:123-144): block Thomas over the remaining planes.
-static void factor_apex(PartRun& R, int lvl) {
+static void factor_apex(PartRun& R, int lvl, const std::function<void()>& after_first = nullptr) {
     acrgpu_fact* F = R.F;
     Engine& E = *F->eng;
     E.level_tag = lvl;
@@ -1901,6 +2078,7 @@ static void factor_apex(PartRun& R, int lvl) {
         SP out = E.new_store(0);
         E.invert({root_view(out)}, {root_view(Di)}, lvl, {i});
         F->apexDinv.push_back(out);
+        if (i == 0 && after_first) after_first();
     }
     E.recompress(views(F->apexDinv));
 }
@@ -1986,15 +2164,95 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
     const int stop = F->eng->cfg.stop_planes;
     int lvl = 0;
     mark_level(R);
-    while ((int)R.D.size() > stop) {
-        const std::vector<char> all(R.D.size(), 1);
-        Level L = level_invert(R, lvl, all);
-        level_update(R, L, all);
-        F->levels.push_back(std::move(L));
-        mark_level(R);
-        ++lvl;
+    Engine& E = *F->eng;
+    Ctx& C = *E.ctx;
+    // C5-sized planes keep both lane groups' work on lanes 0, 1 (twice the transient arena
+    // per lane; the persistent-arena compaction drains them at its safe points).
+    static const bool no_pipe = getenv("ACRGPU_NO_PIPELINE") != nullptr;
+    const bool pipelined = !no_pipe && E.S.dim <= 4096 && C.factoring == 1 && !E.gc_enabled();
+    if (C.factoring == 1) C.carve(E.S.dim <= 4096 ? NLANES : 2);
+    if (!pipelined) {
+        while ((int)R.D.size() > stop) {
+            const std::vector<char> all(R.D.size(), 1);
+            Level L = level_invert(R, lvl, all);
+            level_update(R, L, all);
+            F->levels.push_back(std::move(L));
+            mark_level(R);
+            ++lvl;
+        }
+        factor_apex(R, lvl);
+    } else {
+        // Pipelined levels.  The invert_node chain of a level is ~10^3 dependent small
+        // launches whatever the plane count (latency-bound), while the Schur updates are few
+        // large launches.  The chain of level l+1 needs only the updated diagonal blocks of
+        // the planes it eliminates, so each level's update is split: part 1 (those diagonal
+        // blocks) runs on group 0 right after the chain; part 2 (the other diagonal blocks,
+        // every new coupling block, the recompression of the stored inverses) runs on the
+        // low-priority group 1 while group 0 already runs the next level's chain.
+        std::vector<SP> hold;  // part-2 temporaries, kept until group 0 has joined group 1
+        // ACRGPU_VERBOSE timeline: (label, event) pairs printed relative to the factor start
+        std::vector<std::pair<std::string, cudaEvent_t>> tl;
+        auto stamp = [&](const std::string& what, cudaStream_t st) {
+            if (!verbose_levels()) return;
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            CK(cudaEventRecord(e, st));
+            tl.push_back({what, e});
+        };
+        bool pending = false;
+        auto join = [&] {
+            if (pending) C.group_depend(0, 1);
+            pending = false;
+            hold.clear();
+        };
+        while ((int)R.D.size() > stop) {
+            const std::vector<char> all(R.D.size(), 1);
+            C.set_group(0);
+            Level L = level_invert(R, lvl, all);  // needs only part 1 of the previous level
+            stamp("chain" + std::to_string(lvl), C.lanes[0].st);
+            join();
+            LevelUpdate U = update_begin(R, L, all);
+            // planes the next step inverts first: the next level's eliminated positions, or
+            // plane 0 of the apex
+            std::vector<char> first(U.mn, 0);
+            if (U.mn > stop) {
+                for (int e : eliminated_positions(U.mn)) first[e] = 1;
+            } else if (U.mn > 0) {
+                first[0] = 1;
+            }
+            C.group_depend(1, 0);  // group 1 starts once the chain (and the allocations) are done
+            update_T(R, U, first, 1);
+            CK(cudaEventRecord(C.aux_ev, C.lanes[0].st));  // T of the `first` planes
+            update_D_split(R, U, first, 1);
+            stamp("part1_" + std::to_string(lvl), C.lanes[0].st);
+            C.set_group(1);
+            update_T(R, U, first, 0);
+            for (int i = 0; i < 2; ++i) CK(cudaStreamWaitEvent(C.lanes[2 + i].st, C.aux_ev, 0));
+            update_DN(R, U, first, 0, true);
+            for (auto& sd : U.side)
+                for (auto& t : sd.Ts) hold.push_back(t);
+            update_finish(R, L, U, all);
+            stamp("part2_" + std::to_string(lvl), C.lanes[2].st);
+            pending = true;
+            C.set_group(0);
+            F->levels.push_back(std::move(L));
+            mark_level(R);
+            ++lvl;
+        }
+        factor_apex(R, lvl, join);
+        join();
+        if (!tl.empty()) {
+            CK(cudaDeviceSynchronize());
+            fprintf(stderr, "[acrgpu] pipeline timeline (ms since start):");
+            for (auto& [what, e] : tl) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, R.e0, e);
+                fprintf(stderr, " %s %.0f |", what.c_str(), ms);
+                cudaEventDestroy(e);
+            }
+            fprintf(stderr, "\n");
+        }
     }
-    factor_apex(R, lvl);
     F->timing_host_enqueue_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - R.host_t0).count();
     factor_finish(R);
 }
