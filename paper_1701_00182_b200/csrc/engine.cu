@@ -379,7 +379,7 @@ struct Plan {
 // their device uploads).  Keyed by the structure's parameters and a hash of the coordinates.
 struct PlanCache {
     std::string key;
-    std::map<std::tuple<int, int, int, int>, std::unique_ptr<Plan>> plans;
+    std::map<std::tuple<int, int, int, int, int>, std::unique_ptr<Plan>> plans;
     std::vector<void*> dev;  // device arrays of the plans
     ~PlanCache() {
         for (void* p : dev) cudaFree(p);
@@ -805,12 +805,46 @@ struct Engine {
         deposit(pb, c, p, croot);
     }
 
-    Plan* plan(int c, int a, int b, double alpha) {
-        const auto key = std::make_tuple(c, a, b, alpha > 0 ? 1 : -1);
+    // mult_rec restricted to the target block (I, J) at `depth` levels below (c, a, b): the
+    // products A_(I,K) B_(K,J) in the order the full recursion emits them for that block, so
+    // every target leaf sees the same part list as in the unsplit plan.
+    void mult_rec_block(PlanBuild& pb, int c, int a, int b, double alpha, int croot, int aroot, int broot, int depth,
+                        int I, int J) {
+        if (depth == 0) {
+            mult_rec(pb, c, a, b, alpha, croot, aroot, broot);
+            return;
+        }
+        const SNode& Cn = S.node(c);
+        const SNode& A = S.node(a);
+        const SNode& Bn = S.node(b);
+        const int i = (I >> (depth - 1)) & 1, j = (J >> (depth - 1)) & 1;
+        for (int k = 0; k < 2; ++k)
+            mult_rec_block(pb, Cn.ch[i * 2 + j], A.ch[i * 2 + k], Bn.ch[k * 2 + j], alpha, croot, aroot, broot, depth - 1, I,
+                           J);
+    }
+    // levels (<= 2) for which (c, a, b) and all their descendants are branch nodes
+    int split_depth(int c, int a, int b, int want) const {
+        if (want == 0) return 0;
+        const SNode& Cn = S.node(c);
+        const SNode& A = S.node(a);
+        const SNode& Bn = S.node(b);
+        if (Cn.kind != K_BRANCH || A.kind != K_BRANCH || Bn.kind != K_BRANCH) return 0;
+        int d = want - 1;
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j)
+                for (int k = 0; k < 2; ++k)
+                    d = std::min(d, split_depth(Cn.ch[i * 2 + j], A.ch[i * 2 + k], Bn.ch[k * 2 + j], want - 1));
+        return 1 + d;
+    }
+
+    // depth > 0: the plan of target block (I, J) only (task ids stay relative to the roots
+    // c, a, b, so it runs on the same batch views as the whole plan)
+    Plan* plan(int c, int a, int b, double alpha, int depth = 0, int I = 0, int J = 0) {
+        const auto key = std::make_tuple(c, a, b, alpha > 0 ? 1 : -1, depth * 256 + I * 16 + J);
         auto it = pc->plans.find(key);
         if (it != pc->plans.end()) return it->second.get();
         PlanBuild pb;
-        mult_rec(pb, c, a, b, alpha, c, a, b);
+        mult_rec_block(pb, c, a, b, alpha, c, a, b, depth, I, J);
         const SNode& CR = S.node(c);
         for (auto& [leaf, list] : pb.rk_t) {
             const SNode& L = S.node(S.k_node[leaf]);
@@ -869,7 +903,26 @@ struct Engine {
         if (C.empty()) return;
         const double eps = cfg.eps * 0.5;  // arithmetic tolerance, acr.hpp:178-181
         gc_check();
-        Plan* P = plan(C[0].node, A[0].node, B[0].node, alpha);
+        // C5-sized planes: a root product keeps ~7 GB of products per plane alive until its
+        // flush, so only one plane fits a batch and the top agglomeration phases run a
+        // handful of CTAs.  The root plan is split into its 4 x 4 target blocks (each with all
+        // of its A_(I,K) B_(K,J) terms: identical part lists per target leaf, identical
+        // arithmetic), run one after the other with ~16x more planes per batch.
+        // ACRGPU_NO_SPLIT / ACRGPU_FORCE_SPLIT (any plane size): A/B switch and test hook
+        const bool no_split = getenv("ACRGPU_NO_SPLIT") != nullptr;
+        const bool force_split = getenv("ACRGPU_FORCE_SPLIT") != nullptr;
+        int depth = 0;
+        // (measured at C5: level 0, 32 planes per product, 16.6 -> 14.7 s; from 8 planes per
+        // product down the 16 sequential block products cost more than the larger batches
+        // gain -- the kernels are bound by their per-task rate, not by the CTA count)
+        if (((S.dim > 4096 && C.size() >= 24) || force_split) && !no_split && S.node(C[0].node).rows() == S.dim)
+            depth = split_depth(C[0].node, A[0].node, B[0].node, 2);
+        const int nblk = 1 << depth;
+        for (int I = 0; I < nblk; ++I)
+            for (int J = 0; J < nblk; ++J) mult_add_plan(plan(C[0].node, A[0].node, B[0].node, alpha, depth, I, J), C, A, B);
+    }
+    void mult_add_plan(Plan* P, const std::vector<View>& C, const std::vector<View>& A, const std::vector<View>& B) {
+        const double eps = cfg.eps * 0.5;  // arithmetic tolerance, acr.hpp:178-181
         // Planes per batch.  Up to C2-sized planes (dim <= 4096) the transient arena holds
         // MAXB planes (8.9 GB peak measured at C2).  Larger planes (C5: 16384) size the batch
         // from the plan's measured transient use per plane: the first batch of a plan at each
@@ -1192,7 +1245,7 @@ struct Engine {
             t.re = n.re;
             if (n.rows() != n.cols() || n.rows() > DENSE_MAX)
                 throw AcrError{ACRGPU_E_USAGE, "GPU path: dense diagonal leaf larger than 64"};
-            auto key = std::make_tuple(node, -1000, -1000, 0);
+            auto key = std::make_tuple(node, -1000, -1000, 0, 0);
             auto it = pc->plans.find(key);
             Plan* P;
             if (it == pc->plans.end()) {
@@ -2168,7 +2221,7 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
     Ctx& C = *E.ctx;
     // C5-sized planes keep both lane groups' work on lanes 0, 1 (twice the transient arena
     // per lane; the persistent-arena compaction drains them at its safe points).
-    static const bool no_pipe = getenv("ACRGPU_NO_PIPELINE") != nullptr;
+    const bool no_pipe = getenv("ACRGPU_NO_PIPELINE") != nullptr;
     const bool pipelined = !no_pipe && E.S.dim <= 4096 && C.factoring == 1 && !E.gc_enabled();
     if (C.factoring == 1) C.carve(E.S.dim <= 4096 ? NLANES : 2);
     if (!pipelined) {

@@ -235,6 +235,10 @@ __device__ void gemm_nt_tiled(double* C, int ldc, const double* A, int lda, cons
     __syncthreads();
 }
 
+// shared memory of the QR-route kernel beyond the DMAX / RPCAP layout, up to the 227 KB a CTA
+// may opt into (room for cores a little above DMAX, see core_mid)
+constexpr int BIG_SMEM_EXTRA = 1400;
+
 // QR = false: dense route only (the <= 64 class never takes the QR route); without the
 // blocked-QR code the kernel fits 128 registers per thread, so two CTAs share an SM.
 template <int DMAX, int RPCAP, int NTH, bool QR = true>
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, Ba
     // workspace: Uc (m x K) | Vc (n x K) | tau_u (K) | tau_v (K) | [core engine work if too big for smem]
     const int pmax = ku > kv ? ku : kv;
     const bool core_in_smem = pmax <= DMAX;
-    const size_t smem_doubles = (size_t)DMAX * DMAX + (size_t)DMAX * RPCAP + (size_t)RPCAP * RPCAP + 5 * DMAX;
+    const size_t smem_doubles = (size_t)DMAX * DMAX + (size_t)DMAX * RPCAP + (size_t)RPCAP * RPCAP + 5 * DMAX + BIG_SMEM_EXTRA;
     // blocked QR staging (panel, W, T) in shared memory, or in global workspace for panels too
     // tall for it (C5's 2048-row leaves)
     const size_t bneed = bqr_smem_doubles(m > n ? m : n, K);
@@ -344,7 +348,10 @@ __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, Ba
     const int npan = (K + BQR_NB - 1) / BQR_NB + 1;
     const unsigned long long base_need =
         (unsigned long long)(m + n) * K + 2ull * K + 32 + 2ull * npan * BQR_NB * BQR_NB;
-    const unsigned long long core_need = core_in_smem ? 0ull : 3ull * pmax * pmax + 6ull * pmax + 64;
+    // a core a little above DMAX (K up to ~155) still fits shared memory on its own: W = R^T
+    // takes what is left (cols x rp, rp small) or spills to the arena like any oversized W
+    const bool core_mid = !core_in_smem && (size_t)ku * kv + (size_t)5 * pmax + 8 + 2304 <= smem_doubles;
+    const unsigned long long core_need = (core_in_smem || core_mid) ? 0ull : 3ull * pmax * pmax + 6ull * pmax + 64;
     if (threadIdx.x == 0) sh_ws = arena_alloc(args.work, base_need + core_need + (blocked ? 0ull : bneed));
     __syncthreads();
     double* ws = sh_ws;
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, Ba
         atomicAdd(&g_phase_cnt, 1ull);
         atomicAdd(&g_phase_cyc[6], (unsigned long long)K);
         atomicAdd(&g_phase_cyc[7], (unsigned long long)(m > n ? m : n));
-        if (!core_in_smem) atomicAdd(&g_phase_cyc[8], 1ull);
+        if (!core_in_smem && !core_mid) atomicAdd(&g_phase_cyc[8], 1ull);
         if (!blocked) atomicAdd(&g_phase_cyc[9], 1ull);
     }
     double* Uc = ws;
@@ -365,6 +372,37 @@ __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, Ba
     double* Tv = Tu + (size_t)npan * BQR_NB * BQR_NB;
     CtaSvdWork w = core_in_smem ? cta_smem_work(smem, DMAX, RPCAP)
                                 : cta_smem_work(Tv + (size_t)npan * BQR_NB * BQR_NB, pmax, pmax);
+    // Core too large for shared memory (K > 128; a quarter of C5's tasks): the core itself stays
+    // in the global workspace (pivoted QR), but the per-column arrays the QR reads every step
+    // and the Jacobi working matrix W = R^T (cols x rp, rp small) move to shared memory, which
+    // is idle between the blocked QRs and the Q application.
+    double* w_alt = nullptr;
+    size_t w_alt_cap = 0;
+    int rp_cap = core_in_smem ? RPCAP : pmax;
+    if (core_mid) {
+        double* small = smem + (smem_doubles - (size_t)5 * pmax - 8);
+        w.A = smem;
+        w.lda = ku;
+        w.W = smem + (size_t)ku * kv;
+        w.ldw = kv;
+        w.J = nullptr;
+        w.ldj = 0;
+        w.tau = small;
+        w.nrm = w.tau + pmax;
+        w.sig = w.nrm + pmax;
+        w.perm = (int*)(w.sig + pmax);
+        w.order = w.perm + pmax;
+        rp_cap = (int)((size_t)(small - w.W) / (size_t)kv);
+    } else if (!core_in_smem && (size_t)5 * pmax + 64 <= smem_doubles / 4) {
+        double* small = smem + (smem_doubles - (size_t)5 * pmax - 8);
+        w.tau = small;
+        w.nrm = w.tau + pmax;
+        w.sig = w.nrm + pmax;
+        w.perm = (int*)(w.sig + pmax);
+        w.order = w.perm + pmax;
+        w_alt = smem;
+        w_alt_cap = (size_t)(small - smem);
+    }
     for (size_t e = threadIdx.x; e < (size_t)(m + n) * K; e += NTH) ws[e] = 0.0;
     __syncthreads();
     {
@@ -398,21 +436,23 @@ __global__ void __launch_bounds__(NTH, QR ? 1 : 2) k_truncate(TruncArgs args, Ba
         for (int e = threadIdx.x; e < ku * kv; e += NTH) core[e] = 0.0;
         gemm_nt_tiled<NTH, DMAX * 16 / NTH, DMAX / 16, true>(core, ku, Uc, m, Vc, n, ku, kv, K, 1.0, w.W,
                                                                DMAX * RPCAP + RPCAP * RPCAP);
-    } else {  // core in global workspace: 128 x 128 output tiles
+    } else {  // core above DMAX (shared memory or global workspace): 128 x 128 output tiles
         for (size_t e = threadIdx.x; e < (size_t)ku * kv; e += NTH) core[e] = 0.0;
         __syncthreads();
+        double* stage = core_mid ? w.W : smem;
+        const int stage_doubles = core_mid ? (int)(w.tau - w.W) : DMAX * RPCAP + RPCAP * RPCAP;
         for (int r0 = 0; r0 < ku; r0 += DMAX)
             for (int c0 = 0; c0 < kv; c0 += DMAX)
                 gemm_nt_tiled<NTH, DMAX * 16 / NTH, DMAX / 16, true>(core + r0 + (size_t)c0 * ku, ku, Uc + r0, m,
                                                                        Vc + c0, n, min(DMAX, ku - r0),
-                                                                       min(DMAX, kv - c0), K, 1.0, smem,
-                                                                       DMAX * RPCAP + RPCAP * RPCAP, r0, c0);
+                                                                       min(DMAX, kv - c0), K, 1.0, stage,
+                                                                       stage_doubles, r0, c0);
     }
     PHASE_MARK(2);
     int rp;
     double smax;
     const int r = cta_trunc_svd<NTH>(w, ku, kv, args.eps, abs_cut, args.values_only != 0, &rp, &smax,
-                                    core_in_smem ? RPCAP : pmax, &args.work);
+                                    rp_cap, &args.work, w_alt, w_alt_cap);
     PHASE_MARK(3);
     if (args.values_only) {
         if (threadIdx.x == 0) args.sig_out[(size_t)blockIdx.x * B + b] = smax;
@@ -1344,6 +1384,175 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
     if (threadIdx.x == 0) add_flops(args.flops, F_APPLY, fl);
 }
 
+// ------------------------------------------------------------------ solve, few right-hand sides
+// With 1-4 right-hand sides the DMMA tiles above are mostly padding (16 RHS columns) and the
+// per-leaf bookkeeping dominates: C2's leaves are 32 x 32 dense blocks and rank-5 factors.
+// The same two phases on the FP64 FMA pipe, one coalesced 256-byte column segment per warp load:
+//   phase 1 (k_mv_t1):    warp per (item, Rk leaf); lanes stride the leaf's columns j, eight
+//                         rank columns of V per pass, a fixed shuffle tree per rank tile.
+//   phase 2 (k_mv_slab1): CTA per (slab, item); warp (kc, rg) owns rows 32 rg .. 32 rg + 31
+//                         (lane = row) and the slab's leaves q with q mod 4 == kc, accumulated in
+//                         leaf order; the four partial sums are combined in a fixed order.  No
+//                         staging and no barrier inside the leaf loop; x / T entries are
+//                         warp-uniform loads from L1/L2.
+// Per right-hand-side column the arithmetic is a fixed sequence, so solves with 1 to 4 columns
+// are bitwise equal column by column; the 16-column DMMA path rounds differently (its own
+// fixed sequence).
+constexpr int MV1_KW = 4;
+
+// lanes end with the warp sum of v[lane & 7]
+__device__ __forceinline__ double reduce_scatter8(double (&v)[8], int lane) {
+#pragma unroll
+    for (int h = 4; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double send = up ? v[i] : v[i + h];
+            const double keep = up ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+    }
+    double s = v[0];
+    s += __shfl_xor_sync(0xffffffffu, s, 8);
+    s += __shfl_xor_sync(0xffffffffu, s, 16);
+    return s;
+}
+
+template <int NR>
+__global__ void __launch_bounds__(NT) k_mv_t1(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
+    const int lane = threadIdx.x & 31;
+    const long total = (long)args.nrk * mb.count;
+    const long stride = (long)gridDim.x * (NT / 32);
+    double fl = 0;
+    for (long w = (long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); w < total; w += stride) {
+        const int b = (int)(w / args.nrk), li = (int)(w % args.nrk);
+        const MvLeaf L = args.rk[li];
+        const HView& H = mb.h[b];
+        const int rr = H.rank[L.k];
+        double* T = nullptr;
+        if (lane == 0) {
+            T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)rr * args.nrhs) : nullptr;
+            mv_tptr(args)[(size_t)b * args.nrk + li] = T;
+        }
+        T = (double*)__shfl_sync(0xffffffffu, (unsigned long long)T, 0);
+        if (T == nullptr) continue;
+        const double* V = H.V[L.k];
+        const int n = L.n, ld = args.dim;
+        const double* X = mb.x[b] + L.in_off;
+        for (int tc = 0; tc < rr; tc += 8) {
+            const int nt = min(8, rr - tc);
+            const double* Vt = V + (size_t)tc * n;
+            double acc[NR][8];
+#pragma unroll
+            for (int c = 0; c < NR; ++c)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[c][u] = 0.0;
+#pragma unroll 2
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const int j = j0 + lane;
+                const bool ok = j < n;
+                double v[8], xv[NR];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = (ok && u < nt) ? Vt[(size_t)u * n + j] : 0.0;
+#pragma unroll
+                for (int c = 0; c < NR; ++c) xv[c] = (ok && c < args.nrhs) ? X[j + (size_t)c * ld] : 0.0;
+#pragma unroll
+                for (int c = 0; c < NR; ++c)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc[c][u] = fma(v[u], xv[c], acc[c][u]);
+            }
+#pragma unroll
+            for (int c = 0; c < NR; ++c) {
+                const double sv = reduce_scatter8(acc[c], lane);
+                if (lane < nt && c < args.nrhs) T[tc + lane + (size_t)c * rr] = sv;
+            }
+        }
+        if (lane == 0) fl += 2.0 * rr * n * args.nrhs;
+    }
+    if (lane == 0 && fl > 0) add_flops(args.flops, F_APPLY, fl);
+}
+
+template <int NR>
+__global__ void __launch_bounds__(NT) k_mv_slab1(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
+    static_assert(NT == 256, "8 warps: 4 leaf classes x 2 row groups");
+    __shared__ double part[MV1_KW][64][NR];
+    const SlabTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    const HView& H = mb.h[b];
+    const double* X = mb.x[b];
+    const double* base = mb.base[b];
+    double* Y = mb.y[b];
+    const int ld = args.dim;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kc = warp >> 1, rg = warp & 1;
+    const int g0 = task.r0 + 32 * rg, g1 = min(task.r1, g0 + 32);  // this warp's rows
+    const int row = g0 + lane;
+    double* const* Tp = mv_tptr(args) + (size_t)b * args.nrk;
+    double acc[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) acc[c] = 0.0;
+    double fl = 0;
+    if (g0 < g1) {
+        for (int q = task.lbeg + kc; q < task.lend; q += MV1_KW) {
+            const ApplyLeaf L = args.leaves[q];
+            const int o0 = max(g0, L.out_off), o1 = min(g1, L.out_off + L.m);
+            if (o0 >= o1) continue;
+            const double* A;
+            const double* xin;
+            int len, ldx;
+            if (L.kind == K_DENSE) {
+                A = H.dense + L.doff;
+                len = L.n;
+                xin = X + L.in_off;
+                ldx = ld;
+            } else {
+                const int rr = H.rank[L.id];
+                const double* T = rr > 0 ? Tp[L.id] : nullptr;
+                if (T == nullptr) continue;
+                A = H.U[L.id];
+                len = rr;
+                xin = T;
+                ldx = rr;
+            }
+            const bool rok = row >= o0 && row < o1;
+            const double* Ar = A + (rok ? row - L.out_off : 0);
+            const int lda = L.m;
+            for (int j = 0; j < len; j += 8) {
+                double a[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] = (rok && j + u < len) ? Ar[(size_t)(j + u) * lda] : 0.0;
+#pragma unroll
+                for (int c = 0; c < NR; ++c) {
+                    if (c < args.nrhs) {
+                        const double* xc = xin + (size_t)c * ldx;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const double xv = j + u < len ? xc[j + u] : 0.0;
+                            acc[c] = fma(a[u], xv, acc[c]);
+                        }
+                    }
+                }
+            }
+            if (lane == 0) fl += 2.0 * (o1 - o0) * len * args.nrhs;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NR; ++c) part[kc][32 * rg + lane][c] = acc[c];
+    __syncthreads();
+    if (kc == 0 && row < g1) {
+        const int r = 32 * rg + lane;
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+            if (c < args.nrhs) {
+                const double sv = ((part[0][r][c] + part[1][r][c]) + part[2][r][c]) + part[3][r][c];
+                const size_t o = row + (size_t)c * ld;
+                Y[o] = base ? base[o] - sv : sv;
+            }
+        }
+    }
+    if (lane == 0 && fl > 0) add_flops(args.flops, F_APPLY, fl);
+}
+
 // ------------------------------------------------------------------ misc kernels
 // gather: out[j][r][i] = in[r][j][perm[i]] (to tree order);  scatter: inverse.
 __global__ void k_permute_in(const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
@@ -1886,8 +2095,8 @@ std::string prof_report(bool reset) {
 static size_t trunc_smem() { return SMEM_TRUNC; }
 constexpr int BIG_DMAX = 128, BIG_RPCAP = 56, BIG_NT = 512;
 static size_t trunc_smem_big() {
-    return ((size_t)BIG_DMAX * BIG_DMAX + (size_t)BIG_DMAX * BIG_RPCAP + (size_t)BIG_RPCAP * BIG_RPCAP + 5 * BIG_DMAX + 64) *
-           sizeof(double);
+    return ((size_t)BIG_DMAX * BIG_DMAX + (size_t)BIG_DMAX * BIG_RPCAP + (size_t)BIG_RPCAP * BIG_RPCAP + 5 * BIG_DMAX + 64 +
+            BIG_SMEM_EXTRA) * sizeof(double);
 }
 
 void setup_kernels() {
@@ -2016,13 +2225,24 @@ void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const App
         ProfScope _ps(st, "k_set_counter", 1);
         k_set_counter<<<1, 1, 0, st>>>(arena.ctr, ((unsigned long long)mb.count * nrk + 15ull) & ~15ull);
     }
+    // 1-4 right-hand sides: FMA-pipe kernels (lane = row / column, no padding);
+    // more: 16-column DMMA tiles
+    const int nr = nrhs <= 1 ? 1 : (nrhs <= 2 ? 2 : (nrhs <= 4 ? 4 : 0));
     if (nrk > 0) {
         ProfScope _ps(st, "k_mv_t", (long)nrk * mb.count);
-        k_mv_t<<<item_grid((long)nrk * mb.count, 4), NT, 0, st>>>(a, mb);
+        const unsigned grid = nr ? warp_grid((long)nrk * mb.count) : item_grid((long)nrk * mb.count, 4);
+        if (nr == 1) k_mv_t1<1><<<grid, NT, 0, st>>>(a, mb);
+        else if (nr == 2) k_mv_t1<2><<<grid, NT, 0, st>>>(a, mb);
+        else if (nr == 4) k_mv_t1<4><<<grid, NT, 0, st>>>(a, mb);
+        else k_mv_t<<<grid, NT, 0, st>>>(a, mb);
     }
     a.flops = ledger(flops, "k_mv_slab");
     ProfScope _ps(st, "k_mv_slab", (long)ntasks * mb.count);
-    k_mv_slab<<<dim3(ntasks, mb.count), NT, 0, st>>>(a, mb);
+    const dim3 grid(ntasks, mb.count);
+    if (nr == 1) k_mv_slab1<1><<<grid, NT, 0, st>>>(a, mb);
+    else if (nr == 2) k_mv_slab1<2><<<grid, NT, 0, st>>>(a, mb);
+    else if (nr == 4) k_mv_slab1<4><<<grid, NT, 0, st>>>(a, mb);
+    else k_mv_slab<<<grid, NT, 0, st>>>(a, mb);
 }
 void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
     ProfScope _ps(st, "k_permute_in", (long)(1184));

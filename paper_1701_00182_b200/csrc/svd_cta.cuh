@@ -313,7 +313,8 @@ __device__ void cta_jacobi(double* W, int ldw, int rows, int cols, double* J, in
 // W and J to `spill` (device arena) -- CTA-uniform decision.
 template <int NT>
 __device__ int cta_trunc_svd(CtaSvdWork& w, int rows, int cols, double eps, double abs_cut, bool values_only,
-                             int* rp_out, double* smax_out, int rp_cap, const Arena* spill) {
+                             int* rp_out, double* smax_out, int rp_cap, const Arena* spill, double* w_alt = nullptr,
+                             size_t w_alt_cap = 0) {
     __shared__ int sh_r;
     __shared__ double sh_smax;
     __shared__ double* sh_spill;
@@ -365,6 +366,11 @@ __device__ int cta_trunc_svd(CtaSvdWork& w, int rows, int cols, double eps, doub
         w.ldw = cols;
         w.J = sh_spill + (size_t)cols * rp;
         w.ldj = rp;
+    }
+    // a faster home for W offered by the caller (shared memory while the core is in global)
+    if (w_alt != nullptr && rp <= rp_cap && (size_t)cols * rp <= w_alt_cap) {
+        w.W = w_alt;
+        w.ldw = cols;
     }
     // A' = R^T (cols x rp)
     for (int e = threadIdx.x; e < cols * rp; e += NT) {

@@ -153,6 +153,28 @@ def test_factorization_deterministic(acr):
     assert np.array_equal(u1, u2)
 
 
+def test_root_plan_block_split_and_level_pipeline_are_bitwise_neutral(acr, monkeypatch):
+    # Two schedules that only regroup work: root products run as their 4 x 4 target blocks
+    # (Engine::mult_add, C5-sized planes; forced here at a small size) and the pipelined
+    # levels of the single-GPU driver (do_factor).  Same per-leaf part lists and per-plane
+    # arithmetic, so solutions, ranks and bytes are bitwise those of the plain schedule.
+    sysm = P.config_system(2, n=16)
+    cfg = acr.AcrConfig(eps=1e-6)
+    f1 = acr.acr_factor(sysm, cfg)
+    u1 = f1.solve(sysm.rhs)
+    for env in ("ACRGPU_FORCE_SPLIT", "ACRGPU_NO_PIPELINE"):
+        monkeypatch.setenv(env, "1")
+        f2 = acr.acr_factor(sysm, cfg)
+        u2 = f2.solve(sysm.rhs)
+        monkeypatch.delenv(env)
+        assert np.array_equal(u1, u2), env
+        s1, s2 = f1.inverse_rank_stats(), f2.inverse_rank_stats()
+        assert (s1.largest_rank, s1.average_rank) == (s2.largest_rank, s2.average_rank)
+        assert f1.factor_bytes() == f2.factor_bytes()
+        for li in (0, 1):
+            assert np.array_equal(f1.dinv_ranks(li, 0), f2.dinv_ranks(li, 0))
+
+
 @pytest.mark.parametrize("at", ["0", "0.000001"])
 def test_persistent_arena_compaction_is_bitwise_neutral(acr, monkeypatch, at):
     # Engine::gc (C5-sized planes compact live low-rank data into the other semi-space of the
