@@ -417,6 +417,7 @@ struct Engine {
     int nslabs = 0;
     MvLeaf* mv_rk = nullptr;          // matvec phase 1: every Rk leaf of the root
     int n_mv_rk = 0;
+    int n_mv_big = 0;
 
     ~Engine() {
         gc_release_all();
@@ -1404,7 +1405,12 @@ struct Engine {
             const SNode& L = S.node(S.k_node[k]);
             rk.push_back(MvLeaf{k, L.cb, L.cols(), L.rows()});
         }
+        // widest leaves first: the leading ones (n >= 512) take a whole CTA each in the
+        // few-RHS phase-1 kernel (k_mv_t1)
+        std::stable_sort(rk.begin(), rk.end(), [](const MvLeaf& a, const MvLeaf& b) { return a.n > b.n; });
         n_mv_rk = (int)rk.size();
+        n_mv_big = 0;
+        while (n_mv_big < n_mv_rk && rk[n_mv_big].n >= 512) ++n_mv_big;
         mv_rk = up(rk);
     }
 };
@@ -2329,7 +2335,7 @@ static void matvec(Engine& E, const std::vector<MV>& items, int nrhs) {
             mb.base[b] = it.base;
             mb.y[b] = it.y;
         }
-        launch_matvec(E.st(), E.nslabs, E.slabs, E.slab_leaves, E.mv_rk, E.n_mv_rk, nrhs, E.S.dim, E.ctx->lane().trans,
+        launch_matvec(E.st(), E.nslabs, E.slabs, E.slab_leaves, E.mv_rk, E.n_mv_rk, E.n_mv_big, nrhs, E.S.dim, E.ctx->lane().trans,
                       E.ctx->flops, mb);
     }
 }
@@ -2935,7 +2941,16 @@ static void solve_runs(std::vector<SolveRun>& runs, const std::vector<std::vecto
         for (int e : elim) is_elim[e] = 1;
         for (auto& R : runs) {
             cudaStream_t st = R.F->eng->st();
-            for (size_t t = 0; t < ret.size(); ++t)
+            // retained planes t -> positions ret[t] = 2 t + 1 (and the odd count's last plane):
+            // one strided copy for the run of planes this rank owns from t = 0
+            size_t t0 = 0;
+            while (t0 < ret.size() && ret[t0] == 2 * (int)t0 + 1 && owner(li, ret[t0]) == R.rank) ++t0;
+            if (t0 > 1)
+                CK(cudaMemcpy2DAsync(R.ub[cur ^ 1] + pv, 2 * pv * sizeof(double), R.ub[cur], pv * sizeof(double),
+                                     pv * sizeof(double), t0, cudaMemcpyDeviceToDevice, st));
+            else
+                t0 = 0;
+            for (size_t t = t0; t < ret.size(); ++t)
                 if (owner(li, ret[t]) == R.rank)
                     CK(cudaMemcpyAsync(R.ub[cur ^ 1] + (size_t)ret[t] * pv, R.ub[cur] + t * pv, pv * sizeof(double),
                                        cudaMemcpyDeviceToDevice, st));

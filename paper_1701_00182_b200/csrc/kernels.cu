@@ -1160,6 +1160,7 @@ struct MatvecArgs {
     const ApplyLeaf* leaves;
     const MvLeaf* rk;     // Rk leaves of the root (phase 1)
     int nrk;
+    int nbig;             // leading leaves of rk (sorted by decreasing n) with n >= MV1_BIG
     int nrhs;
     int dim;
     Arena arena;          // transient: [count x nrk T pointers | T blocks]
@@ -1191,7 +1192,7 @@ __global__ void __launch_bounds__(NT) k_mv_t(MatvecArgs args, const __grid_const
         double* T = nullptr;
         if (lane == 0) {
             T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)rr * args.nrhs) : nullptr;
-            mv_tptr(args)[(size_t)b * args.nrk + li] = T;
+            mv_tptr(args)[(size_t)b * args.nrk + L.k] = T;
         }
         T = (double*)__shfl_sync(0xffffffffu, (unsigned long long)T, 0);
         if (T == nullptr) continue;
@@ -1390,15 +1391,14 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
 // The same two phases on the FP64 FMA pipe, one coalesced 256-byte column segment per warp load:
 //   phase 1 (k_mv_t1):    warp per (item, Rk leaf); lanes stride the leaf's columns j, eight
 //                         rank columns of V per pass, a fixed shuffle tree per rank tile.
-//   phase 2 (k_mv_slab1): CTA per (slab, item); warp (kc, rg) owns rows 32 rg .. 32 rg + 31
-//                         (lane = row) and the slab's leaves q with q mod 4 == kc, accumulated in
-//                         leaf order; the four partial sums are combined in a fixed order.  No
-//                         staging and no barrier inside the leaf loop; x / T entries are
-//                         warp-uniform loads from L1/L2.
+//   phase 2 (k_mv_slab1): CTA per (32-row half slab, item), lane = row; the leaves are
+//                         flattened into a column table in shared memory and warp kc streams
+//                         the columns s = kc (mod 8); the eight partial sums are combined in
+//                         warp order.  x / T entries are warp-uniform loads from L1/L2.
 // Per right-hand-side column the arithmetic is a fixed sequence, so solves with 1 to 4 columns
 // are bitwise equal column by column; the 16-column DMMA path rounds differently (its own
 // fixed sequence).
-constexpr int MV1_KW = 4;
+constexpr int MV1_KW = 8;
 
 // lanes end with the warp sum of v[lane & 7]
 __device__ __forceinline__ double reduce_scatter8(double (&v)[8], int lane) {
@@ -1418,65 +1418,147 @@ __device__ __forceinline__ double reduce_scatter8(double (&v)[8], int lane) {
     return s;
 }
 
+// one rank tile (8 columns of V from column tc) of T = V^T X over the chunks j0 = 32 (c0 + i dc):
+// lanes end with the partial sum of rank column tc + (lane & 7), per right-hand side
+template <int NR>
+__device__ __forceinline__ void mv_t1_tile(const double* Vt, const double* X, int n, int ld, int nt, int nrhs, int c0, int dc,
+                                           int lane, double (&out)[NR]) {
+    double acc[NR][8];
+#pragma unroll
+    for (int c = 0; c < NR; ++c)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[c][u] = 0.0;
+#pragma unroll 2
+    for (int j0 = 32 * c0; j0 < n; j0 += 32 * dc) {
+        const int j = j0 + lane;
+        const bool ok = j < n;
+        double v[8], xv[NR];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (ok && u < nt) ? Vt[(size_t)u * n + j] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NR; ++c) xv[c] = (ok && c < nrhs) ? X[j + (size_t)c * ld] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NR; ++c)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[c][u] = fma(v[u], xv[c], acc[c][u]);
+    }
+#pragma unroll
+    for (int c = 0; c < NR; ++c) out[c] = reduce_scatter8(acc[c], lane);
+}
+
+// The Rk leaf list is sorted by decreasing column count; the first nbig leaves
+// take a whole CTA each (n >= 512): the eight warps interleave the leaf's 32-column chunks and their
+// partial sums are added in warp order (a lone warp streaming a 2048-column factor was the
+// critical path of the small-batch launches).  Every other leaf takes one warp.
+// (threshold applied on the host: Engine::prepare_structure, n >= 512)
+constexpr int MV1_RW = 32;  // rank columns per pass of the cooperative path
 template <int NR>
 __global__ void __launch_bounds__(NT) k_mv_t1(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
-    const int lane = threadIdx.x & 31;
-    const long total = (long)args.nrk * mb.count;
-    const long stride = (long)gridDim.x * (NT / 32);
+    __shared__ double part[NT / 32][MV1_RW][NR];
+    __shared__ double* sh_T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ld = args.dim;
+    const long nbig_ctas = (long)args.nbig * mb.count;
     double fl = 0;
-    for (long w = (long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); w < total; w += stride) {
-        const int b = (int)(w / args.nrk), li = (int)(w % args.nrk);
+    if ((long)blockIdx.x < nbig_ctas) {
+        const int b = (int)(blockIdx.x / args.nbig), li = (int)(blockIdx.x % args.nbig);
+        const MvLeaf L = args.rk[li];
+        const HView& H = mb.h[b];
+        const int rr = H.rank[L.k];
+        if (threadIdx.x == 0) {
+            sh_T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)rr * args.nrhs) : nullptr;
+            mv_tptr(args)[(size_t)b * args.nrk + L.k] = sh_T;
+        }
+        __syncthreads();
+        double* T = sh_T;
+        if (T == nullptr) return;
+        const double* V = H.V[L.k];
+        const double* X = mb.x[b] + L.in_off;
+        for (int t0 = 0; t0 < rr; t0 += MV1_RW) {
+            const int tw = min(MV1_RW, rr - t0);
+            for (int tc = 0; tc < tw; tc += 8) {
+                const int nt = min(8, tw - tc);
+                double sv[NR];
+                mv_t1_tile<NR>(V + (size_t)(t0 + tc) * L.n, X, L.n, ld, nt, args.nrhs, warp, NT / 32, lane, sv);
+                if (lane < nt) {
+#pragma unroll
+                    for (int c = 0; c < NR; ++c) part[warp][tc + lane][c] = sv[c];
+                }
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < tw * NR; e += NT) {
+                const int t = e % tw, c = e / tw;
+                if (c < args.nrhs) {
+                    double sum = part[0][t][c];
+#pragma unroll
+                    for (int w = 1; w < NT / 32; ++w) sum += part[w][t][c];
+                    T[t0 + t + (size_t)c * rr] = sum;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) add_flops(args.flops, F_APPLY, 2.0 * rr * L.n * args.nrhs);
+        return;
+    }
+    const long nsmall = (long)(args.nrk - args.nbig) * mb.count;
+    const long stride = (long)(gridDim.x - nbig_ctas) * (NT / 32);
+    for (long w = ((long)blockIdx.x - nbig_ctas) * (NT / 32) + warp; w < nsmall; w += stride) {
+        const int nsm = args.nrk - args.nbig;
+        const int b = (int)(w / nsm), li = args.nbig + (int)(w % nsm);
         const MvLeaf L = args.rk[li];
         const HView& H = mb.h[b];
         const int rr = H.rank[L.k];
         double* T = nullptr;
         if (lane == 0) {
             T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)rr * args.nrhs) : nullptr;
-            mv_tptr(args)[(size_t)b * args.nrk + li] = T;
+            mv_tptr(args)[(size_t)b * args.nrk + L.k] = T;
         }
         T = (double*)__shfl_sync(0xffffffffu, (unsigned long long)T, 0);
         if (T == nullptr) continue;
         const double* V = H.V[L.k];
-        const int n = L.n, ld = args.dim;
         const double* X = mb.x[b] + L.in_off;
         for (int tc = 0; tc < rr; tc += 8) {
             const int nt = min(8, rr - tc);
-            const double* Vt = V + (size_t)tc * n;
-            double acc[NR][8];
+            double sv[NR];
+            mv_t1_tile<NR>(V + (size_t)tc * L.n, X, L.n, ld, nt, args.nrhs, 0, 1, lane, sv);
 #pragma unroll
             for (int c = 0; c < NR; ++c)
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc[c][u] = 0.0;
-#pragma unroll 2
-            for (int j0 = 0; j0 < n; j0 += 32) {
-                const int j = j0 + lane;
-                const bool ok = j < n;
-                double v[8], xv[NR];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = (ok && u < nt) ? Vt[(size_t)u * n + j] : 0.0;
-#pragma unroll
-                for (int c = 0; c < NR; ++c) xv[c] = (ok && c < args.nrhs) ? X[j + (size_t)c * ld] : 0.0;
-#pragma unroll
-                for (int c = 0; c < NR; ++c)
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) acc[c][u] = fma(v[u], xv[c], acc[c][u]);
-            }
-#pragma unroll
-            for (int c = 0; c < NR; ++c) {
-                const double sv = reduce_scatter8(acc[c], lane);
-                if (lane < nt && c < args.nrhs) T[tc + lane + (size_t)c * rr] = sv;
-            }
+                if (lane < nt && c < args.nrhs) T[tc + lane + (size_t)c * rr] = sv[c];
         }
-        if (lane == 0) fl += 2.0 * rr * n * args.nrhs;
+        if (lane == 0) fl += 2.0 * rr * L.n * args.nrhs;
     }
     if (lane == 0 && fl > 0) add_flops(args.flops, F_APPLY, fl);
 }
 
+// Phase 2.  The slab's leaves are resolved cooperatively (record, rank, U / T pointers: one
+// round of parallel loads) and flattened into a column table in shared memory: entry s = one
+// column of one leaf restricted to the slab's rows (pointer to its element at slab row 0,
+// valid row range, pointer and stride of the x / T entry it multiplies).  Warp kc then
+// streams the columns s = kc (mod 8) for row `lane`, sixteen loads in flight whatever the
+// leaf boundaries.
+constexpr int MV1_ML = 128;    // leaves per window
+constexpr int MV1_KMAX = 1024; // columns per window
+struct Mv1Leaf {
+    const double* A;    // column 0, slab row 0
+    const double* xin;
+    int len, lda, ldx, o;  // o = o0 | o1 << 8 (rows relative to the slab)
+};
 template <int NR>
 __global__ void __launch_bounds__(NT) k_mv_slab1(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
-    static_assert(NT == 256, "8 warps: 4 leaf classes x 2 row groups");
-    __shared__ double part[MV1_KW][64][NR];
-    const SlabTask task = args.tasks[blockIdx.x];
+    static_assert(NT == 256 && MV1_KW == NT / 32, "8 warps = 8 column classes; one 32-row group per CTA");
+    __shared__ Mv1Leaf meta[MV1_ML];
+    __shared__ int pre[MV1_ML + 1];
+    __shared__ const double* cA[MV1_KMAX];
+    __shared__ const double* cX[MV1_KMAX];
+    __shared__ int cLdx[MV1_KMAX];
+    __shared__ int cO[MV1_KMAX];
+    __shared__ double part[MV1_KW][32][NR];
+    // CTA = one 32-row half of a slab (blockIdx.x = 2 slab + half): twice the CTAs per plane
+    // for the small batches of the upper levels
+    SlabTask task = args.tasks[blockIdx.x >> 1];
+    task.r0 += 32 * (int)(blockIdx.x & 1);
+    task.r1 = min(task.r1, task.r0 + 32);
+    if (task.r0 >= task.r1) return;
     const int b = blockIdx.y;
     const HView& H = mb.h[b];
     const double* X = mb.x[b];
@@ -1484,72 +1566,135 @@ __global__ void __launch_bounds__(NT) k_mv_slab1(MatvecArgs args, const __grid_c
     double* Y = mb.y[b];
     const int ld = args.dim;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int kc = warp >> 1, rg = warp & 1;
-    const int g0 = task.r0 + 32 * rg, g1 = min(task.r1, g0 + 32);  // this warp's rows
-    const int row = g0 + lane;
+    const int kc = warp;
+    const int rrel = lane;  // this lane's row, relative to the half slab
+    const int nrows = task.r1 - task.r0;
     double* const* Tp = mv_tptr(args) + (size_t)b * args.nrk;
     double acc[NR];
 #pragma unroll
     for (int c = 0; c < NR; ++c) acc[c] = 0.0;
     double fl = 0;
-    if (g0 < g1) {
-        for (int q = task.lbeg + kc; q < task.lend; q += MV1_KW) {
-            const ApplyLeaf L = args.leaves[q];
-            const int o0 = max(g0, L.out_off), o1 = min(g1, L.out_off + L.m);
-            if (o0 >= o1) continue;
-            const double* A;
-            const double* xin;
-            int len, ldx;
-            if (L.kind == K_DENSE) {
-                A = H.dense + L.doff;
-                len = L.n;
-                xin = X + L.in_off;
-                ldx = ld;
-            } else {
-                const int rr = H.rank[L.id];
-                const double* T = rr > 0 ? Tp[L.id] : nullptr;
-                if (T == nullptr) continue;
-                A = H.U[L.id];
-                len = rr;
-                xin = T;
-                ldx = rr;
+    for (int l0 = task.lbeg; l0 < task.lend; l0 += MV1_ML) {
+        const int nl = min(MV1_ML, task.lend - l0);
+        __syncthreads();
+        if (threadIdx.x < nl) {
+            const ApplyLeaf L = args.leaves[l0 + threadIdx.x];
+            Mv1Leaf m{nullptr, nullptr, 0, L.m, 0, 0};
+            const int o0 = max(task.r0, L.out_off) - task.r0, o1 = min(task.r1, L.out_off + L.m) - task.r0;
+            if (o0 < o1) {
+                const double* A = nullptr;
+                if (L.kind == K_DENSE) {
+                    A = H.dense + L.doff;
+                    m.len = L.n;
+                    m.xin = X + L.in_off;
+                    m.ldx = ld;
+                } else {
+                    const int rr = H.rank[L.id];
+                    const double* T = rr > 0 ? Tp[L.id] : nullptr;
+                    if (T) {
+                        A = H.U[L.id];
+                        m.len = rr;
+                        m.xin = T;
+                        m.ldx = rr;
+                    }
+                }
+                // element (slab row 0, column 0): leaf row = slab row + r0 - out_off
+                m.A = (const double*)((long long)A + 8ll * ((long long)task.r0 - L.out_off));
+                m.o = o0 | (o1 << 8);
             }
-            const bool rok = row >= o0 && row < o1;
-            const double* Ar = A + (rok ? row - L.out_off : 0);
-            const int lda = L.m;
-            for (int j = 0; j < len; j += 8) {
-                double a[8];
+            meta[threadIdx.x] = m;
+        }
+        __syncthreads();
+        if (warp == 0) {  // exclusive prefix of the leaf lengths
+            int v[MV1_ML / 32], run = 0;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) a[u] = (rok && j + u < len) ? Ar[(size_t)(j + u) * lda] : 0.0;
+            for (int i = 0; i < MV1_ML / 32; ++i) {
+                const int q = lane * (MV1_ML / 32) + i;
+                v[i] = q < nl ? meta[q].len : 0;
+                run += v[i];
+            }
+            int incl = run;
 #pragma unroll
-                for (int c = 0; c < NR; ++c) {
-                    if (c < args.nrhs) {
-                        const double* xc = xin + (size_t)c * ldx;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            int excl = incl - run;
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const double xv = j + u < len ? xc[j + u] : 0.0;
-                            acc[c] = fma(a[u], xv, acc[c]);
+            for (int i = 0; i < MV1_ML / 32; ++i) {
+                const int q = lane * (MV1_ML / 32) + i;
+                if (q <= MV1_ML - 1) pre[q] = excl;
+                excl += v[i];
+            }
+            if (lane == 31) pre[MV1_ML] = incl;
+        }
+        __syncthreads();
+        const int K = pre[MV1_ML];
+        for (int k0 = 0; k0 < K; k0 += MV1_KMAX) {
+            const int kn = min(MV1_KMAX, K - k0);
+            __syncthreads();
+            for (int sidx = threadIdx.x; sidx < kn; sidx += NT) {
+                const int k = k0 + sidx;
+                int lo = 0, hi = MV1_ML - 1;  // last leaf q with pre[q] <= k
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (pre[mid] <= k) lo = mid; else hi = mid - 1;
+                }
+                const Mv1Leaf& m = meta[lo];
+                const int j = k - pre[lo];
+                cA[sidx] = m.A + (size_t)j * m.lda;
+                cX[sidx] = m.xin + j;
+                cLdx[sidx] = m.ldx;
+                cO[sidx] = m.o;
+                fl += 2.0 * ((m.o >> 8) - (m.o & 0xff)) * args.nrhs;
+            }
+            __syncthreads();
+            {
+                for (int s0 = kc; s0 < kn; s0 += MV1_KW * 16) {
+                    double a[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const int sx = s0 + MV1_KW * u;
+                        bool ok = sx < kn;
+                        const int sc = ok ? sx : 0;
+                        const int o = cO[sc];
+                        ok = ok && rrel >= (o & 0xff) && rrel < (o >> 8);
+                        a[u] = ok ? cA[sc][rrel] : 0.0;
+                    }
+#pragma unroll
+                    for (int c = 0; c < NR; ++c) {
+                        if (c < args.nrhs) {
+                            double xv[16];
+#pragma unroll
+                            for (int u = 0; u < 16; ++u) {
+                                const int sx = s0 + MV1_KW * u;
+                                xv[u] = sx < kn ? cX[sx][(size_t)c * cLdx[sx]] : 0.0;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 16; ++u) acc[c] = fma(a[u], xv[u], acc[c]);
                         }
                     }
                 }
             }
-            if (lane == 0) fl += 2.0 * (o1 - o0) * len * args.nrhs;
         }
     }
-#pragma unroll
-    for (int c = 0; c < NR; ++c) part[kc][32 * rg + lane][c] = acc[c];
     __syncthreads();
-    if (kc == 0 && row < g1) {
-        const int r = 32 * rg + lane;
+#pragma unroll
+    for (int c = 0; c < NR; ++c) part[kc][rrel][c] = acc[c];
+    __syncthreads();
+    if (kc == 0 && rrel < nrows) {
 #pragma unroll
         for (int c = 0; c < NR; ++c) {
             if (c < args.nrhs) {
-                const double sv = ((part[0][r][c] + part[1][r][c]) + part[2][r][c]) + part[3][r][c];
-                const size_t o = row + (size_t)c * ld;
+                double sv = part[0][rrel][c];
+#pragma unroll
+                for (int w = 1; w < MV1_KW; ++w) sv += part[w][rrel][c];
+                const size_t o = task.r0 + rrel + (size_t)c * ld;
                 Y[o] = base ? base[o] - sv : sv;
             }
         }
     }
+    fl = warp_sum(fl);
     if (lane == 0 && fl > 0) add_flops(args.flops, F_APPLY, fl);
 }
 
@@ -2217,9 +2362,9 @@ void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const dou
 }
 
 void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, const MvLeaf* rk,
-                   int nrk, int nrhs, int dim, Arena arena, FlopLedger* flops, const MatvecBatch& mb) {
+                   int nrk, int nbig, int nrhs, int dim, Arena arena, FlopLedger* flops, const MatvecBatch& mb) {
     if (ntasks == 0 || mb.count == 0) return;
-    MatvecArgs a{tasks, leaves, rk, nrk, nrhs, dim, arena, ledger(flops, "k_mv_t")};
+    MatvecArgs a{tasks, leaves, rk, nrk, nbig, nrhs, dim, arena, ledger(flops, "k_mv_t")};
     {
         // T pointer table [count][nrk] at the arena base, T blocks bump-allocated after it
         ProfScope _ps(st, "k_set_counter", 1);
@@ -2230,7 +2375,8 @@ void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const App
     const int nr = nrhs <= 1 ? 1 : (nrhs <= 2 ? 2 : (nrhs <= 4 ? 4 : 0));
     if (nrk > 0) {
         ProfScope _ps(st, "k_mv_t", (long)nrk * mb.count);
-        const unsigned grid = nr ? warp_grid((long)nrk * mb.count) : item_grid((long)nrk * mb.count, 4);
+        const unsigned grid = nr ? (unsigned)((long)nbig * mb.count) + warp_grid((long)(nrk - nbig) * mb.count)
+                                 : item_grid((long)nrk * mb.count, 4);
         if (nr == 1) k_mv_t1<1><<<grid, NT, 0, st>>>(a, mb);
         else if (nr == 2) k_mv_t1<2><<<grid, NT, 0, st>>>(a, mb);
         else if (nr == 4) k_mv_t1<4><<<grid, NT, 0, st>>>(a, mb);
@@ -2238,10 +2384,10 @@ void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const App
     }
     a.flops = ledger(flops, "k_mv_slab");
     ProfScope _ps(st, "k_mv_slab", (long)ntasks * mb.count);
-    const dim3 grid(ntasks, mb.count);
-    if (nr == 1) k_mv_slab1<1><<<grid, NT, 0, st>>>(a, mb);
-    else if (nr == 2) k_mv_slab1<2><<<grid, NT, 0, st>>>(a, mb);
-    else if (nr == 4) k_mv_slab1<4><<<grid, NT, 0, st>>>(a, mb);
+    const dim3 grid(ntasks, mb.count), grid1(2 * ntasks, mb.count);
+    if (nr == 1) k_mv_slab1<1><<<grid1, NT, 0, st>>>(a, mb);
+    else if (nr == 2) k_mv_slab1<2><<<grid1, NT, 0, st>>>(a, mb);
+    else if (nr == 4) k_mv_slab1<4><<<grid1, NT, 0, st>>>(a, mb);
     else k_mv_slab<<<grid, NT, 0, st>>>(a, mb);
 }
 void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs) {
