@@ -993,6 +993,23 @@ __global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
             anorm = fmax(anorm, s2);
         }
         const bool r0 = lane < n, r1 = lane + 32 < n;
+        // The estimate is this kernel's critical path (up to 11 triangular sweeps of n dependent
+        // steps on one warp, next to ~5 inverse columns per warp on the others): its sweeps
+        // multiply by reciprocal pivots computed once instead of dividing at every step.  Only
+        // the estimate (compared with 1e-14) sees the different rounding; the inverse divides.
+        const double rd0 = (r0 && !zero_pivot) ? 1.0 / LU[lane + lane * n] : 0.0;
+        const double rd1 = (r1 && !zero_pivot) ? 1.0 / LU[lane + 32 + (lane + 32) * n] : 0.0;
+        auto usolve_r = [&](double& y0, double& y1) {  // U y = y, reciprocal pivots
+            for (int k = n - 1; k >= 0; --k) {
+                if (lane == (k & 31)) {
+                    if (k < 32) y0 *= rd0;
+                    else y1 *= rd1;
+                }
+                const double xk = own(k, y0, y1);
+                if (lane < k) y0 = fma(-LU[lane + k * n], xk, y0);
+                if (lane + 32 < k) y1 = fma(-LU[lane + 32 + k * n], xk, y1);
+            }
+        };
         auto solve = [&](double& y0, double& y1) {  // A x = b: x = U^-1 L^-1 P b
             __syncwarp();
             if (r0) vx[lane] = y0;
@@ -1001,13 +1018,13 @@ __global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
             y0 = r0 ? vx[perm[lane]] : 0.0;
             y1 = r1 ? vx[perm[lane + 32]] : 0.0;
             lsolve(y0, y1);
-            usolve(y0, y1);
+            usolve_r(y0, y1);
         };
         auto solve_t = [&](double& y0, double& y1) {  // A^T x = b: x = P^T L^-T U^-T b
             for (int k = 0; k < n; ++k) {  // U^T w = b (forward, column-oriented)
                 if (lane == (k & 31)) {
-                    if (k < 32) y0 /= LU[k + k * n];
-                    else y1 /= LU[k + k * n];
+                    if (k < 32) y0 *= rd0;
+                    else y1 *= rd1;
                 }
                 const double xk = own(k, y0, y1);
                 if (lane > k && r0) y0 = fma(-LU[k + lane * n], xk, y0);
@@ -1453,7 +1470,7 @@ __device__ __forceinline__ void mv_t1_tile(const double* Vt, const double* X, in
 // (threshold applied on the host: Engine::prepare_structure, n >= 512)
 constexpr int MV1_RW = 32;  // rank columns per pass of the cooperative path
 template <int NR>
-__global__ void __launch_bounds__(NT) k_mv_t1(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
+__global__ void __launch_bounds__(NT, NR == 1 ? 4 : (NR == 2 ? 3 : 2)) k_mv_t1(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
     __shared__ double part[NT / 32][MV1_RW][NR];
     __shared__ double* sh_T;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
