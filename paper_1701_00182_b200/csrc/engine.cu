@@ -1273,6 +1273,57 @@ struct Engine {
             return;
         }
         if (n.kind != K_BRANCH) throw AcrError{ACRGPU_E_INTERNAL, "invert_node: admissible diagonal block"};
+        // leaf level of the recursion (all four children dense, <= 32): one fused kernel per
+        // batch instead of 2 LU launches and 6 mult_adds (k_invert2x2).  ACRGPU_NO_FUSED_INV: A/B.
+        {
+            const SNode& c0 = S.node(n.ch[0]);
+            const SNode& c1 = S.node(n.ch[1]);
+            const SNode& c2 = S.node(n.ch[2]);
+            const SNode& c3 = S.node(n.ch[3]);
+            static const bool no_fused = getenv("ACRGPU_NO_FUSED_INV") != nullptr;
+            if (!no_fused && !exact_dd && c0.kind == K_DENSE && c1.kind == K_DENSE && c2.kind == K_DENSE &&
+                c3.kind == K_DENSE && c0.rows() == c0.cols() && c3.rows() == c3.cols() && c0.rows() <= 32 &&
+                c3.rows() <= 32) {
+                auto key = std::make_tuple(node, -2000, -2000, 0, 0);
+                auto it = pc->plans.find(key);
+                Plan* P;
+                if (it == pc->plans.end()) {
+                    Inv2Task t;
+                    t.d11 = S.d_off[c0.leaf] - n.doff0;
+                    t.d12 = S.d_off[c1.leaf] - n.doff0;
+                    t.d21 = S.d_off[c2.leaf] - n.doff0;
+                    t.d22 = S.d_off[c3.leaf] - n.doff0;
+                    t.m1 = c0.rows();
+                    t.m2 = c3.rows();
+                    t.rb1 = c0.rb;
+                    t.re1 = c0.re;
+                    t.rb2 = c3.rb;
+                    t.re2 = c3.re;
+                    auto np = std::make_unique<Plan>();
+                    np->deps = (DepTask*)upc(std::vector<Inv2Task>{t});
+                    P = np.get();
+                    pc->plans[key] = std::move(np);
+                } else {
+                    P = it->second.get();
+                }
+                for (size_t i0 = 0; i0 < out.size(); i0 += MAXB) {
+                    BatchViews bv{};
+                    bv.count = (int)std::min<size_t>(MAXB, out.size() - i0);
+                    std::vector<int> pl;
+                    for (int b = 0; b < bv.count; ++b) {
+                        bv.c[b] = hview(out[i0 + b]);
+                        bv.a[b] = hview(in[i0 + b]);
+                        pl.push_back(planes[i0 + b]);
+                    }
+                    const unsigned long long cid = ctx->call_id;
+                    ctx->call_id += 2;  // A11's inversion, then the Schur complement's
+                    ctx->call_planes.push_back({level, pl});
+                    ctx->call_planes.push_back({level, pl});
+                    launch_invert2x2(st(), (const Inv2Task*)P->deps, ctx->err, cid, cfg.eps * 0.5, ctx->flops, bv);
+                }
+                return;
+            }
+        }
         auto ch = [&](const std::vector<View>& v, int c) {
             std::vector<View> r;
             for (auto& x : v) r.push_back(child(x, *this, c));

@@ -890,16 +890,14 @@ struct LuArgs {
     FlopLedger* flops;
 };
 
-__global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
-    extern __shared__ double smem[];
+// CTA-wide (NT threads): Out = A^{-1} (n x n, n <= DENSE_MAX; A and Out in global or shared
+// memory, ld n) by partial-pivot LU, and the reciprocal condition estimate (CTA-uniform
+// return value).  smem: 2 n^2 + n doubles of workspace.  Ends with a barrier.
+__device__ double lu_inverse_cta(const double* A, double* Out, const int n, double* smem) {
     __shared__ int piv[DENSE_MAX];
     __shared__ int sh_p;
     __shared__ double sh_rcond;
-    const LuTask task = args.tasks[blockIdx.x];
-    const int b = blockIdx.y;
-    const int n = task.m;
-    const double* A = bv.a[b].dense + task.doff;
-    double* Out = bv.c[b].dense + task.doff;
+    __syncthreads();
     double* LU = smem;                 // n x n
     double* Ao = LU + n * n;           // original (for the 1-norm)
     double* vx = Ao + n * n;           // work vector (permutations of the condition estimate)
@@ -1096,19 +1094,30 @@ __global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
         }
     }
     __syncthreads();
-    const double rcond = sh_rcond;
-    if (!(rcond > 1e-14)) {
-        if (threadIdx.x == 0) {
-            const unsigned long long key = (args.call_id << 16) | (unsigned long long)b;
-            const unsigned long long prev = atomicMin(&args.err->key, key);
-            if (key < prev) {
-                args.err->code = 2;
-                args.err->rb = task.rb;
-                args.err->re = task.re;
-                args.err->rcond = rcond;
-            }
+    return sh_rcond;
+}
+
+// rcond guard of the reference (hmatrix.cpp:485-494): the first failure by (call, plane) wins
+__device__ __forceinline__ void lu_report(DevError* err, unsigned long long call_id, int b, double rcond, int rb, int re) {
+    if (!(rcond > 1e-14) && threadIdx.x == 0) {
+        const unsigned long long key = (call_id << 16) | (unsigned long long)b;
+        const unsigned long long prev = atomicMin(&err->key, key);
+        if (key < prev) {
+            err->code = 2;
+            err->rb = rb;
+            err->re = re;
+            err->rcond = rcond;
         }
     }
+}
+
+__global__ void __launch_bounds__(NT) k_lu_inverse(LuArgs args, BatchViews bv) {
+    extern __shared__ double smem[];
+    const LuTask task = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    const int n = task.m;
+    const double rcond = lu_inverse_cta(bv.a[b].dense + task.doff, bv.c[b].dense + task.doff, n, smem);
+    lu_report(args.err, args.call_id, b, rcond, task.rb, task.re);
     if (threadIdx.x == 0) add_flops(args.flops, F_LU, 2.0 * n * n * n);
 }
 
@@ -2027,6 +2036,128 @@ __global__ void __launch_bounds__(64, 6) k_small32(TruncArgs targs, DDArgs dargs
     }
 }
 
+// ------------------------------------------------------------------ fused leaf-level invert_node
+// invert_node (hmatrix.cpp:483-534) of a branch whose four children are dense leaves <= 32:
+// X11 = A11^-1;  T12 = X11 A12, T21 = A21 X11;  S = A22 - A21 T12;  X22 = S^-1;
+// C12 = -T12 X22, C21 = -X22 T21;  X11 -= T12 C21 -- every product SVD-truncated at the
+// arithmetic tolerance before it is added (the reference's dense * dense rule,
+// hmatrix.cpp:411-413), as in the unfused plan.  One CTA per plane does the whole node in
+// shared memory: the host-driven recursion spends 2 LU launches and 6 mult_adds (~25 dependent
+// launches with their stream hand-overs, ~0.85 ms) on each of the dim/64 such nodes of every
+// invert chain; here the six truncations (warp engine, T12 || T21 and C12 || C21 on two warps)
+// and the two LU inversions run back to back.
+struct Inv2Args {
+    const Inv2Task* tasks;
+    DevError* err;
+    unsigned long long call_id;  // call_id: A11's inversion, call_id + 1: the Schur complement's
+    double eps;
+    FlopLedger* flops;
+};
+
+// warp: (Ad (m x k) Bd (k x n)) truncated at eps -> Uo (m x r, ld m), Vo (n x r, ld n); returns r
+__device__ int warp_prod_trunc32(const double* Ad, const double* Bd, int m, int k, int n, double eps, Warp32Smem& sm,
+                                 double* Uo, double* Vo, FlopLedger* flops) {
+    const int lane = threadIdx.x & 31;
+    double a[32], v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = 0.0;
+    const int nz = warp_dd32_mma(a, Ad, Bd, m, k, n, sm);
+    double fsvd = 0, fqr = 0, fgemm = fl_gemm(m, n, k);  // nominal work of the reference
+    fl_svd(m, n, fsvd, fqr, fgemm);
+    if (lane == 0) {
+        add_flops(flops, F_SVD, fsvd);
+        add_flops(flops, F_GEQRF, fqr);
+        add_flops(flops, F_GEMM, fgemm);
+    }
+    if (!__any_sync(0xffffffffu, nz & 1) || !__any_sync(0xffffffffu, nz & 2)) {
+        if (lane == 0) add_flops(flops, F_SKIP, fsvd + fqr + fgemm);  // zero operand: rank 0, not executed
+        return 0;
+    }
+    const int rp = warp_rrqr_jacobi32(a, v, m, n, 1.8e-4 * eps, 0.0, true, sm, nullptr);
+    double sig, smax;
+    int pos, r;
+    warp_sigma_pos32(a, rp, eps, 0.0, sig, pos, r, smax);
+    if (r > 0) warp_write32(a, m, n, rp, sig, pos, r, sm, Uo, Vo);
+    return r;
+}
+
+// CTA: C (m x n, ld m) = C0 + alpha U V^T (C0 null: zero; C0 may alias C)
+__device__ void cta_lowrank_set(double* C, int m, int n, const double* U, const double* V, int r, double alpha,
+                                const double* C0, FlopLedger* flops) {
+    for (int e = threadIdx.x; e < m * n; e += NT) {
+        const int i = e % m, j = e / m;
+        double acc = 0.0;
+        for (int t = 0; t < r; ++t) acc = fma(U[i + t * m], V[j + t * n], acc);
+        C[e] = fma(alpha, acc, C0 ? C0[e] : 0.0);
+    }
+    if (threadIdx.x == 0 && r > 0) add_flops(flops, F_GEMM, 2.0 * m * n * r);
+}
+
+constexpr int INV2_LU = 2 * 32 * 32 + 32;  // lu_inverse_cta workspace (doubles)
+constexpr size_t INV2_SMEM = (INV2_LU + 3 * 1024 + 4 * 1024) * sizeof(double) + 2 * sizeof(Warp32Smem);
+__global__ void __launch_bounds__(NT) k_invert2x2(Inv2Args args, BatchViews bv) {
+    extern __shared__ double smem[];
+    __shared__ int sh_r[2];
+    const Inv2Task t = args.tasks[blockIdx.x];
+    const int b = blockIdx.y;
+    const double* A = bv.a[b].dense;
+    double* X = bv.c[b].dense;
+    const int m1 = t.m1, m2 = t.m2;
+    double* luw = smem;
+    double* T12 = luw + INV2_LU;
+    double* T21 = T12 + 1024;
+    double* S = T21 + 1024;
+    double* UV = S + 1024;  // warp w: U at UV + 2048 w, V at UV + 2048 w + 1024
+    Warp32Smem* wsm = (Warp32Smem*)(UV + 4096);
+    const int warp = threadIdx.x >> 5;
+    const double eps = args.eps;
+    // X11 = A11^-1
+    double rc = lu_inverse_cta(A + t.d11, X + t.d11, m1, luw);
+    lu_report(args.err, args.call_id, b, rc, t.rb1, t.re1);
+    // T12 = X11 A12 || T21 = A21 X11
+    if (warp == 0) {
+        const int r = warp_prod_trunc32(X + t.d11, A + t.d12, m1, m1, m2, eps, wsm[0], UV, UV + 1024, args.flops);
+        if ((threadIdx.x & 31) == 0) sh_r[0] = r;
+    } else if (warp == 1) {
+        const int r = warp_prod_trunc32(A + t.d21, X + t.d11, m2, m1, m1, eps, wsm[1], UV + 2048, UV + 3072, args.flops);
+        if ((threadIdx.x & 31) == 0) sh_r[1] = r;
+    }
+    __syncthreads();
+    cta_lowrank_set(T12, m1, m2, UV, UV + 1024, sh_r[0], 1.0, nullptr, args.flops);
+    cta_lowrank_set(T21, m2, m1, UV + 2048, UV + 3072, sh_r[1], 1.0, nullptr, args.flops);
+    __syncthreads();
+    // S = A22 - A21 T12
+    if (warp == 0) {
+        const int r = warp_prod_trunc32(A + t.d21, T12, m2, m1, m2, eps, wsm[0], UV, UV + 1024, args.flops);
+        if ((threadIdx.x & 31) == 0) sh_r[0] = r;
+    }
+    __syncthreads();
+    cta_lowrank_set(S, m2, m2, UV, UV + 1024, sh_r[0], -1.0, A + t.d22, args.flops);
+    // X22 = S^-1 (lu_inverse_cta starts and ends with a barrier)
+    rc = lu_inverse_cta(S, X + t.d22, m2, luw);
+    lu_report(args.err, args.call_id + 1, b, rc, t.rb2, t.re2);
+    // C12 = -T12 X22 || C21 = -X22 T21
+    if (warp == 0) {
+        const int r = warp_prod_trunc32(T12, X + t.d22, m1, m2, m2, eps, wsm[0], UV, UV + 1024, args.flops);
+        if ((threadIdx.x & 31) == 0) sh_r[0] = r;
+    } else if (warp == 1) {
+        const int r = warp_prod_trunc32(X + t.d22, T21, m2, m2, m1, eps, wsm[1], UV + 2048, UV + 3072, args.flops);
+        if ((threadIdx.x & 31) == 0) sh_r[1] = r;
+    }
+    __syncthreads();
+    cta_lowrank_set(X + t.d12, m1, m2, UV, UV + 1024, sh_r[0], -1.0, nullptr, args.flops);
+    cta_lowrank_set(X + t.d21, m2, m1, UV + 2048, UV + 3072, sh_r[1], -1.0, nullptr, args.flops);
+    __syncthreads();
+    // X11 -= T12 C21
+    if (warp == 0) {
+        const int r = warp_prod_trunc32(T12, X + t.d21, m1, m2, m1, eps, wsm[0], UV, UV + 1024, args.flops);
+        if ((threadIdx.x & 31) == 0) sh_r[0] = r;
+    }
+    __syncthreads();
+    cta_lowrank_set(X + t.d11, m1, m1, UV, UV + 1024, sh_r[0], -1.0, X + t.d11, args.flops);
+    if (threadIdx.x == 0) add_flops(args.flops, F_LU, 2.0 * m1 * m1 * m1 + 2.0 * m2 * m2 * m2);
+}
+
 // sigma_1 of dense leaves (scale_walk, hmatrix.cpp:630-633), values only; <= 32: one warp per leaf.
 __global__ void __launch_bounds__(64) k_sigma1_32(Sig1Args args, BatchViews bv) {
     __shared__ Warp32Smem smem[2];
@@ -2265,6 +2396,7 @@ void setup_kernels() {
     cudaFuncSetAttribute(k_truncate<64, 64, 256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
     cudaFuncSetAttribute(k_truncate<BIG_DMAX, BIG_RPCAP, BIG_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_big());
     cudaFuncSetAttribute(k_dd_product, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
+    cudaFuncSetAttribute(k_invert2x2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)INV2_SMEM);
     cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((2 * DENSE_MAX * DENSE_MAX + 2 * DENSE_MAX) * sizeof(double)));
     cudaFuncSetAttribute(k_sigma1_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
@@ -2369,6 +2501,14 @@ void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, 
     const size_t sm = (2 * (size_t)maxm * maxm + 2 * maxm) * sizeof(double);
     ProfScope _ps(st, "k_lu_inverse", (long)((ntasks)*(bv.count)));
     k_lu_inverse<<<dim3(ntasks, bv.count), NT, sm, st>>>(a, bv);
+}
+
+void launch_invert2x2(cudaStream_t st, const Inv2Task* task, DevError* err, unsigned long long call_id, double eps,
+                      FlopLedger* flops, const BatchViews& bv) {
+    if (bv.count == 0) return;
+    Inv2Args a{task, err, call_id, eps, ledger(flops, "k_invert2x2")};
+    ProfScope _ps(st, "k_invert2x2", (long)bv.count);
+    k_invert2x2<<<dim3(1, bv.count), NT, INV2_SMEM, st>>>(a, bv);
 }
 
 void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,

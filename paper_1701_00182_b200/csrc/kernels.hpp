@@ -106,6 +106,8 @@ void launch_deposit(cudaStream_t st, int ntasks, const DepTask* tasks, const Par
                     FlopLedger* flops, const BatchViews& bv);
 void launch_lu(cudaStream_t st, int ntasks, const LuTask* tasks, DevError* err, unsigned long long call_id,
                FlopLedger* flops, const BatchViews& bv, int maxm);
+void launch_invert2x2(cudaStream_t st, const Inv2Task* task, DevError* err, unsigned long long call_id, double eps,
+                      FlopLedger* flops, const BatchViews& bv);
 void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const double* sig_k, int nk, int B, double eps,
                          double* abs_cut);
 // Batched solve matvec y = base - H x (two phases, see kernels.cu).  arena: transient

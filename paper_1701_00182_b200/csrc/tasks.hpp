@@ -134,6 +134,13 @@ struct LuTask {
     int rb, re;      // tree-order rows, for SingularBlockError messages
 };
 
+// invert_node of a branch whose four children are dense leaves <= 32 (k_invert2x2)
+struct Inv2Task {
+    long d11, d12, d21, d22;  // dense pool offsets of the children, relative to the node's view
+    int m1, m2;               // rows of the first / second cluster
+    int rb1, re1, rb2, re2;   // tree-order rows of the diagonal leaves (SingularBlockError)
+};
+
 // Error record (first error by (call, batch index) order wins).
 struct DevError {
     unsigned long long key;  // (call_id << 16) | b ; ~0 = none
