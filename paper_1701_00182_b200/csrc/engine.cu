@@ -1034,6 +1034,7 @@ struct Engine {
     struct GcMark {
         cudaEvent_t ev = nullptr;
         unsigned long long* slot = nullptr;
+        int group = 0;  // lane group that issued the mult_add (pipelined levels)
     };
     std::deque<GcMark> gc_marks;  // issue order
     std::vector<GcMark> gc_free;
@@ -1069,10 +1070,23 @@ struct Engine {
         GcMark m = gc_take();
         CK(cudaMemcpyAsync(m.slot, ctx->persist.ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st()));
         CK(cudaEventRecord(m.ev, st()));
+        m.group = ctx->base / 2;
         gc_marks.push_back(m);
     }
-    void gc_poll(bool wait_oldest) {
-        if (wait_oldest && !gc_marks.empty()) CK(cudaEventSynchronize(gc_marks.front().ev));
+    // wait_group: -1 no wait; -2 wait for the oldest mark; g >= 0 wait for the oldest mark of
+    // lane group g (with pipelined levels the other group's marks complete much later: the
+    // chain's host enqueue must not be throttled to the low-priority updates' progress)
+    void gc_poll(int wait_group) {
+        if (wait_group != -1 && !gc_marks.empty()) {
+            const GcMark* w = &gc_marks.front();
+            if (wait_group >= 0)
+                for (const auto& m : gc_marks)
+                    if (m.group == wait_group) {
+                        w = &m;
+                        break;
+                    }
+            CK(cudaEventSynchronize(w->ev));
+        }
         for (auto it = gc_marks.begin(); it != gc_marks.end();) {
             const cudaError_t q = cudaEventQuery(it->ev);
             if (q == cudaErrorNotReady) {
@@ -1093,16 +1107,21 @@ struct Engine {
         if (!gc_enabled()) return;
         const double cap = (double)ctx->persist.cap;
         const double g = std::max(gc_growth, 0.01 * cap);
-        gc_poll(false);
+        gc_poll(-1);
         // worst case once the next mult_add is issued: every pending one (and it) grows by 1.5 g
-        while (!gc_marks.empty() &&
-               (gc_marks.size() > 16 || (double)gc_known + 1.5 * g * (double)(gc_marks.size() + 1) > 0.92 * cap))
-            gc_poll(true);
+        const int grp = ctx->base / 2;
+        while (!gc_marks.empty()) {
+            const bool over = (double)gc_known + 1.5 * g * (double)(gc_marks.size() + 1) > 0.92 * cap;
+            size_t mine = 0;
+            for (const auto& m : gc_marks) mine += m.group == grp;
+            if (!over && mine <= 16) break;
+            gc_poll(over ? -2 : grp);
+        }
         const char* force = getenv("ACRGPU_GC_FORCE");
         const double at = force ? atof(force) : gc_next;
         if (gc_known == 0 || (double)gc_known < at * cap) return;
         for (auto& l : ctx->lanes) CK(cudaStreamSynchronize(l.st));
-        gc_poll(false);
+        gc_poll(-1);
         gc();
     }
     void gc() {
@@ -2279,8 +2298,12 @@ static void do_factor(acrgpu_fact* F, const DSys& sys) {
     // C5-sized planes keep both lane groups' work on lanes 0, 1 (twice the transient arena
     // per lane; the persistent-arena compaction drains them at its safe points).
     const bool no_pipe = getenv("ACRGPU_NO_PIPELINE") != nullptr;
-    const bool pipelined = !no_pipe && E.S.dim <= 4096 && C.factoring == 1 && !E.gc_enabled();
-    if (C.factoring == 1) C.carve(E.S.dim <= 4096 ? NLANES : 2);
+    // C5-sized planes stay sequential: with four lanes the transient arena per lane (~10 GB)
+    // chunks the chain's products into tiny batches and a root product no longer fits with
+    // margin (measured: the level-1 chain 1 s -> 36 s, then arena exhaustion).
+    const bool big = E.S.dim > 4096;
+    const bool pipelined = !no_pipe && C.factoring == 1 && !big && !E.gc_enabled();
+    if (C.factoring == 1) C.carve(big ? 2 : NLANES);
     if (!pipelined) {
         while ((int)R.D.size() > stop) {
             const std::vector<char> all(R.D.size(), 1);
