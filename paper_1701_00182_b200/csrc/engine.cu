@@ -414,6 +414,10 @@ struct Engine {
     int* d_kn = nullptr;
     SlabTask* slabs = nullptr;        // matvec slabs of the root
     ApplyLeaf* slab_leaves = nullptr;
+    int n_slab_leaves = 0;
+    MvCluster* mv_cl = nullptr;       // leaf clusters with their packed-x blocks (k_mv_slab_tma)
+    int n_mv_cl = 0;
+    long mv_xp_group = 0;
     int nslabs = 0;
     MvLeaf* mv_rk = nullptr;          // matvec phase 1: every Rk leaf of the root
     int n_mv_rk = 0;
@@ -1443,6 +1447,21 @@ struct Engine {
         // matvec slabs over leaf clusters (non-transposed apply of the root)
         std::vector<int> lv;
         subtree_leaves(0, lv);
+        // packed-x blocks, one per leaf cluster: 16 right-hand sides x ldx, ldx = the cluster size rounded
+        // up to a k-step and then to == 4 (mod 16) (conflict-free DMMA B fragments, 16-byte rows)
+        std::vector<MvCluster> cls;
+        std::map<int, int> xoff_of;  // cluster start -> xoff
+        long xp = 0;
+        for (size_t i = 0; i < S.cl_begin.size(); ++i) {
+            const int n = S.cl_end[i] - S.cl_begin[i], n4 = (n + 3) & ~3;
+            const int ldx = n4 + ((20 - (n4 & 15)) & 15);
+            cls.push_back(MvCluster{S.cl_begin[i], n, (int)xp, ldx});
+            xoff_of[S.cl_begin[i]] = (int)xp;
+            xp += 16L * ldx;
+        }
+        n_mv_cl = (int)cls.size();
+        mv_xp_group = xp;
+        mv_cl = up(cls);
         std::vector<SlabTask> sl;
         std::vector<ApplyLeaf> al;
         for (auto [r0, r1] : slabs_of(0, S.dim)) {
@@ -1461,7 +1480,7 @@ struct Engine {
                 a.n = L.cols();
                 a.in_off = L.cb;
                 a.out_off = L.rb;
-                a.tl = -1;
+                a.tl = (L.kind == K_DENSE && xoff_of.count(L.cb) && L.cols() == S.cl_end[S.cl_index[L.cb]] - L.cb) ? xoff_of[L.cb] : -1;
                 al.push_back(a);
             }
             t.lend = (int)al.size();
@@ -1470,6 +1489,7 @@ struct Engine {
         nslabs = (int)sl.size();
         slabs = up(sl);
         slab_leaves = up(al);
+        n_slab_leaves = (int)al.size();
         std::vector<MvLeaf> rk;
         for (int k = 0; k < S.n_rk(); ++k) {
             const SNode& L = S.node(S.k_node[k]);
@@ -2409,8 +2429,9 @@ static void matvec(Engine& E, const std::vector<MV>& items, int nrhs) {
             mb.base[b] = it.base;
             mb.y[b] = it.y;
         }
-        launch_matvec(E.st(), E.nslabs, E.slabs, E.slab_leaves, E.mv_rk, E.n_mv_rk, E.n_mv_big, nrhs, E.S.dim, E.ctx->lane().trans,
-                      E.ctx->flops, mb);
+        const MatvecPlan mp{E.nslabs, E.slabs, E.slab_leaves, E.n_slab_leaves, E.mv_rk, E.n_mv_rk, E.n_mv_big, E.mv_cl, E.n_mv_cl,
+                            E.mv_xp_group};
+        launch_matvec(E.st(), mp, nrhs, E.S.dim, E.ctx->lane().trans, E.ctx->flops, mb);
     }
 }
 

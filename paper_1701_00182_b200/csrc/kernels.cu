@@ -61,6 +61,10 @@ __device__ double* arena_alloc(const Arena& a, unsigned long long n) {
 // QR-route phase timing (clock64 deltas of thread 0, summed over CTAs): diagnostics only
 __device__ unsigned long long g_phase_cyc[16];
 __device__ unsigned long long g_phase_cnt;
+// k_mv_slab_tma diagnostics (warp 0 / producer warp 0, lane 0): CTAs, CTA cycles, consumer cycles
+// waiting for a full stage, consumer cycles between wait and release, producer cycles waiting for
+// an empty stage, stages, leaf entries, producer cycles
+__device__ unsigned long long g_mv_cyc[8];
 #define PHASE_MARK(i)                                                          \
     do {                                                                       \
         if (threadIdx.x == 0) {                                                \
@@ -1191,10 +1195,56 @@ struct MatvecArgs {
     int dim;
     Arena arena;          // transient: [count x nrk T pointers | T blocks]
     FlopLedger* flops;
+    int tma;              // 1: T blocks in the padded layout of the bulk-copy slab kernel (k_mv_slab_tma)
+};
+struct MatvecTma {        // extra arguments of k_mv_resolve / k_mv_slab_tma
+    int nleaves;          // slab leaf records in total (tasks[ntasks - 1].lend)
+    int* rec_cnt;         // resolved records per (item, slab)  [count x ntasks]
+    void* rec;            // resolved records (TsMeta)          [count x nleaves], slab t of item b from b * nleaves + tasks[t].lbeg
+    const MvCluster* cl;  // leaf clusters (packed-x blocks)
+    int ncl;
+    long xp_group;        // packed-x doubles per (item, RHS group)
+    double* xp;           // packed x  [count][RHS group][xp_group]
 };
 constexpr int MV_RHS = 16;      // right-hand sides per pass (fixed register slots)
 
+// Leading dimension of a rank-r T block in the padded layout: the smallest value >= r that is
+// == 4 (mod 8).  Even (16-byte rows for cp.async.bulk) and conflict-free for the DMMA B
+// fragment (lanes (g, t) read T[k + t][rhs g] = g * ld + t: 16 distinct 8-byte banks).
+__host__ __device__ __forceinline__ int mv_ldt(int r) { return ((r + 3) & ~7) + 4; }
+
+// Contraction order of a dense leaf whose column count is a multiple of 32 (both slab kernels):
+// position p = 4 s + t (k-step s, DMMA k index t) contracts column mv_col(p) = 32 v + 8 t + u with
+// s = 8 v + u, i.e. the four columns of a k-step come from four different 8-column groups.  The
+// bulk-copy kernel brings such a leaf in as 8-column groups (one 4 KB copy each for 64 x 64),
+// padded by 4 doubles between groups, and this order makes its A fragments conflict-free; the
+// packed x block of the leaf's column cluster is stored in position order.  Other leaves: p.
+__host__ __device__ __forceinline__ int mv_col(int p) { return (p & ~31) | ((p & 3) << 3) | ((p >> 2) & 7); }
+__host__ __device__ __forceinline__ int mv_pos(int c) { return (c & ~31) | ((c & 7) << 2) | ((c >> 3) & 3); }
+
 __device__ __forceinline__ double** mv_tptr(const MatvecArgs& a) { return (double**)a.arena.base; }
+
+// Accumulation order of phase 2 (both slab kernels): every output element keeps FOUR partial
+// sums; k-step s (four contracted entries) of the leaf at position i of the slab's leaf list
+// goes to partial sum (s + 2 (i & 1)) mod 4, and the result is (p0 + p1) + (p2 + p3).  One DMMA
+// chain per output tile would leave the FP64 tensor pipe idle two thirds of the time (its latency
+// is far above its issue interval: profiles/r02_ncu_mv_slab_tma.txt); four chains per tile, and a
+// different pair for consecutive short (rank <= 8) leaves, keep it fed.
+template <int K>
+__device__ __forceinline__ void mv_step(double (&acc)[4][4], double a, double b0, double b1) {
+    dmma8x8x4(acc[K][0], acc[K][1], a, b0);
+    dmma8x8x4(acc[K][2], acc[K][3], a, b1);
+}
+__device__ __forceinline__ void mv_acc_zero(double (&acc)[4][4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[k][i] = 0.0;
+}
+// element i (0: d00, 1: d01, 2: d10, 3: d11) of the combined accumulator
+__device__ __forceinline__ double mv_acc_sum(const double (&acc)[4][4], int i) {
+    return (acc[0][i] + acc[1][i]) + (acc[2][i] + acc[3][i]);
+}
 
 // Both phases run on the FP64 tensor cores (mma.sync.m8n8k4.f64, DMMA; fragment layout in
 // bqr.cuh): the right-hand sides are always 16 zero-padded columns, so every output element
@@ -1216,12 +1266,19 @@ __global__ void __launch_bounds__(NT) k_mv_t(MatvecArgs args, const __grid_const
         const HView& H = mb.h[b];
         const int rr = H.rank[L.k];
         double* T = nullptr;
+        // T block: rank x nrhs (ld = rank), or -- for the bulk-copy slab kernel -- groups of 16
+        // right-hand sides with ld = mv_ldt(rank), pad rows and pad columns zero
+        const int ldt = args.tma ? mv_ldt(rr) : rr;
+        const int ncol = args.tma ? (args.nrhs + MV_RHS - 1) / MV_RHS * MV_RHS : args.nrhs;
         if (lane == 0) {
-            T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)rr * args.nrhs) : nullptr;
+            T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)ldt * ncol) : nullptr;
             mv_tptr(args)[(size_t)b * args.nrk + L.k] = T;
         }
         T = (double*)__shfl_sync(0xffffffffu, (unsigned long long)T, 0);
         if (T == nullptr) continue;
+        if (args.tma)
+            for (int e = lane; e < ldt * ncol; e += 32)
+                if (e % ldt >= rr || e / ldt >= args.nrhs) T[e] = 0.0;
         const double* V = H.V[L.k];
         const int n = L.n, ld = args.dim;
         for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
@@ -1262,8 +1319,8 @@ __global__ void __launch_bounds__(NT) k_mv_t(MatvecArgs args, const __grid_const
                 for (int i = 0; i < 2; ++i) {
                     const int tr = tc + 2 * t4 + i;
                     if (tr < rr) {
-                        if (c_lo) T[tr + (size_t)(c0 + g) * rr] = i ? d01 : d00;
-                        if (c_hi) T[tr + (size_t)(c0 + g + 8) * rr] = i ? d11 : d10;
+                        if (c_lo) T[tr + (size_t)(c0 + g) * ldt] = i ? d01 : d00;
+                        if (c_hi) T[tr + (size_t)(c0 + g + 8) * ldt] = i ? d11 : d10;
                     }
                 }
             }
@@ -1285,6 +1342,7 @@ struct MvMeta {
     const double* A;    // operand column 0 at row 0 of the leaf (ld lda)
     const double* xin;  // contracted vector, column c at xin + c * ldx
     int len, lda, ldx, o0, o1, out_off;
+    int perm;           // dense leaf with len % 32 == 0: contraction in mv_col order
 };
 __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
     __shared__ double Xs[MV_RHS * MV_SLD];
@@ -1302,17 +1360,19 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
     double fl = 0;
     for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
         const int nc = min(MV_RHS, args.nrhs - c0);
-        double d00 = 0, d01 = 0, d10 = 0, d11 = 0;  // rows 8w+g, RHS 2t4+i (tile 0) / 8+2t4+i (tile 1)
+        double acc[4][4];  // [partial sum][rows 8w+g: RHS 2t4, 2t4+1 (tile 0), 8+2t4, 8+2t4+1 (tile 1)]
+        mv_acc_zero(acc);
         for (int l0 = task.lbeg; l0 < task.lend; l0 += MV_META) {
             const int nl = min(MV_META, task.lend - l0);
             __syncthreads();
             if (threadIdx.x < nl) {
                 const ApplyLeaf L = args.leaves[l0 + threadIdx.x];
-                MvMeta m{nullptr, nullptr, 0, L.m, 0, max(task.r0, L.out_off), min(task.r1, L.out_off + L.m), L.out_off};
+                MvMeta m{nullptr, nullptr, 0, L.m, 0, max(task.r0, L.out_off), min(task.r1, L.out_off + L.m), L.out_off, 0};
                 if (m.o0 < m.o1) {
                     if (L.kind == K_DENSE) {
                         m.A = H.dense + L.doff;
                         m.len = L.n;
+                        m.perm = (L.n & 31) == 0;
                         m.xin = X + L.in_off + (size_t)c0 * ld;
                         m.ldx = ld;
                     } else {
@@ -1344,7 +1404,7 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
                         if (p < jn && c < nc) {
                             int q = q0, pos = j0 + p;
                             while (pos >= ((meta[q].len + 3) & ~3)) pos -= (meta[q++].len + 3) & ~3;
-                            if (pos < meta[q].len) v = meta[q].xin[pos + (size_t)c * meta[q].ldx];
+                            if (pos < meta[q].len) v = meta[q].xin[(meta[q].perm ? mv_col(pos) : pos) + (size_t)c * meta[q].ldx];
                         }
                         Xs[c * MV_SLD + p] = v;
                     }
@@ -1360,28 +1420,37 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
                         // B fragment of tile ct: B[k = t4][n = g] = x[j][RHS 8 ct + g]
                         const double* b0 = Xs + (size_t)g * MV_SLD + (off - j0);
                         const double* b1 = Xs + (size_t)(g + 8) * MV_SLD + (off - j0);
-                        int j = lo - off;
+                        int j = lo - off;  // a multiple of 16 (leaf start, or a 256-entry chunk of a long leaf)
                         const int je = hi - off;
-                        for (; j + 16 <= je; j += 16) {
-                            double a[4];
+                        const bool par = ((l0 + q - task.lbeg) & 1) != 0;
+                        auto run = [&](auto rot) {
+                            constexpr int R = decltype(rot)::value;
+                            for (; j + 16 <= je; j += 16) {
+                                double a[4];
 #pragma unroll
-                            for (int s = 0; s < 4; ++s) {
-                                const int jj = j + 4 * s + t4;
-                                a[s] = (rok && jj < m.len) ? A[(size_t)jj * m.lda] : 0.0;
+                                for (int s = 0; s < 4; ++s) {
+                                    const int jj = j + 4 * s + t4;
+                                    a[s] = (rok && jj < m.len) ? A[(size_t)(m.perm ? mv_col(jj) : jj) * m.lda] : 0.0;
+                                }
+                                mv_step<(0 + R) & 3>(acc, a[0], b0[j + t4], b1[j + t4]);
+                                mv_step<(1 + R) & 3>(acc, a[1], b0[j + 4 + t4], b1[j + 4 + t4]);
+                                mv_step<(2 + R) & 3>(acc, a[2], b0[j + 8 + t4], b1[j + 8 + t4]);
+                                mv_step<(3 + R) & 3>(acc, a[3], b0[j + 12 + t4], b1[j + 12 + t4]);
                             }
+                            if (j < je) {
+                                double a[3];
 #pragma unroll
-                            for (int s = 0; s < 4; ++s) {
-                                const int jj = j + 4 * s + t4;
-                                dmma8x8x4(d00, d01, a[s], b0[jj]);
-                                dmma8x8x4(d10, d11, a[s], b1[jj]);
+                                for (int s = 0; s < 3; ++s) {
+                                    const int jj = j + 4 * s + t4;
+                                    a[s] = (rok && jj < m.len && j + 4 * s < je) ? A[(size_t)(m.perm ? mv_col(jj) : jj) * m.lda] : 0.0;
+                                }
+                                mv_step<(0 + R) & 3>(acc, a[0], b0[j + t4], b1[j + t4]);
+                                if (j + 4 < je) mv_step<(1 + R) & 3>(acc, a[1], b0[j + 4 + t4], b1[j + 4 + t4]);
+                                if (j + 8 < je) mv_step<(2 + R) & 3>(acc, a[2], b0[j + 8 + t4], b1[j + 8 + t4]);
                             }
-                        }
-                        for (; j < je; j += 4) {
-                            const int jj = j + t4;
-                            const double a = (rok && jj < m.len) ? A[(size_t)jj * m.lda] : 0.0;
-                            dmma8x8x4(d00, d01, a, b0[jj]);
-                            dmma8x8x4(d10, d11, a, b1[jj]);
-                        }
+                        };
+                        if (par) run(std::integral_constant<int, 2>{});
+                        else run(std::integral_constant<int, 0>{});
                     }
                 }
                 if (threadIdx.x == 0 && c0 == 0)
@@ -1397,18 +1466,462 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
                 const int ca = 2 * t4 + i, cb = 8 + 2 * t4 + i;
                 if (ca < nc) {
                     const size_t o = (task.r0 + r) + (size_t)(c0 + ca) * ld;
-                    const double s = i ? d01 : d00;
+                    const double s = mv_acc_sum(acc, i);
                     Y[o] = base ? base[o] - s : s;
                 }
                 if (cb < nc) {
                     const size_t o = (task.r0 + r) + (size_t)(c0 + cb) * ld;
-                    const double s = i ? d11 : d10;
+                    const double s = mv_acc_sum(acc, 2 + i);
                     Y[o] = base ? base[o] - s : s;
                 }
             }
         }
     }
     if (threadIdx.x == 0) add_flops(args.flops, F_APPLY, fl);
+}
+
+// ------------------------------------------------------------------ solve, phase 2 on the bulk-copy engine
+// k_mv_slab_tma: the same slab contraction as k_mv_slab (same leaf order, same k-steps of 4 per
+// leaf, one accumulator chain per output element: bitwise the same result), fed by TMA bulk
+// copies (cp.async.bulk global -> shared, completion on an mbarrier) instead of per-lane loads.
+// One CTA per (<= 64-row slab, item): warps 0-7 are consumers (warp w owns slab rows 8w .. 8w+7
+// and all 16 right-hand sides, DMMA fragments read from shared memory), warps 8-11 are producers
+// (one warp can issue a bulk copy only every ~57-90 cycles, four keep 512-byte copies at the HBM
+// rate: tools/tma_bench.cu, profiles/r02_tma_bench.txt).
+// The producers walk the slab's leaf list, resolves ranks and pointers (32 leaves per round,
+// one per lane), and packs leaves into the stages of a ring: a stage holds up to 64 operand
+// columns (each column's slab rows copied to its own 68-double slot: ld == 4 (mod 16), so the A
+// fragment loads are conflict-free) and the matching contracted vectors (the x chunk of a dense
+// leaf, 16 per-RHS copies; the padded T block of an Rk leaf, one copy).  Pad columns of the
+// last k-step of a leaf hold stale finite operand data and multiply zeros of the contracted
+// vector.  Sources or sizes that are not 16-byte aligned (odd cluster sizes) are copied by the
+// producer lanes with ordinary loads and stores.  HBM-bound by design: every stored entry is
+// read once, several stages (tens of KB per SM) are in flight, no register staging.
+constexpr int TS_STAGES = 4;
+constexpr int TS_SLOTS = 64;                 // operand column slots per stage
+constexpr int TS_ALD = 68;                   // slot stride in doubles
+constexpr int TS_XCAP = 1536;                // contracted-vector doubles per stage
+constexpr int TS_XLD = 68;                   // x chunk stride between right-hand sides
+constexpr int TS_MAXENT = 16;                // leaves per stage
+constexpr int TS_PROD = 4;                   // producer warps (one warp issues a bulk copy every ~57-90 cycles: tools/tma_bench.cu)
+constexpr int TS_NT = NT + 32 * TS_PROD;
+constexpr int TS_STAGE_DOUBLES = TS_SLOTS * TS_ALD + TS_XCAP;
+struct TsEnt {
+    short slot, ksteps, xoff, ldx, o0, o1, par, gm;  // par: parity of the leaf's position in the slab's list; gm > 0: 8-column groups of a gm-row dense leaf
+};
+struct TsDesc {
+    int nent, last;
+    int dirty;  // acquire count of the last use in which a producer lane wrote stage data with ordinary stores
+    int pad1;
+    TsEnt ent[TS_MAXENT];
+};
+struct TsMeta {        // one resolved, non-empty leaf of a slab (k_mv_resolve -> producers), 32 bytes
+    const double* A;   // operand column 0 at leaf row 0 (ld lda)
+    const double* xin; // dense: x at the leaf's first column (ld = dim); Rk: padded T block (first RHS group)
+    int len, lda;      // contracted length (columns / rank), operand leading dimension
+    short o0, o1;      // slab-relative output rows covered
+    short roff;        // o0's row inside the leaf
+    unsigned char dense, par;  // par: parity of the leaf's position in the slab's list
+};
+static_assert(sizeof(TsMeta) == 32, "TsMeta is one 32-byte record");
+constexpr size_t TS_SMEM = (size_t)TS_STAGES * TS_STAGE_DOUBLES * sizeof(double) + TS_STAGES * sizeof(TsDesc) +
+                           TS_PROD * 32 * sizeof(TsMeta) + 2 * TS_STAGES * sizeof(unsigned long long);
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    unsigned spins = 0;
+    while (!mbar_try(b, parity))
+        if (++spins > (1u << 27)) __trap();  // a lost arrival must not hang the device
+}
+// global -> shared bulk copy (TMA, SASS UBLKCP), bytes a multiple of 16, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// n doubles global -> shared by one lane: a bulk copy when everything is 16-byte aligned, else scalar
+__device__ __forceinline__ bool ts_copy(double* dst, const double* src, int n, unsigned long long* bar, unsigned& tx) {
+    if ((((unsigned long long)src | (unsigned long long)smem_u32(dst)) & 15ull) == 0 && (n & 1) == 0) {
+        bulk_g2s(dst, src, (unsigned)n * 8u, bar);
+        tx += (unsigned)n * 8u;
+        return false;
+    }
+    for (int i = 0; i < n; ++i) dst[i] = src[i];
+    return true;  // ordinary stores: the stage's next bulk copies need a proxy fence first
+}
+
+// Phase 1.5: one warp per (slab, item) resolves the slab's leaf list against the item's ranks and
+// pointers and writes the non-empty leaves as compact 32-byte records, in list order.  The
+// producers of k_mv_slab_tma then stream records (one coalesced load per 32 leaves, prefetched)
+// instead of chasing record -> rank -> pointer chains, which is what bounded them.
+__global__ void __launch_bounds__(NT) k_mv_resolve(MatvecArgs args, const MatvecTma tm, const __grid_constant__ MatvecBatch mb, const int ntasks) {
+    const int lane = threadIdx.x & 31;
+    const int ngroups = (args.nrhs + MV_RHS - 1) / MV_RHS;
+    const long total = (long)ntasks * mb.count;
+    const long npack = (long)tm.ncl * mb.count * ngroups;
+    const long stride = (long)gridDim.x * (NT / 32);
+    for (long w = (long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); w < total + npack; w += stride) {
+        if (w >= total) {
+            // pack task: the x entries of one leaf cluster, 16 right-hand sides, in contraction order
+            const long u = w - total;
+            const MvCluster C = tm.cl[u % tm.ncl];
+            const int gi = (int)((u / tm.ncl) % ngroups), b = (int)(u / ((long)tm.ncl * ngroups));
+            const double* x = mb.x[b] + C.in_off + (size_t)gi * MV_RHS * args.dim;
+            double* dst = tm.xp + ((size_t)b * ngroups + gi) * tm.xp_group + C.xoff;
+            const bool perm = (C.n & 31) == 0;
+            for (int e = lane; e < MV_RHS * C.ldx; e += 32) {
+                const int c = e / C.ldx, pp = e - c * C.ldx;
+                const int col = perm ? mv_col(pp) : pp;
+                dst[e] = (pp < C.n && gi * MV_RHS + c < args.nrhs) ? x[col + (size_t)c * args.dim] : 0.0;
+            }
+            continue;
+        }
+        const int t = (int)(w % ntasks), b = (int)(w / ntasks);
+        const SlabTask task = args.tasks[t];
+        const HView& H = mb.h[b];
+        double* const* Tp = mv_tptr(args) + (size_t)b * args.nrk;
+        TsMeta* out = (TsMeta*)tm.rec + (size_t)b * tm.nleaves + task.lbeg;
+        int n = 0;
+        for (int l0 = task.lbeg; l0 < task.lend; l0 += 32) {
+            TsMeta m{};
+            bool ok = false;
+            if (l0 + lane < task.lend) {
+                const ApplyLeaf L = args.leaves[l0 + lane];
+                const int o0 = max(task.r0, L.out_off), o1 = min(task.r1, L.out_off + L.m);
+                if (o0 < o1) {
+                    m.lda = L.m;
+                    m.o0 = (short)(o0 - task.r0);
+                    m.o1 = (short)(o1 - task.r0);
+                    m.roff = (short)(o0 - L.out_off);
+                    m.par = (unsigned char)((l0 + lane - task.lbeg) & 1);
+                    if (L.kind == K_DENSE) {
+                        m.A = H.dense + L.doff;
+                        m.len = L.n;
+                        // packed x block of the column cluster (tl < 0: not one leaf cluster -> raw x, per-RHS copies)
+                        m.xin = L.tl >= 0 ? tm.xp + (size_t)b * ngroups * tm.xp_group + L.tl : mb.x[b] + L.in_off;
+                        m.dense = L.tl >= 0 ? 1 : 2;
+                        ok = L.n > 0;
+                    } else {
+                        const int rr = H.rank[L.id];
+                        const double* T = rr > 0 ? Tp[L.id] : nullptr;
+                        if (T) {
+                            m.A = H.U[L.id];
+                            m.len = rr;
+                            m.xin = T;
+                            ok = true;
+                        }
+                    }
+                }
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, ok);
+            if (ok) out[n + __popc(mask & ((1u << lane) - 1u))] = m;
+            n += __popc(mask);
+        }
+        if (lane == 0) tm.rec_cnt[(size_t)b * ntasks + t] = n;
+    }
+}
+
+__global__ void __launch_bounds__(TS_NT, 1) k_mv_slab_tma(MatvecArgs args, const MatvecTma tm, const __grid_constant__ MatvecBatch mb, const int ntasks) {
+    extern __shared__ __align__(128) unsigned char ts_raw[];
+    double* stage0 = (double*)ts_raw;
+    TsDesc* desc = (TsDesc*)(stage0 + (size_t)TS_STAGES * TS_STAGE_DOUBLES);
+    TsMeta* meta_all = (TsMeta*)(desc + TS_STAGES);
+    unsigned long long* full = (unsigned long long*)(meta_all + TS_PROD * 32);
+    unsigned long long* empty = full + TS_STAGES;
+    const int ld = args.dim;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // persistent CTAs: work item w = (RHS group, item, slab), slab fastest (neighbouring CTAs share
+    // one item's x in L2); the stage ring runs on across work items, so the producers fetch the
+    // next slab while the consumers finish the current one
+    const int ngroups = (args.nrhs + MV_RHS - 1) / MV_RHS;
+    const long total_work = (long)ntasks * mb.count * ngroups;
+    // zeroed once: whatever a pad slot holds later is stale finite matrix data
+    for (int e = threadIdx.x; e < TS_STAGES * TS_STAGE_DOUBLES; e += TS_NT) stage0[e] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TS_STAGES; ++s) {
+            mbar_init(full + s, TS_PROD);
+            mbar_init(empty + s, NT / 32);
+            desc[s].dirty = -2 * TS_STAGES;
+        }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    int stage = 0;
+    unsigned phase = 0;
+    if (warp >= NT / 32) {
+        // ------------------------------------------------ producers: every producer warp runs the same
+        // packing (same decisions from the same data); warp pw issues the copies of the columns
+        // == pw (mod TS_PROD), warp 0 writes the descriptors and the zero pads
+        const int pw = warp - NT / 32;
+        TsMeta* meta = meta_all + pw * 32;
+        double fl = 0;
+        unsigned long long pc_wait = 0, pc_stages = 0, pc_ent = 0;
+        const unsigned long long pc_t0 = clock64();
+        int use = 0;  // stages acquired so far (the same sequence in every producer warp)
+        for (long w = blockIdx.x; w < total_work; w += gridDim.x) {
+            const SlabTask task = args.tasks[w % ntasks];
+            const int b = (int)((w / ntasks) % mb.count);
+            const int c0 = (int)(w / ((long)ntasks * mb.count)) * MV_RHS;
+            const int nc = min(MV_RHS, args.nrhs - c0);
+            int slots = 0, xs = 0, nent = 0;
+            unsigned tx = 0;
+            bool open = false;  // stage acquired (empty barrier passed)
+            double* As = nullptr;
+            double* Xs = nullptr;
+            auto acquire = [&]() {
+                const unsigned long long tw = clock64();
+                mbar_wait(empty + stage, phase ^ 1u);
+                pc_wait += clock64() - tw;
+                ++pc_stages;
+                // bulk copies over data this stage received by ordinary stores in its previous use
+                // (unaligned copies, zero pads) are ordered behind them by a proxy fence; the common
+                // path (aligned leaves, 16 right-hand sides) never needs it -- and must not pay it:
+                // the fence also waits for the bulk copies already in flight
+                if (desc[stage].dirty >= use - TS_STAGES) fence_proxy_async();
+                ++use;
+                As = stage0 + (size_t)stage * TS_STAGE_DOUBLES;
+                Xs = As + TS_SLOTS * TS_ALD;
+                slots = 0, xs = 0, nent = 0, tx = 0;
+                open = true;
+            };
+            auto commit = [&](int last) {
+                if (lane == 0 && pw == 0) {
+                    desc[stage].nent = nent;
+                    desc[stage].last = last;
+                }
+                tx = (unsigned)__reduce_add_sync(0xffffffffu, tx);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_tx(full + stage, tx);
+                stage = stage + 1 == TS_STAGES ? 0 : stage + 1;
+                phase ^= (stage == 0);
+                open = false;
+            };
+            const int nrec = tm.rec_cnt[(size_t)b * ntasks + (int)(w % ntasks)];
+            const TsMeta* recs = (const TsMeta*)tm.rec + (size_t)b * tm.nleaves + task.lbeg;
+            TsMeta nxt{};
+            if (lane < nrec) nxt = recs[lane];
+            for (int l0 = 0; l0 < nrec; l0 += 32) {
+                const int nl = min(32, nrec - l0);
+                __syncwarp();
+                meta[lane] = nxt;
+                if (l0 + 32 + lane < nrec) nxt = recs[l0 + 32 + lane];  // in flight while this batch is issued
+                __syncwarp();
+                for (int q = 0; q < nl; ++q) {
+                    const TsMeta m = meta[q];
+                    if (lane == 0 && pw == 0 && c0 == 0) fl += 2.0 * (m.o1 - m.o0) * m.len * args.nrhs;
+                    const int ldt = mv_ldt(m.len);
+                    const int n4 = (m.len + 3) & ~3;
+                    const int ldxp = n4 + ((20 - (n4 & 15)) & 15);  // packed-x stride of a dense leaf's column cluster
+                    // this RHS group's contracted vectors
+                    const double* xin = m.xin + (m.dense == 1 ? (size_t)(c0 / MV_RHS) * tm.xp_group
+                                                              : (size_t)c0 * (m.dense ? ld : ldt));
+                    const bool perm = m.dense && (m.len & 31) == 0;
+                    const int nrow = m.o1 - m.o0;
+                    for (int j0 = 0; j0 < m.len; j0 += TS_SLOTS) {
+                        const int plen = min(TS_SLOTS, m.len - j0);
+                        const int pslots = (plen + 3) & ~3;
+                        // one copy brings the contracted vectors: the packed x block of a dense leaf, the
+                        // padded T block of an Rk leaf that fits one piece
+                        const bool xblock = m.dense == 1 || (!m.dense && m.len <= TS_SLOTS);
+                        const int ldx = m.dense == 1 ? ldxp : (xblock ? ldt : TS_XLD);
+                        const int xneed = MV_RHS * ldx;
+                        // 8-column groups of a whole dense leaf (contiguous in the dense pool)
+                        const int gs = 8 * m.lda + 4;
+                        const bool grouped = perm && m.roff == 0 && nrow == m.lda && (m.lda & 1) == 0 &&
+                                             (((unsigned long long)m.A) & 15ull) == 0;
+                        const int aslots = grouped ? ((plen >> 3) * gs + TS_ALD - 1) / TS_ALD : pslots;
+                        if (open && (slots + aslots > TS_SLOTS || xs + xneed > TS_XCAP || nent == TS_MAXENT)) commit(0);
+                        if (!open) acquire();
+                        if (lane == 0 && pw == 0) {
+                            TsEnt e{(short)slots, (short)(pslots >> 2), (short)xs, (short)ldx, m.o0, m.o1, (short)m.par,
+                                    (short)(grouped ? m.lda : 0)};
+                            desc[stage].ent[nent] = e;
+                        }
+                        if (grouped) {
+                            const int G = pw + TS_PROD * lane;
+                            if (G < (plen >> 3))
+                                ts_copy(As + (size_t)slots * TS_ALD + (size_t)G * gs, m.A + (size_t)G * 8 * m.lda, 8 * m.lda,
+                                        full + stage, tx);  // aligned by the test above
+                        } else {
+                            for (int c = pw + TS_PROD * lane; c < plen; c += 32 * TS_PROD)
+                                if (ts_copy(As + (size_t)(slots + (perm ? mv_pos(c) : c)) * TS_ALD + m.o0,
+                                            m.A + (size_t)(j0 + c) * m.lda + m.roff, nrow, full + stage, tx))
+                                    desc[stage].dirty = use - 1;
+                        }
+                        double* xd = Xs + xs;
+                        if (xblock) {
+                            if (lane == 0 && pw == nent % TS_PROD && ts_copy(xd, xin, xneed, full + stage, tx))
+                                desc[stage].dirty = use - 1;
+                        } else {
+                            // per right-hand side: plen entries (raw x chunk, or rows j0.. of a wide T block), zero pads
+                            const int ldsrc = m.dense ? ld : ldt;
+                            const int c = pw + TS_PROD * lane;
+                            if (c < MV_RHS) {
+                                double* d = xd + (size_t)c * TS_XLD;
+                                bool wrote = pslots > plen || c >= nc;
+                                if (c < nc) {
+                                    if (perm) {
+                                        for (int j = 0; j < plen; ++j) d[j] = xin[mv_col(j) + (size_t)c * ldsrc];
+                                        wrote = true;
+                                    } else {
+                                        wrote |= ts_copy(d, xin + j0 + (size_t)c * ldsrc, plen, full + stage, tx);
+                                    }
+                                    for (int j = plen; j < pslots; ++j) d[j] = 0.0;
+                                } else {
+                                    for (int j = 0; j < pslots; ++j) d[j] = 0.0;
+                                }
+                                if (wrote) desc[stage].dirty = use - 1;
+                            }
+                        }
+                        slots += aslots;
+                        xs += xneed;
+                        ++nent;
+                        ++pc_ent;
+                    }
+                }
+            }
+            if (!open) acquire();
+            commit(1);
+        }
+        if (lane == 0 && pw == 0) {
+            add_flops(args.flops, F_APPLY, fl);
+            atomicAdd(&g_mv_cyc[4], pc_wait);
+            atomicAdd(&g_mv_cyc[5], pc_stages);
+            atomicAdd(&g_mv_cyc[6], pc_ent);
+            atomicAdd(&g_mv_cyc[7], clock64() - pc_t0);
+        }
+    } else {
+        // ------------------------------------------------ consumers
+        const int g = lane >> 2, t4 = lane & 3;
+        const int r = 8 * warp + g;  // this lane's slab row
+        unsigned long long cc_wait = 0, cc_work = 0;
+        const unsigned long long cc_t0 = clock64();
+        for (long w = blockIdx.x; w < total_work; w += gridDim.x) {
+            const SlabTask task = args.tasks[w % ntasks];
+            const int b = (int)((w / ntasks) % mb.count);
+            const int c0 = (int)(w / ((long)ntasks * mb.count)) * MV_RHS;
+            const double* base = mb.base[b];
+            double* Y = mb.y[b];
+            const int nc = min(MV_RHS, args.nrhs - c0);
+            double acc[4][4];  // [partial sum][rows 8w+g: RHS 2t4, 2t4+1 (tile 0), 8+2t4, 8+2t4+1 (tile 1)]
+            mv_acc_zero(acc);
+            // the base entries of this lane's four outputs, fetched ahead of the contraction
+            double bs[4] = {0.0, 0.0, 0.0, 0.0};
+            if (base && r < task.r1 - task.r0) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int ca = 2 * t4 + i, cb = 8 + 2 * t4 + i;
+                    if (ca < nc) bs[i] = base[(task.r0 + r) + (size_t)(c0 + ca) * ld];
+                    if (cb < nc) bs[2 + i] = base[(task.r0 + r) + (size_t)(c0 + cb) * ld];
+                }
+            }
+            for (;;) {
+                const unsigned long long tw0 = clock64();
+                mbar_wait(full + stage, phase);
+                const unsigned long long tw1 = clock64();
+                cc_wait += tw1 - tw0;
+                const double* As = stage0 + (size_t)stage * TS_STAGE_DOUBLES;
+                const double* Xs = As + TS_SLOTS * TS_ALD;
+                const TsDesc& D = desc[stage];
+                const int nent = D.nent, last = D.last;
+                for (int e = 0; e < nent; ++e) {
+                    const TsEnt E = D.ent[e];
+                    if (8 * warp >= E.o1 || 8 * warp + 8 <= E.o0) continue;  // no rows of this warp
+                    const bool rok = r >= E.o0 && r < E.o1;
+                    // per-column slots: position p at slot p (stride TS_ALD), rows at their slab position;
+                    // 8-column groups: k-step s = 8 v + u reads column u of group 4 v + t4 (group stride gs)
+                    const int gs = 8 * E.gm + 4;
+                    const double* A = E.gm ? As + (size_t)E.slot * TS_ALD + (size_t)t4 * gs + (r - E.o0)
+                                           : As + (size_t)E.slot * TS_ALD + r + (size_t)t4 * TS_ALD;
+                    const int st_u = E.gm ? E.gm : 4 * TS_ALD;        // stride of one k-step inside a block of 8
+                    const int st_v = E.gm ? 4 * gs - 8 * E.gm : 0;    // extra stride every 8 k-steps
+                    const double* b0 = Xs + E.xoff + g * E.ldx + t4;
+                    const double* b1 = b0 + 8 * E.ldx;
+                    const int ks = E.ksteps;
+                    auto run = [&](auto rot) {
+                        constexpr int R = decltype(rot)::value;
+                        int s = 0;
+                        for (; s + 4 <= ks; s += 4) {
+                            double a[4], x0[4], x1[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                a[q] = rok ? A[(size_t)(s + q) * st_u + (size_t)((s + q) >> 3) * st_v] : 0.0;
+                                x0[q] = b0[4 * (s + q)];
+                                x1[q] = b1[4 * (s + q)];
+                            }
+                            mv_step<(0 + R) & 3>(acc, a[0], x0[0], x1[0]);
+                            mv_step<(1 + R) & 3>(acc, a[1], x0[1], x1[1]);
+                            mv_step<(2 + R) & 3>(acc, a[2], x0[2], x1[2]);
+                            mv_step<(3 + R) & 3>(acc, a[3], x0[3], x1[3]);
+                        }
+                        if (s < ks) {
+                            double a[3], x0[3], x1[3];
+#pragma unroll
+                            for (int q = 0; q < 3; ++q) {
+                                const bool ok = s + q < ks;
+                                a[q] = (rok && ok) ? A[(size_t)(s + q) * st_u + (size_t)((s + q) >> 3) * st_v] : 0.0;
+                                x0[q] = ok ? b0[4 * (s + q)] : 0.0;
+                                x1[q] = ok ? b1[4 * (s + q)] : 0.0;
+                            }
+                            mv_step<(0 + R) & 3>(acc, a[0], x0[0], x1[0]);
+                            if (s + 1 < ks) mv_step<(1 + R) & 3>(acc, a[1], x0[1], x1[1]);
+                            if (s + 2 < ks) mv_step<(2 + R) & 3>(acc, a[2], x0[2], x1[2]);
+                        }
+                    };
+                    if (E.par) run(std::integral_constant<int, 2>{});
+                    else run(std::integral_constant<int, 0>{});
+                }
+                __syncwarp();
+                cc_work += clock64() - tw1;
+                if (lane == 0) mbar_arrive(empty + stage);
+                stage = stage + 1 == TS_STAGES ? 0 : stage + 1;
+                phase ^= (stage == 0);
+                if (last) break;
+            }
+            if (r < task.r1 - task.r0) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int ca = 2 * t4 + i, cb = 8 + 2 * t4 + i;
+                    if (ca < nc) {
+                        const size_t o = (task.r0 + r) + (size_t)(c0 + ca) * ld;
+                        const double sv = mv_acc_sum(acc, i);
+                        Y[o] = base ? bs[i] - sv : sv;
+                    }
+                    if (cb < nc) {
+                        const size_t o = (task.r0 + r) + (size_t)(c0 + cb) * ld;
+                        const double sv = mv_acc_sum(acc, 2 + i);
+                        Y[o] = base ? bs[2 + i] - sv : sv;
+                    }
+                }
+            }
+        }
+        if (threadIdx.x == 0) {
+            atomicAdd(&g_mv_cyc[0], 1ull);
+            atomicAdd(&g_mv_cyc[1], clock64() - cc_t0);
+            atomicAdd(&g_mv_cyc[2], cc_wait);
+            atomicAdd(&g_mv_cyc[3], cc_work);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ solve, few right-hand sides
@@ -2362,8 +2875,16 @@ std::string prof_report(bool reset) {
         snprintf(buf, sizeof(buf), "#phase warp32 tasks %llu (cycles per task): load %.0f qr %.0f jacobi %.0f sigma %.0f "
                  "write %.0f | sweeps %.2f rp %.2f\n", wc, w[0] / d, w[1] / d, w[2] / d, w[3] / d, w[4] / d, w[6] / d, w[7] / d);
         out += buf;
+        unsigned long long mv[8];
+        cudaMemcpyFromSymbol(mv, g_mv_cyc, sizeof(mv));
+        const double mc = mv[0] ? (double)mv[0] : 1.0;
+        snprintf(buf, sizeof(buf), "#phase mv-slab-tma CTAs %llu (kcycles per CTA): total %.1f consumer wait %.1f work %.1f | "
+                 "producer total %.1f wait-empty %.1f | stages %.1f entries %.1f per CTA\n", mv[0], mv[1] / mc / 1e3,
+                 mv[2] / mc / 1e3, mv[3] / mc / 1e3, mv[7] / mc / 1e3, mv[4] / mc / 1e3, mv[5] / mc, mv[6] / mc);
+        out += buf;
         if (reset) {
             const unsigned long long z8[8] = {};
+            cudaMemcpyToSymbol(g_mv_cyc, z8, sizeof(z8));
             cudaMemcpyToSymbol(g_w32_cyc, z8, sizeof(z8));
             cudaMemcpyToSymbol(g_w32_cnt, z8, sizeof(unsigned long long));
             const unsigned long long z[16] = {};
@@ -2400,6 +2921,7 @@ void setup_kernels() {
     cudaFuncSetAttribute(k_lu_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((2 * DENSE_MAX * DENSE_MAX + 2 * DENSE_MAX) * sizeof(double)));
     cudaFuncSetAttribute(k_sigma1_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem());
+    cudaFuncSetAttribute(k_mv_slab_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TS_SMEM);
 }
 
 void launch_truncate(cudaStream_t st, int ntasks, const TruncTask* tasks, const Part* parts, Slot* slots, int B,
@@ -2518,14 +3040,30 @@ void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const dou
     k_scale_reduce<<<B, 256, 0, st>>>(sig_d, nd, sig_k, nk, B, eps, abs_cut);
 }
 
-void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, const MvLeaf* rk,
-                   int nrk, int nbig, int nrhs, int dim, Arena arena, FlopLedger* flops, const MatvecBatch& mb) {
+void launch_matvec(cudaStream_t st, const MatvecPlan& mp, int nrhs, int dim, Arena arena, FlopLedger* flops, const MatvecBatch& mb) {
+    const int ntasks = mp.ntasks, nrk = mp.nrk, nbig = mp.nbig;
     if (ntasks == 0 || mb.count == 0) return;
-    MatvecArgs a{tasks, leaves, rk, nrk, nbig, nrhs, dim, arena, ledger(flops, "k_mv_t")};
+    // > 4 right-hand sides: phase 2 on the bulk-copy engine (ACRGPU_MV_LDG=1: the per-lane load kernel, A/B)
+    const char* mv_env = getenv("ACRGPU_MV_LDG");  // read per call: the tests flip it between two solves
+    const bool mv_ldg = mv_env && atoi(mv_env) != 0;
+    // transient arena: [T pointers: count x nrk] [record counts: count x ntasks ints] [records: count x
+    // nleaves x 32 bytes] [packed x: count x RHS groups x xp_group] then the bump-allocated T blocks
+    const int ngroups = (nrhs + MV_RHS - 1) / MV_RHS;
+    const unsigned long long tbl = ((unsigned long long)mb.count * nrk + 15ull) & ~15ull;
+    const unsigned long long cnt_d = (((unsigned long long)mb.count * ntasks + 1) / 2 + 15ull) & ~15ull;
+    const unsigned long long rec_d = ((unsigned long long)mb.count * mp.nleaves * 4 + 15ull) & ~15ull;
+    const unsigned long long xp_d = ((unsigned long long)mb.count * ngroups * mp.xp_group + 15ull) & ~15ull;
+    const bool tma = nrhs > 4 && !mv_ldg && tbl + cnt_d + rec_d + xp_d < arena.cap / 2;
+    MatvecArgs a{mp.tasks, mp.leaves, mp.rk, nrk, nbig, nrhs, dim, arena, ledger(flops, "k_mv_t"), tma ? 1 : 0};
+    MatvecTma tm{mp.nleaves, nullptr, nullptr, mp.cl, mp.ncl, mp.xp_group, nullptr};
+    if (tma) {
+        tm.rec_cnt = (int*)(arena.base + tbl);
+        tm.rec = (void*)(arena.base + tbl + cnt_d);
+        tm.xp = arena.base + tbl + cnt_d + rec_d;
+    }
     {
-        // T pointer table [count][nrk] at the arena base, T blocks bump-allocated after it
         ProfScope _ps(st, "k_set_counter", 1);
-        k_set_counter<<<1, 1, 0, st>>>(arena.ctr, ((unsigned long long)mb.count * nrk + 15ull) & ~15ull);
+        k_set_counter<<<1, 1, 0, st>>>(arena.ctr, tma ? tbl + cnt_d + rec_d + xp_d : tbl);
     }
     // 1-4 right-hand sides: FMA-pipe kernels (lane = row / column, no padding);
     // more: 16-column DMMA tiles
@@ -2539,12 +3077,21 @@ void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const App
         else if (nr == 4) k_mv_t1<4><<<grid, NT, 0, st>>>(a, mb);
         else k_mv_t<<<grid, NT, 0, st>>>(a, mb);
     }
+    if (a.tma) {
+        const long warps = (long)ntasks * mb.count + (long)mp.ncl * mb.count * ngroups;
+        ProfScope _ps(st, "k_mv_resolve", warps);
+        k_mv_resolve<<<warp_grid(warps), NT, 0, st>>>(a, tm, mb, ntasks);
+    }
     a.flops = ledger(flops, "k_mv_slab");
     ProfScope _ps(st, "k_mv_slab", (long)ntasks * mb.count);
     const dim3 grid(ntasks, mb.count), grid1(2 * ntasks, mb.count);
     if (nr == 1) k_mv_slab1<1><<<grid1, NT, 0, st>>>(a, mb);
     else if (nr == 2) k_mv_slab1<2><<<grid1, NT, 0, st>>>(a, mb);
     else if (nr == 4) k_mv_slab1<4><<<grid1, NT, 0, st>>>(a, mb);
+    else if (a.tma) {
+        const long work = (long)ntasks * mb.count * ngroups;
+        k_mv_slab_tma<<<(unsigned)(work < 148 ? work : 148), TS_NT, TS_SMEM, st>>>(a, tm, mb, ntasks);
+    }
     else k_mv_slab<<<grid, NT, 0, st>>>(a, mb);
 }
 void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs) {

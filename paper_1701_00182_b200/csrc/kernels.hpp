@@ -112,8 +112,7 @@ void launch_scale_reduce(cudaStream_t st, const double* sig_d, int nd, const dou
                          double* abs_cut);
 // Batched solve matvec y = base - H x (two phases, see kernels.cu).  arena: transient
 // workspace (reset by the call) for the per-leaf V^T x blocks.
-void launch_matvec(cudaStream_t st, int ntasks, const SlabTask* tasks, const ApplyLeaf* leaves, const MvLeaf* rk,
-                   int nrk, int nbig, int nrhs, int dim, Arena arena, FlopLedger* flops, const MatvecBatch& mb);
+void launch_matvec(cudaStream_t st, const MatvecPlan& mp, int nrhs, int dim, Arena arena, FlopLedger* flops, const MatvecBatch& mb);
 void launch_permute_in(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs);
 void launch_permute_out(cudaStream_t st, const double* in, double* out, const int* perm, int n, int dim, int nrhs);
 void launch_zero_views(cudaStream_t st, const BatchViews& bv, long dsize, int nk);

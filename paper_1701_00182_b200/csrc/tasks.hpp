@@ -169,6 +169,21 @@ struct MvLeaf {         // Rk leaf k of the root: columns [in_off, in_off + n), 
     int in_off;
     int n, m;
 };
+struct MvCluster {      // leaf cluster of the plane: packed-x block of its columns (k_mv_slab_tma)
+    int in_off, n;      // first tree position, size
+    int xoff, ldx;      // block offset (doubles, inside one item's RHS group) and its RHS stride
+};
+struct MatvecPlan {     // per-structure tables of the solve's batched H-matvec
+    int ntasks;
+    const SlabTask* tasks;
+    const ApplyLeaf* leaves;  // slab leaves; dense leaves carry their column cluster's xoff in `tl`
+    int nleaves;
+    const MvLeaf* rk;
+    int nrk, nbig;
+    const MvCluster* cl;
+    int ncl;
+    long xp_group;      // packed-x doubles per (item, RHS group)
+};
 struct MatvecBatch {
     int count;
     HView h[MAXB];

@@ -145,6 +145,28 @@ def test_multi_rhs_bitwise_and_linearity(acr):                                  
     assert np.linalg.norm(u3 - (2.0 * u1 - 0.5 * u2)) <= 1e-12 * np.linalg.norm(u3)
 
 
+@pytest.mark.parametrize("k,n,nrhs", [(5, 16, 16), (5, 32, 16), (2, 16, 5), (1, 10, 7), (3, 14, 20), (2, 22, 33)])
+def test_bulk_copy_slab_kernel_is_bitwise_the_load_kernel(acr, monkeypatch, k, n, nrhs):
+    # Solves with more than 4 right-hand sides run phase 2 of the H-matvec on the TMA bulk-copy
+    # engine (k_mv_slab_tma: cp.async.bulk into a shared-memory ring, DMMA from shared memory).
+    # It performs the per-lane load kernel's arithmetic (k_mv_slab, ACRGPU_MV_LDG=1) in the same
+    # order, so the solutions are bitwise equal -- including plane sizes whose leaf clusters are
+    # odd (n = 10: 25-point leaves; n = 14: {24, 25}; n = 22: {30, 31}), which take the unaligned
+    # copy path, right-hand-side counts that are not multiples of 16, and several 16-column passes.
+    c = P.CONFIGS[k]
+    sysm = P.config_system(k, n=n)
+    f = acr.acr_factor(sysm, acr.AcrConfig(eps=c["eps"], leaf_size=c["leaf"]))
+    g = P.uniform_pm1(77, k, nrhs * sysm.rhs[0].size).reshape((nrhs,) + sysm.rhs[0].shape)
+    u_tma = f.solve(g)
+    monkeypatch.setenv("ACRGPU_MV_LDG", "1")
+    u_ldg = f.solve(g)
+    monkeypatch.delenv("ACRGPU_MV_LDG")
+    assert np.array_equal(u_tma, u_ldg)
+    assert np.array_equal(f.solve(g), u_tma)
+    for j in (0, nrhs - 1):
+        assert sysm.relative_residual(u_tma[j:j + 1], g[j:j + 1]) <= 1e-4
+
+
 def test_factorization_deterministic(acr):
     sysm = P.config_system(3, n=16)
     cfg = acr.AcrConfig(eps=1e-6)

@@ -30,7 +30,7 @@ u_dev = torch.empty_like(f_dev)
 f.solve_device(f_dev.data_ptr(), u_dev.data_ptr(), nrhs)
 res = sysm.relative_residual(u_dev.cpu().numpy())
 acr.profile_report(reset=True)
-acr.profile_select("k_mv_t,k_mv_slab")
+acr.profile_select("k_mv_t,k_mv_slab,k_mv_resolve")
 ms = []
 for _ in range(reps):
     f.solve_device(f_dev.data_ptr(), u_dev.data_ptr(), nrhs)
@@ -39,12 +39,14 @@ torch.cuda.synchronize()
 rows = {}
 for line in acr.profile_report(reset=True).splitlines():
     p = line.split()
+    if line.startswith("#phase mv") or line.startswith("#top"):
+        print(line, file=sys.stderr)
     if line.startswith("#") or len(p) < 5:
         continue
     rows[p[0]] = dict(ms=float(p[1]) / reps, launches=int(p[2]) // reps, flops=float(p[4]) / reps)
 acr.profile_select(None)
 fl = sum(r["flops"] for r in rows.values())
-kms = sum(r["ms"] for r in rows.values())
+kms = sum(r["ms"] for r in rows.values())  # k_mv_t + k_mv_resolve (records, packed x) + k_mv_slab
 bytes_h = 8.0 * fl / (2.0 * nrhs)
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
 out = dict(config=cfgk, n=sysm.n, nrhs=nrhs, residual=res, solve_ms=sorted(ms)[len(ms) // 2], solve_ms_all=ms,
