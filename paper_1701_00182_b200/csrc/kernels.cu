@@ -58,13 +58,48 @@ __device__ double* arena_alloc(const Arena& a, unsigned long long n) {
     return a.base + off;
 }
 
+// ------------------------------------------------------------------ TMA bulk copies and mbarriers (PTX)
+// cp.async.bulk global -> shared (SASS UBLKCP) completing on an mbarrier by transaction bytes; used by
+// the solve's slab kernel (k_mv_slab_tma) and by the dense-leaf staging of k_dd_product.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    unsigned spins = 0;
+    while (!mbar_try(b, parity))
+        if (++spins > (1u << 27)) __trap();  // a lost arrival must not hang the device
+}
+// global -> shared bulk copy (TMA, SASS UBLKCP), bytes a multiple of 16, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // QR-route phase timing (clock64 deltas of thread 0, summed over CTAs): diagnostics only
 __device__ unsigned long long g_phase_cyc[16];
 __device__ unsigned long long g_phase_cnt;
 // k_mv_slab_tma diagnostics (warp 0 / producer warp 0, lane 0): CTAs, CTA cycles, consumer cycles
 // waiting for a full stage, consumer cycles between wait and release, producer cycles waiting for
 // an empty stage, stages, leaf entries, producer cycles
-__device__ unsigned long long g_mv_cyc[8];
+__device__ unsigned long long g_mv_cyc[16];
 #define PHASE_MARK(i)                                                          \
     do {                                                                       \
         if (threadIdx.x == 0) {                                                \
@@ -534,7 +569,37 @@ __global__ void __launch_bounds__(NT, 1) k_dd_product(DDArgs args, BatchViews bv
             add_flops(args.flops, F_SKIP, fsvd + fqr + fgemm);
         }
     };
-    {
+    // Both leaves are contiguous in their dense pools: when sizes and addresses are 16-byte aligned
+    // (always, for even leaf sizes) one thread brings them in as two TMA bulk copies on one mbarrier
+    // -- both in flight at once, no register staging -- and the zero tests read shared memory.
+    __shared__ unsigned long long dd_bar;
+    const bool bulk = ((m * k) & 1) == 0 && ((k * n) & 1) == 0 &&
+                      ((((unsigned long long)Ad | (unsigned long long)Bd) & 15ull) == 0) && ((smem_u32(As) | smem_u32(Bs)) & 15u) == 0;
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            mbar_init(&dd_bar, 1);
+            fence_proxy_async();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            mbar_arrive_tx(&dd_bar, (unsigned)(m * k + k * n) * 8u);
+            bulk_g2s(As, Ad, (unsigned)(m * k) * 8u, &dd_bar);
+            bulk_g2s(Bs, Bd, (unsigned)(k * n) * 8u, &dd_bar);
+        }
+        mbar_wait(&dd_bar, 0);
+        int nz = 0;
+        for (int e = threadIdx.x; e < m * k; e += NT) nz |= As[e] != 0.0;
+        if (!__syncthreads_or(nz)) {
+            zero_product();
+            return;
+        }
+        nz = 0;
+        for (int e = threadIdx.x; e < k * n; e += NT) nz |= Bs[e] != 0.0;
+        if (!__syncthreads_or(nz)) {
+            zero_product();
+            return;
+        }
+    } else {
         int nz = 0;
         for (int e = threadIdx.x; e < m * k; e += NT) {
             const double v = Ad[e];
@@ -1497,10 +1562,10 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
 // vector.  Sources or sizes that are not 16-byte aligned (odd cluster sizes) are copied by the
 // producer lanes with ordinary loads and stores.  HBM-bound by design: every stored entry is
 // read once, several stages (tens of KB per SM) are in flight, no register staging.
-constexpr int TS_STAGES = 4;
+constexpr int TS_STAGES = 2;                 // per CTA; two CTAs per SM
 constexpr int TS_SLOTS = 64;                 // operand column slots per stage
 constexpr int TS_ALD = 68;                   // slot stride in doubles
-constexpr int TS_XCAP = 1536;                // contracted-vector doubles per stage
+constexpr int TS_XCAP = 1152;                // contracted-vector doubles per stage
 constexpr int TS_XLD = 68;                   // x chunk stride between right-hand sides
 constexpr int TS_MAXENT = 16;                // leaves per stage
 constexpr int TS_PROD = 4;                   // producer warps (one warp issues a bulk copy every ~57-90 cycles: tools/tma_bench.cu)
@@ -1515,49 +1580,24 @@ struct TsDesc {
     int pad1;
     TsEnt ent[TS_MAXENT];
 };
-struct TsMeta {        // one resolved, non-empty leaf of a slab (k_mv_resolve -> producers), 32 bytes
+enum : unsigned char { TF_GROUPED = 1, TF_PERM = 2, TF_XBLOCK = 4, TF_BRK = 8, TF_WIDE = 16 };
+struct TsMeta {        // one resolved, non-empty leaf of a slab with its place in the stage ring (k_mv_resolve -> producers)
     const double* A;   // operand column 0 at leaf row 0 (ld lda)
-    const double* xin; // dense: x at the leaf's first column (ld = dim); Rk: padded T block (first RHS group)
+    const double* xin; // contracted vectors of the first RHS group: packed x block / raw x / padded T block
     int len, lda;      // contracted length (columns / rank), operand leading dimension
-    short o0, o1;      // slab-relative output rows covered
+    int ldsrc;         // per-RHS copies (raw x, wide T block): source stride between right-hand sides
+    int gstride;       // xin stride between RHS groups (doubles)
+    TsEnt ent;         // the stage entry, precomputed (wide leaves: o0 / o1 / par only)
     short roff;        // o0's row inside the leaf
-    unsigned char dense, par;  // par: parity of the leaf's position in the slab's list
+    short aslots;      // operand slots taken
+    int xneed;         // contracted-vector doubles taken
+    unsigned char flags;  // TF_GROUPED: 8-column groups; TF_PERM: mv_col order; TF_XBLOCK: one copy brings the vectors;
+                          // TF_BRK: commit the open stage first; TF_WIDE: more than TS_SLOTS columns, one stage per piece
+    unsigned char pad[7];
 };
-static_assert(sizeof(TsMeta) == 32, "TsMeta is one 32-byte record");
+static_assert(sizeof(TsMeta) == 64, "TsMeta is one 64-byte record");
 constexpr size_t TS_SMEM = (size_t)TS_STAGES * TS_STAGE_DOUBLES * sizeof(double) + TS_STAGES * sizeof(TsDesc) +
                            TS_PROD * 32 * sizeof(TsMeta) + 2 * TS_STAGES * sizeof(unsigned long long);
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
-    unsigned ok;
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-    unsigned spins = 0;
-    while (!mbar_try(b, parity))
-        if (++spins > (1u << 27)) __trap();  // a lost arrival must not hang the device
-}
-// global -> shared bulk copy (TMA, SASS UBLKCP), bytes a multiple of 16, both addresses 16-byte aligned
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // n doubles global -> shared by one lane: a bulk copy when everything is 16-byte aligned, else scalar
 __device__ __forceinline__ bool ts_copy(double* dst, const double* src, int n, unsigned long long* bar, unsigned& tx) {
@@ -1602,6 +1642,10 @@ __global__ void __launch_bounds__(NT) k_mv_resolve(MatvecArgs args, const Matvec
         double* const* Tp = mv_tptr(args) + (size_t)b * args.nrk;
         TsMeta* out = (TsMeta*)tm.rec + (size_t)b * tm.nleaves + task.lbeg;
         int n = 0;
+        // packing state of the stage ring (the producers follow the TF_BRK flags): slots and
+        // contracted-vector doubles used and entries in the open stage
+        int slots = 0, xs = 0, nent = 0;
+        bool have_open = false, force = false;
         for (int l0 = task.lbeg; l0 < task.lend; l0 += 32) {
             TsMeta m{};
             bool ok = false;
@@ -1610,16 +1654,19 @@ __global__ void __launch_bounds__(NT) k_mv_resolve(MatvecArgs args, const Matvec
                 const int o0 = max(task.r0, L.out_off), o1 = min(task.r1, L.out_off + L.m);
                 if (o0 < o1) {
                     m.lda = L.m;
-                    m.o0 = (short)(o0 - task.r0);
-                    m.o1 = (short)(o1 - task.r0);
+                    m.ent.o0 = (short)(o0 - task.r0);
+                    m.ent.o1 = (short)(o1 - task.r0);
                     m.roff = (short)(o0 - L.out_off);
-                    m.par = (unsigned char)((l0 + lane - task.lbeg) & 1);
+                    m.ent.par = (short)((l0 + lane - task.lbeg) & 1);
+                    int dense = 0;
                     if (L.kind == K_DENSE) {
                         m.A = H.dense + L.doff;
                         m.len = L.n;
                         // packed x block of the column cluster (tl < 0: not one leaf cluster -> raw x, per-RHS copies)
-                        m.xin = L.tl >= 0 ? tm.xp + (size_t)b * ngroups * tm.xp_group + L.tl : mb.x[b] + L.in_off;
-                        m.dense = L.tl >= 0 ? 1 : 2;
+                        dense = L.tl >= 0 ? 1 : 2;
+                        m.xin = dense == 1 ? tm.xp + (size_t)b * ngroups * tm.xp_group + L.tl : mb.x[b] + L.in_off;
+                        m.gstride = dense == 1 ? (int)tm.xp_group : MV_RHS * args.dim;
+                        m.ldsrc = args.dim;
                         ok = L.n > 0;
                     } else {
                         const int rr = H.rank[L.id];
@@ -1628,12 +1675,57 @@ __global__ void __launch_bounds__(NT) k_mv_resolve(MatvecArgs args, const Matvec
                             m.A = H.U[L.id];
                             m.len = rr;
                             m.xin = T;
+                            m.gstride = MV_RHS * mv_ldt(rr);
+                            m.ldsrc = mv_ldt(rr);
                             ok = true;
                         }
+                    }
+                    if (ok) {
+                        const int n4 = (m.len + 3) & ~3;
+                        const bool perm = dense && (m.len & 31) == 0;
+                        const bool wide = m.len > TS_SLOTS;
+                        const bool xblock = dense == 1 || (!dense && !wide);
+                        const int ldx = dense == 1 ? n4 + ((20 - (n4 & 15)) & 15) : (xblock ? mv_ldt(m.len) : TS_XLD);
+                        const int gs = 8 * m.lda + 4;
+                        const bool grouped = perm && !wide && m.roff == 0 && o1 - o0 == m.lda && (m.lda & 1) == 0 &&
+                                             (((unsigned long long)m.A) & 15ull) == 0;
+                        m.aslots = (short)(grouped ? ((m.len >> 3) * gs + TS_ALD - 1) / TS_ALD : n4);
+                        m.xneed = MV_RHS * ldx;
+                        m.ent.ksteps = (short)(n4 >> 2);
+                        m.ent.ldx = (short)ldx;
+                        m.ent.gm = (short)(grouped ? m.lda : 0);
+                        m.flags = (grouped ? TF_GROUPED : 0) | (perm ? TF_PERM : 0) | (xblock ? TF_XBLOCK : 0) | (wide ? TF_WIDE : 0);
                     }
                 }
             }
             const unsigned mask = __ballot_sync(0xffffffffu, ok);
+            // the packing is sequential in list order: walk the batch's non-empty leaves
+            for (unsigned rest = mask; rest; rest &= rest - 1) {
+                const int i = __ffs(rest) - 1;
+                const int as_i = __shfl_sync(0xffffffffu, (int)m.aslots, i), xn_i = __shfl_sync(0xffffffffu, m.xneed, i);
+                const bool wide_i = (__shfl_sync(0xffffffffu, (int)m.flags, i) & TF_WIDE) != 0;
+                bool brk;
+                if (wide_i) {  // every piece takes a stage of its own; the next leaf starts a new one
+                    brk = have_open;
+                    slots = xs = nent = 0;
+                    have_open = true;
+                    force = true;
+                    if (lane == i && brk) m.flags |= TF_BRK;
+                } else {
+                    brk = have_open && (force || slots + as_i > TS_SLOTS || xs + xn_i > TS_XCAP || nent == TS_MAXENT);
+                    if (brk || !have_open) slots = xs = nent = 0;
+                    if (lane == i) {
+                        m.ent.slot = (short)slots;
+                        m.ent.xoff = (short)xs;
+                        if (brk) m.flags |= TF_BRK;
+                    }
+                    slots += as_i;
+                    xs += xn_i;
+                    ++nent;
+                    have_open = true;
+                    force = false;
+                }
+            }
             if (ok) out[n + __popc(mask & ((1u << lane) - 1u))] = m;
             n += __popc(mask);
         }
@@ -1641,7 +1733,7 @@ __global__ void __launch_bounds__(NT) k_mv_resolve(MatvecArgs args, const Matvec
     }
 }
 
-__global__ void __launch_bounds__(TS_NT, 1) k_mv_slab_tma(MatvecArgs args, const MatvecTma tm, const __grid_constant__ MatvecBatch mb, const int ntasks) {
+__global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const MatvecTma tm, const __grid_constant__ MatvecBatch mb, const int ntasks) {
     extern __shared__ __align__(128) unsigned char ts_raw[];
     double* stage0 = (double*)ts_raw;
     TsDesc* desc = (TsDesc*)(stage0 + (size_t)TS_STAGES * TS_STAGE_DOUBLES);
@@ -1675,7 +1767,7 @@ __global__ void __launch_bounds__(TS_NT, 1) k_mv_slab_tma(MatvecArgs args, const
         const int pw = warp - NT / 32;
         TsMeta* meta = meta_all + pw * 32;
         double fl = 0;
-        unsigned long long pc_wait = 0, pc_stages = 0, pc_ent = 0;
+        unsigned long long pc_wait = 0, pc_stages = 0, pc_ent = 0, pc_meta = 0, pc_copy = 0, pc_commit = 0, pc_items = 0;
         const unsigned long long pc_t0 = clock64();
         int use = 0;  // stages acquired so far (the same sequence in every producer warp)
         for (long w = blockIdx.x; w < total_work; w += gridDim.x) {
@@ -1705,6 +1797,7 @@ __global__ void __launch_bounds__(TS_NT, 1) k_mv_slab_tma(MatvecArgs args, const
                 open = true;
             };
             auto commit = [&](int last) {
+                const unsigned long long tc0 = clock64();
                 if (lane == 0 && pw == 0) {
                     desc[stage].nent = nent;
                     desc[stage].last = last;
@@ -1715,7 +1808,10 @@ __global__ void __launch_bounds__(TS_NT, 1) k_mv_slab_tma(MatvecArgs args, const
                 stage = stage + 1 == TS_STAGES ? 0 : stage + 1;
                 phase ^= (stage == 0);
                 open = false;
+                pc_commit += clock64() - tc0;
             };
+            const unsigned long long tm0 = clock64();
+            ++pc_items;
             const int nrec = tm.rec_cnt[(size_t)b * ntasks + (int)(w % ntasks)];
             const TsMeta* recs = (const TsMeta*)tm.rec + (size_t)b * tm.nleaves + task.lbeg;
             TsMeta nxt{};
@@ -1726,77 +1822,79 @@ __global__ void __launch_bounds__(TS_NT, 1) k_mv_slab_tma(MatvecArgs args, const
                 meta[lane] = nxt;
                 if (l0 + 32 + lane < nrec) nxt = recs[l0 + 32 + lane];  // in flight while this batch is issued
                 __syncwarp();
+                if (l0 == 0) pc_meta += clock64() - tm0;
                 for (int q = 0; q < nl; ++q) {
                     const TsMeta m = meta[q];
-                    if (lane == 0 && pw == 0 && c0 == 0) fl += 2.0 * (m.o1 - m.o0) * m.len * args.nrhs;
-                    const int ldt = mv_ldt(m.len);
-                    const int n4 = (m.len + 3) & ~3;
-                    const int ldxp = n4 + ((20 - (n4 & 15)) & 15);  // packed-x stride of a dense leaf's column cluster
-                    // this RHS group's contracted vectors
-                    const double* xin = m.xin + (m.dense == 1 ? (size_t)(c0 / MV_RHS) * tm.xp_group
-                                                              : (size_t)c0 * (m.dense ? ld : ldt));
-                    const bool perm = m.dense && (m.len & 31) == 0;
-                    const int nrow = m.o1 - m.o0;
-                    for (int j0 = 0; j0 < m.len; j0 += TS_SLOTS) {
-                        const int plen = min(TS_SLOTS, m.len - j0);
-                        const int pslots = (plen + 3) & ~3;
-                        // one copy brings the contracted vectors: the packed x block of a dense leaf, the
-                        // padded T block of an Rk leaf that fits one piece
-                        const bool xblock = m.dense == 1 || (!m.dense && m.len <= TS_SLOTS);
-                        const int ldx = m.dense == 1 ? ldxp : (xblock ? ldt : TS_XLD);
-                        const int xneed = MV_RHS * ldx;
-                        // 8-column groups of a whole dense leaf (contiguous in the dense pool)
-                        const int gs = 8 * m.lda + 4;
-                        const bool grouped = perm && m.roff == 0 && nrow == m.lda && (m.lda & 1) == 0 &&
-                                             (((unsigned long long)m.A) & 15ull) == 0;
-                        const int aslots = grouped ? ((plen >> 3) * gs + TS_ALD - 1) / TS_ALD : pslots;
-                        if (open && (slots + aslots > TS_SLOTS || xs + xneed > TS_XCAP || nent == TS_MAXENT)) commit(0);
+                    const int nrow = m.ent.o1 - m.ent.o0;
+                    if (lane == 0 && pw == 0 && c0 == 0) fl += 2.0 * nrow * m.len * args.nrhs;
+                    const double* xin = m.xin + (size_t)(c0 / MV_RHS) * m.gstride;  // this RHS group's contracted vectors
+                    if (!(m.flags & TF_WIDE)) {
+                        // the stage entry and its place were computed by k_mv_resolve
+                        if ((m.flags & TF_BRK) && open) commit(0);
                         if (!open) acquire();
-                        if (lane == 0 && pw == 0) {
-                            TsEnt e{(short)slots, (short)(pslots >> 2), (short)xs, (short)ldx, m.o0, m.o1, (short)m.par,
-                                    (short)(grouped ? m.lda : 0)};
-                            desc[stage].ent[nent] = e;
-                        }
-                        if (grouped) {
-                            const int G = pw + TS_PROD * lane;
-                            if (G < (plen >> 3))
-                                ts_copy(As + (size_t)slots * TS_ALD + (size_t)G * gs, m.A + (size_t)G * 8 * m.lda, 8 * m.lda,
-                                        full + stage, tx);  // aligned by the test above
+                        if (lane == 0 && pw == 0) desc[stage].ent[nent] = m.ent;
+                        const unsigned long long tk0 = clock64();
+                        double* Ad = As + (size_t)m.ent.slot * TS_ALD;
+                        if (m.flags & TF_GROUPED) {
+                            const int G = pw + TS_PROD * lane, gs = 8 * m.lda + 4;
+                            if (G < (m.len >> 3))
+                                ts_copy(Ad + (size_t)G * gs, m.A + (size_t)G * 8 * m.lda, 8 * m.lda, full + stage, tx);  // aligned (k_mv_resolve)
                         } else {
-                            for (int c = pw + TS_PROD * lane; c < plen; c += 32 * TS_PROD)
-                                if (ts_copy(As + (size_t)(slots + (perm ? mv_pos(c) : c)) * TS_ALD + m.o0,
-                                            m.A + (size_t)(j0 + c) * m.lda + m.roff, nrow, full + stage, tx))
+                            for (int c = pw + TS_PROD * lane; c < m.len; c += 32 * TS_PROD)
+                                if (ts_copy(Ad + (size_t)((m.flags & TF_PERM) ? mv_pos(c) : c) * TS_ALD + m.ent.o0,
+                                            m.A + (size_t)c * m.lda + m.roff, nrow, full + stage, tx))
                                     desc[stage].dirty = use - 1;
                         }
-                        double* xd = Xs + xs;
-                        if (xblock) {
-                            if (lane == 0 && pw == nent % TS_PROD && ts_copy(xd, xin, xneed, full + stage, tx))
+                        double* xd = Xs + m.ent.xoff;
+                        if (m.flags & TF_XBLOCK) {
+                            if (lane == 0 && pw == nent % TS_PROD && ts_copy(xd, xin, m.xneed, full + stage, tx))
                                 desc[stage].dirty = use - 1;
                         } else {
-                            // per right-hand side: plen entries (raw x chunk, or rows j0.. of a wide T block), zero pads
-                            const int ldsrc = m.dense ? ld : ldt;
-                            const int c = pw + TS_PROD * lane;
+                            // raw x of a dense leaf whose columns are not one leaf cluster: per right-hand side
+                            const int c = pw + TS_PROD * lane, pslots = 4 * m.ent.ksteps;
                             if (c < MV_RHS) {
                                 double* d = xd + (size_t)c * TS_XLD;
+                                if (c < nc) {
+                                    for (int j = 0; j < m.len; ++j) d[j] = xin[((m.flags & TF_PERM) ? mv_col(j) : j) + (size_t)c * m.ldsrc];
+                                    for (int j = m.len; j < pslots; ++j) d[j] = 0.0;
+                                } else {
+                                    for (int j = 0; j < pslots; ++j) d[j] = 0.0;
+                                }
+                                desc[stage].dirty = use - 1;
+                            }
+                        }
+                        pc_copy += clock64() - tk0;
+                        ++nent;
+                        ++pc_ent;
+                    } else {
+                        // more than TS_SLOTS columns (an Rk leaf of rank > 64): one stage per piece of 64
+                        for (int j0 = 0; j0 < m.len; j0 += TS_SLOTS) {
+                            const int plen = min(TS_SLOTS, m.len - j0), pslots = (plen + 3) & ~3;
+                            if (open) commit(0);
+                            acquire();
+                            if (lane == 0 && pw == 0) {
+                                TsEnt e{0, (short)(pslots >> 2), 0, (short)TS_XLD, m.ent.o0, m.ent.o1, m.ent.par, 0};
+                                desc[stage].ent[0] = e;
+                            }
+                            for (int c = pw + TS_PROD * lane; c < plen; c += 32 * TS_PROD)
+                                if (ts_copy(As + (size_t)c * TS_ALD + m.ent.o0, m.A + (size_t)(j0 + c) * m.lda + m.roff, nrow,
+                                            full + stage, tx))
+                                    desc[stage].dirty = use - 1;
+                            const int c = pw + TS_PROD * lane;
+                            if (c < MV_RHS) {
+                                double* d = Xs + (size_t)c * TS_XLD;
                                 bool wrote = pslots > plen || c >= nc;
                                 if (c < nc) {
-                                    if (perm) {
-                                        for (int j = 0; j < plen; ++j) d[j] = xin[mv_col(j) + (size_t)c * ldsrc];
-                                        wrote = true;
-                                    } else {
-                                        wrote |= ts_copy(d, xin + j0 + (size_t)c * ldsrc, plen, full + stage, tx);
-                                    }
+                                    wrote |= ts_copy(d, xin + j0 + (size_t)c * m.ldsrc, plen, full + stage, tx);
                                     for (int j = plen; j < pslots; ++j) d[j] = 0.0;
                                 } else {
                                     for (int j = 0; j < pslots; ++j) d[j] = 0.0;
                                 }
                                 if (wrote) desc[stage].dirty = use - 1;
                             }
+                            nent = 1;
+                            ++pc_ent;
                         }
-                        slots += aslots;
-                        xs += xneed;
-                        ++nent;
-                        ++pc_ent;
                     }
                 }
             }
@@ -1809,6 +1907,10 @@ __global__ void __launch_bounds__(TS_NT, 1) k_mv_slab_tma(MatvecArgs args, const
             atomicAdd(&g_mv_cyc[5], pc_stages);
             atomicAdd(&g_mv_cyc[6], pc_ent);
             atomicAdd(&g_mv_cyc[7], clock64() - pc_t0);
+            atomicAdd(&g_mv_cyc[8], pc_meta);
+            atomicAdd(&g_mv_cyc[9], pc_copy);
+            atomicAdd(&g_mv_cyc[10], pc_commit);
+            atomicAdd(&g_mv_cyc[11], pc_items);
         }
     } else {
         // ------------------------------------------------ consumers
@@ -2843,7 +2945,7 @@ std::string prof_report(bool reset) {
     prof_flush();
     fold_ledger();
     std::string out;
-    char buf[320];
+    char buf[512];
     for (auto& [k, v] : g_prof_acc) {
         const double fl = g_flop_acc.count(k) ? g_flop_acc[k] : 0.0;
         const double sk = g_skip_acc.count(k) ? g_skip_acc[k] : 0.0;
@@ -2875,16 +2977,18 @@ std::string prof_report(bool reset) {
         snprintf(buf, sizeof(buf), "#phase warp32 tasks %llu (cycles per task): load %.0f qr %.0f jacobi %.0f sigma %.0f "
                  "write %.0f | sweeps %.2f rp %.2f\n", wc, w[0] / d, w[1] / d, w[2] / d, w[3] / d, w[4] / d, w[6] / d, w[7] / d);
         out += buf;
-        unsigned long long mv[8];
+        unsigned long long mv[16];
         cudaMemcpyFromSymbol(mv, g_mv_cyc, sizeof(mv));
         const double mc = mv[0] ? (double)mv[0] : 1.0;
         snprintf(buf, sizeof(buf), "#phase mv-slab-tma CTAs %llu (kcycles per CTA): total %.1f consumer wait %.1f work %.1f | "
-                 "producer total %.1f wait-empty %.1f | stages %.1f entries %.1f per CTA\n", mv[0], mv[1] / mc / 1e3,
-                 mv[2] / mc / 1e3, mv[3] / mc / 1e3, mv[7] / mc / 1e3, mv[4] / mc / 1e3, mv[5] / mc, mv[6] / mc);
+                 "producer total %.1f wait-empty %.1f first-records %.1f copy-issue %.1f commit %.1f | stages %.1f entries %.1f "
+                 "work items %.1f per CTA\n", mv[0], mv[1] / mc / 1e3, mv[2] / mc / 1e3, mv[3] / mc / 1e3, mv[7] / mc / 1e3,
+                 mv[4] / mc / 1e3, mv[8] / mc / 1e3, mv[9] / mc / 1e3, mv[10] / mc / 1e3, mv[5] / mc, mv[6] / mc, mv[11] / mc);
         out += buf;
         if (reset) {
             const unsigned long long z8[8] = {};
-            cudaMemcpyToSymbol(g_mv_cyc, z8, sizeof(z8));
+            const unsigned long long z16[16] = {};
+            cudaMemcpyToSymbol(g_mv_cyc, z16, sizeof(z16));
             cudaMemcpyToSymbol(g_w32_cyc, z8, sizeof(z8));
             cudaMemcpyToSymbol(g_w32_cnt, z8, sizeof(unsigned long long));
             const unsigned long long z[16] = {};
@@ -3047,11 +3151,11 @@ void launch_matvec(cudaStream_t st, const MatvecPlan& mp, int nrhs, int dim, Are
     const char* mv_env = getenv("ACRGPU_MV_LDG");  // read per call: the tests flip it between two solves
     const bool mv_ldg = mv_env && atoi(mv_env) != 0;
     // transient arena: [T pointers: count x nrk] [record counts: count x ntasks ints] [records: count x
-    // nleaves x 32 bytes] [packed x: count x RHS groups x xp_group] then the bump-allocated T blocks
+    // nleaves x 64 bytes] [packed x: count x RHS groups x xp_group] then the bump-allocated T blocks
     const int ngroups = (nrhs + MV_RHS - 1) / MV_RHS;
     const unsigned long long tbl = ((unsigned long long)mb.count * nrk + 15ull) & ~15ull;
     const unsigned long long cnt_d = (((unsigned long long)mb.count * ntasks + 1) / 2 + 15ull) & ~15ull;
-    const unsigned long long rec_d = ((unsigned long long)mb.count * mp.nleaves * 4 + 15ull) & ~15ull;
+    const unsigned long long rec_d = ((unsigned long long)mb.count * mp.nleaves * (sizeof(TsMeta) / 8) + 15ull) & ~15ull;
     const unsigned long long xp_d = ((unsigned long long)mb.count * ngroups * mp.xp_group + 15ull) & ~15ull;
     const bool tma = nrhs > 4 && !mv_ldg && tbl + cnt_d + rec_d + xp_d < arena.cap / 2;
     MatvecArgs a{mp.tasks, mp.leaves, mp.rk, nrk, nbig, nrhs, dim, arena, ledger(flops, "k_mv_t"), tma ? 1 : 0};
@@ -3090,7 +3194,7 @@ void launch_matvec(cudaStream_t st, const MatvecPlan& mp, int nrhs, int dim, Are
     else if (nr == 4) k_mv_slab1<4><<<grid1, NT, 0, st>>>(a, mb);
     else if (a.tma) {
         const long work = (long)ntasks * mb.count * ngroups;
-        k_mv_slab_tma<<<(unsigned)(work < 148 ? work : 148), TS_NT, TS_SMEM, st>>>(a, tm, mb, ntasks);
+        k_mv_slab_tma<<<(unsigned)(work < 296 ? work : 296), TS_NT, TS_SMEM, st>>>(a, tm, mb, ntasks);
     }
     else k_mv_slab<<<grid, NT, 0, st>>>(a, mb);
 }
