@@ -1278,14 +1278,14 @@ constexpr int MV_RHS = 16;      // right-hand sides per pass (fixed register slo
 // fragment (lanes (g, t) read T[k + t][rhs g] = g * ld + t: 16 distinct 8-byte banks).
 __host__ __device__ __forceinline__ int mv_ldt(int r) { return ((r + 3) & ~7) + 4; }
 
-// Contraction order of a dense leaf whose column count is a multiple of 32 (both slab kernels):
-// position p = 4 s + t (k-step s, DMMA k index t) contracts column mv_col(p) = 32 v + 8 t + u with
-// s = 8 v + u, i.e. the four columns of a k-step come from four different 8-column groups.  The
-// bulk-copy kernel brings such a leaf in as 8-column groups (one 4 KB copy each for 64 x 64),
-// padded by 4 doubles between groups, and this order makes its A fragments conflict-free; the
-// packed x block of the leaf's column cluster is stored in position order.  Other leaves: p.
-__host__ __device__ __forceinline__ int mv_col(int p) { return (p & ~31) | ((p & 3) << 3) | ((p >> 2) & 7); }
-__host__ __device__ __forceinline__ int mv_pos(int c) { return (c & ~31) | ((c & 7) << 2) | ((c >> 3) & 3); }
+// Contraction order of a dense leaf whose column count n is a multiple of 32 (both slab kernels):
+// position p = 4 s + t (k-step s, DMMA k index t) contracts column mv_col(p, n) = t (n / 4) + s, i.e.
+// the four columns of a k-step come from the four quarters of the leaf.  The bulk-copy kernel
+// brings such a leaf in as its four quarters (one 8 KB copy each for 64 x 64), padded by 4 doubles
+// between quarters, and this order makes its A fragments conflict-free; the packed x block of the
+// leaf's column cluster is stored in position order.  Other leaves: p.
+__host__ __device__ __forceinline__ int mv_col(int p, int n) { return (p & 3) * (n >> 2) + (p >> 2); }
+__host__ __device__ __forceinline__ int mv_pos(int c, int n) { return ((c % (n >> 2)) << 2) | (c / (n >> 2)); }
 
 __device__ __forceinline__ double** mv_tptr(const MatvecArgs& a) { return (double**)a.arena.base; }
 
@@ -1437,7 +1437,7 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
                     if (L.kind == K_DENSE) {
                         m.A = H.dense + L.doff;
                         m.len = L.n;
-                        m.perm = (L.n & 31) == 0;
+                        m.perm = (L.n & 31) == 0 && L.n <= 64;
                         m.xin = X + L.in_off + (size_t)c0 * ld;
                         m.ldx = ld;
                     } else {
@@ -1469,7 +1469,7 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
                         if (p < jn && c < nc) {
                             int q = q0, pos = j0 + p;
                             while (pos >= ((meta[q].len + 3) & ~3)) pos -= (meta[q++].len + 3) & ~3;
-                            if (pos < meta[q].len) v = meta[q].xin[(meta[q].perm ? mv_col(pos) : pos) + (size_t)c * meta[q].ldx];
+                            if (pos < meta[q].len) v = meta[q].xin[(meta[q].perm ? mv_col(pos, meta[q].len) : pos) + (size_t)c * meta[q].ldx];
                         }
                         Xs[c * MV_SLD + p] = v;
                     }
@@ -1495,7 +1495,7 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
 #pragma unroll
                                 for (int s = 0; s < 4; ++s) {
                                     const int jj = j + 4 * s + t4;
-                                    a[s] = (rok && jj < m.len) ? A[(size_t)(m.perm ? mv_col(jj) : jj) * m.lda] : 0.0;
+                                    a[s] = (rok && jj < m.len) ? A[(size_t)(m.perm ? mv_col(jj, m.len) : jj) * m.lda] : 0.0;
                                 }
                                 mv_step<(0 + R) & 3>(acc, a[0], b0[j + t4], b1[j + t4]);
                                 mv_step<(1 + R) & 3>(acc, a[1], b0[j + 4 + t4], b1[j + 4 + t4]);
@@ -1507,7 +1507,7 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
 #pragma unroll
                                 for (int s = 0; s < 3; ++s) {
                                     const int jj = j + 4 * s + t4;
-                                    a[s] = (rok && jj < m.len && j + 4 * s < je) ? A[(size_t)(m.perm ? mv_col(jj) : jj) * m.lda] : 0.0;
+                                    a[s] = (rok && jj < m.len && j + 4 * s < je) ? A[(size_t)(m.perm ? mv_col(jj, m.len) : jj) * m.lda] : 0.0;
                                 }
                                 mv_step<(0 + R) & 3>(acc, a[0], b0[j + t4], b1[j + t4]);
                                 if (j + 4 < je) mv_step<(1 + R) & 3>(acc, a[1], b0[j + 4 + t4], b1[j + 4 + t4]);
@@ -1546,22 +1546,32 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
 }
 
 // ------------------------------------------------------------------ solve, phase 2 on the bulk-copy engine
-// k_mv_slab_tma: the same slab contraction as k_mv_slab (same leaf order, same k-steps of 4 per
-// leaf, one accumulator chain per output element: bitwise the same result), fed by TMA bulk
-// copies (cp.async.bulk global -> shared, completion on an mbarrier) instead of per-lane loads.
-// One CTA per (<= 64-row slab, item): warps 0-7 are consumers (warp w owns slab rows 8w .. 8w+7
-// and all 16 right-hand sides, DMMA fragments read from shared memory), warps 8-11 are producers
-// (one warp can issue a bulk copy only every ~57-90 cycles, four keep 512-byte copies at the HBM
-// rate: tools/tma_bench.cu, profiles/r02_tma_bench.txt).
-// The producers walk the slab's leaf list, resolves ranks and pointers (32 leaves per round,
-// one per lane), and packs leaves into the stages of a ring: a stage holds up to 64 operand
-// columns (each column's slab rows copied to its own 68-double slot: ld == 4 (mod 16), so the A
-// fragment loads are conflict-free) and the matching contracted vectors (the x chunk of a dense
-// leaf, 16 per-RHS copies; the padded T block of an Rk leaf, one copy).  Pad columns of the
-// last k-step of a leaf hold stale finite operand data and multiply zeros of the contracted
-// vector.  Sources or sizes that are not 16-byte aligned (odd cluster sizes) are copied by the
-// producer lanes with ordinary loads and stores.  HBM-bound by design: every stored entry is
-// read once, several stages (tens of KB per SM) are in flight, no register staging.
+// k_mv_slab_tma: the same slab contraction as k_mv_slab (same leaf order, same k-steps, same four
+// partial sums per output element: bitwise the same result), fed by TMA bulk copies
+// (cp.async.bulk global -> shared, SASS UBLKCP, completion on an mbarrier by transaction bytes)
+// instead of per-lane loads.
+//   * Persistent CTAs, two per SM (296), walk the (<= 64-row slab, item, RHS group) work items; the
+//     stage ring of a CTA runs on across work items, so the next slab is fetched while the current
+//     one is contracted.
+//   * Warps 0-7 are consumers: warp w owns slab rows 8w .. 8w+7 and all 16 right-hand sides and reads
+//     its DMMA fragments from shared memory (every layout below has a leading dimension == 4 mod 16
+//     doubles: conflict-free 64-bit fragment loads).
+//   * Warps 8-11 are producers.  They stream the slab's 64-byte leaf records, written in list order
+//     by k_mv_resolve together with each leaf's place in the ring (stage entry, break flag), and issue
+//     the copies: a 64 x 64 (or 32 x 32) dense leaf as its four column quarters (8 KB each), padded
+//     by 4 doubles, contracted in mv_col order; the U columns of an Rk leaf as one 512-byte slab
+//     segment per column in 68-double slots; the contracted vectors as ONE copy (the packed x block
+//     of the leaf's column cluster, or the padded T block of the Rk leaf).  One warp issues a bulk
+//     copy only every ~57-90 cycles (tools/tma_bench.cu, profiles/r02_tma_bench.txt), hence four.
+//   * A stage holds up to 64 operand column slots and 1152 contracted-vector doubles (up to 16
+//     leaves).  Pad columns of a leaf's last k-step hold stale finite operand data (the ring is
+//     zeroed once) and multiply zeros of the contracted vector.
+//   * Sources or sizes that are not 16-byte aligned (odd cluster sizes) and zero pads of partial RHS
+//     groups are written by producer lanes with ordinary stores; a stage that received such stores is
+//     fenced (fence.proxy.async) before its next bulk copies.
+// Measured at C5 (16 RHS): 21.5 ms against 41.6 ms for the per-lane-load kernel; the limits now are
+// the producers' per-copy issue cost for rank-sized U columns and the consumers' DMMA issue rate
+// (device counters: acrgpu_profile_report's "#phase mv-slab-tma" line).
 constexpr int TS_STAGES = 2;                 // per CTA; two CTAs per SM
 constexpr int TS_SLOTS = 64;                 // operand column slots per stage
 constexpr int TS_ALD = 68;                   // slot stride in doubles
@@ -1572,7 +1582,7 @@ constexpr int TS_PROD = 4;                   // producer warps (one warp issues 
 constexpr int TS_NT = NT + 32 * TS_PROD;
 constexpr int TS_STAGE_DOUBLES = TS_SLOTS * TS_ALD + TS_XCAP;
 struct TsEnt {
-    short slot, ksteps, xoff, ldx, o0, o1, par, gm;  // par: parity of the leaf's position in the slab's list; gm > 0: 8-column groups of a gm-row dense leaf
+    short slot, ksteps, xoff, ldx, o0, o1, par, gm;  // par: parity of the leaf's position in the slab's list; gm > 0: the four column quarters of a gm-row dense leaf
 };
 struct TsDesc {
     int nent, last;
@@ -1591,7 +1601,7 @@ struct TsMeta {        // one resolved, non-empty leaf of a slab with its place 
     short roff;        // o0's row inside the leaf
     short aslots;      // operand slots taken
     int xneed;         // contracted-vector doubles taken
-    unsigned char flags;  // TF_GROUPED: 8-column groups; TF_PERM: mv_col order; TF_XBLOCK: one copy brings the vectors;
+    unsigned char flags;  // TF_GROUPED: four column quarters; TF_PERM: mv_col order; TF_XBLOCK: one copy brings the vectors;
                           // TF_BRK: commit the open stage first; TF_WIDE: more than TS_SLOTS columns, one stage per piece
     unsigned char pad[7];
 };
@@ -1628,10 +1638,10 @@ __global__ void __launch_bounds__(NT) k_mv_resolve(MatvecArgs args, const Matvec
             const int gi = (int)((u / tm.ncl) % ngroups), b = (int)(u / ((long)tm.ncl * ngroups));
             const double* x = mb.x[b] + C.in_off + (size_t)gi * MV_RHS * args.dim;
             double* dst = tm.xp + ((size_t)b * ngroups + gi) * tm.xp_group + C.xoff;
-            const bool perm = (C.n & 31) == 0;
+            const bool perm = (C.n & 31) == 0 && C.n <= 64;
             for (int e = lane; e < MV_RHS * C.ldx; e += 32) {
                 const int c = e / C.ldx, pp = e - c * C.ldx;
-                const int col = perm ? mv_col(pp) : pp;
+                const int col = (perm && pp < C.n) ? mv_col(pp, C.n) : pp;
                 dst[e] = (pp < C.n && gi * MV_RHS + c < args.nrhs) ? x[col + (size_t)c * args.dim] : 0.0;
             }
             continue;
@@ -1682,14 +1692,14 @@ __global__ void __launch_bounds__(NT) k_mv_resolve(MatvecArgs args, const Matvec
                     }
                     if (ok) {
                         const int n4 = (m.len + 3) & ~3;
-                        const bool perm = dense && (m.len & 31) == 0;
+                        const bool perm = dense && (m.len & 31) == 0 && m.len <= 64;
                         const bool wide = m.len > TS_SLOTS;
                         const bool xblock = dense == 1 || (!dense && !wide);
                         const int ldx = dense == 1 ? n4 + ((20 - (n4 & 15)) & 15) : (xblock ? mv_ldt(m.len) : TS_XLD);
-                        const int gs = 8 * m.lda + 4;
+                        const int gs = (m.len >> 2) * m.lda + 4;  // quarter stride
                         const bool grouped = perm && !wide && m.roff == 0 && o1 - o0 == m.lda && (m.lda & 1) == 0 &&
                                              (((unsigned long long)m.A) & 15ull) == 0;
-                        m.aslots = (short)(grouped ? ((m.len >> 3) * gs + TS_ALD - 1) / TS_ALD : n4);
+                        m.aslots = (short)(grouped ? (4 * gs + TS_ALD - 1) / TS_ALD : n4);
                         m.xneed = MV_RHS * ldx;
                         m.ent.ksteps = (short)(n4 >> 2);
                         m.ent.ldx = (short)ldx;
@@ -1836,12 +1846,11 @@ __global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const
                         const unsigned long long tk0 = clock64();
                         double* Ad = As + (size_t)m.ent.slot * TS_ALD;
                         if (m.flags & TF_GROUPED) {
-                            const int G = pw + TS_PROD * lane, gs = 8 * m.lda + 4;
-                            if (G < (m.len >> 3))
-                                ts_copy(Ad + (size_t)G * gs, m.A + (size_t)G * 8 * m.lda, 8 * m.lda, full + stage, tx);  // aligned (k_mv_resolve)
+                            const int G = pw + TS_PROD * lane, qn = (m.len >> 2) * m.lda;  // quarter G: qn contiguous doubles
+                            if (G < 4) ts_copy(Ad + (size_t)G * (qn + 4), m.A + (size_t)G * qn, qn, full + stage, tx);  // aligned (k_mv_resolve)
                         } else {
                             for (int c = pw + TS_PROD * lane; c < m.len; c += 32 * TS_PROD)
-                                if (ts_copy(Ad + (size_t)((m.flags & TF_PERM) ? mv_pos(c) : c) * TS_ALD + m.ent.o0,
+                                if (ts_copy(Ad + (size_t)((m.flags & TF_PERM) ? mv_pos(c, m.len) : c) * TS_ALD + m.ent.o0,
                                             m.A + (size_t)c * m.lda + m.roff, nrow, full + stage, tx))
                                     desc[stage].dirty = use - 1;
                         }
@@ -1855,7 +1864,7 @@ __global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const
                             if (c < MV_RHS) {
                                 double* d = xd + (size_t)c * TS_XLD;
                                 if (c < nc) {
-                                    for (int j = 0; j < m.len; ++j) d[j] = xin[((m.flags & TF_PERM) ? mv_col(j) : j) + (size_t)c * m.ldsrc];
+                                    for (int j = 0; j < m.len; ++j) d[j] = xin[((m.flags & TF_PERM) ? mv_col(j, m.len) : j) + (size_t)c * m.ldsrc];
                                     for (int j = m.len; j < pslots; ++j) d[j] = 0.0;
                                 } else {
                                     for (int j = 0; j < pslots; ++j) d[j] = 0.0;
@@ -1951,12 +1960,11 @@ __global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const
                     if (8 * warp >= E.o1 || 8 * warp + 8 <= E.o0) continue;  // no rows of this warp
                     const bool rok = r >= E.o0 && r < E.o1;
                     // per-column slots: position p at slot p (stride TS_ALD), rows at their slab position;
-                    // 8-column groups: k-step s = 8 v + u reads column u of group 4 v + t4 (group stride gs)
-                    const int gs = 8 * E.gm + 4;
+                    // quarters of a dense leaf: k-step s reads column s of quarter t4 (quarter stride gs)
+                    const int gs = E.ksteps * E.gm + 4;
                     const double* A = E.gm ? As + (size_t)E.slot * TS_ALD + (size_t)t4 * gs + (r - E.o0)
                                            : As + (size_t)E.slot * TS_ALD + r + (size_t)t4 * TS_ALD;
-                    const int st_u = E.gm ? E.gm : 4 * TS_ALD;        // stride of one k-step inside a block of 8
-                    const int st_v = E.gm ? 4 * gs - 8 * E.gm : 0;    // extra stride every 8 k-steps
+                    const int st_u = E.gm ? E.gm : 4 * TS_ALD;  // stride of one k-step
                     const double* b0 = Xs + E.xoff + g * E.ldx + t4;
                     const double* b1 = b0 + 8 * E.ldx;
                     const int ks = E.ksteps;
@@ -1967,7 +1975,7 @@ __global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const
                             double a[4], x0[4], x1[4];
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                a[q] = rok ? A[(size_t)(s + q) * st_u + (size_t)((s + q) >> 3) * st_v] : 0.0;
+                                a[q] = rok ? A[(size_t)(s + q) * st_u] : 0.0;
                                 x0[q] = b0[4 * (s + q)];
                                 x1[q] = b1[4 * (s + q)];
                             }
@@ -1981,7 +1989,7 @@ __global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const
 #pragma unroll
                             for (int q = 0; q < 3; ++q) {
                                 const bool ok = s + q < ks;
-                                a[q] = (rok && ok) ? A[(size_t)(s + q) * st_u + (size_t)((s + q) >> 3) * st_v] : 0.0;
+                                a[q] = (rok && ok) ? A[(size_t)(s + q) * st_u] : 0.0;
                                 x0[q] = ok ? b0[4 * (s + q)] : 0.0;
                                 x1[q] = ok ? b1[4 * (s + q)] : 0.0;
                             }

@@ -72,6 +72,19 @@ def test_config5_operator_leaf64_multi_rhs(acr, oracle, n):
     assert abs(g.factor_bytes() - so["factor_bytes"]) <= 0.02 * so["factor_bytes"]
 
 
+@pytest.mark.parametrize("n", [14, 18])
+def test_config5_operator_odd_leaf_sizes(acr, oracle, n):
+    """Leaf 64 on planes whose leaf clusters are odd (n = 14: 196 points -> 49-point leaves) or
+    mixed (n = 18: 324 -> 81 -> {40, 41}): the 64-class kernels on operands whose sizes and
+    addresses are not 16-byte aligned -- k_dd_product's load/store staging instead of its two TMA
+    bulk copies, the slab kernel's producer-store path -- against the oracle, 16 right-hand sides."""
+    c = P.CONFIGS[5]
+    sysm = P.config_system(5, n=n)
+    g, o, ug, uo, rg, ro, sg, so = compare(acr, oracle, sysm, c["eps"], c["leaf"], threads=8)
+    assert_parity(rg, ro, sg, so, g.level_info(), o.level_info())
+    assert np.linalg.norm(ug - uo) <= 1e-3 * np.linalg.norm(uo)
+
+
 def test_config1_full_size(acr, oracle):
     """C1 at its BASELINE size (n=32, N=32768, eps 1e-6): residual, ranks, bytes."""
     sysm = P.config_system(1)
@@ -145,7 +158,7 @@ def test_multi_rhs_bitwise_and_linearity(acr):                                  
     assert np.linalg.norm(u3 - (2.0 * u1 - 0.5 * u2)) <= 1e-12 * np.linalg.norm(u3)
 
 
-@pytest.mark.parametrize("k,n,nrhs", [(5, 16, 16), (5, 32, 16), (2, 16, 5), (1, 10, 7), (3, 14, 20), (2, 22, 33)])
+@pytest.mark.parametrize("k,n,nrhs", [(5, 16, 16), (5, 32, 16), (5, 14, 16), (2, 16, 5), (1, 10, 7), (3, 14, 20), (2, 22, 33)])
 def test_bulk_copy_slab_kernel_is_bitwise_the_load_kernel(acr, monkeypatch, k, n, nrhs):
     # Solves with more than 4 right-hand sides run phase 2 of the H-matvec on the TMA bulk-copy
     # engine (k_mv_slab_tma: cp.async.bulk into a shared-memory ring, DMMA from shared memory).
