@@ -1320,13 +1320,102 @@ __device__ __forceinline__ double mv_acc_sum(const double (&acc)[4][4], int i) {
 // X^T (16 x n) V (n x rank), rank tiles of 8, k-steps of 4 rows.  V streams from HBM (each
 // load = 8 rank columns x 4 consecutive rows, full 32-byte sectors), X from L2 (units are
 // item-major, so the warps in flight share one item's X).
+// The Rk leaf list is sorted by decreasing column count; its first nbig leaves (n >= 512) take a
+// whole CTA each: the eight warps interleave the leaf's 32-row chunks and their partial T tiles
+// are added in warp order (a lone warp streaming an 8192-row factor -- 256 dependent load rounds --
+// was the critical path of every launch: ~0.3 ms of floor, 41 launches per solve).
+__device__ __forceinline__ void mv_t_chunks(const double* vcol, bool vok, const double* xlo, const double* xhi, bool c_lo, bool c_hi,
+                                            int n, int k_first, int k_step, int t4, double& d00, double& d01, double& d10,
+                                            double& d11) {
+    int k0 = k_first;
+    for (; k0 + 32 <= n; k0 += k_step) {  // eight k-steps, loads first
+        double va[8], xa[8], xb[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int j = k0 + 4 * s + t4;
+            va[s] = vok ? vcol[j] : 0.0;
+            xa[s] = c_lo ? xlo[j] : 0.0;
+            xb[s] = c_hi ? xhi[j] : 0.0;
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            dmma8x8x4(d00, d01, xa[s], va[s]);
+            dmma8x8x4(d10, d11, xb[s], va[s]);
+        }
+    }
+    // the (< 32-row) tail of the leaf belongs to the chunk sequence of whoever reaches it first
+    if (k0 < n && k0 == (n & ~31)) {
+        for (; k0 < n; k0 += 4) {
+            const int j = k0 + t4;
+            const bool jok = j < n;
+            const double va = (vok && jok) ? vcol[j] : 0.0;
+            dmma8x8x4(d00, d01, (c_lo && jok) ? xlo[j] : 0.0, va);
+            dmma8x8x4(d10, d11, (c_hi && jok) ? xhi[j] : 0.0, va);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(NT) k_mv_t(MatvecArgs args, const __grid_constant__ MatvecBatch mb) {
-    const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
-    const long total = (long)args.nrk * mb.count;
-    const long stride = (long)gridDim.x * (NT / 32);
+    __shared__ double part[NT / 32][MV_RHS][8];
+    __shared__ double* sh_T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+    const int ld = args.dim;
+    const long nbig_ctas = (long)args.nbig * mb.count;
+    if ((long)blockIdx.x < nbig_ctas) {
+        // ---- one wide leaf per CTA
+        const int b = (int)(blockIdx.x / args.nbig), li = (int)(blockIdx.x % args.nbig);
+        const MvLeaf L = args.rk[li];
+        const HView& H = mb.h[b];
+        const int rr = H.rank[L.k];
+        const int ldt = args.tma ? mv_ldt(rr) : rr;
+        const int ncol = args.tma ? (args.nrhs + MV_RHS - 1) / MV_RHS * MV_RHS : args.nrhs;
+        if (threadIdx.x == 0) {
+            sh_T = rr > 0 ? arena_alloc(args.arena, (unsigned long long)ldt * ncol) : nullptr;
+            mv_tptr(args)[(size_t)b * args.nrk + L.k] = sh_T;
+        }
+        __syncthreads();
+        double* T = sh_T;
+        if (T == nullptr) return;
+        if (args.tma)
+            for (int e = threadIdx.x; e < ldt * ncol; e += NT)
+                if (e % ldt >= rr || e / ldt >= args.nrhs) T[e] = 0.0;
+        const double* V = H.V[L.k];
+        const int n = L.n;
+        for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
+            const int nc = min(MV_RHS, args.nrhs - c0);
+            const double* X = mb.x[b] + L.in_off + (size_t)c0 * ld;
+            const bool c_lo = g < nc, c_hi = g + 8 < nc;
+            for (int tc = 0; tc < rr; tc += 8) {
+                const bool vok = tc + g < rr;
+                double d00 = 0, d01 = 0, d10 = 0, d11 = 0;
+                mv_t_chunks(V + (size_t)(vok ? tc + g : 0) * n, vok, X + (size_t)g * ld, X + (size_t)(g + 8) * ld, c_lo, c_hi, n,
+                            32 * warp, 32 * (NT / 32), t4, d00, d01, d10, d11);
+                // C[g][2 t4 + i]: RHS g (+8), rank tc + 2 t4 + i
+                part[warp][g][2 * t4] = d00;
+                part[warp][g][2 * t4 + 1] = d01;
+                part[warp][g + 8][2 * t4] = d10;
+                part[warp][g + 8][2 * t4 + 1] = d11;
+                __syncthreads();
+                if (threadIdx.x < MV_RHS * 8) {
+                    const int c = threadIdx.x >> 3, tr = tc + (threadIdx.x & 7);
+                    double sum = part[0][c][threadIdx.x & 7];
+#pragma unroll
+                    for (int w = 1; w < NT / 32; ++w) sum += part[w][c][threadIdx.x & 7];
+                    if (tr < rr && c < nc) T[tr + (size_t)(c0 + c) * ldt] = sum;
+                }
+                __syncthreads();
+            }
+        }
+        if (threadIdx.x == 0) add_flops(args.flops, F_APPLY, 2.0 * rr * n * args.nrhs);
+        return;
+    }
+    // ---- every other leaf: one (item, leaf) per warp
+    const int nsm = args.nrk - args.nbig;
+    const long total = (long)nsm * mb.count;
+    const long stride = (long)(gridDim.x - nbig_ctas) * (NT / 32);
     double fl = 0;
-    for (long w = (long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); w < total; w += stride) {
-        const int b = (int)(w / args.nrk), li = (int)(w % args.nrk);
+    for (long w = ((long)blockIdx.x - nbig_ctas) * (NT / 32) + warp; w < total; w += stride) {
+        const int b = (int)(w / nsm), li = args.nbig + (int)(w % nsm);
         const MvLeaf L = args.rk[li];
         const HView& H = mb.h[b];
         const int rr = H.rank[L.k];
@@ -1345,41 +1434,17 @@ __global__ void __launch_bounds__(NT) k_mv_t(MatvecArgs args, const __grid_const
             for (int e = lane; e < ldt * ncol; e += 32)
                 if (e % ldt >= rr || e / ldt >= args.nrhs) T[e] = 0.0;
         const double* V = H.V[L.k];
-        const int n = L.n, ld = args.dim;
+        const int n = L.n;
         for (int c0 = 0; c0 < args.nrhs; c0 += MV_RHS) {
             const int nc = min(MV_RHS, args.nrhs - c0);
             const double* X = mb.x[b] + L.in_off + (size_t)c0 * ld;
             const bool c_lo = g < nc, c_hi = g + 8 < nc;  // this lane's A rows (RHS g, g + 8)
-            const double* xlo = X + (size_t)g * ld;
-            const double* xhi = X + (size_t)(g + 8) * ld;
             for (int tc = 0; tc < rr; tc += 8) {
                 const bool vok = tc + g < rr;  // this lane's B column (rank tc + g)
-                const double* vcol = V + (size_t)(vok ? tc + g : 0) * n;
                 double d00 = 0, d01 = 0, d10 = 0, d11 = 0;  // C tiles: RHS 0-7 / 8-15 x rank tc..tc+7
-                int k0 = 0;
-                for (; k0 + 32 <= n; k0 += 32) {  // eight k-steps, loads first
-                    double va[8], xa[8], xb[8];
-#pragma unroll
-                    for (int s = 0; s < 8; ++s) {
-                        const int j = k0 + 4 * s + t4;
-                        va[s] = vok ? vcol[j] : 0.0;
-                        xa[s] = c_lo ? xlo[j] : 0.0;
-                        xb[s] = c_hi ? xhi[j] : 0.0;
-                    }
-#pragma unroll
-                    for (int s = 0; s < 8; ++s) {
-                        dmma8x8x4(d00, d01, xa[s], va[s]);
-                        dmma8x8x4(d10, d11, xb[s], va[s]);
-                    }
-                }
-                for (; k0 < n; k0 += 4) {
-                    const int j = k0 + t4;
-                    const bool jok = j < n;
-                    const double va = (vok && jok) ? vcol[j] : 0.0;
-                    dmma8x8x4(d00, d01, (c_lo && jok) ? xlo[j] : 0.0, va);
-                    dmma8x8x4(d10, d11, (c_hi && jok) ? xhi[j] : 0.0, va);
-                }
-                // C[g][2 t4 + i]: RHS g (+8), rank tc + 2 t4 + i  ->  T[rank + rhs * rr]
+                mv_t_chunks(V + (size_t)(vok ? tc + g : 0) * n, vok, X + (size_t)g * ld, X + (size_t)(g + 8) * ld, c_lo, c_hi, n,
+                            0, 32, t4, d00, d01, d10, d11);
+                // C[g][2 t4 + i]: RHS g (+8), rank tc + 2 t4 + i  ->  T[rank + rhs * ldt]
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                     const int tr = tc + 2 * t4 + i;
@@ -3182,8 +3247,8 @@ void launch_matvec(cudaStream_t st, const MatvecPlan& mp, int nrhs, int dim, Are
     const int nr = nrhs <= 1 ? 1 : (nrhs <= 2 ? 2 : (nrhs <= 4 ? 4 : 0));
     if (nrk > 0) {
         ProfScope _ps(st, "k_mv_t", (long)nrk * mb.count);
-        const unsigned grid = nr ? (unsigned)((long)nbig * mb.count) + warp_grid((long)(nrk - nbig) * mb.count)
-                                 : item_grid((long)nrk * mb.count, 4);
+        const unsigned grid = (unsigned)((long)nbig * mb.count) +
+                              (nr ? warp_grid((long)(nrk - nbig) * mb.count) : item_grid(((long)(nrk - nbig) * mb.count + 7) / 8, 4));
         if (nr == 1) k_mv_t1<1><<<grid, NT, 0, st>>>(a, mb);
         else if (nr == 2) k_mv_t1<2><<<grid, NT, 0, st>>>(a, mb);
         else if (nr == 4) k_mv_t1<4><<<grid, NT, 0, st>>>(a, mb);
