@@ -180,6 +180,25 @@ def test_bulk_copy_slab_kernel_is_bitwise_the_load_kernel(acr, monkeypatch, k, n
         assert sysm.relative_residual(u_tma[j:j + 1], g[j:j + 1]) <= 1e-4
 
 
+def test_bulk_copy_slab_kernel_wide_leaves(acr, monkeypatch):
+    # Rk leaves of rank > 64 take the slab kernel's one-stage-per-piece path (TF_WIDE) and phase 1's
+    # multi-tile loop.  Weak admissibility makes the off-diagonal half blocks of a 48 x 48 plane
+    # low-rank leaves whose rank at eps 1e-12 exceeds 64 (asserted, so the path cannot go untested).
+    sysm = P.config_system(1, n=48)
+    sysm = P.first_planes(sysm, 6)  # six 2304-point planes
+    cfg = acr.AcrConfig(eps=1e-12, leaf_size=32, admissibility=acr.Admissibility.Weak)
+    f = acr.acr_factor(sysm, cfg)
+    assert f.inverse_rank_stats().largest_rank > 64
+    nrhs = 16
+    g = P.uniform_pm1(91, 3, nrhs * sysm.rhs[0].size).reshape((nrhs,) + sysm.rhs[0].shape)
+    u_tma = f.solve(g)
+    monkeypatch.setenv("ACRGPU_MV_LDG", "1")
+    u_ldg = f.solve(g)
+    monkeypatch.delenv("ACRGPU_MV_LDG")
+    assert np.array_equal(u_tma, u_ldg)
+    assert sysm.relative_residual(u_tma, g) <= 1e-8
+
+
 def test_factorization_deterministic(acr):
     sysm = P.config_system(3, n=16)
     cfg = acr.AcrConfig(eps=1e-6)
