@@ -1634,7 +1634,7 @@ __global__ void __launch_bounds__(NT) k_mv_slab(MatvecArgs args, const __grid_co
 //   * Sources or sizes that are not 16-byte aligned (odd cluster sizes) and zero pads of partial RHS
 //     groups are written by producer lanes with ordinary stores; a stage that received such stores is
 //     fenced (fence.proxy.async) before its next bulk copies.
-// Measured at C5 (16 RHS): 21.5 ms against 41.6 ms for the per-lane-load kernel; the limits now are
+// Measured at C5 (16 RHS): 20.6 ms against 41.6 ms for the per-lane-load kernel; the limits now are
 // the producers' per-copy issue cost for rank-sized U columns and the consumers' DMMA issue rate
 // (device counters: acrgpu_profile_report's "#phase mv-slab-tma" line).
 constexpr int TS_STAGES = 2;                 // per CTA; two CTAs per SM
@@ -1913,16 +1913,21 @@ __global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const
                         if (m.flags & TF_GROUPED) {
                             const int G = pw + TS_PROD * lane, qn = (m.len >> 2) * m.lda;  // quarter G: qn contiguous doubles
                             if (G < 4) ts_copy(Ad + (size_t)G * (qn + 4), m.A + (size_t)G * qn, qn, full + stage, tx);  // aligned (k_mv_resolve)
-                        } else {
-                            for (int c = pw + TS_PROD * lane; c < m.len; c += 32 * TS_PROD)
+                        } else if (pw == (int)(pc_ent % TS_PROD)) {
+                            // the columns of a per-column leaf (the U columns of an Rk leaf: rank-many 512-byte
+                            // copies) are all issued by ONE producer warp, one lane each, and consecutive
+                            // leaves go to different warps: the four warps issue in parallel instead of
+                            // walking every leaf in lockstep with one or two copies each
+                            for (int c = lane; c < m.len; c += 32)
                                 if (ts_copy(Ad + (size_t)((m.flags & TF_PERM) ? mv_pos(c, m.len) : c) * TS_ALD + m.ent.o0,
                                             m.A + (size_t)c * m.lda + m.roff, nrow, full + stage, tx))
                                     desc[stage].dirty = use - 1;
                         }
                         double* xd = Xs + m.ent.xoff;
                         if (m.flags & TF_XBLOCK) {
-                            if (lane == 0 && pw == nent % TS_PROD && ts_copy(xd, xin, m.xneed, full + stage, tx))
-                                desc[stage].dirty = use - 1;
+                            const bool xmine = (m.flags & TF_GROUPED) ? (lane == 0 && pw == nent % TS_PROD)
+                                                                      : (lane == 31 && pw == (int)(pc_ent % TS_PROD));
+                            if (xmine && ts_copy(xd, xin, m.xneed, full + stage, tx)) desc[stage].dirty = use - 1;
                         } else {
                             // raw x of a dense leaf whose columns are not one leaf cluster: per right-hand side
                             const int c = pw + TS_PROD * lane, pslots = 4 * m.ent.ksteps;
