@@ -1850,7 +1850,7 @@ __global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const
             const int b = (int)((w / ntasks) % mb.count);
             const int c0 = (int)(w / ((long)ntasks * mb.count)) * MV_RHS;
             const int nc = min(MV_RHS, args.nrhs - c0);
-            int slots = 0, xs = 0, nent = 0;
+            int nent = 0;  // entries of the open stage
             unsigned tx = 0;
             bool open = false;  // stage acquired (empty barrier passed)
             double* As = nullptr;
@@ -1862,13 +1862,12 @@ __global__ void __launch_bounds__(TS_NT, 2) k_mv_slab_tma(MatvecArgs args, const
                 ++pc_stages;
                 // bulk copies over data this stage received by ordinary stores in its previous use
                 // (unaligned copies, zero pads) are ordered behind them by a proxy fence; the common
-                // path (aligned leaves, 16 right-hand sides) never needs it -- and must not pay it:
-                // the fence also waits for the bulk copies already in flight
+                // path (aligned leaves, 16 right-hand sides) never needs one
                 if (desc[stage].dirty >= use - TS_STAGES) fence_proxy_async();
                 ++use;
                 As = stage0 + (size_t)stage * TS_STAGE_DOUBLES;
                 Xs = As + TS_SLOTS * TS_ALD;
-                slots = 0, xs = 0, nent = 0, tx = 0;
+                nent = 0, tx = 0;
                 open = true;
             };
             auto commit = [&](int last) {
