@@ -134,7 +134,7 @@ typedef struct acrgpu_fact acrgpu_fact;
    device resources are released with the last of them.
    One context = one device = one worker of the reference's plane partition
    (parallel.cpp:96-297): a multi-GPU run creates one context per process / GPU and
-   ties them together with an acrgpu_comm (below), rather than passing a device
+   ties them together with a communicator handle (acrgpu_comm, below), rather than passing a device
    list to one context as SURVEY.md's sketch of the boundary did. */
 int acrgpu_ctx_create(int device, acrgpu_ctx** out, acrgpu_error* err);
 void acrgpu_ctx_destroy(acrgpu_ctx* ctx);
